@@ -1,0 +1,154 @@
+/* ggb.h — C ABI of libggb.so, the B200-native (sm_100a) mini-batch GCN
+ * training step of ScaleGNN (arxiv 2604.02651).
+ *
+ * The reference boundary is the C++ API of /root/reference/proj (namespace
+ * gridgnn; there is no FFI). Each entry point below replaces the reference
+ * function cited beside it; the header-only C++ drop-in
+ * paper_2604_02651_b200/cpp/gridgnn/ggb.hpp restores the reference's own
+ * names, by-value results and exception types on top of it, and the Python
+ * mirror paper_2604_02651_b200/gridgnn.py binds it through ctypes.
+ *
+ * Conventions: plain pointers and sizes only; every call returns a status
+ * code and never throws; host arrays are caller-owned; device memory is owned
+ * by the handles and freed by the matching *_destroy. A handle is used by one
+ * host thread at a time (the prefetch producer owns its batches until it hands
+ * them over, as the reference PrefetchQueue does, model.hpp:556-581).
+ */
+#ifndef GGB_H_
+#define GGB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum ggb_status {
+  GGB_OK = 0,
+  GGB_EINVAL = 1,    /* -> std::invalid_argument (e.g. sampling.cpp:12-13) */
+  GGB_ECONTRACT = 2, /* -> CommContract (comm.hpp:44-46, pmm.hpp:67-69)    */
+  GGB_ETIMEOUT = 3,  /* -> CommTimeout (comm.hpp:41-43)                      */
+  GGB_ECUDA = 4,     /* -> std::runtime_error                                */
+  GGB_ENCCL = 5,     /* -> std::runtime_error                                */
+  GGB_EINTERNAL = 9
+};
+
+enum ggb_precision { GGB_FP32 = 0, GGB_BF16_WIRE = 1 }; /* comm.hpp:22 Precision */
+enum ggb_optimizer { GGB_SGD = 0, GGB_ADAM = 1 };       /* model.hpp:45 Optimizer */
+
+typedef struct ggb_ctx_s* ggb_ctx_t;     /* one per (process, GPU): grid coords, streams, comms, sampler */
+typedef struct ggb_graph_s* ggb_graph_t; /* Dataset + RankContext plane shards resident in HBM */
+typedef struct ggb_batch_s* ggb_batch_t; /* StepBatch resident in HBM (model.hpp:238-246) */
+typedef struct ggb_state_s* ggb_state_t; /* ModelState resident in HBM (model.hpp:87-105) */
+
+/* ModelConfig (model.hpp:26-43) */
+typedef struct {
+  int32_t layers;
+  int64_t d_in, d_h, d_out;
+  double dropout_rate;
+  int32_t use_rmsnorm, use_dropout, use_residual;
+} ggb_model_config;
+
+const char* ggb_last_error(void); /* thread-local message of the last failure */
+int ggb_version(void);
+
+/* ---- context: replaces Communicator/RankComm (comm.hpp:203-408) ------------
+ * dims = {g_d, g_x, g_y, g_z}; rank numbering as DeviceGrid (grid.hpp:26-28).
+ * nccl_uid (128 bytes from ggb_get_unique_id on rank 0, broadcast by the
+ * caller) creates the world communicator and one split per axis. With
+ * nccl_uid == NULL the context is "virtual": sampling and single-rank compute
+ * work; any collective over a group larger than one fails GGB_ECONTRACT.
+ * stream: the CUDA stream compute is launched on (NULL = library-owned). */
+int ggb_get_unique_id(uint8_t out[128]);
+int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const uint8_t* nccl_uid,
+                   void* stream, ggb_ctx_t* out);
+int ggb_ctx_destroy(ggb_ctx_t ctx);
+int ggb_ctx_set_stream(ggb_ctx_t ctx, void* stream);
+int ggb_ctx_synchronize(ggb_ctx_t ctx);
+/* counters[0] = kernels this library launched on ctx since creation */
+int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters);
+
+/* ---- sampler: sample_vertices (sampling.cpp:11-33) ------------------------- */
+int ggb_sample_vertices(ggb_ctx_t ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step,
+                        int64_t* host_out);
+
+/* ---- graph: Dataset (dataset.hpp:16-29) + make_rank_context (model.hpp:217-234)
+ * Host CSR of D^-1/2(A+I)D^-1/2 (int64 row_ptr/col_idx, fp64 values). Uploads
+ * this rank's static plane shards (make_csr_shard, shardsample.cpp:19-45) and
+ * their transposes, the feature column slice and the labels. symmetric != 0
+ * asserts A == A^T (always true for normalize_adjacency outputs,
+ * dataset.cpp:47-83) and skips the host transpose. */
+int ggb_graph_create(ggb_ctx_t ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                     const double* values, int32_t symmetric, int64_t d_in, const float* features,
+                     int64_t n_classes, const int32_t* labels, int32_t layers, ggb_graph_t* out);
+/* generate_synthetic (dataset.cpp:85-131) implemented natively (bit-identical
+ * to the reference generator), then uploaded as ggb_graph_create does. */
+int ggb_graph_generate_synthetic(ggb_ctx_t ctx, int64_t n, double avg_degree, int64_t d_in,
+                                 int64_t n_classes, uint64_t seed, int32_t layers,
+                                 ggb_graph_t* out);
+int ggb_graph_destroy(ggb_graph_t g);
+/* info = {n, nnz, d_in, n_classes, distinct_plane_shards, device_bytes} */
+int ggb_graph_info(ggb_graph_t g, int64_t* info);
+
+/* ---- batches: build_step_batch (model.hpp:250-309) / build_local_minibatch
+ * (shardsample.cpp:124-156). Communication-free. The batch handle is reused
+ * (grow-only buffers) when passed back in *inout; NULL creates one. */
+int ggb_build_step_batch(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group_seed,
+                         uint64_t step, ggb_batch_t* inout);
+int ggb_batch_destroy(ggb_batch_t batch);
+/* info = {b, n, planes, x_r0, x_r1, x_c0, x_c1, nnz_extracted, nnz_kept} */
+int ggb_batch_info(ggb_batch_t batch, int64_t* info);
+int ggb_batch_sample(ggb_batch_t batch, int64_t* host_out);
+/* batch_off for axis in {1,2,3}: dims[axis]+1 offsets */
+int ggb_batch_offsets(ggb_batch_t batch, int32_t axis, int64_t* host_out);
+/* dims = {n_rows, n_cols, nnz, r0, r1, c0, c1}; arrays may be NULL (query) */
+int ggb_batch_plane(ggb_batch_t batch, int32_t plane, int32_t transposed, int64_t* dims,
+                    int64_t* row_ptr, int64_t* col_idx, double* values);
+/* x_in block (x_r1-x_r0) x (x_c1-x_c0) as exact fp32 copies of the features */
+int ggb_batch_x_in(ggb_batch_t batch, float* host_out);
+int ggb_batch_labels(ggb_batch_t batch, int32_t* host_out);
+
+/* ---- model state: init_state (model.hpp:175-208) ------------------------------ */
+int ggb_state_create(ggb_ctx_t ctx, const ggb_model_config* cfg, uint64_t seed, ggb_state_t* out);
+int ggb_state_destroy(ggb_state_t st);
+/* parameter views in param_views order (model.hpp:107-133): win, [w_l, gamma_l]*L, wout */
+int ggb_state_num_params(ggb_state_t st);
+/* info = {global_rows, global_cols, r0, r1, c0, c1}; a gamma has rows = 1 */
+int ggb_state_param_info(ggb_state_t st, int32_t idx, int64_t* info);
+/* which: 0 weight, 1 grad, 2 adam m, 3 adam v; local block, row-major */
+int ggb_state_param_get(ggb_state_t st, int32_t idx, int32_t which, float* host_out);
+int ggb_state_param_set(ggb_state_t st, int32_t idx, int32_t which, const float* host_in);
+
+/* ---- training: train_step / forward / dp_sync / optimizer_step (model.hpp:335-478) */
+/* forward + cross-entropy + backward; grads left un-synced. loss_out (host,
+ * nullable: NULL keeps the call asynchronous and the loss on the device). */
+int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, int32_t precision,
+                   uint64_t run_seed, uint64_t global_step, double rmsnorm_eps, float* loss_out);
+/* device-side loss of the last train_step (one float) */
+int ggb_last_loss_device(ggb_state_t st, const float** dev_ptr);
+/* logits block of the last forward: dims = {r0, r1, c0, c1}; out may be NULL */
+int ggb_state_logits(ggb_state_t st, int64_t* dims, float* host_out);
+int ggb_forward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, int32_t precision,
+                int32_t training, uint64_t run_seed, uint64_t global_step, double rmsnorm_eps);
+int ggb_dp_sync(ggb_ctx_t ctx, ggb_state_t st);
+int ggb_optimizer_step(ggb_ctx_t ctx, ggb_state_t st, int32_t optimizer, double lr);
+
+/* ---- kernels exposed for unit tests (device pointers, row-major) ------------- */
+/* C[m x n] = A[m x k] . Bt[n x k]^T in bf16 x bf16 -> fp32 on tcgen05.
+ * c (fp32) and/or c_bf16 may be NULL. Leading dimensions in elements. */
+int ggb_gemm_bf16(ggb_ctx_t ctx, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
+                  const void* bt, int64_t ldb, float* c, int64_t ldc, void* c_bf16, int64_t ldcb);
+/* DW[kw x nw] = X[m x kw]^T . DY[m x nw] (contraction over the m rows). */
+int ggb_gemm_wgrad_bf16(ggb_ctx_t ctx, int64_t m, int64_t kw, int64_t nw, const void* x,
+                        int64_t ldx, const void* dy, int64_t lddy, float* dw, int64_t lddw);
+/* H[rows x f] = A . F with A in CSR (int64 row_ptr, int32 col, fp32 val) and
+ * F bf16; out fp32 (out) and/or bf16 (out_bf16); accumulate != 0 adds into out. */
+int ggb_spmm_csr(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const int32_t* col,
+                 const float* val, const void* f, int64_t ldf, int64_t fcols, float* out,
+                 int64_t ldo, void* out_bf16, int64_t ldob, int32_t accumulate);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GGB_H_ */

@@ -1,0 +1,580 @@
+// extern "C" boundary of libggb.so (include/ggb.h). Every entry point
+// catches, records the message in a thread-local slot and returns a status
+// code; nothing throws across the ABI.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <thread>
+
+#include "comm.hpp"
+#include "dataset.hpp"
+#include "trainer.hpp"
+
+struct ggb_ctx_s : ggb::Ctx {};
+struct ggb_graph_s : ggb::Graph {};
+struct ggb_batch_s : ggb::Batch {};
+struct ggb_state_s : ggb::State {};
+
+namespace ggb {
+
+Ctx::~Ctx() {
+  comm.reset();
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+namespace {
+
+thread_local std::string g_err;
+thread_local DevBuf g_ws;  // unit-test GEMM workspace
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return GGB_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("out of host memory: ") + e.what();
+    return GGB_EINTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GGB_EINTERNAL;
+  }
+}
+
+void use_device(const Ctx& c) { GGB_CUDA(cudaSetDevice(c.device)); }
+
+template <class T>
+void upload(DevBuf& b, const T* host, size_t n, cudaStream_t s) {
+  b.reserve(std::max<size_t>(n, 1) * sizeof(T));
+  if (n) GGB_CUDA(cudaMemcpyAsync(b.p, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+template <class F>
+void parallel_rows(int64_t n, F&& f) {
+  const int T = static_cast<int>(std::max(1u, std::min(std::thread::hardware_concurrency(), 32u)));
+  if (n < 65536 || T == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t chunk = ceil_div(n, T);
+  for (int t = 0; t < T; ++t) {
+    const int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// make_csr_shard (shardsample.cpp:19-45) on the host, then upload.
+void build_shard(Ctx& ctx, int64_t n, const int64_t* rp, const int64_t* col, const double* val, int64_t r0,
+                 int64_t r1, int64_t c0, int64_t c1, PlaneShard& sh) {
+  sh.r0 = r0;
+  sh.r1 = r1;
+  sh.c0 = c0;
+  sh.c1 = c1;
+  const int64_t rows = r1 - r0;
+  std::vector<int64_t> lo(static_cast<size_t>(rows)), hi(static_cast<size_t>(rows));
+  std::vector<int64_t> out_rp(static_cast<size_t>(rows) + 1, 0);
+  const bool full_cols = c0 == 0 && c1 == n;
+  parallel_rows(rows, [&](int64_t a, int64_t b) {
+    for (int64_t r = a; r < b; ++r) {
+      const int64_t* s = col + rp[r0 + r];
+      const int64_t* e = col + rp[r0 + r + 1];
+      lo[r] = full_cols ? rp[r0 + r] : std::lower_bound(s, e, c0) - col;
+      hi[r] = full_cols ? rp[r0 + r + 1] : std::lower_bound(s, e, c1) - col;
+    }
+  });
+  for (int64_t r = 0; r < rows; ++r) out_rp[r + 1] = out_rp[r] + (hi[r] - lo[r]);
+  sh.nnz = out_rp[rows];
+  std::vector<int32_t> c32(static_cast<size_t>(sh.nnz));
+  std::vector<double> v64;
+  const bool contiguous = full_cols;  // values are one contiguous range
+  if (!contiguous) v64.resize(static_cast<size_t>(sh.nnz));
+  parallel_rows(rows, [&](int64_t a, int64_t b) {
+    for (int64_t r = a; r < b; ++r) {
+      const int64_t o = out_rp[r];
+      for (int64_t k = lo[r]; k < hi[r]; ++k) c32[o + k - lo[r]] = static_cast<int32_t>(col[k]);
+      if (!contiguous) std::copy(val + lo[r], val + hi[r], v64.begin() + o);
+    }
+  });
+  upload(sh.row_ptr, out_rp.data(), out_rp.size(), ctx.stream);
+  upload(sh.col, c32.data(), c32.size(), ctx.stream);
+  if (contiguous)
+    upload(sh.val, val + rp[r0], static_cast<size_t>(sh.nnz), ctx.stream);
+  else
+    upload(sh.val, v64.data(), v64.size(), ctx.stream);
+  GGB_CUDA(cudaStreamSynchronize(ctx.stream));  // host vectors go out of scope
+}
+
+void host_transpose(int64_t n, const int64_t* rp, const int64_t* col, const double* val, std::vector<int64_t>& trp,
+                    std::vector<int64_t>& tcol, std::vector<double>& tval) {
+  const int64_t nnz = rp[n];
+  trp.assign(static_cast<size_t>(n) + 1, 0);
+  for (int64_t k = 0; k < nnz; ++k) ++trp[col[k] + 1];
+  for (int64_t v = 0; v < n; ++v) trp[v + 1] += trp[v];
+  tcol.resize(static_cast<size_t>(nnz));
+  tval.resize(static_cast<size_t>(nnz));
+  std::vector<int64_t> cur(trp.begin(), trp.end() - 1);
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+      const int64_t s = cur[col[k]]++;
+      tcol[s] = r;
+      tval[s] = val[k];
+    }
+}
+
+void graph_build(Ctx& ctx, Graph& g, int64_t n, const int64_t* rp, const int64_t* col, const double* val,
+                 bool symmetric, int64_t d_in, const float* feats, int64_t n_classes, const int32_t* labels,
+                 int layers) {
+  require(n >= 1 && n < (int64_t{1} << 31) - 64, "graph: n must be in [1, 2^31)");
+  require(layers >= 1, "graph: layers must be >= 1");
+  require(rp[0] == 0, "graph: row_ptr must start at 0");
+  g.ctx = &ctx;
+  g.n = n;
+  g.nnz = rp[n];
+  g.d_in = d_in;
+  g.n_classes = n_classes;
+  g.layers = layers;
+  g.planes = std::min(layers, 3);
+  std::vector<int64_t> trp, tcol;
+  std::vector<double> tval;
+  const int64_t *Trp = rp, *Tcol = col;
+  const double* Tval = val;
+  struct Key {
+    int t;
+    int64_t r0, r1, c0, c1;
+  };
+  std::vector<Key> keys;
+  g.shards.clear();
+  g.fwd_of.assign(g.planes, -1);
+  g.tr_of.assign(g.planes, -1);
+  auto get = [&](int t, int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+    // a symmetric matrix is its own transpose
+    if (symmetric) t = 0;
+    for (size_t k = 0; k < keys.size(); ++k)
+      if (keys[k].t == t && keys[k].r0 == r0 && keys[k].r1 == r1 && keys[k].c0 == c0 && keys[k].c1 == c1)
+        return static_cast<int>(k);
+    if (t == 1 && trp.empty()) {
+      host_transpose(n, rp, col, val, trp, tcol, tval);
+      Trp = trp.data();
+      Tcol = tcol.data();
+      Tval = tval.data();
+    }
+    keys.push_back({t, r0, r1, c0, c1});
+    g.shards.emplace_back();
+    if (t == 0)
+      build_shard(ctx, n, rp, col, val, r0, r1, c0, c1, g.shards.back());
+    else
+      build_shard(ctx, n, Trp, Tcol, Tval, r0, r1, c0, c1, g.shards.back());
+    return static_cast<int>(keys.size() - 1);
+  };
+  for (int p = 0; p < g.planes; ++p) {
+    const Layout lay = adjacency_layout(p + 1);
+    const auto ro = block_partition(n, ctx.grid.dims[lay.row]);
+    const auto co = block_partition(n, ctx.grid.dims[lay.col]);
+    const int64_t r0 = ro[ctx.coord[lay.row]], r1 = ro[ctx.coord[lay.row] + 1];
+    const int64_t c0 = co[ctx.coord[lay.col]], c1 = co[ctx.coord[lay.col] + 1];
+    g.fwd_of[p] = get(0, r0, r1, c0, c1);
+    g.tr_of[p] = get(1, c0, c1, r0, r1);
+  }
+  // feature Z-slice (kInputFeatureLayout.col) and labels
+  const auto fo = block_partition(d_in, ctx.grid.dims[kInputFeatureLayout.col]);
+  g.feat_c0 = fo[ctx.coord[kInputFeatureLayout.col]];
+  g.feat_c1 = fo[ctx.coord[kInputFeatureLayout.col] + 1];
+  const int64_t fw = g.feat_c1 - g.feat_c0;
+  if (fw == d_in) {
+    upload(g.features, feats, static_cast<size_t>(n * d_in), ctx.stream);
+  } else {
+    std::vector<float> sl(static_cast<size_t>(n * fw));
+    for (int64_t v = 0; v < n; ++v) std::copy(feats + v * d_in + g.feat_c0, feats + v * d_in + g.feat_c1, sl.begin() + v * fw);
+    upload(g.features, sl.data(), sl.size(), ctx.stream);
+    GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
+  upload(g.labels, labels, static_cast<size_t>(n), ctx.stream);
+  GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+  g.device_bytes = g.features.bytes + g.labels.bytes;
+  for (auto& s : g.shards) g.device_bytes += s.row_ptr.bytes + s.col.bytes + s.val.bytes;
+}
+
+template <class T>
+void download(T* host, const void* dev, size_t n, cudaStream_t s) {
+  if (n == 0 || !host) return;
+  GGB_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  GGB_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+}  // namespace ggb
+
+using namespace ggb;
+
+extern "C" {
+
+const char* ggb_last_error(void) { return g_err.c_str(); }
+int ggb_version(void) { return 1; }
+
+int ggb_get_unique_id(uint8_t out[128]) {
+  return guard([&] { comm_get_unique_id(out); });
+}
+
+int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const uint8_t* nccl_uid, void* stream,
+                   ggb_ctx_t* out) {
+  return guard([&] {
+    require(dims && out, "ctx: null argument");
+    for (int a = 0; a < 4; ++a) require(dims[a] >= 1, "DeviceGrid: dims must be >= 1");
+    auto c = std::make_unique<ggb_ctx_s>();
+    for (int a = 0; a < 4; ++a) c->grid.dims[a] = dims[a];
+    require(rank >= 0 && rank < c->grid.total(), "ctx: rank out of range");
+    c->rank = rank;
+    c->grid.coord_of(rank, c->coord);
+    c->device = device;
+    GGB_CUDA(cudaSetDevice(device));
+    GGB_CUDA(cudaFree(nullptr));  // establish the primary context
+    int sms = 0;
+    GGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    c->num_sms = sms;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      GGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    if (nccl_uid && c->grid.total() > 1) c->comm = comm_create(c->grid, rank, nccl_uid);
+    *out = c.release();
+  });
+}
+
+int ggb_ctx_destroy(ggb_ctx_t ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    delete ctx;
+  });
+}
+
+int ggb_ctx_set_stream(ggb_ctx_t ctx, void* stream) {
+  return guard([&] {
+    require(ctx != nullptr, "ctx: null");
+    if (ctx->own_stream && ctx->stream) {
+      GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaStreamDestroy(ctx->stream);
+      ctx->own_stream = false;
+    }
+    if (stream) {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      GGB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+  });
+}
+
+int ggb_ctx_synchronize(ggb_ctx_t ctx) {
+  return guard([&] {
+    use_device(*ctx);
+    GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters) {
+  return guard([&] { counters[0] = ctx->launches; });
+}
+
+int ggb_sample_vertices(ggb_ctx_t ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* host_out) {
+  return guard([&] {
+    use_device(*ctx);
+    require(b >= 1 && b <= n, "sample_vertices: need 1 <= b <= n");
+    DevBuf out;
+    int64_t* d = out.reserve_n<int64_t>(b);
+    sample_set(*ctx, n, b, seed, step, d);
+    download(host_out, d, static_cast<size_t>(b), ctx->stream);
+  });
+}
+
+int ggb_graph_create(ggb_ctx_t ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                     int32_t symmetric, int64_t d_in, const float* features, int64_t n_classes,
+                     const int32_t* labels, int32_t layers, ggb_graph_t* out) {
+  return guard([&] {
+    use_device(*ctx);
+    require(row_ptr && col_idx && values && features && labels && out, "graph: null argument");
+    auto g = std::make_unique<ggb_graph_s>();
+    graph_build(*ctx, *g, n, row_ptr, col_idx, values, symmetric != 0, d_in, features, n_classes, labels, layers);
+    *out = g.release();
+  });
+}
+
+int ggb_graph_generate_synthetic(ggb_ctx_t ctx, int64_t n, double avg_degree, int64_t d_in, int64_t n_classes,
+                                 uint64_t seed, int32_t layers, ggb_graph_t* out) {
+  return guard([&] {
+    use_device(*ctx);
+    HostDataset ds = generate_synthetic(n, avg_degree, d_in, n_classes, seed);
+    auto g = std::make_unique<ggb_graph_s>();
+    graph_build(*ctx, *g, n, ds.adj.row_ptr.data(), ds.adj.col.data(), ds.adj.val.data(), true, d_in,
+                ds.features.data(), n_classes, ds.labels.data(), layers);
+    *out = g.release();
+  });
+}
+
+int ggb_graph_destroy(ggb_graph_t g) {
+  return guard([&] {
+    if (g) cudaSetDevice(g->ctx->device);
+    delete g;
+  });
+}
+
+int ggb_graph_info(ggb_graph_t g, int64_t* info) {
+  return guard([&] {
+    info[0] = g->n;
+    info[1] = g->nnz;
+    info[2] = g->d_in;
+    info[3] = g->n_classes;
+    info[4] = static_cast<int64_t>(g->shards.size());
+    info[5] = static_cast<int64_t>(g->device_bytes);
+  });
+}
+
+int ggb_build_step_batch(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group_seed, uint64_t step,
+                         ggb_batch_t* inout) {
+  return guard([&] {
+    use_device(*ctx);
+    require(inout != nullptr, "batch: null handle slot");
+    std::unique_ptr<ggb_batch_s> fresh;
+    ggb_batch_s* bt = *inout;
+    if (!bt) {
+      fresh = std::make_unique<ggb_batch_s>();
+      bt = fresh.get();
+    }
+    build_step_batch(*ctx, *g, b, group_seed, step, *bt);
+    if (fresh) *inout = fresh.release();
+  });
+}
+
+int ggb_batch_destroy(ggb_batch_t batch) {
+  return guard([&] {
+    if (batch && batch->ctx) cudaSetDevice(batch->ctx->device);
+    delete batch;
+  });
+}
+
+int ggb_batch_info(ggb_batch_t bt, int64_t* info) {
+  return guard([&] {
+    info[0] = bt->b;
+    info[1] = bt->n;
+    info[2] = bt->planes;
+    info[3] = bt->x_r0;
+    info[4] = bt->x_r1;
+    info[5] = bt->x_c0;
+    info[6] = bt->x_c1;
+    info[7] = static_cast<int64_t>(bt->nnz_extracted);
+    info[8] = static_cast<int64_t>(bt->nnz_kept);
+  });
+}
+
+int ggb_batch_sample(ggb_batch_t bt, int64_t* host_out) {
+  return guard([&] {
+    use_device(*bt->ctx);
+    download(host_out, bt->sample.p, static_cast<size_t>(bt->b), bt->ctx->stream);
+  });
+}
+
+int ggb_batch_offsets(ggb_batch_t bt, int32_t axis, int64_t* host_out) {
+  return guard([&] {
+    require(axis >= 1 && axis <= 3, "batch_offsets: axis must be X, Y or Z");
+    std::copy(bt->batch_off[axis].begin(), bt->batch_off[axis].end(), host_out);
+  });
+}
+
+int ggb_batch_plane(ggb_batch_t bt, int32_t plane, int32_t transposed, int64_t* dims, int64_t* row_ptr,
+                    int64_t* col_idx, double* values) {
+  return guard([&] {
+    require(plane >= 0 && plane < bt->planes, "batch_plane: plane out of range");
+    use_device(*bt->ctx);
+    const BatchCsr& c = bt->csrs[transposed ? bt->csrt_of[plane] : bt->csr_of[plane]];
+    dims[0] = c.n_rows;
+    dims[1] = c.n_cols;
+    dims[2] = c.nnz;
+    dims[3] = c.r0;
+    dims[4] = c.r1;
+    dims[5] = c.c0;
+    dims[6] = c.c1;
+    cudaStream_t s = bt->ctx->stream;
+    download(row_ptr, c.row_ptr.p, static_cast<size_t>(c.n_rows + 1), s);
+    if (col_idx) {
+      std::vector<int32_t> c32(static_cast<size_t>(c.nnz));
+      download(c32.data(), c.col.p, c32.size(), s);
+      for (int64_t k = 0; k < c.nnz; ++k) col_idx[k] = c32[k];
+    }
+    download(values, c.val64.p, static_cast<size_t>(c.nnz), s);
+  });
+}
+
+int ggb_batch_x_in(ggb_batch_t bt, float* host_out) {
+  return guard([&] {
+    Ctx& ctx = *bt->ctx;
+    use_device(ctx);
+    const int64_t n = (bt->x_r1 - bt->x_r0) * (bt->x_c1 - bt->x_c0);
+    DevBuf tmp;
+    float* d = tmp.reserve_n<float>(std::max<int64_t>(n, 1));
+    gather_x_in_fp32(ctx, *bt, d);
+    download(host_out, d, static_cast<size_t>(n), ctx.stream);
+  });
+}
+
+int ggb_batch_labels(ggb_batch_t bt, int32_t* host_out) {
+  return guard([&] {
+    use_device(*bt->ctx);
+    download(host_out, bt->labels.p, static_cast<size_t>(bt->b), bt->ctx->stream);
+  });
+}
+
+int ggb_state_create(ggb_ctx_t ctx, const ggb_model_config* cfg, uint64_t seed, ggb_state_t* out) {
+  return guard([&] {
+    use_device(*ctx);
+    require(cfg && out, "state: null argument");
+    auto st = std::make_unique<ggb_state_s>();
+    state_init(*ctx, *st, *cfg, seed);
+    GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = st.release();
+  });
+}
+
+int ggb_state_destroy(ggb_state_t st) {
+  return guard([&] {
+    if (st && st->ctx) cudaSetDevice(st->ctx->device);
+    delete st;
+  });
+}
+
+int ggb_state_num_params(ggb_state_t st) { return st ? static_cast<int>(st->params.size()) : -1; }
+
+int ggb_state_param_info(ggb_state_t st, int32_t idx, int64_t* info) {
+  return guard([&] {
+    require(idx >= 0 && idx < static_cast<int>(st->params.size()), "param index out of range");
+    const Block& b = st->params[idx].blk;
+    info[0] = b.g_rows;
+    info[1] = b.g_cols;
+    info[2] = b.r0;
+    info[3] = b.r1;
+    info[4] = b.c0;
+    info[5] = b.c1;
+  });
+}
+
+static float* which_buf(State& st, int which) {
+  switch (which) {
+    case 0: return st.W.as<float>();
+    case 1: return st.G.as<float>();
+    case 2: return st.M.as<float>();
+    case 3: return st.V.as<float>();
+    default: fail(GGB_EINVAL, "param: which must be 0..3");
+  }
+}
+
+int ggb_state_param_get(ggb_state_t st, int32_t idx, int32_t which, float* host_out) {
+  return guard([&] {
+    require(idx >= 0 && idx < static_cast<int>(st->params.size()), "param index out of range");
+    use_device(*st->ctx);
+    const ParamSlot& p = st->params[idx];
+    download(host_out, which_buf(*st, which) + p.off, static_cast<size_t>(p.n), st->ctx->stream);
+  });
+}
+
+int ggb_state_param_set(ggb_state_t st, int32_t idx, int32_t which, const float* host_in) {
+  return guard([&] {
+    require(idx >= 0 && idx < static_cast<int>(st->params.size()), "param index out of range");
+    use_device(*st->ctx);
+    const ParamSlot& p = st->params[idx];
+    GGB_CUDA(cudaMemcpyAsync(which_buf(*st, which) + p.off, host_in, p.n * 4, cudaMemcpyHostToDevice,
+                             st->ctx->stream));
+    if (which == 0) refresh_bf16(*st);
+    GGB_CUDA(cudaStreamSynchronize(st->ctx->stream));
+  });
+}
+
+int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precision, uint64_t run_seed,
+                   uint64_t global_step, double rmsnorm_eps, float* loss_out) {
+  return guard([&] {
+    use_device(*ctx);
+    contract(st->ctx == ctx && bt->ctx == ctx, "train_step: handles belong to another context");
+    forward(*st, *bt, precision, true, run_seed, global_step, rmsnorm_eps);
+    cross_entropy(*st, *bt);
+    backward(*st, *bt, precision);
+    if (loss_out) download(loss_out, st->loss.p, 1, ctx->stream);
+  });
+}
+
+int ggb_last_loss_device(ggb_state_t st, const float** dev_ptr) {
+  return guard([&] {
+    require(st->loss.p != nullptr, "no loss computed yet");
+    *dev_ptr = st->loss.as<float>();
+  });
+}
+
+int ggb_state_logits(ggb_state_t st, int64_t* dims, float* host_out) {
+  return guard([&] {
+    require(st->have_forward, "no forward pass yet");
+    const Block& b = st->logits_blk;
+    dims[0] = b.r0;
+    dims[1] = b.r1;
+    dims[2] = b.c0;
+    dims[3] = b.c1;
+    use_device(*st->ctx);
+    download(host_out, st->logits.p, static_cast<size_t>(b.rows() * b.cols()), st->ctx->stream);
+  });
+}
+
+int ggb_forward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precision, int32_t training,
+                uint64_t run_seed, uint64_t global_step, double rmsnorm_eps) {
+  return guard([&] {
+    use_device(*ctx);
+    forward(*st, *bt, precision, training != 0, run_seed, global_step, rmsnorm_eps);
+  });
+}
+
+int ggb_dp_sync(ggb_ctx_t ctx, ggb_state_t st) {
+  return guard([&] {
+    use_device(*ctx);
+    dp_sync(*st);
+  });
+}
+
+int ggb_optimizer_step(ggb_ctx_t ctx, ggb_state_t st, int32_t optimizer, double lr) {
+  return guard([&] {
+    use_device(*ctx);
+    optimizer_step(*st, optimizer, lr);
+  });
+}
+
+int ggb_gemm_bf16(ggb_ctx_t ctx, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda, const void* bt,
+                  int64_t ldb, float* c, int64_t ldc, void* c_bf16, int64_t ldcb) {
+  return guard([&] {
+    use_device(*ctx);
+    gemm_bf16(*ctx, m, n, k, static_cast<const bf16*>(a), lda, static_cast<const bf16*>(bt), ldb, c, ldc,
+              static_cast<bf16*>(c_bf16), ldcb);
+  });
+}
+
+int ggb_gemm_wgrad_bf16(ggb_ctx_t ctx, int64_t m, int64_t kw, int64_t nw, const void* x, int64_t ldx,
+                        const void* dy, int64_t lddy, float* dw, int64_t lddw) {
+  return guard([&] {
+    use_device(*ctx);
+    gemm_wgrad_bf16(*ctx, m, kw, nw, static_cast<const bf16*>(x), ldx, static_cast<const bf16*>(dy), lddy, dw, lddw,
+                    g_ws);
+  });
+}
+
+int ggb_spmm_csr(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const int32_t* col, const float* val,
+                 const void* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, void* out_bf16, int64_t ldob,
+                 int32_t accumulate) {
+  return guard([&] {
+    use_device(*ctx);
+    spmm_csr(*ctx, rows, row_ptr, col, val, static_cast<const bf16*>(f), ldf, fcols, out, ldo,
+             static_cast<bf16*>(out_bf16), ldob, accumulate);
+  });
+}
+
+}  // extern "C"

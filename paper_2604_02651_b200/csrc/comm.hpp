@@ -1,0 +1,36 @@
+// Grid collectives (RankComm, comm.hpp:254-408) over NCCL: one world
+// communicator plus one split per grid axis (colour = group id on the axis,
+// key = coordinate on it, mirroring Communicator's per-axis Channels,
+// comm.hpp:209-214). Singleton groups are free and need no communicator.
+#pragma once
+
+#include "runtime.hpp"
+
+namespace ggb {
+
+struct Comm {
+  void* world = nullptr;     // ncclComm_t
+  void* axis[4] = {};        // ncclComm_t per axis (null for singleton groups)
+  int size[4] = {1, 1, 1, 1};
+  int pos[4] = {0, 0, 0, 0};  // coordinate on the axis
+  DevBuf gather;             // all-gather staging
+  DevBuf wire;               // bf16 wire staging
+  ~Comm();
+};
+
+int comm_get_unique_id(uint8_t out[128]);
+std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid);
+
+// In-place sum over the rank's group along `axis`. bf16_wire: each member's
+// contribution is rounded to bf16 (RNE) and the fp32 sum taken in ascending
+// axis order — the reference's Precision::kBf16Roundtrip (comm.hpp:271-303)
+// reproduced exactly by an all-gather of bf16 contributions.
+void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire);
+void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count);
+// Gathers `count` floats from every member of the axis group into out
+// ([size][count], axis order).
+void all_gather(Ctx& ctx, int axis, const float* in, int64_t count, float* out);
+void barrier(Ctx& ctx);
+inline bool trivial(const Ctx& ctx, int axis) { return ctx.grid.dims[axis] == 1; }
+
+}  // namespace ggb

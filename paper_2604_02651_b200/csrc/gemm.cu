@@ -1,0 +1,566 @@
+// Dense GEMMs of the 3D-PMM GCN layer (the `contract` of pmm.hpp:97-130) on
+// the 5th-generation tensor cores: bf16 operands staged by TMA into 128B-
+// swizzled shared memory, tcgen05.mma issued by one thread, fp32 accumulators
+// in TMEM, tcgen05.ld epilogue. No materialized transposes (pmm.hpp:76-92 is
+// eliminated): the forward / dX products read both operands K-major, the
+// weight-gradient product reads both operands MN-major straight from the
+// row-major activations.
+//
+//   k_gemm_kmajor : C[M x N] = A[M x K] . Bt[N x K]^T
+//                   persistent over 128-row tiles; warp 0 = TMA producer,
+//                   warp 1 = MMA issuer, warps 2-5 = epilogue; 2 TMEM
+//                   accumulators so the epilogue of tile t overlaps the
+//                   loads/MMAs of tile t+1.
+//   k_gemm_wgrad  : DW[KW x NW] = X[M x KW]^T . DY[M x NW]
+//                   split over the contraction (M) rows; fp32 partial tiles,
+//                   reduced deterministically by k_reduce_partials.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "runtime.hpp"
+
+namespace ggb {
+namespace {
+
+constexpr int kBM = 128;  // UMMA M (cta_group::1)
+constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16 along K
+constexpr int kThreads = 192;
+constexpr int kSmemBudget = 200 * 1024;
+
+// ---- PTX wrappers --------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// 32 lanes x 16 consecutive fp32 columns of the accumulator
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%"
+      "15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bit.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: bf16 x bf16 -> fp32, M = 128.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(kBM >> 4) << 24);
+}
+
+struct GemmArgs {
+  int M, N, K;
+  int BN;       // MMA N of one tile (multiple of 16, <= 256)
+  int n_tiles;  // ceil(N / BN)
+  int stages;
+  uint32_t tmem_cols;
+  float* c;
+  int64_t ldc;
+  bf16* cb;
+  int64_t ldcb;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_kmajor(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const GemmArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = args.stages, BN = args.BN;
+  const uint32_t bytes_a = kBM * kBK * 2, bytes_b = static_cast<uint32_t>(BN) * kBK * 2;
+  const uint32_t stage_bytes = bytes_a + bytes_b;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;  // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (args.M + kBM - 1) / kBM;
+  const int num_tiles = m_tiles * args.n_tiles;
+  const int k_chunks = (args.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_base_smem, args.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int mt = t / args.n_tiles, nt = t % args.n_tiles;
+        for (int kc = 0; kc < k_chunks; ++kc) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* sa = smem + stage * stage_bytes;
+          mbar_expect_tx(full + stage, stage_bytes);
+          tma_load_2d(sa, &tmA, full + stage, kc * kBK, mt * kBM);
+          tma_load_2d(sa + bytes_a, &tmB, full + stage, kc * kBK, nt * BN);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t idesc = idesc_bf16(BN, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        const uint32_t acc_phase = (lt >> 1) & 1;
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kc = 0; kc < k_chunks; ++kc) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+          const uint32_t sb = sa + bytes_a;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            umma_bf16(d, sdesc(sa + k * 32, 16, 1024), sdesc(sb + k * 32, 16, 1024), idesc,
+                      (kc | k) != 0);
+          }
+          umma_commit(empty + stage);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull + acc);
+      }
+    }
+    __syncwarp();
+  } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4
+    const int q = warp & 3;
+    int lt = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      const int mt = t / args.n_tiles, nt = t % args.n_tiles;
+      const int acc = lt & 1;
+      const uint32_t acc_phase = (lt >> 1) & 1;
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;
+      const bool row_ok = row < args.M;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      for (int c16 = 0; c16 < BN; c16 += 16) {
+        float v[16];
+        tmem_ld16(taddr + c16, v);
+        const int col0 = nt * BN + c16;
+        if (!row_ok || col0 >= args.N) continue;
+        const bool full16 = col0 + 16 <= args.N;
+        if (args.c) {
+          float* dst = args.c + row * args.ldc + col0;
+          if (full16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+            for (int i = 0; i < 16 && col0 + i < args.N; ++i) dst[i] = v[i];
+          }
+        }
+        if (args.cb) {
+          bf16* dst = args.cb + row * args.ldcb + col0;
+          if (full16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+            *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(dst + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          } else {
+            for (int i = 0; i < 16 && col0 + i < args.N; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + acc);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, args.tmem_cols);
+  }
+}
+
+struct WgradArgs {
+  int M, KW, NW;
+  int BN;  // multiple of 64, <= 256
+  int n_tiles, m_tiles, splits, chunks_per_split;
+  int stages;
+  uint32_t tmem_cols;
+  float* part;  // [splits][KW][NW]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_wgrad(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
+                 const WgradArgs args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = args.stages, BN = args.BN;
+  // A' tile: 128 (KW) x 64 (rows): two 64-col boxes of 64 rows x 128 B
+  const uint32_t bytes_a = kBM * kBK * 2, bytes_b = static_cast<uint32_t>(BN) * kBK * 2;
+  const uint32_t stage_bytes = bytes_a + bytes_b;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int mt = tile / args.n_tiles, nt = tile % args.n_tiles;
+  const int total_chunks = (args.M + kBK - 1) / kBK;
+  const int c_begin = split * args.chunks_per_split;
+  const int c_end = min(total_chunks, c_begin + args.chunks_per_split);
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmD);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_base_smem, args.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = c_begin; c < c_end; ++c) {
+        mbar_wait(empty + stage, phase ^ 1);
+        uint8_t* sa = smem + stage * stage_bytes;
+        uint8_t* sb = sa + bytes_a;
+        mbar_expect_tx(full + stage, stage_bytes);
+        for (int h = 0; h < kBM / 64; ++h)
+          tma_load_2d(sa + h * 8192, &tmX, full + stage, mt * kBM + h * 64, c * kBK);
+        for (int h = 0; h < BN / 64; ++h)
+          tma_load_2d(sb + h * 8192, &tmD, full + stage, nt * BN + h * 64, c * kBK);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(BN, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = c_begin; c < c_end; ++c) {
+        mbar_wait(full + stage, phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + stage * stage_bytes);
+        const uint32_t sb = sa + bytes_a;
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)  // 16 K-rows = 2 groups of 8 rows x 128 B
+          umma_bf16(tmem_base, sdesc(sa + k * 2048, 8192, 1024), sdesc(sb + k * 2048, 8192, 1024),
+                    idesc, (c != c_begin || k != 0));
+        umma_commit(empty + stage);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(tfull);
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const bool any = c_end > c_begin;
+    if (any) {
+      mbar_wait(tfull, 0);
+      tc_fence_after();
+    }
+    const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;  // KW index
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    float* dst_base = args.part + static_cast<int64_t>(split) * args.KW * args.NW;
+    for (int c16 = 0; c16 < BN; c16 += 16) {
+      float v[16];
+      if (any) {
+        tmem_ld16(taddr + c16, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      const int col0 = nt * BN + c16;
+      if (row >= args.KW || col0 >= args.NW) continue;
+      float* dst = dst_base + row * args.NW + col0;
+      for (int i = 0; i < 16 && col0 + i < args.NW; ++i) dst[i] = v[i];
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, args.tmem_cols);
+  }
+}
+
+__global__ void k_reduce_partials(const float* __restrict__ part, int splits, int64_t kw, int64_t nw,
+                                  float* __restrict__ out, int64_t ldo) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = kw * nw;
+  if (i >= total) return;
+  float s = 0.f;
+  for (int k = 0; k < splits; ++k) s += part[k * total + i];
+  out[(i / nw) * ldo + (i % nw)] = s;
+}
+
+// ---- host: TMA descriptors through the driver entry point ---------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  if (!fn) fail(GGB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2D bf16 row-major tensor [rows][cols] with row stride ld (elements); box
+// {box_inner (cols), box_outer (rows)}; 128-byte swizzle; OOB -> zeros.
+CUtensorMap make_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_inner,
+                      int box_outer) {
+  require((reinterpret_cast<uintptr_t>(base) & 15) == 0, "gemm: operand must be 16-byte aligned");
+  require((ld * 2) % 16 == 0, "gemm: leading dimension must be a multiple of 8 elements");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(GGB_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+uint32_t tmem_cols_for(int n) {
+  uint32_t c = 32;
+  while (c < static_cast<uint32_t>(n)) c <<= 1;
+  return c;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+// C[m x n] = A[m x k] . Bt[n x k]^T
+void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t lda, const bf16* bt,
+               int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb) {
+  if (m <= 0 || n <= 0) return;
+  require(k > 0, "gemm: k must be positive");
+  require(m < (int64_t{1} << 31) && n < (int64_t{1} << 31) && k < (int64_t{1} << 31), "gemm: dims");
+  GemmArgs ga{};
+  ga.M = static_cast<int>(m);
+  ga.N = static_cast<int>(n);
+  ga.K = static_cast<int>(k);
+  ga.BN = static_cast<int>(std::min<int64_t>(256, round_up(n, 16)));
+  ga.n_tiles = static_cast<int>(ceil_div(n, ga.BN));
+  const int stage_bytes = kBM * kBK * 2 + ga.BN * kBK * 2;
+  ga.stages = std::min(8, (kSmemBudget - 1024 - 256) / stage_bytes);
+  ga.tmem_cols = tmem_cols_for(2 * ga.BN);
+  ga.c = c;
+  ga.ldc = ldc;
+  ga.cb = cb;
+  ga.ldcb = ldcb;
+  const CUtensorMap ta = make_tmap(a, m, k, lda, kBK, kBM);
+  const CUtensorMap tb = make_tmap(bt, n, k, ldb, kBK, ga.BN);
+  const int smem = ga.stages * stage_bytes + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    GGB_CUDA(cudaFuncSetAttribute(k_gemm_kmajor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemBudget + 1024));
+    attr = true;
+  }
+  const int64_t tiles = ceil_div(m, kBM) * ga.n_tiles;
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
+  k_gemm_kmajor<<<grid, kThreads, smem, ctx.stream>>>(ta, tb, ga);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+// DW[kw x nw] = X[m x kw]^T . DY[m x nw]; ws: scratch
+void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x, int64_t ldx,
+                     const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws) {
+  if (kw <= 0 || nw <= 0) return;
+  if (m <= 0) {
+    for (int64_t r = 0; r < kw; ++r)
+      GGB_CUDA(cudaMemsetAsync(dw + r * lddw, 0, nw * 4, ctx.stream));
+    return;
+  }
+  WgradArgs wa{};
+  wa.M = static_cast<int>(m);
+  wa.KW = static_cast<int>(kw);
+  wa.NW = static_cast<int>(nw);
+  wa.BN = static_cast<int>(std::min<int64_t>(256, round_up(nw, 64)));
+  wa.n_tiles = static_cast<int>(ceil_div(nw, wa.BN));
+  wa.m_tiles = static_cast<int>(ceil_div(kw, kBM));
+  const int tiles = wa.m_tiles * wa.n_tiles;
+  const int total_chunks = static_cast<int>(ceil_div(m, kBK));
+  int splits = std::max(1, sm_count() / tiles);
+  splits = std::min(splits, std::max(1, total_chunks / 4));
+  wa.chunks_per_split = static_cast<int>(ceil_div(total_chunks, splits));
+  wa.splits = static_cast<int>(ceil_div(total_chunks, wa.chunks_per_split));
+  const int stage_bytes = kBM * kBK * 2 + wa.BN * kBK * 2;
+  wa.stages = std::min(8, (kSmemBudget - 1024 - 256) / stage_bytes);
+  wa.tmem_cols = tmem_cols_for(wa.BN);
+  wa.part = ws.reserve_n<float>(static_cast<size_t>(wa.splits) * kw * nw);
+  const CUtensorMap tx = make_tmap(x, m, kw, ldx, 64, kBK);
+  const CUtensorMap td = make_tmap(dy, m, nw, lddy, 64, kBK);
+  const int smem = wa.stages * stage_bytes + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    GGB_CUDA(cudaFuncSetAttribute(k_gemm_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemBudget + 1024));
+    attr = true;
+  }
+  dim3 grid(tiles, wa.splits);
+  k_gemm_wgrad<<<grid, kThreads, smem, ctx.stream>>>(tx, td, wa);
+  const int64_t total = kw * nw;
+  k_reduce_partials<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, ctx.stream>>>(
+      wa.part, wa.splits, kw, nw, dw, lddw);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 2;
+}
+
+}  // namespace ggb

@@ -1,0 +1,99 @@
+// Kernel launchers (ops.cu, gemm.cu, spmm.cu) used by the trainer.
+#pragma once
+
+#include "runtime.hpp"
+
+namespace ggb {
+
+struct FwdApply {
+  int64_t rows, cols;
+  const float* x;  // xw (GEMM output), fp32 [rows][ldx]
+  int64_t ldx;
+  const float* ss;  // row sums of squares over the FULL feature dim (after all-reduce) or null
+  const float* gamma;
+  float d, eps;
+  float* rms;        // out: per-row rms (nullable)
+  const float* res;  // residual (nullable)
+  int64_t ldres;
+  uint64_t mask_key;
+  int64_t row_g0, col_g0;  // global batch coordinates of this block
+  int drop;
+  uint64_t thresh;  // ceil(rate * 2^53)
+  float keep_scale;
+  float* out;  // fp32 output (nullable)
+  int64_t ldo;
+  bf16* outb;  // bf16 copy (nullable)
+  int64_t ldob;
+  uint8_t* mask;  // [rows][ldm] keep bits
+  int64_t ldm;
+};
+
+struct BwdApply {
+  int64_t rows, cols;
+  const float* dy;  // upstream gradient fp32
+  int64_t lddy;
+  const uint8_t* mask;
+  int64_t ldm;
+  float keep_scale;  // scale value of a kept element (1 without dropout)
+  const float* x;    // xw
+  int64_t ldx;
+  const float* gamma;
+  const float* rms;  // null: no rmsnorm
+  float* s;          // row dot products (stats out / apply in)
+  float d;
+  bf16* dxb;  // out: dxw bf16
+  int64_t lddxb;
+  float* dgamma_part;  // [blocks][cols] or null
+};
+
+struct CeArgs {
+  int64_t rows, cols;
+  const float* logits;
+  int64_t ld;
+  const int32_t* labels;  // full batch labels
+  int64_t row_g0, c0;
+  float* mx;         // [rows]
+  float* zt;         // [2 rows]
+  float invb;
+  float* dlog;       // nullable fp32 grad
+  int64_t lddlog;
+  bf16* dlogb;       // nullable bf16 grad
+  int64_t lddlogb;
+  float* loss_part;  // [blocks]
+  float* loss_acc;   // [1]
+};
+
+void init_weight(Ctx& ctx, float* w, int64_t rows, int64_t cols, int64_t g_rows, int64_t g_cols,
+                 int64_t r0, int64_t c0, uint64_t key);
+void fill(Ctx& ctx, float* x, int64_t n, float v);
+void weight_bf16(Ctx& ctx, const float* w, int64_t rows, int64_t cols, bf16* wb, int64_t ldb, bf16* wt,
+                 int64_t ldt);
+void cast_bf16(Ctx& ctx, const float* x, int64_t rows, int64_t cols, int64_t ldx, bf16* y, int64_t ldy);
+void add_inplace(Ctx& ctx, float* a, int64_t lda, const float* b, int64_t ldb, int64_t rows, int64_t cols);
+void rowsumsq(Ctx& ctx, const float* x, int64_t ldx, int64_t rows, int64_t cols, float* ss);
+void fwd_apply(Ctx& ctx, const FwdApply& p);
+void bwd_stats(Ctx& ctx, const BwdApply& p);
+int bwd_apply_blocks(Ctx& ctx, int64_t rows, int64_t cols);
+void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks);
+void reduce_rows(Ctx& ctx, const float* part, int parts, int64_t cols, float* out);
+void ce_rowmax(Ctx& ctx, const CeArgs& p);
+void ce_rowsum(Ctx& ctx, const CeArgs& p);
+int ce_grad_blocks(int64_t rows);
+void ce_grad(Ctx& ctx, const CeArgs& p);
+void scale_scalar(Ctx& ctx, const float* in, float s, float* out);
+void adam(Ctx& ctx, float* w, const float* g, float* m, float* v, int64_t n, double lr, double bc1,
+          double bc2);
+void sgd(Ctx& ctx, float* w, const float* g, int64_t n, float lr);
+void scale(Ctx& ctx, float* x, int64_t n, float s);
+
+// gemm.cu
+void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t lda, const bf16* bt,
+               int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb);
+void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x, int64_t ldx,
+                     const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws);
+// spmm.cu
+void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
+              const bf16* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb,
+              int64_t ldob, int accumulate);
+
+}  // namespace ggb

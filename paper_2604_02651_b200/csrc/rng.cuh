@@ -1,0 +1,40 @@
+// Device copies of the reference RNG (include/gridgnn/rng.hpp:10-76),
+// bit-identical 64-bit integer arithmetic.
+#pragma once
+#include <cstdint>
+
+namespace ggb {
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += kGolden;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t hash_combine(uint64_t a, uint64_t b) {
+  return splitmix64(a ^ (kGolden + (b << 6) + (b >> 2)));
+}
+
+/// The k-th (0-based) next_u64() of Stream(seed) when no earlier call was a
+/// rejection: the state advances by kGolden per call (rng.hpp:26-32).
+__host__ __device__ __forceinline__ uint64_t stream_draw(uint64_t seed, uint64_t k) {
+  return splitmix64(seed + k * kGolden);
+}
+
+/// element_unit(key, i, j) >= rate, evaluated exactly on the 53-bit integer:
+/// (h >> 11) * 2^-53 >= rate  <=>  (h >> 11) >= thresh, thresh = ceil(rate * 2^53).
+__host__ __device__ __forceinline__ bool element_keep(uint64_t row_key, uint64_t j, uint64_t thresh) {
+  const uint64_t h = splitmix64(hash_combine(row_key, j));
+  return (h >> 11) >= thresh;
+}
+
+/// rng.hpp:73-76 as a double.
+__host__ __device__ __forceinline__ double element_unit(uint64_t key, uint64_t i, uint64_t j) {
+  const uint64_t h = splitmix64(hash_combine(hash_combine(key, i), j));
+  return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+
+}  // namespace ggb

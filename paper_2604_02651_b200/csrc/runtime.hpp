@@ -1,0 +1,105 @@
+// Host-side runtime objects behind the opaque ggb_* handles.
+#pragma once
+
+#include <array>
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+
+namespace ggb {
+
+struct Comm;  // comm.cpp (NCCL per-axis communicators)
+
+/// Sampler scratch, reused across steps (one build at a time per context).
+struct SamplerWork {
+  DevBuf head;      // uint64 [n]: step-tagged (tag<<32 | step index) list heads
+  int64_t head_n = 0;
+  uint32_t tag = 0;
+  DevBuf j, next;   // int32 [b]
+  DevBuf flag;      // int32 rejection flag
+  DevBuf bitmap;    // uint32 [n/32 + 2]
+  DevBuf wcount;    // int32 [words]
+  DevBuf wpfx;      // int32 [words + 1]: sampled ids below each word
+  DevBuf scan_tmp;  // scan partials
+  DevBuf cnt;       // int32 per-row kept counts
+  DevBuf dev_misc;  // small device scalars (offsets, totals, counters)
+  PinnedBuf host_misc;
+};
+
+struct Ctx {
+  Grid grid;
+  int rank = 0;
+  int coord[4] = {0, 0, 0, 0};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::unique_ptr<Comm> comm;
+  SamplerWork sw;
+  uint64_t launches = 0;
+  int num_sms = 148;
+  ~Ctx();
+};
+
+/// One static plane shard (shardsample.hpp:18-25): rows [r0,r1) with local
+/// row ids, global column ids restricted to [c0,c1).
+struct PlaneShard {
+  int64_t r0 = 0, r1 = 0, c0 = 0, c1 = 0, nnz = 0;
+  DevBuf row_ptr;  // int64 [r1-r0+1]
+  DevBuf col;      // int32 [nnz]
+  DevBuf val;      // double [nnz]
+};
+
+struct Graph {
+  Ctx* ctx = nullptr;
+  int64_t n = 0, nnz = 0, d_in = 0, n_classes = 0;
+  int layers = 0;
+  int planes = 0;  // min(layers, 3)
+  // plane p -> index into shards for the static shard and its transpose
+  std::vector<int> fwd_of, tr_of;
+  std::vector<PlaneShard> shards;
+  int64_t feat_c0 = 0, feat_c1 = 0;  // Z-slice of the feature columns held here
+  DevBuf features;                   // fp32 [n][feat_c1-feat_c0]
+  DevBuf labels;                     // int32 [n]
+  size_t device_bytes = 0;
+};
+
+/// One rank's CSR block of a rescaled batch adjacency (ShardedSparse,
+/// tensor.hpp:88-96) with device arrays for the kernels.
+struct BatchCsr {
+  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int64_t r0 = 0, r1 = 0, c0 = 0, c1 = 0;  // global batch coordinates
+  DevBuf row_ptr;  // int64 [n_rows+1]
+  DevBuf col;      // int32
+  DevBuf val;      // float (SpMM operand, = (float)val64 as pmm.hpp:160)
+  DevBuf val64;    // double (exact reference values, for export)
+};
+
+struct Batch {
+  Ctx* ctx = nullptr;
+  int64_t b = 0, n = 0;
+  int planes = 0;
+  DevBuf sample;  // int64 [b], strictly increasing
+  std::array<std::vector<int64_t>, 4> batch_off;
+  std::vector<int> csr_of;   // plane -> index in csrs (forward block)
+  std::vector<int> csrt_of;  // plane -> index in csrs (transposed block)
+  std::vector<BatchCsr> csrs;
+  int64_t x_r0 = 0, x_r1 = 0, x_c0 = 0, x_c1 = 0, x_ld = 0;
+  DevBuf x_in;    // bf16 [x_r1-x_r0][x_ld], zero padded
+  DevBuf labels;  // int32 [b]
+  uint64_t nnz_extracted = 0, nnz_kept = 0;
+  const Graph* graph = nullptr;
+};
+
+// sampler.cu
+void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* d_sample);
+void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
+                      Batch& out);
+void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out);
+
+// scan.cu: out[0..n] = exclusive prefix sums of in[0..n), out[n] = total.
+void exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, DevBuf& tmp,
+                               cudaStream_t s);
+void exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, DevBuf& tmp, cudaStream_t s);
+
+}  // namespace ggb

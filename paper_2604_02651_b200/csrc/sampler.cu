@@ -1,0 +1,454 @@
+// Communication-free uniform vertex sampling and induced-subgraph CSR
+// construction (ScaleGNN Alg. 2) as sm_100a kernels, bit-exact with the
+// reference:
+//   sample_vertices      src/sampling.cpp:11-33  (partial Fisher-Yates, sorted)
+//   locate_ranges        src/shardsample.cpp:47-56
+//   extract_rows         src/shardsample.cpp:58-87
+//   filter_and_remap     src/shardsample.cpp:89-109
+//   assemble_shard       src/shardsample.cpp:111-122 (+ csr.cpp:29-94)
+//   build_step_batch     include/gridgnn/model.hpp:250-309
+//
+// Sampling. The reference swaps perm[i] <-> perm[j_i], j_i = i +
+// next_below(n-i), for i < b, then sorts the first b entries. Only the SET
+// of the first b entries matters, and it is resolved in parallel:
+//   val(k) = value at position k just before step k
+//          = val(m) for the last m < k with j_m == k, else k;
+//   out(i) = val(i) if j_i == i, else val(m) for the last m < i with
+//            j_m == j_i, else j_i.
+// Steps sharing a target are chained through a step-tagged head table (the
+// analogue of the reference RemapTable tags, shardsample.hpp:29-55), the
+// chosen ids are set in an n-bit bitmap, and a popcount prefix over the
+// bitmap words both compacts the sorted sample and serves as the O(1)
+// global-id -> sample-rank table that replaces every binary search of the
+// reference (locate_ranges, filter_and_remap, sample_partition).
+//
+// Extraction. One warp per sampled row streams the row's column ids with
+// coalesced loads, tests membership in the bitmap, ballots, and writes the
+// kept entries in order: rows arrive in increasing global id and columns are
+// sorted within a static shard row, so the output is canonical CSR
+// (csr_from_triples order) without a sort. The transposed block is extracted
+// the same way from the static transposed shard, which yields exactly the
+// stable csr_transpose order.
+#include <cmath>
+
+#include "rng.cuh"
+#include "runtime.hpp"
+
+namespace ggb {
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void k_draw(int64_t n, int64_t b, uint64_t s0, int32_t* __restrict__ j,
+                       int* __restrict__ reject) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  const uint64_t bound = static_cast<uint64_t>(n - i);
+  const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+  const uint64_t x = stream_draw(s0, static_cast<uint64_t>(i));
+  if (x >= limit) atomicOr(reject, 1);
+  j[i] = static_cast<int32_t>(i + static_cast<int64_t>(x % bound));
+}
+
+// Exact sequential replay when any draw was rejected (probability < n/2^64
+// per draw); a no-op otherwise.
+__global__ void k_draw_fixup(int64_t n, int64_t b, uint64_t s0, int32_t* j, const int* reject) {
+  if (*reject == 0) return;
+  uint64_t k = 0;
+  for (int64_t i = 0; i < b; ++i) {
+    const uint64_t bound = static_cast<uint64_t>(n - i);
+    const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+    uint64_t x;
+    do {
+      x = stream_draw(s0, k++);
+    } while (x >= limit);
+    j[i] = static_cast<int32_t>(i + static_cast<int64_t>(x % bound));
+  }
+}
+
+__global__ void k_link(int64_t b, const int32_t* __restrict__ j, unsigned long long* head,
+                       uint32_t tag, int32_t* __restrict__ next) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= b) return;
+  const unsigned long long mine = (static_cast<unsigned long long>(tag) << 32) | static_cast<uint32_t>(i);
+  const unsigned long long old = atomicExch(head + j[i], mine);
+  next[i] = (static_cast<uint32_t>(old >> 32) == tag) ? static_cast<int32_t>(old & 0xffffffffu) : -1;
+}
+
+// Largest step m < limit whose target is t, or -1.
+__device__ __forceinline__ int32_t last_before(const unsigned long long* head, const int32_t* next,
+                                               uint32_t tag, int32_t t, int32_t limit) {
+  const unsigned long long h = head[t];
+  if (static_cast<uint32_t>(h >> 32) != tag) return -1;
+  int32_t m = static_cast<int32_t>(h & 0xffffffffu), best = -1;
+  while (m >= 0) {
+    if (m < limit && m > best) best = m;
+    m = next[m];
+  }
+  return best;
+}
+
+__global__ void k_resolve(int64_t b, const int32_t* __restrict__ j,
+                          const unsigned long long* __restrict__ head,
+                          const int32_t* __restrict__ next, uint32_t tag, uint32_t* bitmap) {
+  const int64_t i64 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i64 >= b) return;
+  const int32_t i = static_cast<int32_t>(i64);
+  const int32_t ji = j[i];
+  int32_t cur;
+  bool chain = true;  // cur is a position whose pre-step value val(cur) is wanted
+  if (ji == i) {
+    cur = i;
+  } else {
+    cur = last_before(head, next, tag, ji, i);
+    if (cur < 0) {  // position ji untouched before step i: it still holds ji
+      cur = ji;
+      chain = false;
+    }
+  }
+  if (chain) {
+    for (;;) {
+      const int32_t p = last_before(head, next, tag, cur, cur);
+      if (p < 0) break;
+      cur = p;
+    }
+  }
+  atomicOr(bitmap + (cur >> 5), 1u << (cur & 31));
+}
+
+__global__ void k_popc(int64_t words, const uint32_t* __restrict__ bitmap, int32_t* __restrict__ cnt) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w < words) cnt[w] = __popc(bitmap[w]);
+}
+
+__global__ void k_compact(int64_t words, const uint32_t* __restrict__ bitmap,
+                          const int32_t* __restrict__ wpfx, int64_t* __restrict__ out) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= words) return;
+  uint32_t m = bitmap[w];
+  int64_t pos = wpfx[w];
+  while (m) {
+    const int bit = __ffs(m) - 1;
+    out[pos++] = w * 32 + bit;
+    m &= m - 1;
+  }
+}
+
+__device__ __forceinline__ int64_t rank_of(const uint32_t* bitmap, const int32_t* wpfx, int64_t v) {
+  const int64_t w = v >> 5;
+  return wpfx[w] + __popc(bitmap[w] & ((1u << (v & 31)) - 1u));
+}
+
+// batch_off: ranks of the block_partition boundaries (sample_partition)
+__global__ void k_ranks(int m, const int64_t* __restrict__ q, const uint32_t* __restrict__ bitmap,
+                        const int32_t* __restrict__ wpfx, int64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = rank_of(bitmap, wpfx, q[i]);
+}
+
+// Pass 1: kept entries per sampled row; block totals of the extracted count.
+__global__ void k_extract_count(int64_t nr, const int64_t* __restrict__ sample, int64_t row_lo,
+                                int64_t shard_r0, const int64_t* __restrict__ srp,
+                                const int32_t* __restrict__ scol, const uint32_t* __restrict__ bitmap,
+                                int32_t* __restrict__ cnt, unsigned long long* extracted) {
+  __shared__ unsigned long long part[kThreads / 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + wib;
+  unsigned long long ext = 0;
+  if (w < nr) {
+    const int64_t v = sample[row_lo + w];
+    const int64_t e0 = srp[v - shard_r0], e1 = srp[v - shard_r0 + 1];
+    int32_t c = 0;
+    for (int64_t e = e0; e < e1; e += 32) {
+      const int64_t k = e + lane;
+      bool keep = false;
+      if (k < e1) {
+        const int32_t col = scol[k];
+        keep = (__ldg(bitmap + (col >> 5)) >> (col & 31)) & 1u;
+      }
+      c += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    if (lane == 0) cnt[w] = c;
+    ext = static_cast<unsigned long long>(e1 - e0);
+  }
+  if (lane == 0) part[wib] = ext;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int k = 0; k < kThreads / 32; ++k) s += part[k];
+    if (s) atomicAdd(extracted, s);
+  }
+}
+
+// Pass 2: write the kept entries (canonical order), fp64 rescale by 1/p of
+// off-diagonal entries (global ids), compact column ids via the rank table.
+__global__ void k_extract_fill(int64_t nr, const int64_t* __restrict__ sample, int64_t row_lo,
+                               int64_t shard_r0, const int64_t* __restrict__ srp,
+                               const int32_t* __restrict__ scol, const double* __restrict__ sval,
+                               const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ wpfx,
+                               int64_t col_lo, double p, const int64_t* __restrict__ row_ptr,
+                               int32_t* __restrict__ col_out, float* __restrict__ val_out,
+                               double* __restrict__ val64_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5);
+  if (w >= nr) return;
+  const int64_t v = sample[row_lo + w];
+  const int64_t e0 = srp[v - shard_r0], e1 = srp[v - shard_r0 + 1];
+  int64_t pos = row_ptr[w];
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int64_t e = e0; e < e1; e += 32) {
+    const int64_t k = e + lane;
+    bool keep = false;
+    int32_t col = 0;
+    uint32_t word = 0;
+    if (k < e1) {
+      col = scol[k];
+      word = __ldg(bitmap + (col >> 5));
+      keep = (word >> (col & 31)) & 1u;
+    }
+    const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int64_t dst = pos + __popc(mask & lt);
+      const int64_t rk = wpfx[col >> 5] + __popc(word & ((1u << (col & 31)) - 1u));
+      col_out[dst] = static_cast<int32_t>(rk - col_lo);
+      double x = sval[k];
+      if (v != static_cast<int64_t>(col)) x = x / p;
+      val_out[dst] = static_cast<float>(x);
+      val64_out[dst] = x;
+    }
+    pos += __popc(mask);
+  }
+}
+
+__global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t* __restrict__ sample,
+                           int64_t row_lo, const float* __restrict__ feats, int64_t fld,
+                           bf16* __restrict__ xb, float* __restrict__ xf) {
+  const int64_t r = blockIdx.x;
+  if (r >= rows) return;
+  const float* src = feats + sample[row_lo + r] * fld;
+  for (int64_t c = threadIdx.x; c < ld; c += blockDim.x) {
+    const float x = c < cols ? src[c] : 0.0f;
+    if (xb) xb[r * ld + c] = __float2bfloat16_rn(x);
+    if (xf && c < cols) xf[r * cols + c] = x;
+  }
+}
+
+__global__ void k_gather_labels(int64_t b, const int64_t* __restrict__ sample,
+                                const int32_t* __restrict__ labels, int32_t* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < b) out[i] = labels[sample[i]];
+}
+
+inline unsigned blocks(int64_t n, int t = kThreads) { return static_cast<unsigned>(ceil_div(n, t)); }
+
+}  // namespace
+
+void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* d_sample) {
+  require(b >= 1 && b <= n, "sample_vertices: need 1 <= b <= n");
+  require(n < (int64_t{1} << 31) - 64, "sample_vertices: n must be < 2^31");
+  SamplerWork& sw = ctx.sw;
+  cudaStream_t s = ctx.stream;
+  if (sw.head_n < n) {
+    sw.head.reserve(static_cast<size_t>(n) * 8);
+    GGB_CUDA(cudaMemsetAsync(sw.head.p, 0, static_cast<size_t>(n) * 8, s));
+    sw.head_n = n;
+    sw.tag = 0;
+  }
+  if (++sw.tag == 0) {  // tag wrap: clear the table
+    GGB_CUDA(cudaMemsetAsync(sw.head.p, 0, static_cast<size_t>(sw.head_n) * 8, s));
+    sw.tag = 1;
+  }
+  const int64_t words = n / 32 + 2;
+  int32_t* j = sw.j.reserve_n<int32_t>(b);
+  int32_t* next = sw.next.reserve_n<int32_t>(b);
+  int* flag = sw.flag.reserve_n<int>(1);
+  uint32_t* bitmap = sw.bitmap.reserve_n<uint32_t>(words);
+  int32_t* wcount = sw.wcount.reserve_n<int32_t>(words);
+  int32_t* wpfx = sw.wpfx.reserve_n<int32_t>(words + 1);
+  GGB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  GGB_CUDA(cudaMemsetAsync(bitmap, 0, static_cast<size_t>(words) * 4, s));
+  const uint64_t s0 = splitmix64(seed + step);  // sampling.cpp:16
+  k_draw<<<blocks(b), kThreads, 0, s>>>(n, b, s0, j, flag);
+  k_draw_fixup<<<1, 1, 0, s>>>(n, b, s0, j, flag);
+  k_link<<<blocks(b), kThreads, 0, s>>>(b, j, sw.head.as<unsigned long long>(), sw.tag, next);
+  k_resolve<<<blocks(b), kThreads, 0, s>>>(b, j, sw.head.as<unsigned long long>(), next, sw.tag,
+                                           bitmap);
+  k_popc<<<blocks(words), kThreads, 0, s>>>(words, bitmap, wcount);
+  exclusive_scan_i32(wcount, wpfx, words, sw.scan_tmp, s);
+  k_compact<<<blocks(words), kThreads, 0, s>>>(words, bitmap, wpfx, d_sample);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 9;
+}
+
+namespace {
+
+void extract_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t row_lo,
+                   int64_t row_hi, int64_t col_lo, int64_t col_hi, int64_t b, int64_t n,
+                   BatchCsr& out, int32_t* d_cnt, unsigned long long* d_ext) {
+  out.n_rows = row_hi - row_lo;
+  out.n_cols = col_hi - col_lo;
+  int64_t* rp = out.row_ptr.reserve_n<int64_t>(out.n_rows + 1);
+  if (out.n_rows > 0) {
+    k_extract_count<<<blocks(out.n_rows, kThreads / 32), kThreads, 0, ctx.stream>>>(
+        out.n_rows, d_sample, row_lo, sh.r0, sh.row_ptr.as<int64_t>(), sh.col.as<int32_t>(),
+        ctx.sw.bitmap.as<uint32_t>(), d_cnt, d_ext);
+    ctx.launches += 1;
+  }
+  exclusive_scan_i32_to_i64(d_cnt, rp, out.n_rows, ctx.sw.scan_tmp, ctx.stream);
+  ctx.launches += 3;
+  (void)b;
+  (void)n;
+}
+
+void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t row_lo,
+                int64_t col_lo, int64_t b, int64_t n, BatchCsr& out) {
+  out.col.reserve_n<int32_t>(out.nnz);
+  out.val.reserve_n<float>(out.nnz);
+  out.val64.reserve_n<double>(out.nnz);
+  if (out.n_rows == 0 || out.nnz == 0) return;
+  const double p = static_cast<double>(b - 1) / static_cast<double>(n - 1);  // shardsample.cpp:116
+  k_extract_fill<<<blocks(out.n_rows, kThreads / 32), kThreads, 0, ctx.stream>>>(
+      out.n_rows, d_sample, row_lo, sh.r0, sh.row_ptr.as<int64_t>(), sh.col.as<int32_t>(),
+      sh.val.as<double>(), ctx.sw.bitmap.as<uint32_t>(), ctx.sw.wpfx.as<int32_t>(), col_lo, p,
+      out.row_ptr.as<int64_t>(), out.col.as<int32_t>(), out.val.as<float>(), out.val64.as<double>());
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+}  // namespace
+
+void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
+                      Batch& bt) {
+  require(b >= 2 && b <= g.n, "build_local_minibatch: need 2 <= b <= N");
+  cudaStream_t s = ctx.stream;
+  bt.ctx = &ctx;
+  bt.graph = &g;
+  bt.b = b;
+  bt.n = g.n;
+  bt.planes = g.planes;
+  int64_t* d_sample = bt.sample.reserve_n<int64_t>(b);
+  sample_set(ctx, g.n, b, group_seed, step, d_sample);
+
+  // batch_off[a] = sample_partition(S, block_partition(N, g_a)) (model.hpp:257-259)
+  std::vector<int64_t> q;
+  for (int a = 1; a < 4; ++a) {
+    auto off = block_partition(g.n, ctx.grid.dims[a]);
+    q.insert(q.end(), off.begin(), off.end());
+  }
+  const int m = static_cast<int>(q.size());
+  // device scratch: [0,m) queries, [m,2m) ranks, [2m, 2m+2) extracted counters
+  int64_t* dmisc = ctx.sw.dev_misc.reserve_n<int64_t>(2 * m + 64);
+  int64_t* hmisc = static_cast<int64_t*>(ctx.sw.host_misc.reserve((2 * m + 64) * 8));
+  std::copy(q.begin(), q.end(), hmisc);
+  GGB_CUDA(cudaMemcpyAsync(dmisc, hmisc, m * 8, cudaMemcpyHostToDevice, s));
+  k_ranks<<<1, 128, 0, s>>>(m, dmisc, ctx.sw.bitmap.as<uint32_t>(), ctx.sw.wpfx.as<int32_t>(),
+                            dmisc + m);
+  ctx.launches += 1;
+  GGB_CUDA(cudaMemcpyAsync(hmisc + m, dmisc + m, m * 8, cudaMemcpyDeviceToHost, s));
+  GGB_CUDA(cudaStreamSynchronize(s));
+  {
+    int k = 0;
+    for (int a = 1; a < 4; ++a) {
+      bt.batch_off[a].assign(hmisc + m + k, hmisc + m + k + ctx.grid.dims[a] + 1);
+      k += ctx.grid.dims[a] + 1;
+    }
+  }
+
+  // Plane blocks. Identical static shards (e.g. every plane on 1x1x1 grids)
+  // share one extracted block.
+  struct Key {
+    int shard;
+    int64_t rl, rh, cl, ch;
+  };
+  std::vector<Key> keys;
+  bt.csr_of.assign(g.planes, -1);
+  bt.csrt_of.assign(g.planes, -1);
+  auto find_or_add = [&](int shard, int64_t rl, int64_t rh, int64_t cl, int64_t ch) {
+    for (size_t k = 0; k < keys.size(); ++k)
+      if (keys[k].shard == shard && keys[k].rl == rl && keys[k].rh == rh && keys[k].cl == cl &&
+          keys[k].ch == ch)
+        return static_cast<int>(k);
+    keys.push_back({shard, rl, rh, cl, ch});
+    return static_cast<int>(keys.size() - 1);
+  };
+  for (int p = 0; p < g.planes; ++p) {
+    const Layout lay = adjacency_layout(p + 1);
+    const auto& ro = bt.batch_off[lay.row];
+    const auto& co = bt.batch_off[lay.col];
+    const int cr = ctx.coord[lay.row], cc = ctx.coord[lay.col];
+    const int64_t rl = ro[cr], rh = ro[cr + 1], cl = co[cc], ch = co[cc + 1];
+    bt.csr_of[p] = find_or_add(g.fwd_of[p], rl, rh, cl, ch);
+    bt.csrt_of[p] = find_or_add(g.tr_of[p], cl, ch, rl, rh);
+  }
+  if (bt.csrs.size() < keys.size()) bt.csrs.resize(keys.size());
+
+  int64_t max_rows = 0;
+  for (auto& k : keys) max_rows = std::max(max_rows, k.rh - k.rl);
+  // per block: counts region, one extracted counter
+  int32_t* d_cnt = ctx.sw.cnt.reserve_n<int32_t>((max_rows + 1) * keys.size() + 1);
+  unsigned long long* d_ext = reinterpret_cast<unsigned long long*>(dmisc + 2 * m);
+  GGB_CUDA(cudaMemsetAsync(d_ext, 0, 8 * keys.size(), s));
+  for (size_t k = 0; k < keys.size(); ++k) {
+    const Key& kk = keys[k];
+    BatchCsr& out = bt.csrs[k];
+    out.r0 = kk.rl;
+    out.r1 = kk.rh;
+    out.c0 = kk.cl;
+    out.c1 = kk.ch;
+    extract_block(ctx, g.shards[kk.shard], d_sample, kk.rl, kk.rh, kk.cl, kk.ch, b, g.n, out,
+                  d_cnt + k * (max_rows + 1), d_ext + k);
+  }
+  // totals: row_ptr[n_rows] of every block, plus the extracted counters
+  const size_t nk = keys.size();
+  for (size_t k = 0; k < nk; ++k)
+    GGB_CUDA(cudaMemcpyAsync(hmisc + k, bt.csrs[k].row_ptr.as<int64_t>() + bt.csrs[k].n_rows, 8,
+                             cudaMemcpyDeviceToHost, s));
+  GGB_CUDA(cudaMemcpyAsync(hmisc + nk, d_ext, 8 * nk, cudaMemcpyDeviceToHost, s));
+  GGB_CUDA(cudaStreamSynchronize(s));
+  for (size_t k = 0; k < nk; ++k) bt.csrs[k].nnz = hmisc[k];
+  // counters as build_step_batch accumulates them (model.hpp:265-268): one
+  // build_local_minibatch per plane, counting its forward block
+  bt.nnz_extracted = 0;
+  bt.nnz_kept = 0;
+  for (int p = 0; p < g.planes; ++p) {
+    bt.nnz_extracted += static_cast<uint64_t>(hmisc[nk + bt.csr_of[p]]);
+    bt.nnz_kept += static_cast<uint64_t>(bt.csrs[bt.csr_of[p]].nnz);
+  }
+  for (size_t k = 0; k < nk; ++k)
+    fill_block(ctx, g.shards[keys[k].shard], d_sample, keys[k].rl, keys[k].cl, b, g.n, bt.csrs[k]);
+
+  // x_in (X,Z) = features[S rows of this X block, Z column block] (model.hpp:293-303)
+  {
+    const auto& xo = bt.batch_off[kInputFeatureLayout.row];
+    const int cx = ctx.coord[kInputFeatureLayout.row];
+    bt.x_r0 = xo[cx];
+    bt.x_r1 = xo[cx + 1];
+    bt.x_c0 = g.feat_c0;
+    bt.x_c1 = g.feat_c1;
+    const int64_t cols = bt.x_c1 - bt.x_c0;
+    bt.x_ld = round_up(std::max<int64_t>(cols, 1), 8);
+    const int64_t rows = bt.x_r1 - bt.x_r0;
+    bf16* xb = bt.x_in.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
+    if (rows > 0) {
+      k_gather_x<<<static_cast<unsigned>(rows), 128, 0, s>>>(rows, cols, bt.x_ld, d_sample, bt.x_r0,
+                                                            g.features.as<float>(), cols, xb, nullptr);
+      ctx.launches += 1;
+    }
+  }
+  int32_t* lab = bt.labels.reserve_n<int32_t>(b);
+  k_gather_labels<<<blocks(b), kThreads, 0, s>>>(b, d_sample, g.labels.as<int32_t>(), lab);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out) {
+  const int64_t rows = bt.x_r1 - bt.x_r0, cols = bt.x_c1 - bt.x_c0;
+  if (rows <= 0 || cols <= 0) return;
+  k_gather_x<<<static_cast<unsigned>(rows), 128, 0, ctx.stream>>>(
+      rows, cols, cols, bt.sample.as<int64_t>(), bt.x_r0, bt.graph->features.as<float>(), cols,
+      nullptr, d_out);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+}  // namespace ggb

@@ -1,0 +1,555 @@
+// Device training step: init_state (model.hpp:175-208), forward
+// (model.hpp:335-376), parallel_cross_entropy (pmm.hpp:352-401), backward
+// (model.hpp:378-420), dp_sync (model.hpp:423-433) and optimizer_step
+// (model.hpp:435-456). Every contraction follows the reference's 3D-PMM
+// rule (pmm.hpp:17-29): local product, then an all-reduce along the
+// contraction axis (a no-op for singleton groups).
+#include <cmath>
+
+#include "comm.hpp"
+#include "rng.cuh"
+#include "trainer.hpp"
+
+namespace ggb {
+
+Block make_block(const Ctx& ctx, Layout lay, int64_t g_rows, int64_t g_cols,
+                 const std::vector<int64_t>& row_off, const std::vector<int64_t>& col_off) {
+  Block b;
+  b.lay = lay;
+  b.g_rows = g_rows;
+  b.g_cols = g_cols;
+  const int cr = ctx.coord[lay.row], cc = ctx.coord[lay.col];
+  b.r0 = row_off[cr];
+  b.r1 = row_off[cr + 1];
+  b.c0 = col_off[cc];
+  b.c1 = col_off[cc + 1];
+  return b;
+}
+
+namespace {
+
+inline int64_t ld8(int64_t c) { return round_up(std::max<int64_t>(c, 1), 8); }
+
+template <class T>
+T* grow(DevBuf& b, int64_t n) {
+  return b.reserve_n<T>(static_cast<size_t>(std::max<int64_t>(n, 1)));
+}
+
+std::vector<int64_t> hoff(const Ctx& ctx, int64_t d, int axis) { return block_partition(d, ctx.grid.dims[axis]); }
+
+// ---- reshard (pmm.hpp:171-204): gather the full matrix, slice the new block ---------
+__global__ void k_slice(const float* __restrict__ full, int gr, int64_t maxr, int64_t maxc,
+                        const int64_t* __restrict__ roff, int gc, const int64_t* __restrict__ coff,
+                        int64_t R0, int64_t C0, int64_t rows, int64_t cols, float* __restrict__ out,
+                        int64_t ldo) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows * cols) return;
+  const int64_t i = R0 + t / cols, j = C0 + t % cols;
+  int kr = 0, kc = 0;
+  while (kr + 1 < gr && roff[kr + 1] <= i) ++kr;
+  while (kc + 1 < gc && coff[kc + 1] <= j) ++kc;
+  const int64_t li = i - roff[kr], lj = j - coff[kc];
+  out[(t / cols) * ldo + (t % cols)] = full[((static_cast<int64_t>(kc) * gr + kr) * maxr + li) * maxc + lj];
+}
+
+__global__ void k_pad_copy(const float* __restrict__ in, int64_t ld, int64_t rows, int64_t cols,
+                           float* __restrict__ out, int64_t maxc) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows * cols) return;
+  out[(t / cols) * maxc + t % cols] = in[(t / cols) * ld + t % cols];
+}
+
+struct ReshardWork {
+  DevBuf pad, stage1, full, offs;
+  PinnedBuf hoffs;
+};
+
+// dst block of the same global matrix under another layout / partition.
+void reshard(Ctx& ctx, ReshardWork& w, const Block& sb, const std::vector<int64_t>& s_roff,
+             const std::vector<int64_t>& s_coff, const float* src, int64_t lds, const Block& db,
+             float* dst, int64_t ldd) {
+  const int gr = static_cast<int>(s_roff.size()) - 1, gc = static_cast<int>(s_coff.size()) - 1;
+  int64_t maxr = 1, maxc = 1;
+  for (int k = 0; k < gr; ++k) maxr = std::max(maxr, s_roff[k + 1] - s_roff[k]);
+  for (int k = 0; k < gc; ++k) maxc = std::max(maxc, s_coff[k + 1] - s_coff[k]);
+  const int64_t blk = maxr * maxc;
+  float* pad = w.pad.reserve_n<float>(blk);
+  GGB_CUDA(cudaMemsetAsync(pad, 0, blk * 4, ctx.stream));
+  if (sb.rows() * sb.cols() > 0)
+    k_pad_copy<<<static_cast<unsigned>(ceil_div(sb.rows() * sb.cols(), 256)), 256, 0, ctx.stream>>>(
+        src, lds, sb.rows(), sb.cols(), pad, maxc);
+  float* s1 = w.stage1.reserve_n<float>(blk * gr);
+  all_gather(ctx, sb.lay.row, pad, blk, s1);
+  float* full = w.full.reserve_n<float>(blk * gr * gc);
+  all_gather(ctx, sb.lay.col, s1, blk * gr, full);
+  int64_t* ho = static_cast<int64_t*>(w.hoffs.reserve((gr + gc + 2) * 8));
+  std::copy(s_roff.begin(), s_roff.end(), ho);
+  std::copy(s_coff.begin(), s_coff.end(), ho + gr + 1);
+  int64_t* doffs = w.offs.reserve_n<int64_t>(gr + gc + 2);
+  GGB_CUDA(cudaMemcpyAsync(doffs, ho, (gr + gc + 2) * 8, cudaMemcpyHostToDevice, ctx.stream));
+  const int64_t n = db.rows() * db.cols();
+  if (n > 0)
+    k_slice<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, ctx.stream>>>(
+        full, gr, maxr, maxc, doffs, gc, doffs + gr + 1, db.r0, db.c0, db.rows(), db.cols(), dst, ldd);
+  GGB_CUDA(cudaStreamSynchronize(ctx.stream));  // pinned offsets are reused
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 3;
+}
+
+ReshardWork& reshard_work() {
+  static thread_local ReshardWork w;
+  return w;
+}
+
+bool pmm_trivial(const Ctx& ctx) { return ctx.grid.dims[1] == 1 && ctx.grid.dims[2] == 1 && ctx.grid.dims[3] == 1; }
+
+uint64_t dropout_key(uint64_t seed, int dp, uint64_t gstep, int layer) {  // model.hpp:164-171
+  return hash_combine(hash_combine(hash_combine(hash_combine(seed, 0xd509), static_cast<uint64_t>(dp)), gstep),
+                      static_cast<uint64_t>(layer));
+}
+
+}  // namespace
+
+// ---- init_state (model.hpp:175-208) -------------------------------------------------
+void state_init(Ctx& ctx, State& st, const ggb_model_config& cfg, uint64_t seed) {
+  require(cfg.layers >= 1, "ModelConfig: layers must be >= 1");
+  require(cfg.d_in >= 1 && cfg.d_h >= 1 && cfg.d_out >= 1, "ModelConfig: dims must be >= 1");
+  require(cfg.dropout_rate >= 0.0 && cfg.dropout_rate < 1.0, "ModelConfig: dropout rate must be in [0, 1)");
+  st.ctx = &ctx;
+  st.cfg = cfg;
+  st.seed = seed;
+  st.params.clear();
+  st.wl.clear();
+  st.gamma.clear();
+  int64_t off = 0;
+  auto add_mat = [&](Layout lay, int64_t rows, int64_t cols) {
+    ParamSlot p;
+    p.blk = make_block(ctx, lay, rows, cols, hoff(ctx, rows, lay.row), hoff(ctx, cols, lay.col));
+    p.off = off;
+    p.n = p.blk.rows() * p.blk.cols();
+    p.ldb = ld8(p.blk.cols());
+    p.ldt = ld8(p.blk.rows());
+    off += round_up(std::max<int64_t>(p.n, 1), 64);
+    st.params.push_back(std::move(p));
+    return static_cast<int>(st.params.size() - 1);
+  };
+  st.win = add_mat(weight_layout_for(kInputFeatureLayout), cfg.d_in, cfg.d_h);
+  for (int l = 1; l <= cfg.layers; ++l) {
+    st.wl.push_back(add_mat(weight_layout(l), cfg.d_h, cfg.d_h));
+    if (cfg.use_rmsnorm) {
+      const Layout out = feature_layout(l + 1);
+      ParamSlot p;
+      p.is_vec = true;
+      p.row_axis = out.row;
+      p.col_axis = out.col;
+      const auto o = hoff(ctx, cfg.d_h, out.col);
+      p.blk.lay = out;
+      p.blk.g_rows = 1;
+      p.blk.g_cols = cfg.d_h;
+      p.blk.r0 = 0;
+      p.blk.r1 = 1;
+      p.blk.c0 = o[ctx.coord[out.col]];
+      p.blk.c1 = o[ctx.coord[out.col] + 1];
+      p.off = off;
+      p.n = p.blk.cols();
+      off += round_up(std::max<int64_t>(p.n, 1), 64);
+      st.params.push_back(std::move(p));
+      st.gamma.push_back(static_cast<int>(st.params.size() - 1));
+    }
+  }
+  st.wout = add_mat(weight_layout_for(feature_layout(cfg.layers + 1)), cfg.d_h, cfg.d_out);
+  st.total = off;
+  float* W = st.W.reserve_n<float>(off);
+  float* G = st.G.reserve_n<float>(off);
+  float* M = st.M.reserve_n<float>(off);
+  float* V = st.V.reserve_n<float>(off);
+  GGB_CUDA(cudaMemsetAsync(W, 0, off * 4, ctx.stream));
+  GGB_CUDA(cudaMemsetAsync(G, 0, off * 4, ctx.stream));
+  GGB_CUDA(cudaMemsetAsync(M, 0, off * 4, ctx.stream));
+  GGB_CUDA(cudaMemsetAsync(V, 0, off * 4, ctx.stream));
+  auto init_mat = [&](int idx, uint64_t key) {
+    ParamSlot& p = st.params[idx];
+    init_weight(ctx, W + p.off, p.blk.rows(), p.blk.cols(), p.blk.g_rows, p.blk.g_cols, p.blk.r0, p.blk.c0, key);
+  };
+  init_mat(st.win, hash_combine(seed, 101));
+  for (int l = 1; l <= cfg.layers; ++l) init_mat(st.wl[l - 1], hash_combine(seed, 200 + static_cast<uint64_t>(l)));
+  for (int gi : st.gamma) fill(ctx, W + st.params[gi].off, st.params[gi].n, 1.0f);
+  init_mat(st.wout, hash_combine(seed, 102));
+  st.opt_step = 0;
+  st.have_forward = false;
+  for (auto& p : st.params)
+    if (!p.is_vec) {
+      p.wb.reserve_n<bf16>(std::max<int64_t>(p.blk.rows(), 1) * p.ldb);
+      p.wt.reserve_n<bf16>(std::max<int64_t>(p.blk.cols(), 1) * p.ldt);
+      GGB_CUDA(cudaMemsetAsync(p.wb.p, 0, p.wb.bytes, ctx.stream));
+      GGB_CUDA(cudaMemsetAsync(p.wt.p, 0, p.wt.bytes, ctx.stream));
+    }
+  refresh_bf16(st);
+}
+
+void refresh_bf16(State& st) {
+  Ctx& ctx = *st.ctx;
+  for (auto& p : st.params)
+    if (!p.is_vec)
+      weight_bf16(ctx, st.W.as<float>() + p.off, p.blk.rows(), p.blk.cols(), p.wb.as<bf16>(), p.ldb,
+                  p.wt.as<bf16>(), p.ldt);
+}
+
+// ---- forward (model.hpp:335-376) ----------------------------------------------------
+void forward(State& st, const Batch& bt, int precision, bool training, uint64_t run_seed, uint64_t global_step,
+             double eps) {
+  Ctx& ctx = *st.ctx;
+  const auto& cfg = st.cfg;
+  const bool wire = precision == GGB_BF16_WIRE;
+  const int64_t H = cfg.d_h;
+  const int dp = ctx.coord[0];
+  contract(bt.planes == std::min(cfg.layers, 3), "forward: batch planes do not match the model layers");
+  float* W = st.W.as<float>();
+
+  // X0 = x_in (X,Z) . W_in (Z,Y) -> (X,Y), all-reduce Z
+  {
+    const ParamSlot& w = st.params[st.win];
+    Block ob = make_block(ctx, feature_layout(1), bt.b, H, bt.batch_off[feature_layout(1).row],
+                          hoff(ctx, H, feature_layout(1).col));
+    contract(ob.rows() == bt.x_r1 - bt.x_r0 && w.blk.rows() == bt.x_c1 - bt.x_c0,
+             "contract: local inner blocks differ");
+    st.x0.blk = ob;
+    st.x0.ldf = ob.cols();
+    st.x0.ldb = ld8(ob.cols());
+    st.x0.f = grow<float>(st.x0_f, ob.rows() * st.x0.ldf);
+    st.x0.b = grow<bf16>(st.x0_b, ob.rows() * st.x0.ldb);
+    const bool ar = !trivial(ctx, kInputFeatureLayout.col);
+    gemm_bf16(ctx, ob.rows(), ob.cols(), w.blk.rows(), bt.x_in.as<bf16>(), bt.x_ld, w.wt.as<bf16>(), w.ldt,
+              st.x0.f, st.x0.ldf, ar ? nullptr : st.x0.b, st.x0.ldb);
+    if (ar) {
+      all_reduce_sum(ctx, kInputFeatureLayout.col, st.x0.f, ob.rows() * st.x0.ldf, wire);
+      cast_bf16(ctx, st.x0.f, ob.rows(), ob.cols(), st.x0.ldf, st.x0.b, st.x0.ldb);
+    }
+  }
+  if (st.layers.size() < static_cast<size_t>(cfg.layers)) st.layers.resize(cfg.layers);
+  const double rate = cfg.use_dropout ? cfg.dropout_rate : 0.0;
+  const bool drop = training && rate > 0.0;
+  st.fwd_drop = drop;
+  st.fwd_keep_scale = drop ? static_cast<float>(1.0 / (1.0 - rate)) : 1.0f;
+  const uint64_t thresh = drop ? static_cast<uint64_t>(std::ceil(rate * 0x1.0p53)) : 0;
+
+  const Tensor* prev = &st.x0;
+  for (int l = 1; l <= cfg.layers; ++l) {
+    LayerBufs& L = st.layers[l - 1];
+    const int p = (l - 1) % 3;
+    const BatchCsr& A = bt.csrs[bt.csr_of[p]];
+    const Layout alay = adjacency_layout(l);
+    const Block& F = prev->blk;
+    contract(alay.col == F.lay.row && A.c0 == F.r0 && A.c1 == F.r1, "spmm: inner partitions differ");
+    // hagg = A . F -> (A.row, F.col), all-reduce A.col
+    Block hb;
+    hb.lay = {alay.row, F.lay.col};
+    hb.g_rows = bt.b;
+    hb.g_cols = H;
+    hb.r0 = A.r0;
+    hb.r1 = A.r1;
+    hb.c0 = F.c0;
+    hb.c1 = F.c1;
+    L.hagg.blk = hb;
+    L.hagg.ldb = ld8(hb.cols());
+    L.hagg.b = grow<bf16>(L.hagg_b, hb.rows() * L.hagg.ldb);
+    const bool ar_h = !trivial(ctx, alay.col);
+    if (ar_h) {
+      L.hagg.ldf = hb.cols();
+      L.hagg.f = grow<float>(L.hagg_f, hb.rows() * L.hagg.ldf);
+      spmm_csr(ctx, A.n_rows, A.row_ptr.as<int64_t>(), A.col.as<int32_t>(), A.val.as<float>(), prev->b, prev->ldb,
+               F.cols(), L.hagg.f, L.hagg.ldf, nullptr, 0, 0);
+      all_reduce_sum(ctx, alay.col, L.hagg.f, hb.rows() * L.hagg.ldf, wire);
+      cast_bf16(ctx, L.hagg.f, hb.rows(), hb.cols(), L.hagg.ldf, L.hagg.b, L.hagg.ldb);
+    } else {
+      spmm_csr(ctx, A.n_rows, A.row_ptr.as<int64_t>(), A.col.as<int32_t>(), A.val.as<float>(), prev->b, prev->ldb,
+               F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
+    }
+    // xw = hagg . W_l -> (A.row, third), all-reduce F.col
+    const ParamSlot& w = st.params[st.wl[l - 1]];
+    contract(w.blk.lay.row == hb.lay.col && w.blk.r0 == hb.c0 && w.blk.r1 == hb.c1,
+             "contract: inner partitions differ");
+    Block xb;
+    xb.lay = {hb.lay.row, w.blk.lay.col};
+    xb.g_rows = bt.b;
+    xb.g_cols = H;
+    xb.r0 = hb.r0;
+    xb.r1 = hb.r1;
+    xb.c0 = w.blk.c0;
+    xb.c1 = w.blk.c1;
+    L.xw_t.blk = xb;
+    L.xw_t.ldf = xb.cols();
+    L.xw_t.f = grow<float>(L.xw, xb.rows() * L.xw_t.ldf);
+    gemm_bf16(ctx, xb.rows(), xb.cols(), hb.cols(), L.hagg.b, L.hagg.ldb, w.wt.as<bf16>(), w.ldt, L.xw_t.f,
+              L.xw_t.ldf, nullptr, 0);
+    all_reduce_sum(ctx, hb.lay.col, L.xw_t.f, xb.rows() * L.xw_t.ldf, wire);
+    // RMSNorm statistics: row sum of squares, all-reduce along the column axis (fp32)
+    float* ss = nullptr;
+    float* rms = nullptr;
+    const float* gam = nullptr;
+    if (cfg.use_rmsnorm) {
+      ss = grow<float>(L.ss, xb.rows());
+      rms = grow<float>(L.rms, xb.rows());
+      rowsumsq(ctx, L.xw_t.f, L.xw_t.ldf, xb.rows(), xb.cols(), ss);
+      all_reduce_sum(ctx, xb.lay.col, ss, xb.rows(), false);
+      const ParamSlot& gp = st.params[st.gamma[l - 1]];
+      contract(gp.blk.c0 == xb.c0 && gp.blk.c1 == xb.c1, "rmsnorm: gamma slice does not match the column block");
+      gam = W + gp.off;
+    }
+    // residual: X_{l-1} resharded to feature_layout(l+1)
+    const Layout out = feature_layout(l + 1);
+    const float* res = nullptr;
+    int64_t ldres = 0;
+    if (cfg.use_residual) {
+      Block rb = make_block(ctx, out, bt.b, H, bt.batch_off[out.row], hoff(ctx, H, out.col));
+      contract(rb.r0 == xb.r0 && rb.r1 == xb.r1 && rb.c0 == xb.c0 && rb.c1 == xb.c1,
+               "fused_elementwise: residual layout mismatch");
+      if (pmm_trivial(ctx)) {
+        res = prev->f;
+        ldres = prev->ldf;
+      } else {
+        float* r = grow<float>(st.dres, rb.rows() * rb.cols());
+        reshard(ctx, reshard_work(), F, bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), prev->f, prev->ldf, rb,
+                r, rb.cols());
+        res = r;
+        ldres = rb.cols();
+      }
+    }
+    // fused RMSNorm apply + ReLU + dropout + residual -> X_l
+    L.x.blk = xb;
+    L.x.ldf = xb.cols();
+    L.x.ldb = ld8(xb.cols());
+    L.x.f = grow<float>(L.x_f, xb.rows() * L.x.ldf);
+    L.x.b = grow<bf16>(L.x_b, xb.rows() * L.x.ldb);
+    L.ldm = ceil_div(std::max<int64_t>(xb.cols(), 1), 8);
+    FwdApply fa{};
+    fa.rows = xb.rows();
+    fa.cols = xb.cols();
+    fa.x = L.xw_t.f;
+    fa.ldx = L.xw_t.ldf;
+    fa.ss = ss;
+    fa.gamma = gam;
+    fa.d = static_cast<float>(H);
+    fa.eps = static_cast<float>(eps);
+    fa.rms = rms;
+    fa.res = res;
+    fa.ldres = ldres;
+    fa.mask_key = dropout_key(run_seed, dp, global_step, l);
+    fa.row_g0 = xb.r0;
+    fa.col_g0 = xb.c0;
+    fa.drop = drop;
+    fa.thresh = thresh;
+    fa.keep_scale = st.fwd_keep_scale;
+    fa.out = L.x.f;
+    fa.ldo = L.x.ldf;
+    fa.outb = L.x.b;
+    fa.ldob = L.x.ldb;
+    fa.mask = grow<uint8_t>(L.mask, xb.rows() * L.ldm);
+    fa.ldm = L.ldm;
+    fwd_apply(ctx, fa);
+    prev = &L.x;
+  }
+  // logits = X_L . W_out, all-reduce X_L.col
+  {
+    const ParamSlot& w = st.params[st.wout];
+    const Block& F = prev->blk;
+    contract(w.blk.lay.row == F.lay.col && w.blk.r0 == F.c0 && w.blk.r1 == F.c1, "contract: inner partitions differ");
+    Block lb;
+    lb.lay = {F.lay.row, w.blk.lay.col};
+    lb.g_rows = bt.b;
+    lb.g_cols = cfg.d_out;
+    lb.r0 = F.r0;
+    lb.r1 = F.r1;
+    lb.c0 = w.blk.c0;
+    lb.c1 = w.blk.c1;
+    st.logits_blk = lb;
+    float* lg = grow<float>(st.logits, lb.rows() * lb.cols());
+    gemm_bf16(ctx, lb.rows(), lb.cols(), F.cols(), prev->b, prev->ldb, w.wt.as<bf16>(), w.ldt, lg, lb.cols(),
+              nullptr, 0);
+    all_reduce_sum(ctx, F.lay.col, lg, lb.rows() * lb.cols(), wire);
+  }
+  st.have_forward = true;
+}
+
+// ---- parallel_cross_entropy (pmm.hpp:352-401) ---------------------------------------
+void cross_entropy(State& st, const Batch& bt) {
+  Ctx& ctx = *st.ctx;
+  const Block& lb = st.logits_blk;
+  CeArgs c{};
+  c.rows = lb.rows();
+  c.cols = lb.cols();
+  c.logits = st.logits.as<float>();
+  c.ld = lb.cols();
+  c.labels = bt.labels.as<int32_t>();
+  c.row_g0 = lb.r0;
+  c.c0 = lb.c0;
+  c.mx = grow<float>(st.ce_mx, c.rows);
+  c.zt = grow<float>(st.ce_zt, 2 * c.rows);
+  c.invb = 1.0f / static_cast<float>(lb.g_rows);
+  c.dlogb = grow<bf16>(st.dlog_b, c.rows * ld8(c.cols));
+  c.lddlogb = ld8(c.cols);
+  c.loss_part = grow<float>(st.ce_part, ce_grad_blocks(c.rows) + 1);
+  c.loss_acc = grow<float>(st.loss_acc, 1);
+  ce_rowmax(ctx, c);
+  all_reduce_max(ctx, lb.lay.col, c.mx, c.rows);
+  ce_rowsum(ctx, c);
+  all_reduce_sum(ctx, lb.lay.col, c.zt, 2 * c.rows, false);
+  ce_grad(ctx, c);
+  all_reduce_sum(ctx, lb.lay.row, c.loss_acc, 1, false);
+  scale_scalar(ctx, c.loss_acc, c.invb, grow<float>(st.loss, 1));
+}
+
+// ---- backward (model.hpp:378-420) ---------------------------------------------------
+void backward(State& st, const Batch& bt, int precision) {
+  Ctx& ctx = *st.ctx;
+  const auto& cfg = st.cfg;
+  contract(st.have_forward && st.layers.size() >= static_cast<size_t>(cfg.layers),
+           "backward: cache does not match the model");
+  const bool wire = precision == GGB_BF16_WIRE;
+  const int64_t H = cfg.d_h;
+  float* W = st.W.as<float>();
+  float* G = st.G.as<float>();
+  GGB_CUDA(cudaMemsetAsync(G, 0, st.total * 4, ctx.stream));  // zero_grads (model.hpp:98-104)
+  const Block& lb = st.logits_blk;
+  const int64_t lddlog = ld8(lb.cols());
+  const Tensor& XL = st.layers[cfg.layers - 1].x;
+
+  // dW_out = X_L^T . dlogits, all-reduce X_L.row
+  {
+    const ParamSlot& w = st.params[st.wout];
+    gemm_wgrad_bf16(ctx, lb.rows(), XL.blk.cols(), lb.cols(), XL.b, XL.ldb, st.dlog_b.as<bf16>(), lddlog,
+                    G + w.off, w.blk.cols(), st.ws_wgrad);
+    all_reduce_sum(ctx, XL.blk.lay.row, G + w.off, w.n, wire);
+  }
+  // dxh = dlogits . W_out^T -> (X_L.row, X_L.col), all-reduce logits.col
+  Block db = XL.blk;
+  float* dxh = grow<float>(st.dxh, db.rows() * db.cols());
+  {
+    const ParamSlot& w = st.params[st.wout];
+    gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, dxh,
+              db.cols(), nullptr, 0);
+    all_reduce_sum(ctx, lb.lay.col, dxh, db.rows() * db.cols(), wire);
+  }
+  for (int l = cfg.layers; l >= 1; --l) {
+    LayerBufs& L = st.layers[l - 1];
+    const Block& xb = L.xw_t.blk;  // == db
+    contract(xb.lay == db.lay && xb.r0 == db.r0 && xb.c0 == db.c0, "backward: gradient layout mismatch");
+    const int64_t rows = xb.rows(), cols = xb.cols();
+    // residual gradient dres = reshard(dxh -> feature_layout(l))
+    const Block& F = (l == 1) ? st.x0.blk : st.layers[l - 2].x.blk;
+    float* dres = nullptr;
+    if (cfg.use_residual) {
+      if (pmm_trivial(ctx)) {
+        dres = dxh;  // identical block; the SpMM below accumulates into it
+      } else {
+        dres = grow<float>(st.dres, F.rows() * F.cols());
+        reshard(ctx, reshard_work(), db, bt.batch_off[db.lay.row], hoff(ctx, H, db.lay.col), dxh, db.cols(), F, dres,
+                F.cols());
+      }
+    }
+    // fused element-wise backward + RMSNorm backward -> dxw (bf16), dgamma
+    BwdApply ba{};
+    ba.rows = rows;
+    ba.cols = cols;
+    ba.dy = dxh;
+    ba.lddy = db.cols();
+    ba.mask = L.mask.as<uint8_t>();
+    ba.ldm = L.ldm;
+    ba.keep_scale = st.fwd_keep_scale;
+    ba.x = L.xw_t.f;
+    ba.ldx = L.xw_t.ldf;
+    ba.d = static_cast<float>(H);
+    const int64_t lddxw = ld8(cols);
+    ba.dxb = grow<bf16>(st.dxw_b, rows * lddxw);
+    ba.lddxb = lddxw;
+    if (cfg.use_rmsnorm) {
+      const ParamSlot& gp = st.params[st.gamma[l - 1]];
+      ba.gamma = W + gp.off;
+      ba.rms = L.rms.as<float>();
+      ba.s = grow<float>(st.s_row, rows);
+      bwd_stats(ctx, ba);
+      all_reduce_sum(ctx, xb.lay.col, ba.s, rows, false);
+      const int blocks = bwd_apply_blocks(ctx, rows, cols);
+      ba.dgamma_part = grow<float>(st.dg_part, static_cast<int64_t>(blocks) * cols);
+      bwd_apply(ctx, ba, blocks);
+      reduce_rows(ctx, ba.dgamma_part, blocks, cols, G + gp.off);
+      all_reduce_sum(ctx, xb.lay.row, G + gp.off, cols, false);
+    } else {
+      bwd_apply(ctx, ba, bwd_apply_blocks(ctx, rows, cols));
+    }
+    // dW_l = hagg^T . dxw, all-reduce hagg.row
+    const ParamSlot& w = st.params[st.wl[l - 1]];
+    const Tensor& hg = L.hagg;
+    gemm_wgrad_bf16(ctx, rows, hg.blk.cols(), cols, hg.b, hg.ldb, ba.dxb, lddxw, G + w.off, w.blk.cols(),
+                    st.ws_wgrad);
+    all_reduce_sum(ctx, hg.blk.lay.row, G + w.off, w.n, wire);
+    // dhagg = dxw . W_l^T -> (xw.row, hagg.col), all-reduce xw.col
+    const int64_t hc = hg.blk.cols();
+    const bool ar_d = !trivial(ctx, xb.lay.col);
+    const int64_t ldhb = ld8(hc);
+    bf16* dhb = grow<bf16>(st.dhagg_b, rows * ldhb);
+    if (ar_d) {
+      float* dhf = grow<float>(st.dhagg_f, rows * hc);
+      gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, dhf, hc, nullptr, 0);
+      all_reduce_sum(ctx, xb.lay.col, dhf, rows * hc, wire);
+      cast_bf16(ctx, dhf, rows, hc, hc, dhb, ldhb);
+    } else {
+      gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, nullptr, 0, dhb, ldhb);
+    }
+    // dxh = A_t . dhagg (+ dres) -> (A.col, hagg.col) = F's layout, all-reduce A.row
+    const int p = (l - 1) % 3;
+    const BatchCsr& At = bt.csrs[bt.csrt_of[p]];
+    const Layout alay = adjacency_layout(l);
+    contract(At.c0 == hg.blk.r0 && At.c1 == hg.blk.r1, "spmm: inner partitions differ");
+    const bool ar_s = !trivial(ctx, alay.row);
+    if (pmm_trivial(ctx) && cfg.use_residual) {
+      // dxh (== dres) += A_t . dhagg
+      spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
+               dxh, F.cols(), nullptr, 0, 1);
+    } else {
+      float* nd = grow<float>(st.dxh2, F.rows() * F.cols());
+      spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
+               nd, F.cols(), nullptr, 0, 0);
+      if (ar_s) all_reduce_sum(ctx, alay.row, nd, F.rows() * F.cols(), wire);
+      if (dres) add_inplace(ctx, nd, F.cols(), dres, F.cols(), F.rows(), F.cols());
+      std::swap(st.dxh, st.dxh2);
+      dxh = nd;
+    }
+    db = F;
+  }
+  // dW_in = x_in^T . dxh, all-reduce x_in.row (X)
+  {
+    const ParamSlot& w = st.params[st.win];
+    const int64_t rows = db.rows(), cols = db.cols();
+    const int64_t ldb = ld8(cols);
+    bf16* dxb = grow<bf16>(st.dxh_b, rows * ldb);
+    cast_bf16(ctx, dxh, rows, cols, cols, dxb, ldb);
+    gemm_wgrad_bf16(ctx, rows, bt.x_c1 - bt.x_c0, cols, bt.x_in.as<bf16>(), bt.x_ld, dxb, ldb, G + w.off,
+                    w.blk.cols(), st.ws_wgrad);
+    all_reduce_sum(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
+  }
+}
+
+// ---- dp_sync (model.hpp:423-433) ------------------------------------------------------
+void dp_sync(State& st) {
+  Ctx& ctx = *st.ctx;
+  const int gd = ctx.grid.dims[0];
+  all_reduce_sum(ctx, kD, st.G.as<float>(), st.total, false);
+  if (gd > 1) scale(ctx, st.G.as<float>(), st.total, 1.0f / static_cast<float>(gd));
+}
+
+// ---- optimizer_step (model.hpp:435-456) -----------------------------------------------
+void optimizer_step(State& st, int optimizer, double lr) {
+  Ctx& ctx = *st.ctx;
+  st.opt_step += 1;
+  if (optimizer == GGB_SGD) {
+    sgd(ctx, st.W.as<float>(), st.G.as<float>(), st.total, static_cast<float>(lr));
+  } else {
+    const double bc1 = 1.0 - std::pow(0.9, static_cast<double>(st.opt_step));
+    const double bc2 = 1.0 - std::pow(0.999, static_cast<double>(st.opt_step));
+    adam(ctx, st.W.as<float>(), st.G.as<float>(), st.M.as<float>(), st.V.as<float>(), st.total, lr, bc1, bc2);
+  }
+  refresh_bf16(st);
+}
+
+}  // namespace ggb

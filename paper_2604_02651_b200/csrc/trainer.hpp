@@ -1,0 +1,73 @@
+// ModelState and the training step (model.hpp:60-478) on the device.
+#pragma once
+
+#include "ops.hpp"
+
+namespace ggb {
+
+/// One rank's block of a 2D-sharded matrix (ShardedTensor metadata,
+/// tensor.hpp:75-86).
+struct Block {
+  Layout lay{kX, kY};
+  int64_t g_rows = 0, g_cols = 0, r0 = 0, r1 = 0, c0 = 0, c1 = 0;
+  int64_t rows() const { return r1 - r0; }
+  int64_t cols() const { return c1 - c0; }
+};
+
+Block make_block(const Ctx& ctx, Layout lay, int64_t g_rows, int64_t g_cols,
+                 const std::vector<int64_t>& row_off, const std::vector<int64_t>& col_off);
+
+struct ParamSlot {
+  bool is_vec = false;
+  Block blk;       // matrices: layout + ranges; vectors: c0/c1 (rows = 1)
+  int row_axis = 0, col_axis = 0;  // vectors: VecParam axes (model.hpp:70-76)
+  int64_t off = 0, n = 0;          // into the flat W/G/M/V arrays
+  int64_t ldb = 0, ldt = 0;        // bf16 copies: wb [rows][ldb], wt [cols][ldt]
+  DevBuf wb, wt;
+};
+
+struct Tensor {  // device activation block: fp32 and/or bf16 copy
+  Block blk;
+  float* f = nullptr;
+  int64_t ldf = 0;
+  bf16* b = nullptr;
+  int64_t ldb = 0;
+};
+
+struct LayerBufs {
+  DevBuf hagg_f, hagg_b, xw, ss, rms, mask, x_f, x_b;
+  Tensor hagg, xw_t, x;  // x = layer output X_l
+  int64_t ldm = 0;
+};
+
+struct State {
+  Ctx* ctx = nullptr;
+  ggb_model_config cfg{};
+  uint64_t seed = 0;
+  std::vector<ParamSlot> params;  // param_views order
+  int win = 0, wout = 0;
+  std::vector<int> wl, gamma;
+  int64_t total = 0;
+  DevBuf W, G, M, V;  // flat fp32
+  int64_t opt_step = 0;
+  // activations (grow-only)
+  DevBuf x0_f, x0_b, logits, dlog_b, ce_mx, ce_zt, ce_part, loss_acc, loss;
+  DevBuf dxh, dxh_b, dxh2, dxw_b, dhagg_f, dhagg_b, s_row, dg_part, ws_wgrad, dres, tmp;
+  std::vector<LayerBufs> layers;
+  Tensor x0;
+  Block logits_blk;
+  bool fwd_drop = false;
+  float fwd_keep_scale = 1.f;
+  bool have_forward = false;
+};
+
+void state_init(Ctx& ctx, State& st, const ggb_model_config& cfg, uint64_t seed);
+void refresh_bf16(State& st);
+void forward(State& st, const Batch& bt, int precision, bool training, uint64_t run_seed,
+             uint64_t global_step, double eps);
+void cross_entropy(State& st, const Batch& bt);
+void backward(State& st, const Batch& bt, int precision);
+void dp_sync(State& st);
+void optimizer_step(State& st, int optimizer, double lr);
+
+}  // namespace ggb

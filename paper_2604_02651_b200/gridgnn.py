@@ -1,0 +1,476 @@
+"""Python mirror of the reference's hot-path API (namespace gridgnn, /root/reference/proj)
+over the C ABI of libggb.so. Names, argument meaning and error behaviour follow
+the reference so parity tests read like the reference's own tests:
+
+    sample_vertices            sampling.hpp:33
+    block_partition            shardsample.hpp:14
+    sample_partition           shardsample.hpp:118
+    Dataset / RankContext      dataset.hpp:16-29, model.hpp:212-234  -> Graph
+    build_step_batch           model.hpp:250-309                     -> StepBatch
+    init_state                 model.hpp:175-208                     -> ModelState
+    forward / train_step       model.hpp:335-478
+    dp_sync / optimizer_step   model.hpp:423-456
+    steps_per_epoch            model.hpp:539-542
+
+Errors raise InvalidArgument (std::invalid_argument), CommContract and
+CommTimeout like the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import (ADAM, BF16_WIRE, FP32, SGD, CommContract, CommTimeout, GgbError,  # noqa: F401
+                   InvalidArgument, ModelConfigC, check, lib)
+
+P = C.c_void_p
+AXIS_D, AXIS_X, AXIS_Y, AXIS_Z = 0, 1, 2, 3
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(P)
+
+
+# ---- host-side layout algebra (grid.hpp, shardsample.cpp:8-17, pmm.hpp:31-63) -------
+
+def block_partition(n: int, g: int) -> np.ndarray:
+    if g < 1:
+        raise InvalidArgument(1, "block_partition: g must be >= 1")
+    base, extra = divmod(n, g)
+    sizes = [base + (1 if k < extra else 0) for k in range(g)]
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
+def sample_partition(s: np.ndarray, offsets: np.ndarray) -> np.ndarray:
+    return np.searchsorted(np.asarray(s), np.asarray(offsets), side="left").astype(np.int64)
+
+
+def steps_per_epoch(n: int, b: int, gd: int) -> int:
+    per = b * gd
+    return (n + per - 1) // per
+
+
+def adjacency_layout(layer: int) -> tuple[int, int]:
+    return [(AXIS_Z, AXIS_X), (AXIS_Y, AXIS_Z), (AXIS_X, AXIS_Y)][(layer - 1) % 3]
+
+
+def feature_layout(layer: int) -> tuple[int, int]:
+    return [(AXIS_X, AXIS_Y), (AXIS_Z, AXIS_X), (AXIS_Y, AXIS_Z)][(layer - 1) % 3]
+
+
+@dataclass(frozen=True)
+class DeviceGrid:
+    """4D grid (g_d, g_x, g_y, g_z), lexicographic rank numbering (grid.hpp:18-73)."""
+
+    gd: int = 1
+    gx: int = 1
+    gy: int = 1
+    gz: int = 1
+
+    def __post_init__(self):
+        if min(self.dims) < 1:
+            raise InvalidArgument(1, "DeviceGrid: dims must be >= 1")
+
+    @property
+    def dims(self) -> tuple[int, int, int, int]:
+        return (self.gd, self.gx, self.gy, self.gz)
+
+    def total(self) -> int:
+        return self.gd * self.gx * self.gy * self.gz
+
+    def coord_of(self, rank: int) -> tuple[int, int, int, int]:
+        z = rank % self.gz
+        rank //= self.gz
+        y = rank % self.gy
+        rank //= self.gy
+        x = rank % self.gx
+        return (rank // self.gx, x, y, z)
+
+    def rank_of(self, c) -> int:
+        return ((c[0] * self.gx + c[1]) * self.gy + c[2]) * self.gz + c[3]
+
+    def dp_group(self, rank: int) -> int:
+        return self.coord_of(rank)[0]
+
+    @staticmethod
+    def parse(s: str) -> "DeviceGrid":
+        """'GdxGxxGyxGz' as the reference CLI (gridgnn_main.cpp:57-66)."""
+        parts = [int(x) for x in s.lower().split("x")]
+        if len(parts) != 4:
+            raise InvalidArgument(1, "grid must be GdxGxxGyxGz")
+        return DeviceGrid(*parts)
+
+
+# ---- context ---------------------------------------------------------------------------
+
+def get_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib().ggb_get_unique_id(buf))
+    return bytes(buf)
+
+
+class Context:
+    """One rank on one GPU: replaces Communicator + RankComm (comm.hpp:203-408).
+
+    ``nccl_uid`` (from get_unique_id() on rank 0, broadcast by the caller)
+    creates NCCL communicators for the grid axes. Without it the context is
+    virtual: sampling and single-rank work run, multi-rank collectives raise
+    CommContract.
+    """
+
+    def __init__(self, grid: DeviceGrid = DeviceGrid(), rank: int = 0, device: int = 0,
+                 nccl_uid: bytes | None = None, stream: int | None = None):
+        self.grid = grid
+        self.rank = rank
+        self.coord = grid.coord_of(rank)
+        dims = (C.c_int32 * 4)(*grid.dims)
+        uid = (C.c_uint8 * 128).from_buffer_copy(nccl_uid) if nccl_uid else None
+        h = P()
+        check(lib().ggb_ctx_create(dims, rank, device, uid, stream, C.byref(h)))
+        self.h = h
+
+    def set_stream(self, stream: int | None):
+        check(lib().ggb_ctx_set_stream(self.h, stream))
+
+    def synchronize(self):
+        check(lib().ggb_ctx_synchronize(self.h))
+
+    def launches(self) -> int:
+        c = (C.c_uint64 * 1)()
+        check(lib().ggb_ctx_counters(self.h, c))
+        return int(c[0])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ggb_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context()
+    return _default_ctx
+
+
+@dataclass
+class SampleSet:
+    vertices: np.ndarray
+    batch_size: int
+    graph_size: int
+    seed: int
+    step: int
+
+
+def sample_vertices(n: int, b: int, seed: int, step: int, ctx: Context | None = None) -> SampleSet:
+    """sampling.hpp:33, sampled on the GPU (bit-exact with the reference)."""
+    ctx = ctx or default_context()
+    if b <= 0 or b > n:
+        raise InvalidArgument(1, "sample_vertices: need 1 <= b <= n")
+    out = np.empty(b, np.int64)
+    check(lib().ggb_sample_vertices(ctx.h, n, b, seed, step, _ptr(out)))
+    return SampleSet(out, b, n, seed, step)
+
+
+# ---- graph (Dataset + RankContext resident in HBM) ----------------------------------------
+
+class Graph:
+    def __init__(self, ctx: Context, h):
+        self.ctx = ctx
+        self.h = h
+        info = np.zeros(6, np.int64)
+        check(lib().ggb_graph_info(h, _ptr(info)))
+        self.n, self.nnz, self.d_in, self.n_classes, self.distinct_shards, self.device_bytes = (
+            int(x) for x in info)
+
+    @staticmethod
+    def from_csr(ctx: Context, n: int, row_ptr, col_idx, values, features, labels, n_classes: int,
+                 layers: int, symmetric: bool = True) -> "Graph":
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        ci = np.ascontiguousarray(col_idx, np.int64)
+        va = np.ascontiguousarray(values, np.float64)
+        fe = np.ascontiguousarray(features, np.float32)
+        la = np.ascontiguousarray(labels, np.int32)
+        h = P()
+        check(lib().ggb_graph_create(ctx.h, n, _ptr(rp), _ptr(ci), _ptr(va), int(symmetric),
+                                     fe.shape[1] if fe.ndim == 2 else 1, _ptr(fe), n_classes, _ptr(la),
+                                     layers, C.byref(h)))
+        return Graph(ctx, h)
+
+    @staticmethod
+    def generate_synthetic(ctx: Context, n: int, avg_degree: float, d_in: int, n_classes: int,
+                           seed: int, layers: int) -> "Graph":
+        """generate_synthetic (dataset.cpp:85-131), built natively then uploaded."""
+        h = P()
+        check(lib().ggb_graph_generate_synthetic(ctx.h, n, avg_degree, d_in, n_classes, seed, layers,
+                                                 C.byref(h)))
+        return Graph(ctx, h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ggb_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class Csr:
+    n_rows: int
+    n_cols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    r0: int = 0
+    r1: int = 0
+    c0: int = 0
+    c1: int = 0
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1]) if len(self.row_ptr) else 0
+
+
+class StepBatch:
+    """StepBatch (model.hpp:238-246) resident in HBM; exports are host copies."""
+
+    def __init__(self, graph: Graph, h):
+        self.graph = graph
+        self.h = h
+
+    def info(self):
+        v = np.zeros(9, np.int64)
+        check(lib().ggb_batch_info(self.h, _ptr(v)))
+        return v
+
+    @property
+    def b(self) -> int:
+        return int(self.info()[0])
+
+    @property
+    def planes(self) -> int:
+        return int(self.info()[2])
+
+    @property
+    def nnz_extracted(self) -> int:
+        return int(self.info()[7])
+
+    @property
+    def nnz_kept(self) -> int:
+        return int(self.info()[8])
+
+    @property
+    def sample(self) -> np.ndarray:
+        out = np.empty(self.b, np.int64)
+        check(lib().ggb_batch_sample(self.h, _ptr(out)))
+        return out
+
+    def batch_off(self, axis: int) -> np.ndarray:
+        out = np.empty(self.graph.ctx.grid.dims[axis] + 1, np.int64)
+        check(lib().ggb_batch_offsets(self.h, axis, _ptr(out)))
+        return out
+
+    def _plane(self, p: int, t: int) -> Csr:
+        dims = np.zeros(7, np.int64)
+        check(lib().ggb_batch_plane(self.h, p, t, _ptr(dims), None, None, None))
+        rp = np.empty(dims[0] + 1, np.int64)
+        col = np.empty(dims[2], np.int64)
+        val = np.empty(dims[2], np.float64)
+        check(lib().ggb_batch_plane(self.h, p, t, _ptr(dims), _ptr(rp), _ptr(col), _ptr(val)))
+        return Csr(int(dims[0]), int(dims[1]), rp, col, val, *(int(x) for x in dims[3:7]))
+
+    def a(self, p: int) -> Csr:
+        return self._plane(p, 0)
+
+    def a_t(self, p: int) -> Csr:
+        return self._plane(p, 1)
+
+    @property
+    def x_in(self) -> tuple[tuple[int, int, int, int], np.ndarray]:
+        i = self.info()
+        r0, r1, c0, c1 = (int(x) for x in i[3:7])
+        out = np.empty((r1 - r0, c1 - c0), np.float32)
+        check(lib().ggb_batch_x_in(self.h, _ptr(out)))
+        return (r0, r1, c0, c1), out
+
+    @property
+    def labels(self) -> np.ndarray:
+        out = np.empty(self.b, np.int32)
+        check(lib().ggb_batch_labels(self.h, _ptr(out)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ggb_batch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_step_batch(ctx: Context, graph: Graph, b: int, group_seed: int, step: int,
+                     reuse: StepBatch | None = None) -> StepBatch:
+    """model.hpp:250-309: the rank-local batch; communication-free."""
+    h = P(reuse.h.value if reuse is not None else None)
+    check(lib().ggb_build_step_batch(ctx.h, graph.h, b, group_seed, step, C.byref(h)))
+    if reuse is not None:
+        return reuse
+    return StepBatch(graph, h)
+
+
+# ---- model ------------------------------------------------------------------------------
+
+@dataclass
+class ModelConfig:
+    layers: int = 2
+    d_in: int = 0
+    d_h: int = 64
+    d_out: int = 0
+    dropout_rate: float = 0.1
+    use_rmsnorm: bool = True
+    use_dropout: bool = True
+    use_residual: bool = True
+
+    def c(self) -> ModelConfigC:
+        return ModelConfigC(self.layers, self.d_in, self.d_h, self.d_out, self.dropout_rate,
+                            int(self.use_rmsnorm), int(self.use_dropout), int(self.use_residual))
+
+    def param_names(self) -> list[str]:
+        out = ["win"]
+        for l in range(1, self.layers + 1):
+            out.append(f"w{l}")
+            if self.use_rmsnorm:
+                out.append(f"gamma{l}")
+        out.append("wout")
+        return out
+
+
+@dataclass
+class ParamBlock:
+    name: str
+    g_rows: int
+    g_cols: int
+    r0: int
+    r1: int
+    c0: int
+    c1: int
+    is_vec: bool = False
+
+
+class ModelState:
+    """ModelState (model.hpp:87-105) resident in HBM (fp32 master weights,
+    gradients and Adam moments; bf16 operand copies for the tensor cores)."""
+
+    def __init__(self, ctx: Context, cfg: ModelConfig, seed: int):
+        self.ctx = ctx
+        self.cfg = cfg
+        h = P()
+        c = cfg.c()
+        check(lib().ggb_state_create(ctx.h, C.byref(c), seed, C.byref(h)))
+        self.h = h
+        self.blocks: list[ParamBlock] = []
+        for i, name in enumerate(cfg.param_names()):
+            info = np.zeros(6, np.int64)
+            check(lib().ggb_state_param_info(h, i, _ptr(info)))
+            self.blocks.append(ParamBlock(name, *(int(x) for x in info), is_vec=name.startswith("gamma")))
+
+    def _get(self, i: int, which: int) -> np.ndarray:
+        b = self.blocks[i]
+        shape = (b.c1 - b.c0,) if b.is_vec else (b.r1 - b.r0, b.c1 - b.c0)
+        out = np.empty(shape, np.float32)
+        check(lib().ggb_state_param_get(self.h, i, which, _ptr(out)))
+        return out
+
+    def weights(self) -> list[np.ndarray]:
+        return [self._get(i, 0) for i in range(len(self.blocks))]
+
+    def grads(self) -> list[np.ndarray]:
+        return [self._get(i, 1) for i in range(len(self.blocks))]
+
+    def moments(self) -> tuple[list[np.ndarray], list[np.ndarray]]:
+        return ([self._get(i, 2) for i in range(len(self.blocks))],
+                [self._get(i, 3) for i in range(len(self.blocks))])
+
+    def set_weight(self, i: int, w: np.ndarray):
+        w = np.ascontiguousarray(w, np.float32)
+        check(lib().ggb_state_param_set(self.h, i, 0, _ptr(w)))
+
+    def logits(self) -> tuple[tuple[int, int, int, int], np.ndarray]:
+        dims = np.zeros(4, np.int64)
+        check(lib().ggb_state_logits(self.h, _ptr(dims), None))
+        out = np.empty((dims[1] - dims[0], dims[3] - dims[2]), np.float32)
+        check(lib().ggb_state_logits(self.h, _ptr(dims), _ptr(out)))
+        return tuple(int(x) for x in dims), out
+
+    def loss_device_ptr(self) -> int:
+        p = P()
+        check(lib().ggb_last_loss_device(self.h, C.byref(p)))
+        return int(p.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ggb_state_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def init_state(ctx: Context, cfg: ModelConfig, seed: int) -> ModelState:
+    return ModelState(ctx, cfg, seed)
+
+
+def forward(ctx: Context, st: ModelState, batch: StepBatch, prec: int, training: bool, run_seed: int,
+            global_step: int, rmsnorm_eps: float = 1e-6) -> None:
+    check(lib().ggb_forward(ctx.h, st.h, batch.h, prec, int(training), run_seed, global_step, rmsnorm_eps))
+
+
+def train_step(ctx: Context, st: ModelState, batch: StepBatch, prec: int, run_seed: int, global_step: int,
+               rmsnorm_eps: float = 1e-6, sync_loss: bool = True) -> float | None:
+    """forward + cross-entropy + backward; gradients left un-synced (model.hpp:459-478)."""
+    loss = C.c_float()
+    check(lib().ggb_train_step(ctx.h, st.h, batch.h, prec, run_seed, global_step, rmsnorm_eps,
+                               C.byref(loss) if sync_loss else None))
+    return float(loss.value) if sync_loss else None
+
+
+def dp_sync(ctx: Context, st: ModelState) -> None:
+    check(lib().ggb_dp_sync(ctx.h, st.h))
+
+
+def optimizer_step(ctx: Context, st: ModelState, optimizer: int = ADAM, lr: float = 1e-3) -> None:
+    check(lib().ggb_optimizer_step(ctx.h, st.h, optimizer, lr))
+
+
+def hash_combine(a: int, b: int) -> int:
+    """rng.hpp:17-19 (host-side seed derivation, e.g. group seeds model.hpp:620-621)."""
+    m = (1 << 64) - 1
+
+    def sm(x):
+        x = (x + 0x9E3779B97F4A7C15) & m
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+        return x ^ (x >> 31)
+
+    return sm((a ^ ((0x9E3779B97F4A7C15 + ((b << 6) & m) + (b >> 2)) & m)) & m)

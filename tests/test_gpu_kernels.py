@@ -1,0 +1,97 @@
+"""GPU numerics of the dense and sparse kernels through the C ABI against a
+plain PyTorch fp32 reference of the same op (bf16-rounded operands, fp32
+accumulation): the tcgen05 GEMMs (contract, pmm.hpp:97-130, and its
+transposed-operand forms) and the row-split SpMM (spmm, pmm.hpp:134-167)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(gg):
+    import torch
+    ctx = gg.Context()
+    return ctx, torch
+
+
+def _ld8(c):
+    return ((max(c, 1) + 7) // 8) * 8
+
+
+def _bf16_matrix(torch, rows, cols, seed, scale=1.0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    ld = _ld8(cols)
+    full = torch.zeros(rows, ld, dtype=torch.bfloat16, device="cuda")
+    full[:, :cols] = (torch.randn(rows, cols, generator=g, device="cuda") * scale).to(torch.bfloat16)
+    return full, ld
+
+
+GEMM_SHAPES = [(128, 256, 256), (1000, 256, 256), (517, 48, 256), (300, 47, 256), (4096, 256, 100),
+               (129, 16, 8), (77, 5, 24), (2000, 320, 64), (256, 256, 602), (1, 16, 16), (612, 128, 301)]
+
+
+@pytest.mark.parametrize("m,n,k", GEMM_SHAPES)
+def test_gemm_bf16(env, gg, m, n, k):
+    ctx, torch = env
+    a, lda = _bf16_matrix(torch, m, k, 1)
+    bt, ldb = _bf16_matrix(torch, n, k, 2)
+    c = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    ldcb = _ld8(n)
+    cb = torch.zeros(m, ldcb, dtype=torch.bfloat16, device="cuda")
+    gg.check(gg.lib().ggb_gemm_bf16(ctx.h, m, n, k, a.data_ptr(), lda, bt.data_ptr(), ldb, c.data_ptr(), n,
+                                    cb.data_ptr(), ldcb))
+    ctx.synchronize()
+    want = a[:, :k].float() @ bt[:, :k].float().T
+    err = (c - want).abs().max().item()
+    assert err <= 1e-3 * max(1.0, want.abs().max().item()), err
+    assert torch.equal(cb[:, :n], c.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("m,kw,nw", [(128, 128, 256), (10000, 256, 256), (612, 100, 256), (5000, 256, 47),
+                                     (333, 16, 16), (64, 8, 5), (20000, 301, 128), (1, 64, 64)])
+def test_gemm_wgrad(env, gg, m, kw, nw):
+    ctx, torch = env
+    x, ldx = _bf16_matrix(torch, m, kw, 3)
+    dy, lddy = _bf16_matrix(torch, m, nw, 4)
+    dw = torch.full((kw, nw), float("nan"), dtype=torch.float32, device="cuda")
+    gg.check(gg.lib().ggb_gemm_wgrad_bf16(ctx.h, m, kw, nw, x.data_ptr(), ldx, dy.data_ptr(), lddy, dw.data_ptr(),
+                                          nw))
+    ctx.synchronize()
+    want = x[:, :kw].float().T @ dy[:, :nw].float()
+    err = (dw - want).abs().max().item()
+    assert err <= 1e-3 * max(1.0, want.abs().max().item()), err
+
+
+def _random_csr(rows, cols, nnz_per_row, seed):
+    rng = np.random.default_rng(seed)
+    deg = rng.poisson(nnz_per_row, rows)
+    deg[rng.integers(0, rows, max(1, rows // 10))] = 0  # empty rows
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    col = np.concatenate([np.sort(rng.choice(cols, d, replace=False)) if d else np.zeros(0, np.int64)
+                          for d in np.minimum(deg, cols)]).astype(np.int32)
+    rp = np.concatenate([[0], np.cumsum(np.minimum(deg, cols))]).astype(np.int64)
+    val = rng.random(len(col)).astype(np.float32)
+    return rp, col, val
+
+
+@pytest.mark.parametrize("rows,fcols,deg", [(1000, 256, 13), (777, 128, 30), (500, 64, 5), (300, 40, 9),
+                                            (257, 16, 3), (1200, 300, 7), (64, 256, 200)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_spmm(env, gg, rows, fcols, deg, accumulate):
+    ctx, torch = env
+    frows = 900
+    rp, col, val = _random_csr(rows, frows, deg, rows + fcols)
+    f, ldf = _bf16_matrix(torch, frows, fcols, 5)
+    trp, tcol, tval = (torch.from_numpy(x).cuda() for x in (rp, col, val))
+    base = torch.randn(rows, fcols, device="cuda")
+    out = base.clone() if accumulate else torch.full((rows, fcols), float("nan"), device="cuda")
+    ldob = _ld8(fcols)
+    outb = torch.zeros(rows, ldob, dtype=torch.bfloat16, device="cuda")
+    gg.check(gg.lib().ggb_spmm_csr(ctx.h, rows, trp.data_ptr(), tcol.data_ptr(), tval.data_ptr(), f.data_ptr(), ldf,
+                                   fcols, out.data_ptr(), fcols, outb.data_ptr(), ldob, accumulate))
+    ctx.synchronize()
+    A = torch.sparse_csr_tensor(trp, tcol.long(), tval, size=(rows, frows)).to_dense()
+    want = A @ f[:, :fcols].float() + (base if accumulate else 0)
+    assert (out - want).abs().max().item() < 1e-4 * max(1.0, want.abs().max().item())
+    assert torch.equal(outb[:, :fcols], out.to(torch.bfloat16))

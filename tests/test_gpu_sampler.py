@@ -1,0 +1,193 @@
+"""GPU parity of the sampler kernels through the C ABI: bit-exact against the
+oracle restatement and against the reference compiled in place
+(sampling.cpp:11-33, shardsample.cpp:47-156, model.hpp:250-309)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KATS = [
+    ((100, 5, 7, 3), [7, 35, 43, 44, 54]),
+    ((10, 3, 555, 0), [0, 1, 5]),
+    ((1000, 8, 1, 0), [158, 205, 277, 528, 657, 698, 776, 817]),
+    ((65536, 6, 1, 0), [6604, 10460, 16125, 24862, 36307, 55068]),
+    ((2450000, 6, 9, 4), [809699, 840244, 883996, 2075223, 2216277, 2247394]),
+    ((5, 5, 123, 0), [0, 1, 2, 3, 4]),
+]
+
+
+@pytest.mark.parametrize("args,want", KATS)
+def test_sample_vertices_kat(gg, args, want):
+    assert list(gg.sample_vertices(*args).vertices) == want
+
+
+def test_sample_vertices_random_cases(gg, orc):
+    rng = np.random.default_rng(0)
+    cases = [(1, 1), (2, 1), (2, 2), (33, 33), (64, 63), (1000, 999), (4096, 1), (100000, 50000),
+             (65536, 16384)]
+    cases += [(int(n), int(rng.integers(1, n + 1))) for n in rng.integers(1, 5000, size=40)]
+    for n, b in cases:
+        seed, step = int(rng.integers(0, 2**63)), int(rng.integers(0, 1000))
+        got = gg.sample_vertices(n, b, seed, step).vertices
+        assert np.array_equal(got, orc.sample_vertices(n, b, seed, step)), (n, b, seed, step)
+
+
+def test_sample_vertices_large(gg, orc):
+    # products-shaped batch (C2): 612,500 of 2.45M
+    got = gg.sample_vertices(2_450_000, 612_500, 9, 4).vertices
+    assert np.array_equal(got, orc.sample_vertices(2_450_000, 612_500, 9, 4))
+
+
+def test_sample_vertices_errors(gg):
+    with pytest.raises(gg.InvalidArgument):
+        gg.sample_vertices(10, 0, 0, 0)
+    with pytest.raises(gg.InvalidArgument):
+        gg.sample_vertices(10, 11, 0, 0)
+
+
+def test_inclusion_frequency_uniform(gg):
+    # test_sampling.cpp:41-53 (Monte Carlo), 20k draws on the GPU
+    n, b, trials = 10, 3, 20000
+    hits = np.zeros(n)
+    for t in range(trials):
+        hits[gg.sample_vertices(n, b, 555, t).vertices] += 1
+    assert np.all(np.abs(hits / trials - 0.3) < 0.02)
+
+
+def _graph(gg, ctx, ds, layers):
+    return gg.Graph.from_csr(ctx, ds.n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels,
+                             ds.n_classes, layers)
+
+
+def _coord(dims, rank):
+    r = rank
+    z = r % dims[3]; r //= dims[3]
+    y = r % dims[2]; r //= dims[2]
+    x = r % dims[1]
+    return (r // dims[1], x, y, z)
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1, 1), (1, 2, 1, 1), (1, 2, 2, 1), (1, 2, 2, 2), (1, 3, 2, 2),
+                                  (2, 2, 1, 1), (1, 1, 1, 3)])
+def test_step_batch_bit_exact(gg, orc, ref, dims):
+    """acceptance.cpp:93-160 on the GPU: every rank's StepBatch (sample,
+    offsets, per-plane a_loc/a_t_loc with fp64 values, x_in, labels,
+    counters) equals the reference's, with no communication."""
+    n, b, layers = 3000, 700, 3
+    ds = orc.generate_synthetic(n, 12.0, 10, 6, 3)
+    h = ref.dataset_from(ds, orc.synthetic_edges(n, 12.0, 3))
+    try:
+        grid = gg.DeviceGrid(*dims)
+        for rank in range(grid.total()):
+            ctx = gg.Context(grid, rank)
+            g = _graph(gg, ctx, ds, layers)
+            batch = None
+            for seed, step in [(7, 4), (1, 0), (3, 9)]:
+                gs = orc.hash_combine(seed, grid.dp_group(rank))
+                want = ref.step_batch(h, dims, rank, layers, b, gs, step)
+                batch = gg.build_step_batch(ctx, g, b, gs, step, reuse=batch)
+                assert np.array_equal(batch.sample, want["sample"])
+                for ax in (1, 2, 3):
+                    assert np.array_equal(batch.batch_off(ax), want["batch_off"][ax])
+                for p in range(3):
+                    for t, mine in ((0, batch.a(p)), (1, batch.a_t(p))):
+                        theirs = want["planes"][p][t]
+                        assert list(theirs["dims"]) == [mine.n_rows, mine.n_cols, mine.nnz, mine.r0, mine.r1,
+                                                        mine.c0, mine.c1]
+                        c = theirs["csr"]
+                        assert np.array_equal(mine.row_ptr, c.row_ptr)
+                        assert np.array_equal(mine.col_idx, c.col_idx)
+                        assert np.array_equal(mine.values.view(np.uint64), c.values.view(np.uint64))
+                xd, x = batch.x_in
+                assert list(xd) == list(want["x_in"][0])
+                assert np.array_equal(x.view(np.uint32), want["x_in"][1].view(np.uint32))
+                assert np.array_equal(batch.labels, want["labels"])
+                assert [batch.nnz_extracted, batch.nnz_kept] == list(want["counters"])
+            del batch, g, ctx
+    finally:
+        ref.free_dataset(h)
+
+
+def test_step_batch_layers_and_edges(gg, orc, ref):
+    """Fewer than three planes, b = n (identity sample), b = 2, empty rows."""
+    n = 500
+    ds = orc.generate_synthetic(n, 3.0, 4, 3, 21)
+    h = ref.dataset_from(ds, orc.synthetic_edges(n, 3.0, 21))
+    try:
+        for dims, layers, b in [((1, 1, 1, 1), 1, n), ((1, 2, 2, 2), 2, 2), ((1, 2, 1, 2), 1, 37)]:
+            grid = gg.DeviceGrid(*dims)
+            for rank in range(grid.total()):
+                ctx = gg.Context(grid, rank)
+                g = _graph(gg, ctx, ds, layers)
+                want = ref.step_batch(h, dims, rank, layers, b, 5, 2)
+                batch = gg.build_step_batch(ctx, g, b, 5, 2)
+                assert batch.planes == len(want["planes"]) == min(layers, 3)
+                for p in range(batch.planes):
+                    for t, mine in ((0, batch.a(p)), (1, batch.a_t(p))):
+                        c = want["planes"][p][t]["csr"]
+                        assert np.array_equal(mine.row_ptr, c.row_ptr)
+                        assert np.array_equal(mine.col_idx, c.col_idx)
+                        assert np.array_equal(mine.values.view(np.uint64), c.values.view(np.uint64))
+        with pytest.raises(gg.InvalidArgument):
+            gg.build_step_batch(ctx, g, 1, 0, 0)  # build_local_minibatch: need 2 <= b <= N
+    finally:
+        ref.free_dataset(h)
+
+
+def test_nonsymmetric_csr_uses_true_transpose(gg, orc):
+    """A non-symmetric adjacency: a_t must be the stable transpose of a."""
+    n, b = 400, 150
+    rng = np.random.default_rng(3)
+    rows, cols = rng.integers(0, n, 3000), rng.integers(0, n, 3000)
+    key = np.unique(rows * n + cols)
+    r, c = key // n, key % n
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, r + 1, 1)
+    rp = np.cumsum(rp)
+    val = rng.random(len(key)) + 0.5
+    adj = orc.Csr(n, n, rp, c.astype(np.int64), val)
+    ctx = gg.Context(gg.DeviceGrid(1, 2, 2, 1), 3)
+    feats = rng.standard_normal((n, 4)).astype(np.float32)
+    g = gg.Graph.from_csr(ctx, n, rp, c, val, feats, np.zeros(n, np.int32), 2, 3, symmetric=False)
+    batch = gg.build_step_batch(ctx, g, b, 9, 1)
+    for p in range(3):
+        a, at = batch.a(p), batch.a_t(p)
+        # reference transpose: csr.cpp:74-94
+        d = np.zeros((a.n_rows, a.n_cols))
+        for i in range(a.n_rows):
+            d[i, a.col_idx[a.row_ptr[i]:a.row_ptr[i + 1]]] = a.values[a.row_ptr[i]:a.row_ptr[i + 1]]
+        dt = np.zeros((at.n_rows, at.n_cols))
+        for i in range(at.n_rows):
+            dt[i, at.col_idx[at.row_ptr[i]:at.row_ptr[i + 1]]] = at.values[at.row_ptr[i]:at.row_ptr[i + 1]]
+        assert np.array_equal(d.T, dt)
+        # and against the restatement for this rank's block
+        lay = {0: (3, 1), 1: (2, 3), 2: (1, 2)}[p]
+        co = _coord((1, 2, 2, 1), 3)
+        ro_, co_ = orc.block_partition(n, (1, 2, 2, 1)[lay[0]]), orc.block_partition(n, (1, 2, 2, 1)[lay[1]])
+        lb = orc.local_minibatch(adj, ro_[co[lay[0]]], ro_[co[lay[0]] + 1], co_[co[lay[1]]], co_[co[lay[1]] + 1],
+                                 b, 9, 1)
+        assert np.array_equal(lb.a.col_idx, a.col_idx) and np.array_equal(lb.a_t.col_idx, at.col_idx)
+        assert np.array_equal(lb.a_t.values.view(np.uint64), at.values.view(np.uint64))
+
+
+def test_native_generator_matches_reference(gg, ref):
+    """ggb_graph_generate_synthetic == reference generate_synthetic (dataset.cpp:85-131)."""
+    n, deg, d_in, ncls, seed = 5000, 14.0, 7, 5, 13
+    h = ref.dataset_synthetic(n, deg, d_in, ncls, seed)
+    try:
+        want = ref.dataset_export(h)
+        ctx = gg.Context()
+        g = gg.Graph.generate_synthetic(ctx, n, deg, d_in, ncls, seed, 3)
+        assert g.nnz == want.adj.nnz
+        # compare through a batch with b = n: the identity sample exports the
+        # full adjacency (values untouched on the diagonal, x1/p = x (n-1)/(n-1))
+        batch = gg.build_step_batch(ctx, g, n, 0, 0)
+        a = batch.a(0)
+        assert np.array_equal(a.row_ptr, want.adj.row_ptr)
+        assert np.array_equal(a.col_idx, want.adj.col_idx)
+        assert np.array_equal(a.values.view(np.uint64), want.adj.values.view(np.uint64))
+        _, x = batch.x_in
+        assert np.array_equal(x.view(np.uint32), want.features.view(np.uint32))
+        assert np.array_equal(batch.labels, want.labels)
+    finally:
+        ref.free_dataset(h)

@@ -1,0 +1,151 @@
+"""GPU parity of the training step (train_step = forward + cross-entropy +
+backward, model.hpp:459-478; dp_sync/optimizer_step, model.hpp:423-456)
+against the reference compiled in place, on the serial grid.
+
+Tolerances (BASELINE.json north star; bf16 tensor-core operands with fp32
+accumulation against the reference's fp32 path):
+  loss      |rel| <= 1e-3
+  logits    max |diff| <= 2e-2 * max(1, max |logit|)
+  gradients ||g - g_ref||_F <= 1e-2 * ||g_ref||_F  per parameter tensor
+Initial weights and Adam/SGD arithmetic are bit-exact given equal inputs.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-3
+GRAD_RTOL = 1e-2
+
+
+def _setup(gg, orc, ref, n, deg, d_in, ncls, seed, layers, grid=(1, 1, 1, 1), rank=0):
+    ds = orc.generate_synthetic(n, deg, d_in, ncls, seed)
+    h = ref.dataset_from(ds, orc.synthetic_edges(n, deg, seed))
+    ctx = gg.Context(gg.DeviceGrid(*grid), rank)
+    g = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls,
+                          layers)
+    return ds, h, ctx, g
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(np.asarray(b, np.float64)), 1e-30)
+
+
+CFGS = [
+    dict(layers=3, d_h=128, dropout_rate=0.1),
+    dict(layers=3, d_h=64, dropout_rate=0.0),
+    dict(layers=2, d_h=32, dropout_rate=0.2, use_rmsnorm=False),
+    dict(layers=4, d_h=48, dropout_rate=0.3, use_residual=False),
+    dict(layers=1, d_h=16, dropout_rate=0.1, use_dropout=False),
+    dict(layers=6, d_h=64, dropout_rate=0.2),
+]
+
+
+@pytest.mark.parametrize("cfg_kw", CFGS)
+def test_train_step_matches_reference(gg, orc, ref, cfg_kw):
+    n, d_in, ncls, b, seed, step = 4000, 24, 7, 1000, 7, 4
+    ds, h, ctx, g = _setup(gg, orc, ref, n, 10.0, d_in, ncls, 3, cfg_kw["layers"])
+    try:
+        ocfg = orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw)
+        gcfg = gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw)
+        st = gg.init_state(ctx, gcfg, seed)
+        for a, w in zip(st.weights(), ref.init_weights(ocfg, seed)):
+            assert np.array_equal(a, w)  # bit-exact init_state (model.hpp:139-149)
+        batch = gg.build_step_batch(ctx, g, b, gg.hash_combine(seed, 0), step)
+        loss = gg.train_step(ctx, st, batch, gg.FP32, seed, step)
+        losses, logits, grads, _ = ref.train(h, (1, 1, 1, 1), ocfg, b, seed, step0=step)
+        assert abs(loss - losses[0]) <= LOSS_RTOL * abs(losses[0])
+        _, lg = st.logits()
+        assert np.max(np.abs(lg - logits)) <= 2e-2 * max(1.0, np.max(np.abs(logits)))
+        for name, mine, want in zip(gcfg.param_names(), st.grads(), grads):
+            assert _rel(mine, want) <= GRAD_RTOL, (name, _rel(mine, want))
+    finally:
+        ref.free_dataset(h)
+
+
+def test_adam_trajectory_matches_reference(gg, orc, ref):
+    """Five train_run steps (model.hpp:646-685 without eval): losses and final
+    weights track the reference."""
+    n, d_in, ncls, b, seed = 3000, 16, 5, 800, 1
+    cfg_kw = dict(layers=3, d_h=64, dropout_rate=0.1)
+    ds, h, ctx, g = _setup(gg, orc, ref, n, 9.0, d_in, ncls, 2, 3)
+    try:
+        st = gg.init_state(ctx, gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), seed)
+        batch = None
+        got = []
+        for t in range(5):
+            batch = gg.build_step_batch(ctx, g, b, gg.hash_combine(seed, 0), t, reuse=batch)
+            got.append(gg.train_step(ctx, st, batch, gg.FP32, seed, t))
+            gg.dp_sync(ctx, st)
+            gg.optimizer_step(ctx, st, gg.ADAM, 1e-3)
+        losses, _, _, W = ref.train(h, (1, 1, 1, 1), orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), b, seed, 0, 5,
+                                    optimizer=1, want_weights=True)
+        assert np.all(np.abs(np.array(got) - losses) <= LOSS_RTOL * np.abs(losses))
+        for mine, want in zip(st.weights(), W):
+            assert _rel(mine, want) <= 1e-3
+    finally:
+        ref.free_dataset(h)
+
+
+def test_optimizer_arithmetic_bit_exact(gg, orc):
+    """Adam (fp64 math, fp32 store) and SGD reproduce the reference update
+    bit-for-bit from the same gradients (model.hpp:435-456)."""
+    n, d_in, ncls = 600, 8, 3
+    ds = orc.generate_synthetic(n, 6.0, d_in, ncls, 4)
+    ctx = gg.Context()
+    g = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls, 2)
+    cfg = gg.ModelConfig(layers=2, d_in=d_in, d_h=16, d_out=ncls, dropout_rate=0.1)
+    st = gg.init_state(ctx, cfg, 3)
+    batch = gg.build_step_batch(ctx, g, 200, 5, 0)
+    ps = st.weights()
+    ms = [np.zeros_like(p) for p in ps]
+    vs = [np.zeros_like(p) for p in ps]
+    for t in range(3):
+        gg.train_step(ctx, st, batch, gg.FP32, 3, t)
+        grads = st.grads()
+        gg.optimizer_step(ctx, st, gg.ADAM, 1e-3)
+        orc.adam_step(ps, grads, ms, vs, t + 1)
+        for a, w in zip(st.weights(), ps):
+            assert np.array_equal(a, w)
+    m2, v2 = st.moments()
+    for a, w in zip(m2, ms):
+        assert np.array_equal(a, w)
+    st2 = gg.init_state(ctx, cfg, 3)
+    gg.train_step(ctx, st2, batch, gg.FP32, 3, 0)
+    g0, w0 = st2.grads(), st2.weights()
+    gg.optimizer_step(ctx, st2, gg.SGD, 0.1)
+    for a, w, gr in zip(st2.weights(), w0, g0):
+        assert np.array_equal(a, (w - np.float32(0.1) * gr).astype(np.float32))
+
+
+def test_dropout_mask_matches_hash(gg, orc, ref):
+    """With identical weights, the GPU forward reproduces the reference
+    logits under dropout only if every mask bit matches
+    element_unit(key, row, col) >= rate (pmm.hpp:317-322)."""
+    n, d_in, ncls, b, seed = 2000, 12, 4, 600, 9
+    cfg_kw = dict(layers=2, d_h=32, dropout_rate=0.5)
+    ds, h, ctx, g = _setup(gg, orc, ref, n, 8.0, d_in, ncls, 6, 2)
+    try:
+        st = gg.init_state(ctx, gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), seed)
+        batch = gg.build_step_batch(ctx, g, b, gg.hash_combine(seed, 0), 2)
+        gg.train_step(ctx, st, batch, gg.FP32, seed, 2)
+        _, logits, _, _ = ref.train(h, (1, 1, 1, 1), orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), b, seed,
+                                    step0=2)
+        _, lg = st.logits()
+        assert np.max(np.abs(lg - logits)) <= 2e-2 * max(1.0, np.max(np.abs(logits)))
+    finally:
+        ref.free_dataset(h)
+
+
+def test_contract_errors(gg, orc):
+    ctx = gg.Context()
+    with pytest.raises(gg.InvalidArgument):
+        gg.init_state(ctx, gg.ModelConfig(layers=0, d_in=4, d_h=8, d_out=2), 1)
+    with pytest.raises(gg.InvalidArgument):
+        gg.init_state(ctx, gg.ModelConfig(layers=1, d_in=4, d_h=8, d_out=2, dropout_rate=1.0), 1)
+    ds = orc.generate_synthetic(300, 5.0, 4, 2, 1)
+    g = gg.Graph.from_csr(ctx, 300, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, 2, 2)
+    st = gg.init_state(ctx, gg.ModelConfig(layers=3, d_in=4, d_h=8, d_out=2), 1)
+    batch = gg.build_step_batch(ctx, g, 100, 1, 0)  # 2 planes for a 3-layer model
+    with pytest.raises(gg.CommContract):
+        gg.train_step(ctx, st, batch, gg.FP32, 1, 0)
