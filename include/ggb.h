@@ -112,6 +112,13 @@ int ggb_batch_labels(ggb_batch_t batch, int32_t* host_out);
 /* ---- model state: init_state (model.hpp:175-208) ------------------------------ */
 int ggb_state_create(ggb_ctx_t ctx, const ggb_model_config* cfg, uint64_t seed, ggb_state_t* out);
 int ggb_state_destroy(ggb_state_t st);
+/* Forward compute precision (not in the reference, whose compute is fp32):
+ * GGB_COMPUTE_ACCURATE (default) keeps forward activations fp32 (fp32 SpMM
+ * gathers, split-bf16 tensor-core GEMMs) so ReLU/dropout decisions match the
+ * fp32 reference; GGB_COMPUTE_FAST uses bf16 operands throughout. The
+ * backward pass uses bf16 operands with fp32 accumulation in both. */
+enum ggb_compute { GGB_COMPUTE_ACCURATE = 0, GGB_COMPUTE_FAST = 1 };
+int ggb_state_set_compute(ggb_state_t st, int32_t mode);
 /* parameter views in param_views order (model.hpp:107-133): win, [w_l, gamma_l]*L, wout */
 int ggb_state_num_params(ggb_state_t st);
 /* info = {global_rows, global_cols, r0, r1, c0, c1}; a gamma has rows = 1 */
@@ -139,6 +146,10 @@ int ggb_optimizer_step(ggb_ctx_t ctx, ggb_state_t st, int32_t optimizer, double 
  * c (fp32) and/or c_bf16 may be NULL. Leading dimensions in elements. */
 int ggb_gemm_bf16(ggb_ctx_t ctx, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,
                   const void* bt, int64_t ldb, float* c, int64_t ldc, void* c_bf16, int64_t ldcb);
+/* Split-bf16: fp32 operands as (hi, lo) bf16 pairs, C = (Ah+Al).(Bh+Bl)^T
+ * minus the Al.Bl term, 3 tcgen05 MMAs per k-step, fp32 accumulate. */
+int ggb_gemm_split_bf16(ggb_ctx_t ctx, int64_t m, int64_t n, int64_t k, const void* a_hi, const void* a_lo,
+                        int64_t lda, const void* bt_hi, const void* bt_lo, int64_t ldb, float* c, int64_t ldc);
 /* DW[kw x nw] = X[m x kw]^T . DY[m x nw] (contraction over the m rows). */
 int ggb_gemm_wgrad_bf16(ggb_ctx_t ctx, int64_t m, int64_t kw, int64_t nw, const void* x,
                         int64_t ldx, const void* dy, int64_t lddy, float* dw, int64_t lddw);

@@ -17,6 +17,7 @@ I32, I64, U64, F64, P = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
 GGB_OK, GGB_EINVAL, GGB_ECONTRACT, GGB_ETIMEOUT, GGB_ECUDA, GGB_ENCCL = 0, 1, 2, 3, 4, 5
 FP32, BF16_WIRE = 0, 1
 SGD, ADAM = 0, 1
+COMPUTE_ACCURATE, COMPUTE_FAST = 0, 1
 
 
 class ModelConfigC(C.Structure):
@@ -52,6 +53,7 @@ _SIGS = [
     ("ggb_batch_labels", C.c_int, [P, P]),
     ("ggb_state_create", C.c_int, [P, P, U64, P]),
     ("ggb_state_destroy", C.c_int, [P]),
+    ("ggb_state_set_compute", C.c_int, [P, I32]),
     ("ggb_state_num_params", C.c_int, [P]),
     ("ggb_state_param_info", C.c_int, [P, I32, P]),
     ("ggb_state_param_get", C.c_int, [P, I32, I32, P]),
@@ -63,6 +65,7 @@ _SIGS = [
     ("ggb_dp_sync", C.c_int, [P, P]),
     ("ggb_optimizer_step", C.c_int, [P, P, I32, F64]),
     ("ggb_gemm_bf16", C.c_int, [P, I64, I64, I64, P, I64, P, I64, P, I64, P, I64]),
+    ("ggb_gemm_split_bf16", C.c_int, [P, I64, I64, I64, P, P, I64, P, P, I64, P, I64]),
     ("ggb_gemm_wgrad_bf16", C.c_int, [P, I64, I64, I64, P, I64, P, I64, P, I64]),
     ("ggb_spmm_csr", C.c_int, [P, I64, P, P, P, P, I64, I64, P, I64, P, I64, I32]),
 ]

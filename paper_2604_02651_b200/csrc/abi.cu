@@ -449,6 +449,13 @@ int ggb_state_destroy(ggb_state_t st) {
   });
 }
 
+int ggb_state_set_compute(ggb_state_t st, int32_t mode) {
+  return guard([&] {
+    require(mode == kAccurate || mode == kFast, "compute mode must be ACCURATE or FAST");
+    st->compute = mode;
+  });
+}
+
 int ggb_state_num_params(ggb_state_t st) { return st ? static_cast<int>(st->params.size()) : -1; }
 
 int ggb_state_param_info(ggb_state_t st, int32_t idx, int64_t* info) {
@@ -555,6 +562,15 @@ int ggb_gemm_bf16(ggb_ctx_t ctx, int64_t m, int64_t n, int64_t k, const void* a,
     use_device(*ctx);
     gemm_bf16(*ctx, m, n, k, static_cast<const bf16*>(a), lda, static_cast<const bf16*>(bt), ldb, c, ldc,
               static_cast<bf16*>(c_bf16), ldcb);
+  });
+}
+
+int ggb_gemm_split_bf16(ggb_ctx_t ctx, int64_t m, int64_t n, int64_t k, const void* a_hi, const void* a_lo,
+                        int64_t lda, const void* bt_hi, const void* bt_lo, int64_t ldb, float* c, int64_t ldc) {
+  return guard([&] {
+    use_device(*ctx);
+    gemm_split(*ctx, m, n, k, static_cast<const bf16*>(a_hi), static_cast<const bf16*>(a_lo), lda,
+               static_cast<const bf16*>(bt_hi), static_cast<const bf16*>(bt_lo), ldb, c, ldc, nullptr, 0);
   });
 }
 

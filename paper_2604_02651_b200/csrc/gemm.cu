@@ -138,6 +138,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int n, bool a_mn, bool b_mn) {
 
 struct GemmArgs {
   int M, N, K;
+  int split;    // 1: operands given as bf16 hi + lo pairs, D += Ah.Bh + Ah.Bl + Al.Bh
   int BN;       // MMA N of one tile (multiple of 16, <= 256)
   int n_tiles;  // ceil(N / BN)
   int stages;
@@ -150,12 +151,15 @@ struct GemmArgs {
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_kmajor(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmBl,
                   const GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = args.stages, BN = args.BN;
+  const int parts = args.split ? 2 : 1;
   const uint32_t bytes_a = kBM * kBK * 2, bytes_b = static_cast<uint32_t>(BN) * kBK * 2;
-  const uint32_t stage_bytes = bytes_a + bytes_b;
+  // stage: [A hi][A lo]?[B hi][B lo]?
+  const uint32_t stage_bytes = parts * (bytes_a + bytes_b);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;  // [2]
@@ -170,6 +174,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (args.split) {
+      prefetch_tmap(&tmAl);
+      prefetch_tmap(&tmBl);
+    }
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
@@ -195,9 +203,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kc = 0; kc < k_chunks; ++kc) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * stage_bytes;
+          uint8_t* sb = sa + parts * bytes_a;
           mbar_expect_tx(full + stage, stage_bytes);
           tma_load_2d(sa, &tmA, full + stage, kc * kBK, mt * kBM);
-          tma_load_2d(sa + bytes_a, &tmB, full + stage, kc * kBK, nt * BN);
+          tma_load_2d(sb, &tmB, full + stage, kc * kBK, nt * BN);
+          if (args.split) {
+            tma_load_2d(sa + bytes_a, &tmAl, full + stage, kc * kBK, mt * kBM);
+            tma_load_2d(sb + bytes_b, &tmBl, full + stage, kc * kBK, nt * BN);
+          }
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -222,11 +235,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * stage_bytes);
-          const uint32_t sb = sa + bytes_a;
+          const uint32_t sb = sa + parts * bytes_a;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
-            umma_bf16(d, sdesc(sa + k * 32, 16, 1024), sdesc(sb + k * 32, 16, 1024), idesc,
-                      (kc | k) != 0);
+            const uint64_t ah = sdesc(sa + k * 32, 16, 1024), bh = sdesc(sb + k * 32, 16, 1024);
+            umma_bf16(d, ah, bh, idesc, (kc | k) != 0);
+            if (args.split) {  // the two cross terms of (Ah + Al)(Bh + Bl); Al.Bl is below fp32 rounding
+              umma_bf16(d, ah, sdesc(sb + bytes_b + k * 32, 16, 1024), idesc, 1);
+              umma_bf16(d, sdesc(sa + bytes_a + k * 32, 16, 1024), bh, idesc, 1);
+            }
           }
           umma_commit(empty + stage);
           if (++stage == S) {
@@ -484,9 +501,10 @@ int sm_count() {
 
 }  // namespace
 
-// C[m x n] = A[m x k] . Bt[n x k]^T
-void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t lda, const bf16* bt,
-               int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb) {
+// C[m x n] = A[m x k] . Bt[n x k]^T; with a_lo/bt_lo (same layouts) the
+// operands are fp32 values carried as bf16 hi + lo pairs (split-bf16).
+void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, const bf16* a_lo, int64_t lda,
+                    const bf16* bt, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb) {
   if (m <= 0 || n <= 0) return;
   require(k > 0, "gemm: k must be positive");
   require(m < (int64_t{1} << 31) && n < (int64_t{1} << 31) && k < (int64_t{1} << 31), "gemm: dims");
@@ -494,10 +512,13 @@ void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t
   ga.M = static_cast<int>(m);
   ga.N = static_cast<int>(n);
   ga.K = static_cast<int>(k);
+  ga.split = (a_lo != nullptr) ? 1 : 0;
+  require((a_lo != nullptr) == (bt_lo != nullptr), "gemm: split mode needs both lo operands");
   ga.BN = static_cast<int>(std::min<int64_t>(256, round_up(n, 16)));
   ga.n_tiles = static_cast<int>(ceil_div(n, ga.BN));
-  const int stage_bytes = kBM * kBK * 2 + ga.BN * kBK * 2;
+  const int stage_bytes = (1 + ga.split) * (kBM * kBK * 2 + ga.BN * kBK * 2);
   ga.stages = std::min(8, (kSmemBudget - 1024 - 256) / stage_bytes);
+  require(ga.stages >= 2, "gemm: tile does not fit shared memory");
   ga.tmem_cols = tmem_cols_for(2 * ga.BN);
   ga.c = c;
   ga.ldc = ldc;
@@ -505,6 +526,8 @@ void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t
   ga.ldcb = ldcb;
   const CUtensorMap ta = make_tmap(a, m, k, lda, kBK, kBM);
   const CUtensorMap tb = make_tmap(bt, n, k, ldb, kBK, ga.BN);
+  const CUtensorMap tal = ga.split ? make_tmap(a_lo, m, k, lda, kBK, kBM) : ta;
+  const CUtensorMap tbl = ga.split ? make_tmap(bt_lo, n, k, ldb, kBK, ga.BN) : tb;
   const int smem = ga.stages * stage_bytes + 1024 + 256;
   static bool attr = false;
   if (!attr) {
@@ -514,9 +537,19 @@ void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t
   }
   const int64_t tiles = ceil_div(m, kBM) * ga.n_tiles;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
-  k_gemm_kmajor<<<grid, kThreads, smem, ctx.stream>>>(ta, tb, ga);
+  k_gemm_kmajor<<<grid, kThreads, smem, ctx.stream>>>(ta, tb, tal, tbl, ga);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
+}
+
+void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t lda, const bf16* bt, int64_t ldb,
+               float* c, int64_t ldc, bf16* cb, int64_t ldcb) {
+  gemm_bf16_impl(ctx, m, n, k, a, nullptr, lda, bt, nullptr, ldb, c, ldc, cb, ldcb);
+}
+
+void gemm_split(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a_hi, const bf16* a_lo, int64_t lda,
+                const bf16* bt_hi, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb) {
+  gemm_bf16_impl(ctx, m, n, k, a_hi, a_lo, lda, bt_hi, bt_lo, ldb, c, ldc, cb, ldcb);
 }
 
 // DW[kw x nw] = X[m x kw]^T . DY[m x nw]; ws: scratch

@@ -36,13 +36,25 @@ __global__ void k_fill(float* __restrict__ x, int64_t n, float v) {
 }
 
 __global__ void k_weight_bf16(const float* __restrict__ w, int64_t rows, int64_t cols, bf16* __restrict__ wb,
-                              int64_t ldb, bf16* __restrict__ wt, int64_t ldt) {
+                              int64_t ldb, bf16* __restrict__ wt, bf16* __restrict__ wtl, int64_t ldt) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= rows * cols) return;
   const int64_t r = i / cols, c = i % cols;
   const bf16 v = __float2bfloat16_rn(w[i]);
   if (wb) wb[r * ldb + c] = v;
   if (wt) wt[c * ldt + r] = v;
+  if (wtl) wtl[c * ldt + r] = __float2bfloat16_rn(w[i] - __bfloat162float(v));
+}
+
+__global__ void k_cast_split(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                             bf16* __restrict__ hi, bf16* __restrict__ lo, int64_t ldy) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  const int64_t r = i / cols, c = i % cols;
+  const float v = x[r * ldx + c];
+  const bf16 h = __float2bfloat16_rn(v);
+  hi[r * ldy + c] = h;
+  lo[r * ldy + c] = __float2bfloat16_rn(v - __bfloat162float(h));
 }
 
 __global__ void k_cast_bf16(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
@@ -109,7 +121,11 @@ __global__ void k_fwd_apply(FwdApply p) {
     float o = y * sc;
     if (p.res) o += p.res[r * p.ldres + c];
     if (p.out) p.out[r * p.ldo + c] = o;
-    if (p.outb) p.outb[r * p.ldob + c] = __float2bfloat16_rn(o);
+    if (p.outb) {
+      const bf16 h = __float2bfloat16_rn(o);
+      p.outb[r * p.ldob + c] = h;
+      if (p.outlo) p.outlo[r * p.ldob + c] = __float2bfloat16_rn(o - __bfloat162float(h));
+    }
   }
   p.mask[r * p.ldm + c0 / 8] = static_cast<uint8_t>(bits);
 }
@@ -303,9 +319,9 @@ void fill(Ctx& ctx, float* x, int64_t n, float v) {
 }
 
 void weight_bf16(Ctx& ctx, const float* w, int64_t rows, int64_t cols, bf16* wb, int64_t ldb, bf16* wt,
-                 int64_t ldt) {
+                 bf16* wt_lo, int64_t ldt) {
   if (rows * cols <= 0) return;
-  k_weight_bf16<<<nb(rows * cols), kT, 0, ctx.stream>>>(w, rows, cols, wb, ldb, wt, ldt);
+  k_weight_bf16<<<nb(rows * cols), kT, 0, ctx.stream>>>(w, rows, cols, wb, ldb, wt, wt_lo, ldt);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
@@ -313,6 +329,13 @@ void weight_bf16(Ctx& ctx, const float* w, int64_t rows, int64_t cols, bf16* wb,
 void cast_bf16(Ctx& ctx, const float* x, int64_t rows, int64_t cols, int64_t ldx, bf16* y, int64_t ldy) {
   if (rows * cols <= 0) return;
   k_cast_bf16<<<nb(rows * cols), kT, 0, ctx.stream>>>(x, rows, cols, ldx, y, ldy);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+void cast_split(Ctx& ctx, const float* x, int64_t rows, int64_t cols, int64_t ldx, bf16* hi, bf16* lo, int64_t ldy) {
+  if (rows * cols <= 0) return;
+  k_cast_split<<<nb(rows * cols), kT, 0, ctx.stream>>>(x, rows, cols, ldx, hi, lo, ldy);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }

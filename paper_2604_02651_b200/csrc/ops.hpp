@@ -22,7 +22,8 @@ struct FwdApply {
   float keep_scale;
   float* out;  // fp32 output (nullable)
   int64_t ldo;
-  bf16* outb;  // bf16 copy (nullable)
+  bf16* outb;  // bf16 copy (nullable) = hi part of the split pair
+  bf16* outlo; // bf16 lo part (nullable): out == hi + lo to ~2^-16
   int64_t ldob;
   uint8_t* mask;  // [rows][ldm] keep bits
   int64_t ldm;
@@ -67,8 +68,10 @@ void init_weight(Ctx& ctx, float* w, int64_t rows, int64_t cols, int64_t g_rows,
                  int64_t r0, int64_t c0, uint64_t key);
 void fill(Ctx& ctx, float* x, int64_t n, float v);
 void weight_bf16(Ctx& ctx, const float* w, int64_t rows, int64_t cols, bf16* wb, int64_t ldb, bf16* wt,
-                 int64_t ldt);
+                 bf16* wt_lo, int64_t ldt);
 void cast_bf16(Ctx& ctx, const float* x, int64_t rows, int64_t cols, int64_t ldx, bf16* y, int64_t ldy);
+// y_hi = bf16(x), y_lo = bf16(x - y_hi)
+void cast_split(Ctx& ctx, const float* x, int64_t rows, int64_t cols, int64_t ldx, bf16* hi, bf16* lo, int64_t ldy);
 void add_inplace(Ctx& ctx, float* a, int64_t lda, const float* b, int64_t ldb, int64_t rows, int64_t cols);
 void rowsumsq(Ctx& ctx, const float* x, int64_t ldx, int64_t rows, int64_t cols, float* ss);
 void fwd_apply(Ctx& ctx, const FwdApply& p);
@@ -89,11 +92,18 @@ void scale(Ctx& ctx, float* x, int64_t n, float s);
 // gemm.cu
 void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t lda, const bf16* bt,
                int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb);
+// split-bf16: fp32 operands carried as (hi, lo) bf16 pairs; 3 tcgen05 MMAs per k-step
+void gemm_split(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a_hi, const bf16* a_lo, int64_t lda,
+                const bf16* bt_hi, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb);
 void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x, int64_t ldx,
                      const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws);
 // spmm.cu
 void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
               const bf16* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb,
               int64_t ldob, int accumulate);
+// fp32 feature operand; optional split-bf16 (hi, lo) outputs
+void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
+                  const float* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* out_hi,
+                  bf16* out_lo, int64_t ldob, int accumulate);
 
 }  // namespace ggb

@@ -85,7 +85,8 @@ struct Batch {
   std::vector<int> csrt_of;  // plane -> index in csrs (transposed block)
   std::vector<BatchCsr> csrs;
   int64_t x_r0 = 0, x_r1 = 0, x_c0 = 0, x_c1 = 0, x_ld = 0;
-  DevBuf x_in;    // bf16 [x_r1-x_r0][x_ld], zero padded
+  DevBuf x_in;    // bf16 [x_r1-x_r0][x_ld], zero padded (hi of the split pair)
+  DevBuf x_in_lo; // bf16 lo residual: x == hi + lo to ~2^-16
   DevBuf labels;  // int32 [b]
   uint64_t nnz_extracted = 0, nnz_kept = 0;
   const Graph* graph = nullptr;

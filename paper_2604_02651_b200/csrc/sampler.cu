@@ -220,15 +220,18 @@ __global__ void k_extract_fill(int64_t nr, const int64_t* __restrict__ sample, i
   }
 }
 
+// x_in rows: bf16 hi (+ lo residual for the split-bf16 GEMM) and/or exact fp32
 __global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t* __restrict__ sample,
                            int64_t row_lo, const float* __restrict__ feats, int64_t fld,
-                           bf16* __restrict__ xb, float* __restrict__ xf) {
+                           bf16* __restrict__ xb, bf16* __restrict__ xl, float* __restrict__ xf) {
   const int64_t r = blockIdx.x;
   if (r >= rows) return;
   const float* src = feats + sample[row_lo + r] * fld;
   for (int64_t c = threadIdx.x; c < ld; c += blockDim.x) {
     const float x = c < cols ? src[c] : 0.0f;
-    if (xb) xb[r * ld + c] = __float2bfloat16_rn(x);
+    const bf16 h = __float2bfloat16_rn(x);
+    if (xb) xb[r * ld + c] = h;
+    if (xl) xl[r * ld + c] = __float2bfloat16_rn(x - __bfloat162float(h));
     if (xf && c < cols) xf[r * cols + c] = x;
   }
 }
@@ -429,9 +432,10 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     bt.x_ld = round_up(std::max<int64_t>(cols, 1), 8);
     const int64_t rows = bt.x_r1 - bt.x_r0;
     bf16* xb = bt.x_in.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
+    bf16* xl = bt.x_in_lo.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
     if (rows > 0) {
       k_gather_x<<<static_cast<unsigned>(rows), 128, 0, s>>>(rows, cols, bt.x_ld, d_sample, bt.x_r0,
-                                                            g.features.as<float>(), cols, xb, nullptr);
+                                                            g.features.as<float>(), cols, xb, xl, nullptr);
       ctx.launches += 1;
     }
   }
@@ -446,7 +450,7 @@ void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out) {
   if (rows <= 0 || cols <= 0) return;
   k_gather_x<<<static_cast<unsigned>(rows), 128, 0, ctx.stream>>>(
       rows, cols, cols, bt.sample.as<int64_t>(), bt.x_r0, bt.graph->features.as<float>(), cols,
-      nullptr, d_out);
+      nullptr, nullptr, d_out);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }

@@ -13,22 +13,60 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kUnroll = 8;
 
-__device__ __forceinline__ void fma8(float* acc, float v, const uint4& u) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+// 8 consecutive feature values of one row: 16 B of bf16 or 32 B of fp32
+template <class T>
+struct Vec8;
+template <>
+struct Vec8<bf16> {
+  uint4 u;
+  __device__ __forceinline__ void load(const bf16* p) { u = __ldg(reinterpret_cast<const uint4*>(p)); }
+  __device__ __forceinline__ void zero() { u = make_uint4(0, 0, 0, 0); }
+  __device__ __forceinline__ void fma(float* acc, float v) const {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 f = __bfloat1622float2(h[i]);
-    acc[2 * i] = fmaf(v, f.x, acc[2 * i]);
-    acc[2 * i + 1] = fmaf(v, f.y, acc[2 * i + 1]);
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      acc[2 * i] = fmaf(v, f.x, acc[2 * i]);
+      acc[2 * i + 1] = fmaf(v, f.y, acc[2 * i + 1]);
+    }
+  }
+};
+template <>
+struct Vec8<float> {
+  float4 a, b;
+  __device__ __forceinline__ void load(const float* p) {
+    a = __ldg(reinterpret_cast<const float4*>(p));
+    b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  }
+  __device__ __forceinline__ void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ __forceinline__ void fma(float* acc, float v) const {
+    acc[0] = fmaf(v, a.x, acc[0]); acc[1] = fmaf(v, a.y, acc[1]);
+    acc[2] = fmaf(v, a.z, acc[2]); acc[3] = fmaf(v, a.w, acc[3]);
+    acc[4] = fmaf(v, b.x, acc[4]); acc[5] = fmaf(v, b.y, acc[5]);
+    acc[6] = fmaf(v, b.z, acc[6]); acc[7] = fmaf(v, b.w, acc[7]);
+  }
+};
+
+__device__ __forceinline__ void store_bf16x8(bf16* dst, const float* v, bool full, int n) {
+  if (full && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+    }
+    *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  } else {
+    for (int i = 0; i < 8 && i < n; ++i) dst[i] = __float2bfloat16_rn(v[i]);
   }
 }
 
-template <int LPR>
+template <int LPR, class TIn>
 __global__ void __launch_bounds__(kThreads)
     k_spmm(int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-           const float* __restrict__ val, const bf16* __restrict__ F, int64_t ldf, int fcols,
-           float* __restrict__ out, int64_t ldo, bf16* __restrict__ outb, int64_t ldob,
-           int accumulate) {
+           const float* __restrict__ val, const TIn* __restrict__ F, int64_t ldf, int fcols,
+           float* __restrict__ out, int64_t ldo, bf16* __restrict__ outb, bf16* __restrict__ outlo,
+           int64_t ldob, int accumulate) {
   constexpr int RPW = 32 / LPR;
   const int lane = threadIdx.x & 31;
   const int g = lane / LPR, gl = lane % LPR;
@@ -42,7 +80,7 @@ __global__ void __launch_bounds__(kThreads)
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-  const bf16* Fc = F + c0;
+  const TIn* Fc = F + c0;
   for (int64_t e = e0; e < e1; e += LPR) {
     const int64_t k = e + gl;
     int32_t mc = 0;
@@ -53,7 +91,7 @@ __global__ void __launch_bounds__(kThreads)
     }
     const int cnt = static_cast<int>(e1 - e < LPR ? e1 - e : LPR);
     for (int kk = 0; kk < cnt; kk += kUnroll) {
-      uint4 fv[kUnroll];
+      Vec8<TIn> fv[kUnroll];
       float vv[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -62,11 +100,13 @@ __global__ void __launch_bounds__(kThreads)
         const float v = __shfl_sync(gmask, mv, src, LPR);
         const bool ok = (kk + u) < cnt;
         vv[u] = ok ? v : 0.f;
-        fv[u] = (ok && col_ok) ? __ldg(reinterpret_cast<const uint4*>(Fc + static_cast<int64_t>(ci) * ldf))
-                               : make_uint4(0, 0, 0, 0);
+        if (ok && col_ok)
+          fv[u].load(Fc + static_cast<int64_t>(ci) * ldf);
+        else
+          fv[u].zero();
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) fma8(acc, vv[u], fv[u]);
+      for (int u = 0; u < kUnroll; ++u) fv[u].fma(acc, vv[u]);
     }
   }
   if (!col_ok) return;
@@ -89,32 +129,44 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
   }
-  if (outb) {
-    bf16* dst = outb + r * ldob + c0;
-    if (full8 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-      uint32_t pk[4];
+  if (outb) store_bf16x8(outb + r * ldob + c0, acc, full8, fcols - c0);
+  if (outlo) {  // residual of the bf16 rounding: acc == hi + lo to ~2^-16
+    float lo[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
-        pk[i] = *reinterpret_cast<uint32_t*>(&h2);
-      }
-      *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    } else {
-      for (int i = 0; i < 8 && c0 + i < fcols; ++i) dst[i] = __float2bfloat16_rn(acc[i]);
-    }
+    for (int i = 0; i < 8; ++i) lo[i] = acc[i] - __bfloat162float(__float2bfloat16_rn(acc[i]));
+    store_bf16x8(outlo + r * ldob + c0, lo, full8, fcols - c0);
   }
 }
 
-template <int LPR>
+template <int LPR, class TIn>
 void launch(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
-            const bf16* f, int64_t ldf, int fcols, float* out, int64_t ldo, bf16* outb, int64_t ldob,
-            int accumulate) {
+            const TIn* f, int64_t ldf, int fcols, float* out, int64_t ldo, bf16* outb, bf16* outlo,
+            int64_t ldob, int accumulate) {
   constexpr int RPB = (kThreads / 32) * (32 / LPR);
   dim3 grid(static_cast<unsigned>(ceil_div(rows, RPB)), static_cast<unsigned>(ceil_div(fcols, LPR * 8)));
-  k_spmm<LPR><<<grid, kThreads, 0, ctx.stream>>>(rows, rp, col, val, f, ldf, fcols, out, ldo, outb,
-                                                 ldob, accumulate);
+  k_spmm<LPR, TIn><<<grid, kThreads, 0, ctx.stream>>>(rows, rp, col, val, f, ldf, fcols, out, ldo, outb,
+                                                      outlo, ldob, accumulate);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
+}
+
+template <class TIn>
+void dispatch(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val, const TIn* f,
+              int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb, bf16* outlo, int64_t ldob,
+              int accumulate) {
+  if (rows <= 0 || fcols <= 0) return;
+  require(ldf % 8 == 0 && (reinterpret_cast<uintptr_t>(f) & 15) == 0,
+          "spmm: feature operand needs 16-byte aligned rows of 8-element multiples");
+  require(!(accumulate && !out), "spmm: accumulate needs an fp32 output");
+  const int fc = static_cast<int>(fcols);
+  if (fcols > 128)
+    launch<32>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, outlo, ldob, accumulate);
+  else if (fcols > 64)
+    launch<16>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, outlo, ldob, accumulate);
+  else if (fcols > 32)
+    launch<8>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, outlo, ldob, accumulate);
+  else
+    launch<4>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, outlo, ldob, accumulate);
 }
 
 }  // namespace
@@ -122,19 +174,13 @@ void launch(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const
 void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
               const bf16* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb,
               int64_t ldob, int accumulate) {
-  if (rows <= 0 || fcols <= 0) return;
-  require(ldf % 8 == 0 && (reinterpret_cast<uintptr_t>(f) & 15) == 0,
-          "spmm: feature operand needs 16-byte aligned rows");
-  require(!(accumulate && !out), "spmm: accumulate needs an fp32 output");
-  const int fc = static_cast<int>(fcols);
-  if (fcols > 128)
-    launch<32>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, ldob, accumulate);
-  else if (fcols > 64)
-    launch<16>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, ldob, accumulate);
-  else if (fcols > 32)
-    launch<8>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, ldob, accumulate);
-  else
-    launch<4>(ctx, rows, rp, col, val, f, ldf, fc, out, ldo, outb, ldob, accumulate);
+  dispatch<bf16>(ctx, rows, rp, col, val, f, ldf, fcols, out, ldo, outb, nullptr, ldob, accumulate);
+}
+
+void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
+                  const float* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* out_hi,
+                  bf16* out_lo, int64_t ldob, int accumulate) {
+  dispatch<float>(ctx, rows, rp, col, val, f, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate);
 }
 
 }  // namespace ggb

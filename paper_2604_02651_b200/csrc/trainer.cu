@@ -181,8 +181,10 @@ void state_init(Ctx& ctx, State& st, const ggb_model_config& cfg, uint64_t seed)
     if (!p.is_vec) {
       p.wb.reserve_n<bf16>(std::max<int64_t>(p.blk.rows(), 1) * p.ldb);
       p.wt.reserve_n<bf16>(std::max<int64_t>(p.blk.cols(), 1) * p.ldt);
+      p.wtl.reserve_n<bf16>(std::max<int64_t>(p.blk.cols(), 1) * p.ldt);
       GGB_CUDA(cudaMemsetAsync(p.wb.p, 0, p.wb.bytes, ctx.stream));
       GGB_CUDA(cudaMemsetAsync(p.wt.p, 0, p.wt.bytes, ctx.stream));
+      GGB_CUDA(cudaMemsetAsync(p.wtl.p, 0, p.wtl.bytes, ctx.stream));
     }
   refresh_bf16(st);
 }
@@ -192,8 +194,21 @@ void refresh_bf16(State& st) {
   for (auto& p : st.params)
     if (!p.is_vec)
       weight_bf16(ctx, st.W.as<float>() + p.off, p.blk.rows(), p.blk.cols(), p.wb.as<bf16>(), p.ldb,
-                  p.wt.as<bf16>(), p.ldt);
+                  p.wt.as<bf16>(), p.wtl.as<bf16>(), p.ldt);
 }
+
+namespace {
+
+// C = A . W (forward contract): split-bf16 in the accurate mode, bf16 otherwise.
+void fwd_gemm(State& st, int64_t m, int64_t n, int64_t k, const Tensor& a, const ParamSlot& w, float* c,
+              int64_t ldc, bf16* cb, int64_t ldcb) {
+  if (st.compute == kAccurate)
+    gemm_split(*st.ctx, m, n, k, a.b, a.lo, a.ldb, w.wt.as<bf16>(), w.wtl.as<bf16>(), w.ldt, c, ldc, cb, ldcb);
+  else
+    gemm_bf16(*st.ctx, m, n, k, a.b, a.ldb, w.wt.as<bf16>(), w.ldt, c, ldc, cb, ldcb);
+}
+
+}  // namespace
 
 // ---- forward (model.hpp:335-376) ----------------------------------------------------
 void forward(State& st, const Batch& bt, int precision, bool training, uint64_t run_seed, uint64_t global_step,
@@ -214,18 +229,25 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     contract(ob.rows() == bt.x_r1 - bt.x_r0 && w.blk.rows() == bt.x_c1 - bt.x_c0,
              "contract: local inner blocks differ");
     st.x0.blk = ob;
-    st.x0.ldf = ob.cols();
+    st.x0.ldf = ld8(ob.cols());
     st.x0.ldb = ld8(ob.cols());
     st.x0.f = grow<float>(st.x0_f, ob.rows() * st.x0.ldf);
     st.x0.b = grow<bf16>(st.x0_b, ob.rows() * st.x0.ldb);
+    // accurate: X0 stays fp32 (the next SpMM gathers fp32); fast: + bf16 operand copy
+    const bool want_b = st.compute != kAccurate;
     const bool ar = !trivial(ctx, kInputFeatureLayout.col);
-    gemm_bf16(ctx, ob.rows(), ob.cols(), w.blk.rows(), bt.x_in.as<bf16>(), bt.x_ld, w.wt.as<bf16>(), w.ldt,
-              st.x0.f, st.x0.ldf, ar ? nullptr : st.x0.b, st.x0.ldb);
+    Tensor xin;
+    xin.b = bt.x_in.as<bf16>();
+    xin.lo = bt.x_in_lo.as<bf16>();
+    xin.ldb = bt.x_ld;
+    fwd_gemm(st, ob.rows(), ob.cols(), w.blk.rows(), xin, w, st.x0.f, st.x0.ldf, (ar || !want_b) ? nullptr : st.x0.b,
+             st.x0.ldb);
     if (ar) {
       all_reduce_sum(ctx, kInputFeatureLayout.col, st.x0.f, ob.rows() * st.x0.ldf, wire);
-      cast_bf16(ctx, st.x0.f, ob.rows(), ob.cols(), st.x0.ldf, st.x0.b, st.x0.ldb);
+      if (want_b) cast_bf16(ctx, st.x0.f, ob.rows(), ob.cols(), st.x0.ldf, st.x0.b, st.x0.ldb);
     }
   }
+  const bool accurate = st.compute == kAccurate;
   if (st.layers.size() < static_cast<size_t>(cfg.layers)) st.layers.resize(cfg.layers);
   const double rate = cfg.use_dropout ? cfg.dropout_rate : 0.0;
   const bool drop = training && rate > 0.0;
@@ -253,17 +275,29 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.hagg.blk = hb;
     L.hagg.ldb = ld8(hb.cols());
     L.hagg.b = grow<bf16>(L.hagg_b, hb.rows() * L.hagg.ldb);
+    L.hagg.lo = accurate ? grow<bf16>(L.hagg_lo, hb.rows() * L.hagg.ldb) : nullptr;
     const bool ar_h = !trivial(ctx, alay.col);
+    const int64_t* arp = A.row_ptr.as<int64_t>();
+    const int32_t* acol = A.col.as<int32_t>();
+    const float* aval = A.val.as<float>();
     if (ar_h) {
-      L.hagg.ldf = hb.cols();
+      L.hagg.ldf = ld8(hb.cols());
       L.hagg.f = grow<float>(L.hagg_f, hb.rows() * L.hagg.ldf);
-      spmm_csr(ctx, A.n_rows, A.row_ptr.as<int64_t>(), A.col.as<int32_t>(), A.val.as<float>(), prev->b, prev->ldb,
-               F.cols(), L.hagg.f, L.hagg.ldf, nullptr, 0, 0);
+      if (accurate)
+        spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), L.hagg.f, L.hagg.ldf, nullptr,
+                     nullptr, 0, 0);
+      else
+        spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), L.hagg.f, L.hagg.ldf, nullptr, 0, 0);
       all_reduce_sum(ctx, alay.col, L.hagg.f, hb.rows() * L.hagg.ldf, wire);
-      cast_bf16(ctx, L.hagg.f, hb.rows(), hb.cols(), L.hagg.ldf, L.hagg.b, L.hagg.ldb);
+      if (accurate)
+        cast_split(ctx, L.hagg.f, hb.rows(), hb.cols(), L.hagg.ldf, L.hagg.b, L.hagg.lo, L.hagg.ldb);
+      else
+        cast_bf16(ctx, L.hagg.f, hb.rows(), hb.cols(), L.hagg.ldf, L.hagg.b, L.hagg.ldb);
+    } else if (accurate) {
+      spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), nullptr, 0, L.hagg.b, L.hagg.lo,
+                   L.hagg.ldb, 0);
     } else {
-      spmm_csr(ctx, A.n_rows, A.row_ptr.as<int64_t>(), A.col.as<int32_t>(), A.val.as<float>(), prev->b, prev->ldb,
-               F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
+      spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
     }
     // xw = hagg . W_l -> (A.row, third), all-reduce F.col
     const ParamSlot& w = st.params[st.wl[l - 1]];
@@ -280,8 +314,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.xw_t.blk = xb;
     L.xw_t.ldf = xb.cols();
     L.xw_t.f = grow<float>(L.xw, xb.rows() * L.xw_t.ldf);
-    gemm_bf16(ctx, xb.rows(), xb.cols(), hb.cols(), L.hagg.b, L.hagg.ldb, w.wt.as<bf16>(), w.ldt, L.xw_t.f,
-              L.xw_t.ldf, nullptr, 0);
+    fwd_gemm(st, xb.rows(), xb.cols(), hb.cols(), L.hagg, w, L.xw_t.f, L.xw_t.ldf, nullptr, 0);
     all_reduce_sum(ctx, hb.lay.col, L.xw_t.f, xb.rows() * L.xw_t.ldf, wire);
     // RMSNorm statistics: row sum of squares, all-reduce along the column axis (fp32)
     float* ss = nullptr;
@@ -317,10 +350,14 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     }
     // fused RMSNorm apply + ReLU + dropout + residual -> X_l
     L.x.blk = xb;
-    L.x.ldf = xb.cols();
+    L.x.ldf = ld8(xb.cols());
     L.x.ldb = ld8(xb.cols());
     L.x.f = grow<float>(L.x_f, xb.rows() * L.x.ldf);
-    L.x.b = grow<bf16>(L.x_b, xb.rows() * L.x.ldb);
+    // bf16 copy: next SpMM operand (fast) and, for the last layer, the
+    // out-head operand (hi + lo in the accurate mode) and dW_out operand
+    const bool last = l == cfg.layers;
+    L.x.b = (!accurate || last) ? grow<bf16>(L.x_b, xb.rows() * L.x.ldb) : nullptr;
+    L.x.lo = (accurate && last) ? grow<bf16>(L.x_lo, xb.rows() * L.x.ldb) : nullptr;
     L.ldm = ceil_div(std::max<int64_t>(xb.cols(), 1), 8);
     FwdApply fa{};
     fa.rows = xb.rows();
@@ -343,6 +380,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     fa.out = L.x.f;
     fa.ldo = L.x.ldf;
     fa.outb = L.x.b;
+    fa.outlo = L.x.lo;
     fa.ldob = L.x.ldb;
     fa.mask = grow<uint8_t>(L.mask, xb.rows() * L.ldm);
     fa.ldm = L.ldm;
@@ -364,8 +402,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     lb.c1 = w.blk.c1;
     st.logits_blk = lb;
     float* lg = grow<float>(st.logits, lb.rows() * lb.cols());
-    gemm_bf16(ctx, lb.rows(), lb.cols(), F.cols(), prev->b, prev->ldb, w.wt.as<bf16>(), w.ldt, lg, lb.cols(),
-              nullptr, 0);
+    fwd_gemm(st, lb.rows(), lb.cols(), F.cols(), *prev, w, lg, lb.cols(), nullptr, 0);
     all_reduce_sum(ctx, F.lay.col, lg, lb.rows() * lb.cols(), wire);
   }
   st.have_forward = true;

@@ -22,20 +22,27 @@ struct ParamSlot {
   Block blk;       // matrices: layout + ranges; vectors: c0/c1 (rows = 1)
   int row_axis = 0, col_axis = 0;  // vectors: VecParam axes (model.hpp:70-76)
   int64_t off = 0, n = 0;          // into the flat W/G/M/V arrays
-  int64_t ldb = 0, ldt = 0;        // bf16 copies: wb [rows][ldb], wt [cols][ldt]
-  DevBuf wb, wt;
+  int64_t ldb = 0, ldt = 0;        // bf16 copies: wb [rows][ldb], wt (+ lo) [cols][ldt]
+  DevBuf wb, wt, wtl;
 };
 
-struct Tensor {  // device activation block: fp32 and/or bf16 copy
+struct Tensor {  // device activation block: fp32 and/or bf16 copy (+ lo of the split pair)
   Block blk;
   float* f = nullptr;
   int64_t ldf = 0;
   bf16* b = nullptr;
+  bf16* lo = nullptr;
   int64_t ldb = 0;
 };
 
+/// Compute precision of the forward pass. kAccurate (default): fp32
+/// activations, fp32 SpMM gathers and split-bf16 (hi+lo, 3 MMAs) tensor-core
+/// GEMMs, so ReLU / dropout decisions match the fp32 reference; the backward
+/// pass runs on bf16 operands either way. kFast: bf16 operands throughout.
+enum Compute : int { kAccurate = 0, kFast = 1 };
+
 struct LayerBufs {
-  DevBuf hagg_f, hagg_b, xw, ss, rms, mask, x_f, x_b;
+  DevBuf hagg_f, hagg_b, hagg_lo, xw, ss, rms, mask, x_f, x_b, x_lo;
   Tensor hagg, xw_t, x;  // x = layer output X_l
   int64_t ldm = 0;
 };
@@ -44,6 +51,7 @@ struct State {
   Ctx* ctx = nullptr;
   ggb_model_config cfg{};
   uint64_t seed = 0;
+  int compute = kAccurate;
   std::vector<ParamSlot> params;  // param_views order
   int win = 0, wout = 0;
   std::vector<int> wl, gamma;

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (ADAM, BF16_WIRE, FP32, SGD, CommContract, CommTimeout, GgbError,  # noqa: F401
+from ._lib import (ADAM, BF16_WIRE, COMPUTE_ACCURATE, COMPUTE_FAST, FP32, SGD, CommContract, CommTimeout, GgbError,  # noqa: F401
                    InvalidArgument, ModelConfigC, check, lib)
 
 P = C.c_void_p
@@ -379,18 +379,24 @@ class ModelState:
     """ModelState (model.hpp:87-105) resident in HBM (fp32 master weights,
     gradients and Adam moments; bf16 operand copies for the tensor cores)."""
 
-    def __init__(self, ctx: Context, cfg: ModelConfig, seed: int):
+    def __init__(self, ctx: Context, cfg: ModelConfig, seed: int, compute: int = COMPUTE_ACCURATE):
         self.ctx = ctx
         self.cfg = cfg
         h = P()
         c = cfg.c()
         check(lib().ggb_state_create(ctx.h, C.byref(c), seed, C.byref(h)))
         self.h = h
+        self.set_compute(compute)
         self.blocks: list[ParamBlock] = []
         for i, name in enumerate(cfg.param_names()):
             info = np.zeros(6, np.int64)
             check(lib().ggb_state_param_info(h, i, _ptr(info)))
             self.blocks.append(ParamBlock(name, *(int(x) for x in info), is_vec=name.startswith("gamma")))
+
+    def set_compute(self, mode: int):
+        """COMPUTE_ACCURATE (fp32 forward activations, split-bf16 GEMMs) or COMPUTE_FAST (bf16)."""
+        check(lib().ggb_state_set_compute(self.h, mode))
+        self.compute = mode
 
     def _get(self, i: int, which: int) -> np.ndarray:
         b = self.blocks[i]
@@ -437,8 +443,8 @@ class ModelState:
             pass
 
 
-def init_state(ctx: Context, cfg: ModelConfig, seed: int) -> ModelState:
-    return ModelState(ctx, cfg, seed)
+def init_state(ctx: Context, cfg: ModelConfig, seed: int, compute: int = COMPUTE_ACCURATE) -> ModelState:
+    return ModelState(ctx, cfg, seed, compute)
 
 
 def forward(ctx: Context, st: ModelState, batch: StepBatch, prec: int, training: bool, run_seed: int,

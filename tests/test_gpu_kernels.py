@@ -48,6 +48,35 @@ def test_gemm_bf16(env, gg, m, n, k):
     assert torch.equal(cb[:, :n], c.to(torch.bfloat16))
 
 
+@pytest.mark.parametrize("m,n,k", [(1000, 256, 256), (300, 47, 256), (4096, 256, 100), (77, 5, 24),
+                                   (2000, 320, 64), (612, 128, 301)])
+def test_gemm_split_bf16_is_fp32_accurate(env, gg, m, n, k):
+    """Split-bf16 (hi + lo pairs, 3 MMAs) reproduces the fp32 product to
+    ~1e-5 relative — the forward contract of the accurate mode."""
+    ctx, torch = env
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = torch.randn(m, k, generator=g, device="cuda")
+    B = torch.randn(n, k, generator=g, device="cuda") * 0.1
+    lda, ldb = _ld8(k), _ld8(k)
+
+    def split(X, ld):
+        hi = torch.zeros(X.shape[0], ld, dtype=torch.bfloat16, device="cuda")
+        lo = torch.zeros_like(hi)
+        hi[:, :X.shape[1]] = X.to(torch.bfloat16)
+        lo[:, :X.shape[1]] = (X - hi[:, :X.shape[1]].float()).to(torch.bfloat16)
+        return hi, lo
+
+    ah, al = split(A, lda)
+    bh, bl = split(B, ldb)
+    c = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    gg.check(gg.lib().ggb_gemm_split_bf16(ctx.h, m, n, k, ah.data_ptr(), al.data_ptr(), lda, bh.data_ptr(),
+                                          bl.data_ptr(), ldb, c.data_ptr(), n))
+    ctx.synchronize()
+    want = (A.double() @ B.double().T)
+    scale = want.abs().max().item()
+    assert (c.double() - want).abs().max().item() <= 2e-5 * scale
+
+
 @pytest.mark.parametrize("m,kw,nw", [(128, 128, 256), (10000, 256, 256), (612, 100, 256), (5000, 256, 47),
                                      (333, 16, 16), (64, 8, 5), (20000, 301, 128), (1, 64, 64)])
 def test_gemm_wgrad(env, gg, m, kw, nw):
