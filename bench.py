@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the mini-batch GCN training step (BASELINE.json metric):
+GCN train epoch time on the products-shaped synthetic graph.
+
+Workload (N=1, BASELINE configs[1]): ogbn-products-shaped ER graph
+(n=2,450,000, avg degree 50.53 -> 126.2M nnz with self-loops), d_in=100,
+47 classes, 3-layer GCN, hidden 256, global batch 612,500 (N/4), epoch =
+ceil(n / batch) = 4 steps (model.hpp:539-542). A step is the reference
+train_run step body (model.hpp:646-685, without the per-epoch eval):
+build_step_batch -> forward + cross-entropy -> backward -> dp_sync ->
+optimizer_step (Adam), all through libggb.so.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C2] [--grid GdxGxxGyxGz] [--compute accurate|fast]
+
+Multi-GPU: launched by torchrun, one process per GPU; NCCL communicators are
+created inside libggb (unique id broadcast over a gloo group); the default
+grid is data-parallel (Gd = N) with the global batch split across the
+groups, so an epoch stays 4 steps (strong scaling of the epoch).
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE configs[0]: the reference's own CPU-runnable case (ER stand-in for RMAT)
+    "C1": dict(workload="synthetic ER 2^16 vertices / 1M edges, 64 feat, 3-layer GCN hidden 128",
+               n=65_536, avg_degree=30.52, d_in=64, n_classes=16, layers=3, d_h=128, batch=16_384),
+    # BASELINE configs[1]: the metric's configuration
+    "C2": dict(workload="ogbn-products-shaped synthetic (2.45M vertices, 61.9M edges, 100 feat, 47 classes), "
+                        "3-layer GCN hidden 256",
+               n=2_450_000, avg_degree=50.53, d_in=100, n_classes=47, layers=3, d_h=256, batch=612_500),
+    # BASELINE configs[2]: Reddit-shaped (2x2x2 grid on 8 GPUs in the reference plan)
+    "C3": dict(workload="Reddit-shaped synthetic (233K vertices, 114.6M edges, 602 feat, 41 classes), "
+                        "3-layer GCN hidden 256",
+               n=232_965, avg_degree=492.5, d_in=602, n_classes=41, layers=3, d_h=256, batch=58_242),
+}
+DATA_SEED, RUN_SEED, LR, DROPOUT = 7, 1, 1e-3, 0.1
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "50"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def reference_baseline(cfg: dict, steps: int, warmup: int, cores: int | None = None) -> dict:
+    """The reference CPU implementation (oracle/_ref: /root/reference compiled
+    in place) timed on this host's cores on a bounded sample of the workload:
+    same graph, model and grid rule, batch reduced by a factor f, step time
+    scaled by f (linear in the batch; this UNDERSTATES the reference's cost,
+    since its SpMM/extraction work grows with batch^2 / n)."""
+    from oracle import oracle as O
+
+    ncores = cores or os.cpu_count() or 1
+    # one std::thread per rank (train_run); the largest PMM grid <= cores, up to 3x3x3
+    best = (1, 1, 1)
+    for gx in (1, 2, 3):
+        for gy in (1, 2, 3):
+            for gz in (1, 2, 3):
+                if gx * gy * gz <= ncores and gx * gy * gz > best[0] * best[1] * best[2]:
+                    best = (gx, gy, gz)
+    dims = (1, *best)
+    target = 20_000  # rows per sampled step: a few seconds of reference work on ~8 cores
+    f = max(1, cfg["batch"] // target)
+    b_s = max(2, cfg["batch"] // f)
+    R = O.Ref()
+    t0 = time.time()
+    h = R.dataset_synthetic(cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"], DATA_SEED)
+    t_data = time.time() - t0
+    try:
+        mcfg = O.ModelConfig(layers=cfg["layers"], d_in=cfg["d_in"], d_h=cfg["d_h"], d_out=cfg["n_classes"],
+                             dropout_rate=DROPOUT)
+        step_ms, phase = R.bench(h, dims, mcfg, b_s, RUN_SEED, warmup, steps)
+    finally:
+        R.free_dataset(h)
+    S = math.ceil(cfg["n"] / cfg["batch"])
+    mean_ms = float(sum(step_ms) / len(step_ms))
+    full_step_s = mean_ms / 1000.0 * f
+    return {
+        "epoch_time_s": S * full_step_s,
+        "cores": best[0] * best[1] * best[2],
+        "grid": "1x%dx%dx%d" % best,
+        "sample": (f"reference train_run step body (sample->fwd+CE->bwd->dp_sync->Adam) on grid 1x{best[0]}x{best[1]}"
+                   f"x{best[2]} ({best[0]*best[1]*best[2]} threads of {ncores} host cores), batch {b_s} = global "
+                   f"batch/{f}, {steps} timed steps after {warmup} warm-up: {mean_ms:.0f} ms/step, scaled x{f} "
+                   f"to the full batch (linear; understates the reference), x{S} steps/epoch; dataset build "
+                   f"{t_data:.0f}s excluded"),
+        "phase_ms": [float(x) for x in phase],
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--grid", default=None, help="GdxGxxGyxGz (default: data-parallel Gd = N)")
+    ap.add_argument("--compute", default="accurate", choices=["accurate", "fast"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-steps", type=int, default=2)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = max(args.gpus, world)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        # each reference step is a bounded sample (seconds of CPU work); cap the count
+        # so the whole run stays within a few minutes
+        steps_run, warm_run = max(1, min(args.steps, 3)), min(args.warmup, 1)
+        rb = reference_baseline(cfg, steps_run, warm_run)
+        S = math.ceil(cfg["n"] / cfg["batch"])
+        v = rb["epoch_time_s"]
+        print(json.dumps({
+            "impl": "reference", "metric": "epoch_time_s", "value": v, "unit": "s", "n_gpus": n_gpus,
+            "steps": steps_run, "warmup": warm_run, "ms_per_step": v / S * 1000.0, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "steps_per_epoch": S,
+                       "grid": rb["grid"]},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": rb["cores"], "kind": "reference",
+                             "sample": rb["sample"]},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }), flush=True)
+        return
+
+    import torch
+
+    from paper_2604_02651_b200 import gridgnn as gg
+
+    dims = tuple(int(x) for x in args.grid.lower().split("x")) if args.grid else (world, 1, 1, 1)
+    grid = gg.DeviceGrid(*dims)
+    assert grid.total() == world, f"grid {dims} needs {grid.total()} ranks, have {world}"
+    torch.cuda.set_device(local_rank)
+    pg = None
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        pg = dist
+        obj = [gg.get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.Stream()  # a real stream: libggb launches on it, torch events bracket it
+    torch.cuda.set_stream(stream)
+    ctx = gg.Context(grid, rank, device=local_rank, nccl_uid=uid, stream=stream.cuda_stream)
+
+    t0 = time.time()
+    graph = gg.Graph.generate_synthetic(ctx, cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"], DATA_SEED,
+                                        cfg["layers"])
+    t_graph = time.time() - t0
+    gd = dims[0]
+    b = cfg["batch"] // gd  # per data-parallel group: the global batch stays fixed
+    S = math.ceil(cfg["n"] / (b * gd))
+    mcfg = gg.ModelConfig(layers=cfg["layers"], d_in=cfg["d_in"], d_h=cfg["d_h"], d_out=cfg["n_classes"],
+                          dropout_rate=DROPOUT)
+    st = gg.init_state(ctx, mcfg, RUN_SEED, gg.COMPUTE_ACCURATE if args.compute == "accurate" else gg.COMPUTE_FAST)
+    group_seed = gg.hash_combine(RUN_SEED, grid.dp_group(rank))
+    batch = None
+
+    def step(gstep: int, sync_loss: bool):
+        nonlocal batch
+        batch = gg.build_step_batch(ctx, graph, b, group_seed, gstep, reuse=batch)
+        loss = gg.train_step(ctx, st, batch, gg.FP32, RUN_SEED, gstep, sync_loss=sync_loss)
+        gg.dp_sync(ctx, st)
+        gg.optimizer_step(ctx, st, gg.ADAM, LR)
+        return loss
+
+    def barrier():
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not pg:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    gstep = 0
+    for _ in range(args.warmup):
+        step(gstep, False)
+        gstep += 1
+    # ---- timed region: device-resident inputs, loss stays on the device
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.1)
+    barrier()
+    ctx.profile(True)
+    ctx.profile_read(reset=True)
+    c0 = ctx.counters()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(gstep, False)
+        gstep += 1
+    ev1.record(stream)
+    barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    c1 = ctx.counters()
+    prof = ctx.profile_read(reset=True)
+    ctx.profile(False)
+    # ---- e2e: the reference-facing call pattern, the loss read back to the host every step
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    losses = []
+    for _ in range(args.steps):
+        losses.append(step(gstep, True))
+        gstep += 1
+    e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    c2 = ctx.counters()
+    clk = clocks.stop()
+
+    if rank != 0:
+        if pg:
+            pg.barrier()
+        return
+
+    ms_step = ms_total / args.steps
+    epoch_s = S * ms_step / 1000.0
+    hbm, bf16_burst, bf16_sust, peak_kind = _peaks()
+    # dominant kernel class of the step
+    kernels = {k: v for k, v in prof.items() if v["launches"] > 0}
+    dom_name, dom = max(kernels.items(), key=lambda kv: kv[1]["ms"])
+    tensor_bound = dom_name.startswith("gemm") and dom["flops"] / max(dom["bytes"], 1) > 200
+    per_launch_ms = dom["ms"] / dom["launches"]
+    if tensor_bound:
+        achieved = dom["flops"] / (dom["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": bf16_sust, "unit": "TFLOP/s"}
+    else:
+        achieved = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = dom_name
+    roof["peak_source"] = peak_kind
+    roof["bytes_per_launch"] = dom["bytes"] / dom["launches"]
+    roof["ms_per_launch"] = per_launch_ms
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(dom_name)
+    except Exception:
+        pass
+    roof["traffic"] = traffic
+    breakdown = {k: {"ms_per_step": v["ms"] / args.steps,
+                     "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
+                     "TFLOP_per_s": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None,
+                     "launches_per_step": v["launches"] / args.steps}
+                 for k, v in kernels.items()}
+    out = {
+        "metric": "epoch_time_s",
+        "value": epoch_s,
+        "unit": "s",
+        "n_gpus": n_gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic",
+        "config": {
+            "workload": cfg["workload"], "config_id": args.config, "global_batch": cfg["batch"],
+            "batch_per_dp_group": b, "steps_per_epoch": S, "grid": "x".join(map(str, dims)),
+            "layers": cfg["layers"], "hidden": cfg["d_h"], "d_in": cfg["d_in"], "classes": cfg["n_classes"],
+            "n_vertices": cfg["n"], "nnz": graph.nnz, "compute": args.compute,
+            "l2": "inputs larger than L2 (graph %.1f GB + features resident in HBM; random gathers)" %
+                  (graph.device_bytes / 1e9),
+            "optimizer": "adam lr 1e-3", "dropout": DROPOUT, "eval": "excluded (per SURVEY 8d)",
+        },
+        "iters_per_s": 1000.0 / ms_step,
+        "sampled_vertices_per_s": b * gd * 1000.0 / ms_step,
+        "roofline": roof,
+        "kernels": breakdown,
+        "e2e": {"value": S * ms_e2e / args.steps / 1000.0, "unit": "s",
+                "h2d_bytes_per_step": (c2["h2d_bytes"] - c1["h2d_bytes"]) / args.steps,
+                "d2h_bytes_per_step": (c2["d2h_bytes"] - c1["d2h_bytes"]) / args.steps,
+                "ms_per_step": ms_e2e / args.steps,
+                "note": "C-ABI loop with the loss read back to the host each step; graph/features uploaded once"},
+        "gpu_launches": c1["launches"] - c0["launches"],
+        "clocks": clk,
+        "loss_last": losses[-1] if losses else None,
+        "graph_build_s": t_graph,
+    }
+    if not args.no_cpu_baseline and n_gpus == 1:
+        try:
+            rb = reference_baseline(cfg, args.ref_steps, 1)
+            out["cpu_baseline"] = {"value": rb["epoch_time_s"], "unit": "s", "cores": rb["cores"],
+                                   "kind": "reference", "sample": rb["sample"]}
+        except Exception as e:  # the baseline is reported, never required
+            out["cpu_baseline"] = {"value": None, "unit": "s", "cores": None, "kind": "reference",
+                                   "sample": f"unavailable: {e}"}
+    print(json.dumps(out), flush=True)
+    if pg:
+        pg.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -66,8 +66,17 @@ int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const ui
 int ggb_ctx_destroy(ggb_ctx_t ctx);
 int ggb_ctx_set_stream(ggb_ctx_t ctx, void* stream);
 int ggb_ctx_synchronize(ggb_ctx_t ctx);
-/* counters[0] = kernels this library launched on ctx since creation */
+/* counters = {kernels launched on ctx since creation, host->device bytes,
+ * device->host bytes} */
 int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters);
+/* Per-kernel-class timing with CUDA events on the ctx stream. Classes:
+ * 0 sampling, 1 SpMM fwd, 2 SpMM bwd, 3 GEMM fwd, 4 GEMM dX, 5 GEMM dW,
+ * 6 element-wise (RMSNorm/ReLU/dropout/CE), 7 optimizer, 8 collectives.
+ * read: totals since the last reset of time (ms), algorithmic bytes, flops
+ * and launch counts (arrays of 9). */
+int ggb_ctx_profile(ggb_ctx_t ctx, int32_t enable);
+int ggb_ctx_profile_read(ggb_ctx_t ctx, double* ms, double* bytes, double* flops, int64_t* counts,
+                         int32_t reset);
 
 /* ---- sampler: sample_vertices (sampling.cpp:11-33) ------------------------- */
 int ggb_sample_vertices(ggb_ctx_t ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step,

@@ -38,6 +38,8 @@ _SIGS = [
     ("ggb_ctx_set_stream", C.c_int, [P, P]),
     ("ggb_ctx_synchronize", C.c_int, [P]),
     ("ggb_ctx_counters", C.c_int, [P, P]),
+    ("ggb_ctx_profile", C.c_int, [P, I32]),
+    ("ggb_ctx_profile_read", C.c_int, [P, P, P, P, P, I32]),
     ("ggb_sample_vertices", C.c_int, [P, I64, I64, U64, U64, P]),
     ("ggb_graph_create", C.c_int, [P, I64, P, P, P, I32, I64, P, I64, P, I32, P]),
     ("ggb_graph_generate_synthetic", C.c_int, [P, I64, F64, I64, I64, U64, I32, P]),

@@ -8,6 +8,7 @@
 
 #include "comm.hpp"
 #include "dataset.hpp"
+#include "prof.hpp"
 #include "trainer.hpp"
 
 struct ggb_ctx_s : ggb::Ctx {};
@@ -19,7 +20,30 @@ namespace ggb {
 
 Ctx::~Ctx() {
   comm.reset();
+  prof.reset();
   if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+Prof& prof_of(Ctx& ctx) {
+  if (!ctx.prof) ctx.prof = std::make_unique<Prof>();
+  return *ctx.prof;
+}
+
+void prof_collect(Ctx& ctx) {
+  Prof& p = prof_of(ctx);
+  if (p.marks.empty()) return;
+  GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+  for (auto& m : p.marks) {
+    float ms = 0.f;
+    GGB_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+    p.ms[m.cat] += ms;
+    p.bytes[m.cat] += m.bytes;
+    p.flops[m.cat] += m.flops;
+    p.count[m.cat] += 1;
+    p.pool.push_back(m.a);
+    p.pool.push_back(m.b);
+  }
+  p.marks.clear();
 }
 
 namespace {
@@ -281,7 +305,37 @@ int ggb_ctx_synchronize(ggb_ctx_t ctx) {
 }
 
 int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters) {
-  return guard([&] { counters[0] = ctx->launches; });
+  return guard([&] {
+    counters[0] = ctx->launches;
+    counters[1] = ctx->h2d_bytes;
+    counters[2] = ctx->d2h_bytes;
+  });
+}
+
+int ggb_ctx_profile(ggb_ctx_t ctx, int32_t enable) {
+  return guard([&] {
+    use_device(*ctx);
+    prof_collect(*ctx);
+    prof_of(*ctx).on = enable != 0;
+  });
+}
+
+int ggb_ctx_profile_read(ggb_ctx_t ctx, double* ms, double* bytes, double* flops, int64_t* counts, int32_t reset) {
+  return guard([&] {
+    use_device(*ctx);
+    prof_collect(*ctx);
+    Prof& p = prof_of(*ctx);
+    for (int c = 0; c < kProfCats; ++c) {
+      if (ms) ms[c] = p.ms[c];
+      if (bytes) bytes[c] = p.bytes[c];
+      if (flops) flops[c] = p.flops[c];
+      if (counts) counts[c] = p.count[c];
+      if (reset) {
+        p.ms[c] = p.bytes[c] = p.flops[c] = 0.0;
+        p.count[c] = 0;
+      }
+    }
+  });
 }
 
 int ggb_sample_vertices(ggb_ctx_t ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* host_out) {
@@ -510,7 +564,10 @@ int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precis
     forward(*st, *bt, precision, true, run_seed, global_step, rmsnorm_eps);
     cross_entropy(*st, *bt);
     backward(*st, *bt, precision);
-    if (loss_out) download(loss_out, st->loss.p, 1, ctx->stream);
+    if (loss_out) {
+      download(loss_out, st->loss.p, 1, ctx->stream);
+      ctx->d2h_bytes += sizeof(float);
+    }
   });
 }
 

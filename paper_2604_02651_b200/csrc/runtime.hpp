@@ -9,7 +9,8 @@
 
 namespace ggb {
 
-struct Comm;  // comm.cpp (NCCL per-axis communicators)
+struct Comm;  // comm.cu (NCCL per-axis communicators)
+struct Prof;  // prof.hpp (per-kernel-class event timing)
 
 /// Sampler scratch, reused across steps (one build at a time per context).
 struct SamplerWork {
@@ -36,8 +37,10 @@ struct Ctx {
   bool own_stream = false;
   std::unique_ptr<Comm> comm;
   SamplerWork sw;
-  uint64_t launches = 0;
+  uint64_t launches = 0;              // kernels this library launched
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of the step path
   int num_sms = 148;
+  std::unique_ptr<Prof> prof;
   ~Ctx();
 };
 

@@ -31,6 +31,7 @@
 // stable csr_transpose order.
 #include <cmath>
 
+#include "prof.hpp"
 #include "rng.cuh"
 #include "runtime.hpp"
 
@@ -323,6 +324,7 @@ void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t
 void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
                       Batch& bt) {
   require(b >= 2 && b <= g.n, "build_local_minibatch: need 2 <= b <= N");
+  ProfScope prof(ctx, kProfSample);
   cudaStream_t s = ctx.stream;
   bt.ctx = &ctx;
   bt.graph = &g;
@@ -348,6 +350,8 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
                             dmisc + m);
   ctx.launches += 1;
   GGB_CUDA(cudaMemcpyAsync(hmisc + m, dmisc + m, m * 8, cudaMemcpyDeviceToHost, s));
+  ctx.h2d_bytes += m * 8;
+  ctx.d2h_bytes += m * 8;
   GGB_CUDA(cudaStreamSynchronize(s));
   {
     int k = 0;
@@ -407,6 +411,7 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     GGB_CUDA(cudaMemcpyAsync(hmisc + k, bt.csrs[k].row_ptr.as<int64_t>() + bt.csrs[k].n_rows, 8,
                              cudaMemcpyDeviceToHost, s));
   GGB_CUDA(cudaMemcpyAsync(hmisc + nk, d_ext, 8 * nk, cudaMemcpyDeviceToHost, s));
+  ctx.d2h_bytes += 16 * nk;
   GGB_CUDA(cudaStreamSynchronize(s));
   for (size_t k = 0; k < nk; ++k) bt.csrs[k].nnz = hmisc[k];
   // counters as build_step_batch accumulates them (model.hpp:265-268): one
@@ -443,6 +448,17 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
   k_gather_labels<<<blocks(b), kThreads, 0, s>>>(b, d_sample, g.labels.as<int32_t>(), lab);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
+  // algorithmic bytes: draws/links/bitmap over b, the bitmap and
+  // its prefix over n/32 words, per block the sampled row pointers, the
+  // extracted column ids, the kept entries (fp64 value read; int32 col, fp32
+  // and fp64 value writes), the feature gather and the labels.
+  double bytes = 8.0 * b * 4 + (g.n / 32.0) * 12;
+  for (size_t k = 0; k < nk; ++k) {
+    const BatchCsr& c = bt.csrs[k];
+    bytes += c.n_rows * 16.0 * 2 + static_cast<double>(hmisc[nk + k]) * 4.0 * 2 + c.nnz * (8.0 + 4 + 4 + 8);
+  }
+  bytes += static_cast<double>(bt.x_r1 - bt.x_r0) * (bt.x_c1 - bt.x_c0) * (4 + 2 + 2) + b * 12.0;
+  prof.bytes = bytes;
 }
 
 void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out) {

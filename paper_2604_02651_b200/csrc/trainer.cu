@@ -7,6 +7,7 @@
 #include <cmath>
 
 #include "comm.hpp"
+#include "prof.hpp"
 #include "rng.cuh"
 #include "trainer.hpp"
 
@@ -199,9 +200,24 @@ void refresh_bf16(State& st) {
 
 namespace {
 
+// Algorithmic traffic of one SpMM launch (SURVEY §8d gather model): the CSR
+// (int32 col + fp32 val per nonzero, int64 row pointers), one e_in-byte
+// feature row per nonzero, and the output rows (e_out bytes per element).
+double spmm_bytes(int64_t rows, int64_t nnz, int64_t cols, int e_in, int e_out) {
+  return static_cast<double>(nnz) * 8.0 + static_cast<double>(rows + 1) * 8.0 +
+         static_cast<double>(nnz) * cols * e_in + static_cast<double>(rows) * cols * e_out;
+}
+
+double gemm_bytes(int64_t m, int64_t n, int64_t k, int ea, int eb, int ec) {
+  return static_cast<double>(m) * k * ea + static_cast<double>(n) * k * eb + static_cast<double>(m) * n * ec;
+}
+
 // C = A . W (forward contract): split-bf16 in the accurate mode, bf16 otherwise.
 void fwd_gemm(State& st, int64_t m, int64_t n, int64_t k, const Tensor& a, const ParamSlot& w, float* c,
               int64_t ldc, bf16* cb, int64_t ldcb) {
+  const int e = st.compute == kAccurate ? 4 : 2;
+  ProfScope ps(*st.ctx, kProfGemmFwd, gemm_bytes(m, n, k, e, e, 4 + (cb ? 2 : 0)),
+               2.0 * m * n * k * (st.compute == kAccurate ? 3 : 1));
   if (st.compute == kAccurate)
     gemm_split(*st.ctx, m, n, k, a.b, a.lo, a.ldb, w.wt.as<bf16>(), w.wtl.as<bf16>(), w.ldt, c, ldc, cb, ldcb);
   else
@@ -280,6 +296,10 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     const int64_t* arp = A.row_ptr.as<int64_t>();
     const int32_t* acol = A.col.as<int32_t>();
     const float* aval = A.val.as<float>();
+    {
+    ProfScope ps(ctx, kProfSpmmFwd,
+                 spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, ar_h ? 4 : (accurate ? 4 : 2)),
+                 2.0 * A.nnz * F.cols());
     if (ar_h) {
       L.hagg.ldf = ld8(hb.cols());
       L.hagg.f = grow<float>(L.hagg_f, hb.rows() * L.hagg.ldf);
@@ -298,6 +318,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
                    L.hagg.ldb, 0);
     } else {
       spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
+    }
     }
     // xw = hagg . W_l -> (A.row, third), all-reduce F.col
     const ParamSlot& w = st.params[st.wl[l - 1]];
@@ -323,6 +344,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     if (cfg.use_rmsnorm) {
       ss = grow<float>(L.ss, xb.rows());
       rms = grow<float>(L.rms, xb.rows());
+      ProfScope ps(ctx, kProfElementwise, 4.0 * xb.rows() * xb.cols());
       rowsumsq(ctx, L.xw_t.f, L.xw_t.ldf, xb.rows(), xb.cols(), ss);
       all_reduce_sum(ctx, xb.lay.col, ss, xb.rows(), false);
       const ParamSlot& gp = st.params[st.gamma[l - 1]];
@@ -384,7 +406,11 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     fa.ldob = L.x.ldb;
     fa.mask = grow<uint8_t>(L.mask, xb.rows() * L.ldm);
     fa.ldm = L.ldm;
-    fwd_apply(ctx, fa);
+    {
+      const double e = static_cast<double>(xb.rows()) * xb.cols();
+      ProfScope ps(ctx, kProfElementwise, e * (4 + (res ? 4 : 0) + 4 + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0)) + e / 8);
+      fwd_apply(ctx, fa);
+    }
     prev = &L.x;
   }
   // logits = X_L . W_out, all-reduce X_L.col
@@ -427,6 +453,7 @@ void cross_entropy(State& st, const Batch& bt) {
   c.lddlogb = ld8(c.cols);
   c.loss_part = grow<float>(st.ce_part, ce_grad_blocks(c.rows) + 1);
   c.loss_acc = grow<float>(st.loss_acc, 1);
+  ProfScope ps(ctx, kProfElementwise, static_cast<double>(c.rows) * c.cols * (3 * 4 + 2));
   ce_rowmax(ctx, c);
   all_reduce_max(ctx, lb.lay.col, c.mx, c.rows);
   ce_rowsum(ctx, c);
@@ -454,8 +481,12 @@ void backward(State& st, const Batch& bt, int precision) {
   // dW_out = X_L^T . dlogits, all-reduce X_L.row
   {
     const ParamSlot& w = st.params[st.wout];
-    gemm_wgrad_bf16(ctx, lb.rows(), XL.blk.cols(), lb.cols(), XL.b, XL.ldb, st.dlog_b.as<bf16>(), lddlog,
-                    G + w.off, w.blk.cols(), st.ws_wgrad);
+    {
+      ProfScope ps(ctx, kProfGemmWgrad, gemm_bytes(XL.blk.cols(), lb.cols(), lb.rows(), 2, 2, 4),
+                   2.0 * lb.rows() * XL.blk.cols() * lb.cols());
+      gemm_wgrad_bf16(ctx, lb.rows(), XL.blk.cols(), lb.cols(), XL.b, XL.ldb, st.dlog_b.as<bf16>(), lddlog,
+                      G + w.off, w.blk.cols(), st.ws_wgrad);
+    }
     all_reduce_sum(ctx, XL.blk.lay.row, G + w.off, w.n, wire);
   }
   // dxh = dlogits . W_out^T -> (X_L.row, X_L.col), all-reduce logits.col
@@ -463,6 +494,8 @@ void backward(State& st, const Batch& bt, int precision) {
   float* dxh = grow<float>(st.dxh, db.rows() * db.cols());
   {
     const ParamSlot& w = st.params[st.wout];
+    ProfScope ps(ctx, kProfGemmDx, gemm_bytes(db.rows(), db.cols(), lb.cols(), 2, 2, 4),
+                 2.0 * db.rows() * db.cols() * lb.cols());
     gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, dxh,
               db.cols(), nullptr, 0);
     all_reduce_sum(ctx, lb.lay.col, dxh, db.rows() * db.cols(), wire);
@@ -499,6 +532,9 @@ void backward(State& st, const Batch& bt, int precision) {
     const int64_t lddxw = ld8(cols);
     ba.dxb = grow<bf16>(st.dxw_b, rows * lddxw);
     ba.lddxb = lddxw;
+    {
+    // reads dy + xw twice (stats, apply) + mask, writes dxw bf16
+    ProfScope ps(ctx, kProfElementwise, static_cast<double>(rows) * cols * (2 * 8 + 2) + rows * cols / 4.0);
     if (cfg.use_rmsnorm) {
       const ParamSlot& gp = st.params[st.gamma[l - 1]];
       ba.gamma = W + gp.off;
@@ -514,17 +550,24 @@ void backward(State& st, const Batch& bt, int precision) {
     } else {
       bwd_apply(ctx, ba, bwd_apply_blocks(ctx, rows, cols));
     }
+    }
     // dW_l = hagg^T . dxw, all-reduce hagg.row
     const ParamSlot& w = st.params[st.wl[l - 1]];
     const Tensor& hg = L.hagg;
-    gemm_wgrad_bf16(ctx, rows, hg.blk.cols(), cols, hg.b, hg.ldb, ba.dxb, lddxw, G + w.off, w.blk.cols(),
-                    st.ws_wgrad);
+    {
+      ProfScope ps(ctx, kProfGemmWgrad, gemm_bytes(hg.blk.cols(), cols, rows, 2, 2, 4),
+                   2.0 * rows * hg.blk.cols() * cols);
+      gemm_wgrad_bf16(ctx, rows, hg.blk.cols(), cols, hg.b, hg.ldb, ba.dxb, lddxw, G + w.off, w.blk.cols(),
+                      st.ws_wgrad);
+    }
     all_reduce_sum(ctx, hg.blk.lay.row, G + w.off, w.n, wire);
     // dhagg = dxw . W_l^T -> (xw.row, hagg.col), all-reduce xw.col
     const int64_t hc = hg.blk.cols();
     const bool ar_d = !trivial(ctx, xb.lay.col);
     const int64_t ldhb = ld8(hc);
     bf16* dhb = grow<bf16>(st.dhagg_b, rows * ldhb);
+    {
+    ProfScope ps(ctx, kProfGemmDx, gemm_bytes(rows, hc, cols, 2, 2, ar_d ? 4 : 2), 2.0 * rows * hc * cols);
     if (ar_d) {
       float* dhf = grow<float>(st.dhagg_f, rows * hc);
       gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, dhf, hc, nullptr, 0);
@@ -533,13 +576,16 @@ void backward(State& st, const Batch& bt, int precision) {
     } else {
       gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, nullptr, 0, dhb, ldhb);
     }
+    }
     // dxh = A_t . dhagg (+ dres) -> (A.col, hagg.col) = F's layout, all-reduce A.row
     const int p = (l - 1) % 3;
     const BatchCsr& At = bt.csrs[bt.csrt_of[p]];
     const Layout alay = adjacency_layout(l);
     contract(At.c0 == hg.blk.r0 && At.c1 == hg.blk.r1, "spmm: inner partitions differ");
     const bool ar_s = !trivial(ctx, alay.row);
-    if (pmm_trivial(ctx) && cfg.use_residual) {
+    const bool inplace = pmm_trivial(ctx) && cfg.use_residual;
+    ProfScope ps(ctx, kProfSpmmBwd, spmm_bytes(At.n_rows, At.nnz, hc, 2, inplace ? 8 : 4), 2.0 * At.nnz * hc);
+    if (inplace) {
       // dxh (== dres) += A_t . dhagg
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
                dxh, F.cols(), nullptr, 0, 1);
@@ -560,9 +606,14 @@ void backward(State& st, const Batch& bt, int precision) {
     const int64_t rows = db.rows(), cols = db.cols();
     const int64_t ldb = ld8(cols);
     bf16* dxb = grow<bf16>(st.dxh_b, rows * ldb);
-    cast_bf16(ctx, dxh, rows, cols, cols, dxb, ldb);
-    gemm_wgrad_bf16(ctx, rows, bt.x_c1 - bt.x_c0, cols, bt.x_in.as<bf16>(), bt.x_ld, dxb, ldb, G + w.off,
-                    w.blk.cols(), st.ws_wgrad);
+    {
+      ProfScope ps(ctx, kProfElementwise, static_cast<double>(rows) * cols * 6);
+      cast_bf16(ctx, dxh, rows, cols, cols, dxb, ldb);
+    }
+    const int64_t kin = bt.x_c1 - bt.x_c0;
+    ProfScope ps(ctx, kProfGemmWgrad, gemm_bytes(kin, cols, rows, 2, 2, 4), 2.0 * rows * kin * cols);
+    gemm_wgrad_bf16(ctx, rows, kin, cols, bt.x_in.as<bf16>(), bt.x_ld, dxb, ldb, G + w.off, w.blk.cols(),
+                    st.ws_wgrad);
     all_reduce_sum(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
   }
 }
@@ -571,6 +622,7 @@ void backward(State& st, const Batch& bt, int precision) {
 void dp_sync(State& st) {
   Ctx& ctx = *st.ctx;
   const int gd = ctx.grid.dims[0];
+  ProfScope ps(ctx, kProfComm, gd > 1 ? 2.0 * (gd - 1) / gd * st.total * 4 : 0.0);
   all_reduce_sum(ctx, kD, st.G.as<float>(), st.total, false);
   if (gd > 1) scale(ctx, st.G.as<float>(), st.total, 1.0f / static_cast<float>(gd));
 }
@@ -579,6 +631,7 @@ void dp_sync(State& st) {
 void optimizer_step(State& st, int optimizer, double lr) {
   Ctx& ctx = *st.ctx;
   st.opt_step += 1;
+  ProfScope ps(ctx, kProfOptimizer, static_cast<double>(st.total) * 4 * 7);
   if (optimizer == GGB_SGD) {
     sgd(ctx, st.W.as<float>(), st.G.as<float>(), st.total, static_cast<float>(lr));
   } else {

@@ -137,10 +137,28 @@ class Context:
     def synchronize(self):
         check(lib().ggb_ctx_synchronize(self.h))
 
-    def launches(self) -> int:
-        c = (C.c_uint64 * 1)()
+    def counters(self) -> dict:
+        c = (C.c_uint64 * 3)()
         check(lib().ggb_ctx_counters(self.h, c))
-        return int(c[0])
+        return {"launches": int(c[0]), "h2d_bytes": int(c[1]), "d2h_bytes": int(c[2])}
+
+    def launches(self) -> int:
+        return self.counters()["launches"]
+
+    PROF_CLASSES = ["sampling", "spmm_fwd", "spmm_bwd", "gemm_fwd", "gemm_dx", "gemm_wgrad", "elementwise",
+                    "optimizer", "collectives"]
+
+    def profile(self, enable: bool):
+        """Per-kernel-class CUDA-event timing on the context's stream."""
+        check(lib().ggb_ctx_profile(self.h, int(enable)))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        k = len(self.PROF_CLASSES)
+        ms, by, fl = (np.zeros(k) for _ in range(3))
+        cnt = np.zeros(k, np.int64)
+        check(lib().ggb_ctx_profile_read(self.h, _ptr(ms), _ptr(by), _ptr(fl), _ptr(cnt), int(reset)))
+        return {name: {"ms": float(ms[i]), "bytes": float(by[i]), "flops": float(fl[i]), "launches": int(cnt[i])}
+                for i, name in enumerate(self.PROF_CLASSES)}
 
     def close(self):
         if getattr(self, "h", None):
