@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--grid", default=None, help="GdxGxxGyxGz (default: data-parallel Gd = N)")
     ap.add_argument("--compute", default="accurate", choices=["accurate", "fast"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prefetch", type=int, default=1, help="overlap sampling of step t+1 with step t")
     ap.add_argument("--ref-steps", type=int, default=2)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -230,10 +231,15 @@ def main():
     st = gg.init_state(ctx, mcfg, RUN_SEED, gg.COMPUTE_ACCURATE if args.compute == "accurate" else gg.COMPUTE_FAST)
     group_seed = gg.hash_combine(RUN_SEED, grid.dp_group(rank))
     batch = None
+    # sampling of step t+1 overlaps training of step t (producer thread + own stream)
+    pf = gg.Prefetcher(ctx, graph, b, group_seed, 0) if args.prefetch else None
 
     def step(gstep: int, sync_loss: bool):
         nonlocal batch
-        batch = gg.build_step_batch(ctx, graph, b, group_seed, gstep, reuse=batch)
+        if pf:
+            batch = pf.next()
+        else:
+            batch = gg.build_step_batch(ctx, graph, b, group_seed, gstep, reuse=batch)
         loss = gg.train_step(ctx, st, batch, gg.FP32, RUN_SEED, gstep, sync_loss=sync_loss)
         gg.dp_sync(ctx, st)
         gg.optimizer_step(ctx, st, gg.ADAM, LR)
@@ -343,6 +349,7 @@ def main():
             "batch_per_dp_group": b, "steps_per_epoch": S, "grid": "x".join(map(str, dims)),
             "layers": cfg["layers"], "hidden": cfg["d_h"], "d_in": cfg["d_in"], "classes": cfg["n_classes"],
             "n_vertices": cfg["n"], "nnz": graph.nnz, "compute": args.compute,
+            "prefetch": bool(args.prefetch),
             "l2": "inputs larger than L2 (graph %.1f GB + features resident in HBM; random gathers)" %
                   (graph.device_bytes / 1e9),
             "optimizer": "adam lr 1e-3", "dropout": DROPOUT, "eval": "excluded (per SURVEY 8d)",

@@ -106,6 +106,19 @@ int ggb_graph_info(ggb_graph_t g, int64_t* info);
 int ggb_build_step_batch(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group_seed,
                          uint64_t step, ggb_batch_t* inout);
 int ggb_batch_destroy(ggb_batch_t batch);
+/* Sampling/training overlap: the train_run prefetch producer and its queue
+ * (model.hpp:556-581, 631-656). A native producer thread builds the batches
+ * of steps first_step, first_step+1, ... on its own CUDA stream into two
+ * slots; next() hands out the batch of the following step, ordering the
+ * ctx stream after it with a CUDA event and releasing the previous batch once
+ * the ctx stream's work on it completes. Handed-out batches are owned by the
+ * prefetcher (do not destroy them); they are bit-identical to
+ * ggb_build_step_batch's. */
+typedef struct ggb_prefetch_s* ggb_prefetch_t;
+int ggb_prefetch_create(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group_seed, uint64_t first_step,
+                        ggb_prefetch_t* out);
+int ggb_prefetch_next(ggb_prefetch_t pf, ggb_batch_t* batch_out);
+int ggb_prefetch_destroy(ggb_prefetch_t pf);
 /* info = {b, n, planes, x_r0, x_r1, x_c0, x_c1, nnz_extracted, nnz_kept} */
 int ggb_batch_info(ggb_batch_t batch, int64_t* info);
 int ggb_batch_sample(ggb_batch_t batch, int64_t* host_out);

@@ -8,6 +8,7 @@
 
 #include "comm.hpp"
 #include "dataset.hpp"
+#include "prefetch.hpp"
 #include "prof.hpp"
 #include "trainer.hpp"
 
@@ -15,6 +16,9 @@ struct ggb_ctx_s : ggb::Ctx {};
 struct ggb_graph_s : ggb::Graph {};
 struct ggb_batch_s : ggb::Batch {};
 struct ggb_state_s : ggb::State {};
+struct ggb_prefetch_s : ggb::Prefetcher {
+  using ggb::Prefetcher::Prefetcher;
+};
 
 namespace ggb {
 
@@ -407,6 +411,26 @@ int ggb_build_step_batch(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group
   });
 }
 
+int ggb_prefetch_create(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group_seed, uint64_t first_step,
+                        ggb_prefetch_t* out) {
+  return guard([&] {
+    use_device(*ctx);
+    require(g && out, "prefetch: null argument");
+    *out = new ggb_prefetch_s(*ctx, *g, b, group_seed, first_step);
+  });
+}
+
+int ggb_prefetch_next(ggb_prefetch_t pf, ggb_batch_t* batch_out) {
+  return guard([&] {
+    use_device(*pf->consumer);
+    *batch_out = reinterpret_cast<ggb_batch_t>(pf->next());  // owned by the prefetcher
+  });
+}
+
+int ggb_prefetch_destroy(ggb_prefetch_t pf) {
+  return guard([&] { delete pf; });
+}
+
 int ggb_batch_destroy(ggb_batch_t batch) {
   return guard([&] {
     if (batch && batch->ctx) cudaSetDevice(batch->ctx->device);
@@ -560,7 +584,8 @@ int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precis
                    uint64_t global_step, double rmsnorm_eps, float* loss_out) {
   return guard([&] {
     use_device(*ctx);
-    contract(st->ctx == ctx && bt->ctx == ctx, "train_step: handles belong to another context");
+    contract(st->ctx == ctx && bt->ctx && bt->ctx->device == ctx->device && bt->ctx->rank == ctx->rank,
+             "train_step: handles belong to another rank");
     forward(*st, *bt, precision, true, run_seed, global_step, rmsnorm_eps);
     cross_entropy(*st, *bt);
     backward(*st, *bt, precision);

@@ -74,8 +74,12 @@ struct DevBuf {
   }
   void* reserve(size_t n) {
     if (n > bytes) {
+      // re-growth gets 25% headroom: per-step sizes (batch nonzeros, local
+      // rows) fluctuate, and a cudaFree/cudaMalloc inside a step stalls it
+      const bool regrow = bytes > 0;
       release();
       size_t want = n < 256 ? 256 : n;
+      if (regrow) want += want / 4;
       GGB_CUDA(cudaMalloc(&p, want));
       bytes = want;
     }

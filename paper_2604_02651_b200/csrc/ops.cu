@@ -91,110 +91,6 @@ __global__ void k_rowsumsq(const float* __restrict__ x, int64_t ldx, int64_t row
   if (lane == 0) ss[r] = s;
 }
 
-// One thread per 8 consecutive columns of a row.
-//   rms_r = sqrt(ss_r / d + eps); y = gamma * x * (1/rms)          (pmm.hpp:230-240)
-//   sc = y > 0 ? (drop ? (keep ? 1/(1-rate) : 0) : 1) : 0           (pmm.hpp:314-322)
-//   out = y * sc + res                                              (pmm.hpp:323-324)
-__global__ void k_fwd_apply(FwdApply p) {
-  const int64_t tpr = (p.cols + 7) / 8;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t r = t / tpr;
-  if (r >= p.rows) return;
-  const int64_t c0 = (t % tpr) * 8;
-  float inv = 1.f;
-  if (p.ss) {
-    const float rms = sqrtf(p.ss[r] / p.d + p.eps);
-    inv = 1.f / rms;
-    if (c0 == 0 && p.rms) p.rms[r] = rms;
-  }
-  const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
-  uint32_t bits = 0;
-  for (int i = 0; i < 8; ++i) {
-    const int64_t c = c0 + i;
-    if (c >= p.cols) break;
-    const float x = p.x[r * p.ldx + c];
-    const float y = p.ss ? p.gamma[c] * x * inv : x;
-    float sc = y > 0.f ? 1.f : 0.f;
-    if (p.drop && sc != 0.f)
-      sc = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + c), p.thresh) ? p.keep_scale : 0.f;
-    if (sc != 0.f) bits |= 1u << i;
-    float o = y * sc;
-    if (p.res) o += p.res[r * p.ldres + c];
-    if (p.out) p.out[r * p.ldo + c] = o;
-    if (p.outb) {
-      const bf16 h = __float2bfloat16_rn(o);
-      p.outb[r * p.ldob + c] = h;
-      if (p.outlo) p.outlo[r * p.ldob + c] = __float2bfloat16_rn(o - __bfloat162float(h));
-    }
-  }
-  p.mask[r * p.ldm + c0 / 8] = static_cast<uint8_t>(bits);
-}
-
-// s_r = sum_j dxn * gamma * x with dxn = dy * scale (pmm.hpp:258-267, 331-341)
-__global__ void k_bwd_stats(BwdApply p) {
-  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= p.rows) return;
-  float s = 0.f;
-  for (int64_t c = lane; c < p.cols; c += 32) {
-    const bool keep = (p.mask[r * p.ldm + c / 8] >> (c & 7)) & 1u;
-    const float dxn = keep ? p.dy[r * p.lddy + c] * p.keep_scale : 0.f;
-    s += dxn * p.gamma[c] * p.x[r * p.ldx + c];
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) p.s[r] = s;
-}
-
-// dx = gamma*dxn/r - x*s/(d r^3); dgamma_j += dxn*x/r (pmm.hpp:269-285).
-// Grid-stride over rows; per-block column partial sums of dgamma.
-__global__ void k_bwd_apply(BwdApply p) {
-  const int tpr = static_cast<int>((p.cols + 7) / 8);
-  const int rpb = blockDim.x / tpr;  // row slots per block
-  const int slot = threadIdx.x / tpr, ct = threadIdx.x % tpr;
-  const int64_t c0 = static_cast<int64_t>(ct) * 8;
-  float dg[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) dg[i] = 0.f;
-  if (slot < rpb) {
-    for (int64_t r = static_cast<int64_t>(blockIdx.x) * rpb + slot; r < p.rows;
-         r += static_cast<int64_t>(gridDim.x) * rpb) {
-      const uint8_t bits = p.mask[r * p.ldm + c0 / 8];
-      float inv = 1.f, coef = 0.f;
-      if (p.rms) {
-        const float rr = p.rms[r];
-        inv = 1.f / rr;
-        coef = p.s[r] / (p.d * rr * rr * rr);
-      }
-      for (int i = 0; i < 8; ++i) {
-        const int64_t c = c0 + i;
-        if (c >= p.cols) break;
-        const float dxn = ((bits >> i) & 1u) ? p.dy[r * p.lddy + c] * p.keep_scale : 0.f;
-        float dx;
-        if (p.rms) {
-          const float x = p.x[r * p.ldx + c];
-          dx = p.gamma[c] * dxn * inv - x * coef;
-          dg[i] += dxn * x * inv;
-        } else {
-          dx = dxn;
-        }
-        p.dxb[r * p.lddxb + c] = __float2bfloat16_rn(dx);
-      }
-    }
-  }
-  if (!p.dgamma_part) return;
-  extern __shared__ float sh[];  // [rpb][cols]
-  if (slot < rpb)
-    for (int i = 0; i < 8; ++i)
-      if (c0 + i < p.cols) sh[slot * p.cols + c0 + i] = dg[i];
-  __syncthreads();
-  for (int64_t c = threadIdx.x; c < p.cols; c += blockDim.x) {
-    float s = 0.f;
-    for (int k = 0; k < rpb; ++k) s += sh[k * p.cols + c];
-    p.dgamma_part[static_cast<int64_t>(blockIdx.x) * p.cols + c] = s;
-  }
-}
-
 __global__ void k_reduce_rows(const float* __restrict__ part, int parts, int64_t cols, float* __restrict__ out) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= cols) return;
@@ -350,42 +246,6 @@ void add_inplace(Ctx& ctx, float* a, int64_t lda, const float* b, int64_t ldb, i
 void rowsumsq(Ctx& ctx, const float* x, int64_t ldx, int64_t rows, int64_t cols, float* ss) {
   if (rows <= 0) return;
   k_rowsumsq<<<nb(rows * 32), kT, 0, ctx.stream>>>(x, ldx, rows, cols, ss);
-  GGB_LAUNCH_CHECK();
-  ctx.launches += 1;
-}
-
-void fwd_apply(Ctx& ctx, const FwdApply& p) {
-  if (p.rows <= 0) return;
-  const int64_t threads = p.rows * ((p.cols + 7) / 8);
-  k_fwd_apply<<<nb(threads), kT, 0, ctx.stream>>>(p);
-  GGB_LAUNCH_CHECK();
-  ctx.launches += 1;
-}
-
-void bwd_stats(Ctx& ctx, const BwdApply& p) {
-  if (p.rows <= 0) return;
-  k_bwd_stats<<<nb(p.rows * 32), kT, 0, ctx.stream>>>(p);
-  GGB_LAUNCH_CHECK();
-  ctx.launches += 1;
-}
-
-int bwd_apply_blocks(Ctx& ctx, int64_t rows, int64_t cols) {
-  const int tpr = static_cast<int>((cols + 7) / 8);
-  const int threads = std::max(32, (kT / tpr) * tpr);
-  const int rpb = threads / tpr;
-  const int64_t want = ceil_div(rows, rpb);
-  (void)threads;
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, 4 * ctx.num_sms)));
-}
-
-void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks) {
-  if (p.rows <= 0) return;
-  const int tpr = static_cast<int>((p.cols + 7) / 8);
-  require(tpr <= 1024, "rmsnorm_bwd: row block too wide");
-  const int threads = std::max(tpr, (kT / tpr) * tpr);
-  const int rpb = threads / tpr;
-  const size_t smem = p.dgamma_part ? static_cast<size_t>(rpb) * p.cols * 4 : 0;
-  k_bwd_apply<<<blocks, threads, smem, ctx.stream>>>(p);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }

@@ -25,16 +25,24 @@ struct FwdApply {
   bf16* outb;  // bf16 copy (nullable) = hi part of the split pair
   bf16* outlo; // bf16 lo part (nullable): out == hi + lo to ~2^-16
   int64_t ldob;
-  uint8_t* mask;  // [rows][ldm] keep bits
-  int64_t ldm;
+  uint32_t* mask;  // [rows][ldm] keep bits, row-kernel layout (see kRowChunk)
+  int64_t ldm;     // words per row = mask_words(cols)
+  int fuse_ss;     // 1: the row is complete here, compute ss in-kernel (ss ignored)
 };
+
+// Row kernels: lane l of a warp owns columns c = 128*j + 4*l + i (i < 4) of
+// its row (one float4 per chunk j); the keep mask of chunk j is 4 ballot
+// words, word i holding bit l for column 128*j + 4*l + i.
+constexpr int kRowChunk = 128;
+inline int64_t mask_words(int64_t cols) { return 4 * ((cols + kRowChunk - 1) / kRowChunk); }
 
 struct BwdApply {
   int64_t rows, cols;
   const float* dy;  // upstream gradient fp32
   int64_t lddy;
-  const uint8_t* mask;
+  const uint32_t* mask;
   int64_t ldm;
+  int fuse_s;  // 1: the row is complete here, compute s in-kernel
   float keep_scale;  // scale value of a kept element (1 without dropout)
   const float* x;    // xw
   int64_t ldx;
@@ -83,6 +91,8 @@ void ce_rowmax(Ctx& ctx, const CeArgs& p);
 void ce_rowsum(Ctx& ctx, const CeArgs& p);
 int ce_grad_blocks(int64_t rows);
 void ce_grad(Ctx& ctx, const CeArgs& p);
+// all three cross-entropy passes in one warp-per-row kernel (row fully local)
+void ce_fused(Ctx& ctx, const CeArgs& p);
 void scale_scalar(Ctx& ctx, const float* in, float s, float* out);
 void adam(Ctx& ctx, float* w, const float* g, float* m, float* v, int64_t n, double lr, double bc1,
           double bc2);

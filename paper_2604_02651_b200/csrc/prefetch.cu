@@ -1,0 +1,100 @@
+// Sampling / training overlap: the reference's prefetch producer
+// (train_run's producer thread + PrefetchQueue, model.hpp:556-581 and
+// 631-656) as a native producer thread with its own CUDA stream and sampler
+// scratch. Two batch slots; the hand-off is by CUDA events, so the compute
+// stream never blocks the host:
+//   producer: wait(released[slot]) on the sampling stream -> build batch k ->
+//             record ready[slot];
+//   consumer: next() records released[previous slot] on the compute stream,
+//             then makes the compute stream wait on ready[slot].
+// Batches are bit-identical to the non-prefetched ones (same seeds/steps), as
+// in the reference (acceptance criterion 8).
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+#include "comm.hpp"
+#include "prefetch.hpp"
+#include "prof.hpp"
+
+namespace ggb {
+
+Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t seed_, uint64_t first_step)
+    : consumer(&consumer_), g(&g_), b(b_), seed(seed_), step0(first_step) {
+  require(b >= 2 && b <= g->n, "prefetch: need 2 <= b <= N");
+  sctx.grid = consumer->grid;
+  sctx.rank = consumer->rank;
+  for (int a = 0; a < 4; ++a) sctx.coord[a] = consumer->coord[a];
+  sctx.device = consumer->device;
+  sctx.num_sms = consumer->num_sms;
+  GGB_CUDA(cudaSetDevice(sctx.device));
+  GGB_CUDA(cudaStreamCreateWithFlags(&sctx.stream, cudaStreamNonBlocking));
+  sctx.own_stream = true;
+  for (int s = 0; s < 2; ++s) {
+    GGB_CUDA(cudaEventCreateWithFlags(&ready[s], cudaEventDisableTiming));
+    GGB_CUDA(cudaEventCreateWithFlags(&released[s], cudaEventDisableTiming));
+  }
+  th = std::thread([this] { run(); });
+}
+
+Prefetcher::~Prefetcher() {
+  {
+    std::lock_guard<std::mutex> lk(m);
+    stop = true;
+  }
+  cv.notify_all();
+  if (th.joinable()) th.join();
+  cudaSetDevice(sctx.device);
+  cudaStreamSynchronize(sctx.stream);
+  for (int s = 0; s < 2; ++s) {
+    cudaEventDestroy(ready[s]);
+    cudaEventDestroy(released[s]);
+  }
+}
+
+void Prefetcher::run() {
+  try {
+    GGB_CUDA(cudaSetDevice(sctx.device));
+    for (int64_t k = 0;; ++k) {
+      const int slot = static_cast<int>(k & 1);
+      {
+        std::unique_lock<std::mutex> lk(m);
+        // slot free once the consumer has released batch k-2
+        cv.wait(lk, [&] { return stop || released_count >= k - 1; });
+        if (stop) return;
+      }
+      if (k >= 2) GGB_CUDA(cudaStreamWaitEvent(sctx.stream, released[slot], 0));
+      build_step_batch(sctx, *g, b, seed, step0 + static_cast<uint64_t>(k), slots[slot]);
+      GGB_CUDA(cudaEventRecord(ready[slot], sctx.stream));
+      {
+        std::lock_guard<std::mutex> lk(m);
+        produced = k + 1;
+      }
+      cv.notify_all();
+    }
+  } catch (...) {
+    std::lock_guard<std::mutex> lk(m);
+    err = std::current_exception();
+    failed = true;
+    cv.notify_all();
+  }
+}
+
+Batch* Prefetcher::next() {
+  std::unique_lock<std::mutex> lk(m);
+  if (consumed > 0) {  // release the batch handed out last time, once its compute is done
+    const int prev = static_cast<int>((consumed - 1) & 1);
+    GGB_CUDA(cudaEventRecord(released[prev], consumer->stream));
+    released_count = consumed;
+    cv.notify_all();
+  }
+  cv.wait(lk, [&] { return failed || produced > consumed; });
+  if (failed && produced <= consumed) std::rethrow_exception(err);
+  const int slot = static_cast<int>(consumed & 1);
+  GGB_CUDA(cudaStreamWaitEvent(consumer->stream, ready[slot], 0));
+  ++consumed;
+  return &slots[slot];
+}
+
+}  // namespace ggb

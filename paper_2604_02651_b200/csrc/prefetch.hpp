@@ -1,0 +1,33 @@
+#pragma once
+
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <thread>
+
+#include "runtime.hpp"
+
+namespace ggb {
+
+struct Prefetcher {
+  Ctx* consumer;
+  const Graph* g;
+  int64_t b;
+  uint64_t seed, step0;
+  Ctx sctx;  // sampling context: own stream + sampler scratch, same grid coords
+  Batch slots[2];
+  cudaEvent_t ready[2] = {}, released[2] = {};
+  std::thread th;
+  std::mutex m;
+  std::condition_variable cv;
+  int64_t produced = 0, consumed = 0, released_count = 0;
+  bool stop = false, failed = false;
+  std::exception_ptr err;
+
+  Prefetcher(Ctx& consumer, const Graph& g, int64_t b, uint64_t seed, uint64_t first_step);
+  ~Prefetcher();
+  void run();
+  Batch* next();  // batch for step first_step + (number of previous calls)
+};
+
+}  // namespace ggb

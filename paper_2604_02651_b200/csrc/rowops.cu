@@ -1,0 +1,331 @@
+// Warp-per-row kernels of the layer's normalization / activation path, fully
+// vectorized (one float4 per lane per 128-column chunk) and fused across the
+// reference's separate passes when the whole row is local to the rank:
+//   forward  : row sum of squares + RMSNorm apply + ReLU + dropout + residual
+//              (parallel_rmsnorm_fwd pmm.hpp:214-243 + fused_elementwise_fwd
+//              pmm.hpp:299-328) in one read of xw and the residual;
+//   backward : fused_elementwise_bwd (pmm.hpp:331-341) + parallel_rmsnorm_bwd
+//              (pmm.hpp:251-287) with the row dot product, dx and the dgamma
+//              column partials in one read of dy and xw;
+//   loss     : parallel_cross_entropy (pmm.hpp:352-401) max / sum-exp /
+//              gradient in one pass over the logits row.
+// When the row is split over the grid's column axis the same kernels run in
+// two phases around the fp32 all-reduce of the row statistic.
+#include "ops.hpp"
+#include "rng.cuh"
+
+namespace ggb {
+namespace {
+
+constexpr int kT = 256;
+constexpr int kRowsPerBlock = kT / 32;
+constexpr int kMaxJ = 4;  // rows up to 512 local columns
+
+__device__ __forceinline__ float warp_sum(float s) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+__device__ __forceinline__ float warp_max(float s) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, o));
+  return s;
+}
+
+// 4 consecutive floats at column c of a row with n valid columns (c % 4 == 0)
+__device__ __forceinline__ float4 ld4(const float* row, int64_t c, int64_t n) {
+  if (c + 4 <= n) return *reinterpret_cast<const float4*>(row + c);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c < n) v.x = row[c];
+  if (c + 1 < n) v.y = row[c + 1];
+  if (c + 2 < n) v.z = row[c + 2];
+  if (c + 3 < n) v.w = row[c + 3];
+  return v;
+}
+__device__ __forceinline__ void st4(float* row, int64_t c, int64_t n, const float* v) {
+  if (c + 4 <= n) {
+    *reinterpret_cast<float4*>(row + c) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    for (int i = 0; i < 4 && c + i < n; ++i) row[c + i] = v[i];
+  }
+}
+__device__ __forceinline__ void st4_bf16(bf16* row, int64_t c, int64_t n, const float* v) {
+  if (c + 4 <= n) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(row + c) = u;
+  } else {
+    for (int i = 0; i < 4 && c + i < n; ++i) row[c + i] = __float2bfloat16_rn(v[i]);
+  }
+}
+__device__ __forceinline__ void f4(const float4& a, float* v) {
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = a.z;
+  v[3] = a.w;
+}
+
+__global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
+  if (r >= p.rows) return;
+  const int nj = static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
+  const float* xr = p.x + r * p.ldx;
+  float x[kMaxJ][4];
+#pragma unroll
+  for (int j = 0; j < kMaxJ; ++j)
+    if (j < nj) f4(ld4(xr, j * kRowChunk + 4 * lane, p.cols), x[j]);
+  float inv = 1.f;
+  if (p.gamma) {  // RMSNorm on
+    float ss;
+    if (p.fuse_ss) {
+      float s = 0.f;
+#pragma unroll
+      for (int j = 0; j < kMaxJ; ++j)
+        if (j < nj)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) s = fmaf(x[j][i], x[j][i], s);
+      ss = warp_sum(s);
+    } else {
+      ss = p.ss[r];
+    }
+    const float rms = sqrtf(ss / p.d + p.eps);
+    inv = 1.f / rms;
+    if (lane == 0 && p.rms) p.rms[r] = rms;
+  }
+  const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
+#pragma unroll
+  for (int j = 0; j < kMaxJ; ++j) {
+    if (j >= nj) break;
+    const int64_t c = j * kRowChunk + 4 * lane;
+    float g[4] = {1.f, 1.f, 1.f, 1.f}, res[4] = {0.f, 0.f, 0.f, 0.f}, o[4];
+    if (p.gamma) f4(ld4(p.gamma, c, p.cols), g);
+    if (p.res) f4(ld4(p.res + r * p.ldres, c, p.cols), res);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float y = p.gamma ? g[i] * x[j][i] * inv : x[j][i];
+      float sc = y > 0.f ? 1.f : 0.f;
+      if (p.drop && sc != 0.f && c + i < p.cols)
+        sc = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + c + i), p.thresh) ? p.keep_scale : 0.f;
+      const unsigned bits = __ballot_sync(0xffffffffu, sc != 0.f && c + i < p.cols);
+      if (lane == i) p.mask[r * p.ldm + 4 * j + i] = bits;
+      o[i] = y * sc + res[i];
+    }
+    if (p.out) st4(p.out + r * p.ldo, c, p.cols, o);
+    if (p.outb) {
+      st4_bf16(p.outb + r * p.ldob, c, p.cols, o);
+      if (p.outlo) {
+        float lo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) lo[i] = o[i] - __bfloat162float(__float2bfloat16_rn(o[i]));
+        st4_bf16(p.outlo + r * p.ldob, c, p.cols, lo);
+      }
+    }
+  }
+}
+
+// Row dot product s_r = sum_j dxn * gamma * x (the all-reduced input of the
+// split-row backward).
+__global__ void __launch_bounds__(kT) k_bwd_row_stats(BwdApply p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
+  if (r >= p.rows) return;
+  const int nj = static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
+  float s = 0.f;
+  for (int j = 0; j < nj; ++j) {
+    const int64_t c = j * kRowChunk + 4 * lane;
+    float dy[4], x[4], g[4];
+    f4(ld4(p.dy + r * p.lddy, c, p.cols), dy);
+    f4(ld4(p.x + r * p.ldx, c, p.cols), x);
+    f4(ld4(p.gamma, c, p.cols), g);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool keep = (p.mask[r * p.ldm + 4 * j + i] >> lane) & 1u;
+      const float dxn = keep ? dy[i] * p.keep_scale : 0.f;
+      s += dxn * g[i] * x[i];
+    }
+  }
+  s = warp_sum(s);
+  if (lane == 0) p.s[r] = s;
+}
+
+// dx = gamma*dxn/r - x*s/(d r^3) (bf16 out); dgamma_j += dxn*x/r accumulated
+// per lane over the block's rows (grid-stride), then reduced across the
+// block's warps into dgamma_part[block][cols].
+__global__ void __launch_bounds__(kT) k_bwd_row(BwdApply p) {
+  __shared__ float sh[kRowsPerBlock][kMaxJ * kRowChunk];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nj = static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
+  float dg[kMaxJ][4];
+#pragma unroll
+  for (int j = 0; j < kMaxJ; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dg[j][i] = 0.f;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib; r < p.rows;
+       r += static_cast<int64_t>(gridDim.x) * kRowsPerBlock) {
+    float dxn[kMaxJ][4], x[kMaxJ][4];
+    const uint32_t* mrow = p.mask + r * p.ldm;
+#pragma unroll
+    for (int j = 0; j < kMaxJ; ++j) {
+      if (j >= nj) break;
+      const int64_t c = j * kRowChunk + 4 * lane;
+      float dy[4];
+      f4(ld4(p.dy + r * p.lddy, c, p.cols), dy);
+      f4(ld4(p.x + r * p.ldx, c, p.cols), x[j]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dxn[j][i] = ((mrow[4 * j + i] >> lane) & 1u) ? dy[i] * p.keep_scale : 0.f;
+    }
+    float inv = 1.f, coef = 0.f;
+    if (p.rms) {
+      float s;
+      if (p.fuse_s) {
+        float a = 0.f;
+#pragma unroll
+        for (int j = 0; j < kMaxJ; ++j) {
+          if (j >= nj) break;
+          float g[4];
+          f4(ld4(p.gamma, j * kRowChunk + 4 * lane, p.cols), g);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a += dxn[j][i] * g[i] * x[j][i];
+        }
+        s = warp_sum(a);
+      } else {
+        s = p.s[r];
+      }
+      const float rr = p.rms[r];
+      inv = 1.f / rr;
+      coef = s / (p.d * rr * rr * rr);
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxJ; ++j) {
+      if (j >= nj) break;
+      const int64_t c = j * kRowChunk + 4 * lane;
+      float dx[4];
+      if (p.rms) {
+        float g[4];
+        f4(ld4(p.gamma, c, p.cols), g);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          dx[i] = g[i] * dxn[j][i] * inv - x[j][i] * coef;
+          dg[j][i] += dxn[j][i] * x[j][i] * inv;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dx[i] = dxn[j][i];
+      }
+      st4_bf16(p.dxb + r * p.lddxb, c, p.cols, dx);
+    }
+  }
+  if (!p.dgamma_part) return;
+#pragma unroll
+  for (int j = 0; j < kMaxJ; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) sh[wib][j * kRowChunk + 4 * lane + i] = dg[j][i];
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < p.cols; c += kT) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kRowsPerBlock; ++k) s += sh[k][c];
+    p.dgamma_part[static_cast<int64_t>(blockIdx.x) * p.cols + c] = s;
+  }
+}
+
+// Cross-entropy in one pass per row (class block fully local): row max,
+// sum of exp, label logit, per-row loss, gradient (softmax - onehot) / B.
+__global__ void __launch_bounds__(kT) k_ce_row(CeArgs p) {
+  __shared__ float part[kRowsPerBlock];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib;
+  float contrib = 0.f;
+  if (r < p.rows) {
+    const float* lr = p.logits + r * p.ld;
+    float m = -3.402823466e38f;
+    for (int64_t j = lane; j < p.cols; j += 32) m = fmaxf(m, lr[j]);
+    m = warp_max(m);
+    float z = 0.f;
+    for (int64_t j = lane; j < p.cols; j += 32) z += expf(lr[j] - m);
+    z = warp_sum(z);
+    const int64_t y = p.labels[p.row_g0 + r];
+    for (int64_t j = lane; j < p.cols; j += 32) {
+      float g = expf(lr[j] - m) / z;
+      if (p.c0 + j == y) g -= 1.f;
+      const float d = g * p.invb;
+      if (p.dlog) p.dlog[r * p.lddlog + j] = d;
+      if (p.dlogb) p.dlogb[r * p.lddlogb + j] = __float2bfloat16_rn(d);
+    }
+    const float zy = (y >= p.c0 && y < p.c0 + p.cols) ? lr[y - p.c0] : 0.f;
+    contrib = (m + logf(z)) - zy;
+  }
+  if (lane == 0) part[wib] = contrib;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int k = 0; k < kRowsPerBlock; ++k) s += part[k];
+    p.loss_part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_sum_parts_row(const float* __restrict__ part, int64_t n, float* __restrict__ out) {
+  __shared__ float sh[kT];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += kT) s += part[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kT / 2; o; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+inline unsigned row_blocks(int64_t rows) { return static_cast<unsigned>(ceil_div(rows, kRowsPerBlock)); }
+
+}  // namespace
+
+void fwd_apply(Ctx& ctx, const FwdApply& p) {
+  if (p.rows <= 0) return;
+  require(p.cols <= kMaxJ * kRowChunk, "row kernels: at most 512 local feature columns");
+  require(p.ldx % 4 == 0 && (!p.res || p.ldres % 4 == 0) && (!p.out || p.ldo % 4 == 0),
+          "row kernels: fp32 rows must be 16-byte aligned");
+  k_fwd_row<<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+void bwd_stats(Ctx& ctx, const BwdApply& p) {
+  if (p.rows <= 0) return;
+  k_bwd_row_stats<<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+int bwd_apply_blocks(Ctx& ctx, int64_t rows, int64_t cols) {
+  (void)cols;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), 8 * ctx.num_sms)));
+}
+
+void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks) {
+  if (p.rows <= 0) return;
+  require(p.cols <= kMaxJ * kRowChunk, "row kernels: at most 512 local feature columns");
+  require(p.lddy % 4 == 0 && p.ldx % 4 == 0, "row kernels: fp32 rows must be 16-byte aligned");
+  k_bwd_row<<<blocks, kT, 0, ctx.stream>>>(p);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+void ce_fused(Ctx& ctx, const CeArgs& p) {
+  const unsigned blocks = std::max(1u, row_blocks(p.rows));
+  if (p.rows > 0) {
+    k_ce_row<<<blocks, kT, 0, ctx.stream>>>(p);
+    ctx.launches += 1;
+  } else {
+    GGB_CUDA(cudaMemsetAsync(p.loss_part, 0, sizeof(float), ctx.stream));
+  }
+  k_sum_parts_row<<<1, kT, 0, ctx.stream>>>(p.loss_part, p.rows > 0 ? blocks : 1, p.loss_acc);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+}  // namespace ggb

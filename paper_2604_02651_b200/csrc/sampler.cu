@@ -225,10 +225,11 @@ __global__ void k_extract_fill(int64_t nr, const int64_t* __restrict__ sample, i
 __global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t* __restrict__ sample,
                            int64_t row_lo, const float* __restrict__ feats, int64_t fld,
                            bf16* __restrict__ xb, bf16* __restrict__ xl, float* __restrict__ xf) {
-  const int64_t r = blockIdx.x;
+  // one warp per gathered row (coalesced over the row's columns)
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (r >= rows) return;
   const float* src = feats + sample[row_lo + r] * fld;
-  for (int64_t c = threadIdx.x; c < ld; c += blockDim.x) {
+  for (int64_t c = threadIdx.x & 31; c < ld; c += 32) {
     const float x = c < cols ? src[c] : 0.0f;
     const bf16 h = __float2bfloat16_rn(x);
     if (xb) xb[r * ld + c] = h;
@@ -306,9 +307,11 @@ void extract_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int6
 
 void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t row_lo,
                 int64_t col_lo, int64_t b, int64_t n, BatchCsr& out) {
-  out.col.reserve_n<int32_t>(out.nnz);
-  out.val.reserve_n<float>(out.nnz);
-  out.val64.reserve_n<double>(out.nnz);
+  // nonzero counts fluctuate step to step: size with headroom once
+  const int64_t cap = out.nnz + out.nnz / 16 + 1024;
+  out.col.reserve_n<int32_t>(cap);
+  out.val.reserve_n<float>(cap);
+  out.val64.reserve_n<double>(cap);
   if (out.n_rows == 0 || out.nnz == 0) return;
   const double p = static_cast<double>(b - 1) / static_cast<double>(n - 1);  // shardsample.cpp:116
   k_extract_fill<<<blocks(out.n_rows, kThreads / 32), kThreads, 0, ctx.stream>>>(
@@ -439,7 +442,7 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     bf16* xb = bt.x_in.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
     bf16* xl = bt.x_in_lo.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
     if (rows > 0) {
-      k_gather_x<<<static_cast<unsigned>(rows), 128, 0, s>>>(rows, cols, bt.x_ld, d_sample, bt.x_r0,
+      k_gather_x<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(rows, cols, bt.x_ld, d_sample, bt.x_r0,
                                                             g.features.as<float>(), cols, xb, xl, nullptr);
       ctx.launches += 1;
     }
@@ -464,7 +467,7 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
 void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out) {
   const int64_t rows = bt.x_r1 - bt.x_r0, cols = bt.x_c1 - bt.x_c0;
   if (rows <= 0 || cols <= 0) return;
-  k_gather_x<<<static_cast<unsigned>(rows), 128, 0, ctx.stream>>>(
+  k_gather_x<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, ctx.stream>>>(
       rows, cols, cols, bt.sample.as<int64_t>(), bt.x_r0, bt.graph->features.as<float>(), cols,
       nullptr, nullptr, d_out);
   GGB_LAUNCH_CHECK();

@@ -62,7 +62,7 @@ __device__ __forceinline__ void store_bf16x8(bf16* dst, const float* v, bool ful
 }
 
 template <int LPR, class TIn>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     k_spmm(int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
            const float* __restrict__ val, const TIn* __restrict__ F, int64_t ldf, int fcols,
            float* __restrict__ out, int64_t ldo, bf16* __restrict__ outb, bf16* __restrict__ outlo,
@@ -90,11 +90,13 @@ __global__ void __launch_bounds__(kThreads)
       mv = __ldg(val + k);
     }
     const int cnt = static_cast<int>(e1 - e < LPR ? e1 - e : LPR);
-    for (int kk = 0; kk < cnt; kk += kUnroll) {
-      Vec8<TIn> fv[kUnroll];
-      float vv[kUnroll];
+    // gathers in flight per lane: 8 x 16 B (bf16) or 4 x 32 B (fp32)
+    constexpr int U = sizeof(TIn) == 2 ? kUnroll : kUnroll / 2;
+    for (int kk = 0; kk < cnt; kk += U) {
+      Vec8<TIn> fv[U];
+      float vv[U];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int src = (kk + u) & (LPR - 1);
         const int ci = __shfl_sync(gmask, mc, src, LPR);
         const float v = __shfl_sync(gmask, mv, src, LPR);
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(kThreads)
           fv[u].zero();
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) fv[u].fma(acc, vv[u]);
+      for (int u = 0; u < U; ++u) fv[u].fma(acc, vv[u]);
     }
   }
   if (!col_ok) return;

@@ -333,7 +333,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     xb.c0 = w.blk.c0;
     xb.c1 = w.blk.c1;
     L.xw_t.blk = xb;
-    L.xw_t.ldf = xb.cols();
+    L.xw_t.ldf = ld8(xb.cols());
     L.xw_t.f = grow<float>(L.xw, xb.rows() * L.xw_t.ldf);
     fwd_gemm(st, xb.rows(), xb.cols(), hb.cols(), L.hagg, w, L.xw_t.f, L.xw_t.ldf, nullptr, 0);
     all_reduce_sum(ctx, hb.lay.col, L.xw_t.f, xb.rows() * L.xw_t.ldf, wire);
@@ -341,12 +341,15 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     float* ss = nullptr;
     float* rms = nullptr;
     const float* gam = nullptr;
+    const bool row_local = trivial(ctx, xb.lay.col);  // whole feature row on this rank
     if (cfg.use_rmsnorm) {
       ss = grow<float>(L.ss, xb.rows());
       rms = grow<float>(L.rms, xb.rows());
-      ProfScope ps(ctx, kProfElementwise, 4.0 * xb.rows() * xb.cols());
-      rowsumsq(ctx, L.xw_t.f, L.xw_t.ldf, xb.rows(), xb.cols(), ss);
-      all_reduce_sum(ctx, xb.lay.col, ss, xb.rows(), false);
+      if (!row_local) {  // partial sums of squares, all-reduced along the column axis
+        ProfScope ps(ctx, kProfElementwise, 4.0 * xb.rows() * xb.cols());
+        rowsumsq(ctx, L.xw_t.f, L.xw_t.ldf, xb.rows(), xb.cols(), ss);
+        all_reduce_sum(ctx, xb.lay.col, ss, xb.rows(), false);
+      }
       const ParamSlot& gp = st.params[st.gamma[l - 1]];
       contract(gp.blk.c0 == xb.c0 && gp.blk.c1 == xb.c1, "rmsnorm: gamma slice does not match the column block");
       gam = W + gp.off;
@@ -363,11 +366,11 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
         res = prev->f;
         ldres = prev->ldf;
       } else {
-        float* r = grow<float>(st.dres, rb.rows() * rb.cols());
+        float* r = grow<float>(st.dres, rb.rows() * ld8(rb.cols()));
         reshard(ctx, reshard_work(), F, bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), prev->f, prev->ldf, rb,
-                r, rb.cols());
+                r, ld8(rb.cols()));
         res = r;
-        ldres = rb.cols();
+        ldres = ld8(rb.cols());
       }
     }
     // fused RMSNorm apply + ReLU + dropout + residual -> X_l
@@ -380,8 +383,9 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     const bool last = l == cfg.layers;
     L.x.b = (!accurate || last) ? grow<bf16>(L.x_b, xb.rows() * L.x.ldb) : nullptr;
     L.x.lo = (accurate && last) ? grow<bf16>(L.x_lo, xb.rows() * L.x.ldb) : nullptr;
-    L.ldm = ceil_div(std::max<int64_t>(xb.cols(), 1), 8);
+    L.ldm = mask_words(std::max<int64_t>(xb.cols(), 1));
     FwdApply fa{};
+    fa.fuse_ss = row_local ? 1 : 0;
     fa.rows = xb.rows();
     fa.cols = xb.cols();
     fa.x = L.xw_t.f;
@@ -404,7 +408,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     fa.outb = L.x.b;
     fa.outlo = L.x.lo;
     fa.ldob = L.x.ldb;
-    fa.mask = grow<uint8_t>(L.mask, xb.rows() * L.ldm);
+    fa.mask = grow<uint32_t>(L.mask, xb.rows() * L.ldm);
     fa.ldm = L.ldm;
     {
       const double e = static_cast<double>(xb.rows()) * xb.cols();
@@ -453,12 +457,17 @@ void cross_entropy(State& st, const Batch& bt) {
   c.lddlogb = ld8(c.cols);
   c.loss_part = grow<float>(st.ce_part, ce_grad_blocks(c.rows) + 1);
   c.loss_acc = grow<float>(st.loss_acc, 1);
-  ProfScope ps(ctx, kProfElementwise, static_cast<double>(c.rows) * c.cols * (3 * 4 + 2));
-  ce_rowmax(ctx, c);
-  all_reduce_max(ctx, lb.lay.col, c.mx, c.rows);
-  ce_rowsum(ctx, c);
-  all_reduce_sum(ctx, lb.lay.col, c.zt, 2 * c.rows, false);
-  ce_grad(ctx, c);
+  if (trivial(ctx, lb.lay.col)) {  // class block complete here: one pass per row
+    ProfScope ps(ctx, kProfElementwise, static_cast<double>(c.rows) * c.cols * (4 + 2));
+    ce_fused(ctx, c);
+  } else {
+    ProfScope ps(ctx, kProfElementwise, static_cast<double>(c.rows) * c.cols * (3 * 4 + 2));
+    ce_rowmax(ctx, c);
+    all_reduce_max(ctx, lb.lay.col, c.mx, c.rows);
+    ce_rowsum(ctx, c);
+    all_reduce_sum(ctx, lb.lay.col, c.zt, 2 * c.rows, false);
+    ce_grad(ctx, c);
+  }
   all_reduce_sum(ctx, lb.lay.row, c.loss_acc, 1, false);
   scale_scalar(ctx, c.loss_acc, c.invb, grow<float>(st.loss, 1));
 }
@@ -491,14 +500,14 @@ void backward(State& st, const Batch& bt, int precision) {
   }
   // dxh = dlogits . W_out^T -> (X_L.row, X_L.col), all-reduce logits.col
   Block db = XL.blk;
-  float* dxh = grow<float>(st.dxh, db.rows() * db.cols());
+  float* dxh = grow<float>(st.dxh, db.rows() * ld8(db.cols()));
   {
     const ParamSlot& w = st.params[st.wout];
     ProfScope ps(ctx, kProfGemmDx, gemm_bytes(db.rows(), db.cols(), lb.cols(), 2, 2, 4),
                  2.0 * db.rows() * db.cols() * lb.cols());
     gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, dxh,
-              db.cols(), nullptr, 0);
-    all_reduce_sum(ctx, lb.lay.col, dxh, db.rows() * db.cols(), wire);
+              ld8(db.cols()), nullptr, 0);
+    all_reduce_sum(ctx, lb.lay.col, dxh, db.rows() * ld8(db.cols()), wire);
   }
   for (int l = cfg.layers; l >= 1; --l) {
     LayerBufs& L = st.layers[l - 1];
@@ -512,9 +521,9 @@ void backward(State& st, const Batch& bt, int precision) {
       if (pmm_trivial(ctx)) {
         dres = dxh;  // identical block; the SpMM below accumulates into it
       } else {
-        dres = grow<float>(st.dres, F.rows() * F.cols());
-        reshard(ctx, reshard_work(), db, bt.batch_off[db.lay.row], hoff(ctx, H, db.lay.col), dxh, db.cols(), F, dres,
-                F.cols());
+        dres = grow<float>(st.dres, F.rows() * ld8(F.cols()));
+        reshard(ctx, reshard_work(), db, bt.batch_off[db.lay.row], hoff(ctx, H, db.lay.col), dxh, ld8(db.cols()), F, dres,
+                ld8(F.cols()));
       }
     }
     // fused element-wise backward + RMSNorm backward -> dxw (bf16), dgamma
@@ -522,9 +531,11 @@ void backward(State& st, const Batch& bt, int precision) {
     ba.rows = rows;
     ba.cols = cols;
     ba.dy = dxh;
-    ba.lddy = db.cols();
-    ba.mask = L.mask.as<uint8_t>();
+    ba.lddy = ld8(db.cols());
+    ba.mask = L.mask.as<uint32_t>();
     ba.ldm = L.ldm;
+    const bool row_local = trivial(ctx, xb.lay.col);
+    ba.fuse_s = row_local ? 1 : 0;
     ba.keep_scale = st.fwd_keep_scale;
     ba.x = L.xw_t.f;
     ba.ldx = L.xw_t.ldf;
@@ -540,8 +551,10 @@ void backward(State& st, const Batch& bt, int precision) {
       ba.gamma = W + gp.off;
       ba.rms = L.rms.as<float>();
       ba.s = grow<float>(st.s_row, rows);
-      bwd_stats(ctx, ba);
-      all_reduce_sum(ctx, xb.lay.col, ba.s, rows, false);
+      if (!row_local) {
+        bwd_stats(ctx, ba);
+        all_reduce_sum(ctx, xb.lay.col, ba.s, rows, false);
+      }
       const int blocks = bwd_apply_blocks(ctx, rows, cols);
       ba.dgamma_part = grow<float>(st.dg_part, static_cast<int64_t>(blocks) * cols);
       bwd_apply(ctx, ba, blocks);
@@ -588,13 +601,13 @@ void backward(State& st, const Batch& bt, int precision) {
     if (inplace) {
       // dxh (== dres) += A_t . dhagg
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
-               dxh, F.cols(), nullptr, 0, 1);
+               dxh, ld8(F.cols()), nullptr, 0, 1);
     } else {
-      float* nd = grow<float>(st.dxh2, F.rows() * F.cols());
+      float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
-               nd, F.cols(), nullptr, 0, 0);
-      if (ar_s) all_reduce_sum(ctx, alay.row, nd, F.rows() * F.cols(), wire);
-      if (dres) add_inplace(ctx, nd, F.cols(), dres, F.cols(), F.rows(), F.cols());
+               nd, ld8(F.cols()), nullptr, 0, 0);
+      if (ar_s) all_reduce_sum(ctx, alay.row, nd, F.rows() * ld8(F.cols()), wire);
+      if (dres) add_inplace(ctx, nd, ld8(F.cols()), dres, ld8(F.cols()), F.rows(), F.cols());
       std::swap(st.dxh, st.dxh2);
       dxh = nd;
     }
@@ -608,7 +621,7 @@ void backward(State& st, const Batch& bt, int precision) {
     bf16* dxb = grow<bf16>(st.dxh_b, rows * ldb);
     {
       ProfScope ps(ctx, kProfElementwise, static_cast<double>(rows) * cols * 6);
-      cast_bf16(ctx, dxh, rows, cols, cols, dxb, ldb);
+      cast_bf16(ctx, dxh, rows, cols, ld8(cols), dxb, ldb);
     }
     const int64_t kin = bt.x_c1 - bt.x_c0;
     ProfScope ps(ctx, kProfGemmWgrad, gemm_bytes(kin, cols, rows, 2, 2, 4), 2.0 * rows * kin * cols);

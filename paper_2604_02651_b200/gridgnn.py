@@ -344,6 +344,41 @@ class StepBatch:
             pass
 
 
+class _BorrowedBatch(StepBatch):
+    """A batch owned by a Prefetcher slot (never destroyed from Python)."""
+
+    def close(self):
+        self.h = None
+
+
+class Prefetcher:
+    """Sampling/training overlap (the train_run producer thread + PrefetchQueue,
+    model.hpp:556-581): a native producer thread samples step t+1 on its own
+    stream while step t trains; next() returns the batch of the following step."""
+
+    def __init__(self, ctx: Context, graph: Graph, b: int, group_seed: int, first_step: int = 0):
+        self.ctx, self.graph = ctx, graph
+        h = P()
+        check(lib().ggb_prefetch_create(ctx.h, graph.h, b, group_seed, first_step, C.byref(h)))
+        self.h = h
+
+    def next(self) -> StepBatch:
+        bh = P()
+        check(lib().ggb_prefetch_next(self.h, C.byref(bh)))
+        return _BorrowedBatch(self.graph, bh)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ggb_prefetch_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def build_step_batch(ctx: Context, graph: Graph, b: int, group_seed: int, step: int,
                      reuse: StepBatch | None = None) -> StepBatch:
     """model.hpp:250-309: the rank-local batch; communication-free."""

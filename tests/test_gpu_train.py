@@ -161,6 +161,34 @@ def test_dropout_mask_matches_hash(gg, orc, ref):
         ref.free_dataset(h)
 
 
+def test_prefetch_is_transparent(gg, orc):
+    """acceptance criterion 8 (acceptance.cpp:419-444): the prefetched run
+    (producer thread, own stream) yields bit-identical batches and identical
+    per-step losses and weights."""
+    n, d_in, ncls, b, seed = 3000, 16, 5, 700, 4
+    ds = orc.generate_synthetic(n, 9.0, d_in, ncls, 8)
+    ctx = gg.Context()
+    g = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls, 3)
+    cfg = gg.ModelConfig(layers=3, d_in=d_in, d_h=32, d_out=ncls, dropout_rate=0.2)
+    gs = gg.hash_combine(seed, 0)
+    st_a, st_b = gg.init_state(ctx, cfg, seed), gg.init_state(ctx, cfg, seed)
+    pf = gg.Prefetcher(ctx, g, b, gs, 0)
+    plain = None
+    for t in range(6):
+        pb = pf.next()
+        plain = gg.build_step_batch(ctx, g, b, gs, t, reuse=plain)
+        assert np.array_equal(pb.sample, plain.sample)
+        assert np.array_equal(pb.a(0).col_idx, plain.a(0).col_idx)
+        la = gg.train_step(ctx, st_a, pb, gg.FP32, seed, t)
+        gg.optimizer_step(ctx, st_a, gg.ADAM, 1e-3)
+        lb = gg.train_step(ctx, st_b, plain, gg.FP32, seed, t)
+        gg.optimizer_step(ctx, st_b, gg.ADAM, 1e-3)
+        assert la == lb
+    for wa, wb in zip(st_a.weights(), st_b.weights()):
+        assert np.array_equal(wa, wb)
+    pf.close()
+
+
 def test_contract_errors(gg, orc):
     ctx = gg.Context()
     with pytest.raises(gg.InvalidArgument):
