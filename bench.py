@@ -232,7 +232,7 @@ def main():
     group_seed = gg.hash_combine(RUN_SEED, grid.dp_group(rank))
     batch = None
     # sampling of step t+1 overlaps training of step t (producer thread + own stream)
-    pf = gg.Prefetcher(ctx, graph, b, group_seed, 0) if args.prefetch else None
+    pf = gg.Prefetcher(ctx, graph, b, group_seed, 0, run_seed=RUN_SEED, cfg=mcfg) if args.prefetch else None
 
     def step(gstep: int, sync_loss: bool):
         nonlocal batch

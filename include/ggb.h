@@ -113,9 +113,14 @@ int ggb_batch_destroy(ggb_batch_t batch);
  * ctx stream after it with a CUDA event and releasing the previous batch once
  * the ctx stream's work on it completes. Handed-out batches are owned by the
  * prefetcher (do not destroy them); they are bit-identical to
- * ggb_build_step_batch's. */
+ * ggb_build_step_batch's. With layers > 0 and dropout_rate > 0 the producer
+ * also evaluates each layer's dropout keep-bits for the step ahead
+ * (element_unit(dropout_key(run_seed, dp, step, l), row, col) >= rate,
+ * pmm.hpp:317-322, model.hpp:164-171), taking the integer hashing off the
+ * training stream; the forward uses them when its keys match. */
 typedef struct ggb_prefetch_s* ggb_prefetch_t;
 int ggb_prefetch_create(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group_seed, uint64_t first_step,
+                        uint64_t run_seed, int32_t layers, int64_t d_h, double dropout_rate,
                         ggb_prefetch_t* out);
 int ggb_prefetch_next(ggb_prefetch_t pf, ggb_batch_t* batch_out);
 int ggb_prefetch_destroy(ggb_prefetch_t pf);

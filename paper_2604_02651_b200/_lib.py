@@ -47,7 +47,7 @@ _SIGS = [
     ("ggb_graph_info", C.c_int, [P, P]),
     ("ggb_build_step_batch", C.c_int, [P, P, I64, U64, U64, P]),
     ("ggb_batch_destroy", C.c_int, [P]),
-    ("ggb_prefetch_create", C.c_int, [P, P, I64, U64, U64, P]),
+    ("ggb_prefetch_create", C.c_int, [P, P, I64, U64, U64, U64, I32, I64, F64, P]),
     ("ggb_prefetch_next", C.c_int, [P, P]),
     ("ggb_prefetch_destroy", C.c_int, [P]),
     ("ggb_batch_info", C.c_int, [P, P]),

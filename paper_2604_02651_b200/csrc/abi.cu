@@ -412,11 +412,12 @@ int ggb_build_step_batch(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group
 }
 
 int ggb_prefetch_create(ggb_ctx_t ctx, ggb_graph_t g, int64_t b, uint64_t group_seed, uint64_t first_step,
+                        uint64_t run_seed, int32_t layers, int64_t d_h, double dropout_rate,
                         ggb_prefetch_t* out) {
   return guard([&] {
     use_device(*ctx);
     require(g && out, "prefetch: null argument");
-    *out = new ggb_prefetch_s(*ctx, *g, b, group_seed, first_step);
+    *out = new ggb_prefetch_s(*ctx, *g, b, group_seed, first_step, run_seed, layers, d_h, dropout_rate);
   });
 }
 

@@ -25,6 +25,7 @@ struct FwdApply {
   bf16* outb;  // bf16 copy (nullable) = hi part of the split pair
   bf16* outlo; // bf16 lo part (nullable): out == hi + lo to ~2^-16
   int64_t ldob;
+  const uint32_t* keep;  // precomputed dropout keep-bits (same layout) or null: hash in-kernel
   uint32_t* mask;  // [rows][ldm] keep bits, row-kernel layout (see kRowChunk)
   int64_t ldm;     // words per row = mask_words(cols)
   int fuse_ss;     // 1: the row is complete here, compute ss in-kernel (ss ignored)
@@ -93,6 +94,9 @@ int ce_grad_blocks(int64_t rows);
 void ce_grad(Ctx& ctx, const CeArgs& p);
 // all three cross-entropy passes in one warp-per-row kernel (row fully local)
 void ce_fused(Ctx& ctx, const CeArgs& p);
+// keep-bits of a rows x cols block at global (row_g0, col_g0), row-kernel layout
+void dropout_keep(Ctx& ctx, uint64_t key, int64_t rows, int64_t cols, int64_t row_g0, int64_t col_g0,
+                  uint64_t thresh, uint32_t* out, int64_t ldm);
 void scale_scalar(Ctx& ctx, const float* in, float s, float* out);
 void adam(Ctx& ctx, float* w, const float* g, float* m, float* v, int64_t n, double lr, double bc1,
           double bc2);

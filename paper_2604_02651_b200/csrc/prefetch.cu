@@ -14,15 +14,22 @@
 #include <mutex>
 #include <thread>
 
+#include <cmath>
+
 #include "comm.hpp"
+#include "ops.hpp"
 #include "prefetch.hpp"
 #include "prof.hpp"
+#include "rng.cuh"
 
 namespace ggb {
 
-Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t seed_, uint64_t first_step)
-    : consumer(&consumer_), g(&g_), b(b_), seed(seed_), step0(first_step) {
+Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t seed_, uint64_t first_step,
+                       uint64_t run_seed_, int drop_layers_, int64_t d_h_, double rate_)
+    : consumer(&consumer_), g(&g_), b(b_), seed(seed_), step0(first_step), run_seed(run_seed_),
+      drop_layers(rate_ > 0.0 ? drop_layers_ : 0), d_h(d_h_), rate(rate_) {
   require(b >= 2 && b <= g->n, "prefetch: need 2 <= b <= N");
+  require(rate >= 0.0 && rate < 1.0, "prefetch: dropout rate must be in [0, 1)");
   sctx.grid = consumer->grid;
   sctx.rank = consumer->rank;
   for (int a = 0; a < 4; ++a) sctx.coord[a] = consumer->coord[a];
@@ -66,6 +73,7 @@ void Prefetcher::run() {
       }
       if (k >= 2) GGB_CUDA(cudaStreamWaitEvent(sctx.stream, released[slot], 0));
       build_step_batch(sctx, *g, b, seed, step0 + static_cast<uint64_t>(k), slots[slot]);
+      if (drop_layers > 0) make_masks(slots[slot], step0 + static_cast<uint64_t>(k));
       GGB_CUDA(cudaEventRecord(ready[slot], sctx.stream));
       {
         std::lock_guard<std::mutex> lk(m);
@@ -78,6 +86,29 @@ void Prefetcher::run() {
     err = std::current_exception();
     failed = true;
     cv.notify_all();
+  }
+}
+
+// Keep-bits of every layer's output block (feature_layout(l+1), the block
+// the forward's fused RMSNorm/ReLU/dropout kernel writes) for global step
+// gstep, keyed exactly as detail::dropout_key (model.hpp:164-171).
+void Prefetcher::make_masks(Batch& bt, uint64_t gstep) {
+  bt.masks.resize(static_cast<size_t>(drop_layers));
+  const uint64_t thresh = static_cast<uint64_t>(std::ceil(rate * 0x1.0p53));
+  for (int l = 1; l <= drop_layers; ++l) {
+    const Layout out = feature_layout(l + 1);
+    const auto& ro = bt.batch_off[out.row];
+    const auto co = block_partition(d_h, sctx.grid.dims[out.col]);
+    DropMask& dm = bt.masks[l - 1];
+    dm.key = dropout_key(run_seed, sctx.coord[0], gstep, l);
+    dm.thresh = thresh;
+    dm.r0 = ro[sctx.coord[out.row]];
+    dm.rows = ro[sctx.coord[out.row] + 1] - dm.r0;
+    dm.c0 = co[sctx.coord[out.col]];
+    dm.cols = co[sctx.coord[out.col] + 1] - dm.c0;
+    dm.ldm = mask_words(std::max<int64_t>(dm.cols, 1));
+    uint32_t* bits = dm.bits.reserve_n<uint32_t>(std::max<int64_t>(dm.rows, 1) * dm.ldm);
+    dropout_keep(sctx, dm.key, dm.rows, dm.cols, dm.r0, dm.c0, thresh, bits, dm.ldm);
   }
 }
 

@@ -24,9 +24,17 @@ struct Prefetcher {
   bool stop = false, failed = false;
   std::exception_ptr err;
 
-  Prefetcher(Ctx& consumer, const Graph& g, int64_t b, uint64_t seed, uint64_t first_step);
+  // dropout keep-bits generated ahead with each batch (drop_layers == 0: none)
+  uint64_t run_seed = 0;
+  int drop_layers = 0;
+  int64_t d_h = 0;
+  double rate = 0.0;
+
+  Prefetcher(Ctx& consumer, const Graph& g, int64_t b, uint64_t seed, uint64_t first_step,
+             uint64_t run_seed = 0, int drop_layers = 0, int64_t d_h = 0, double rate = 0.0);
   ~Prefetcher();
   void run();
+  void make_masks(Batch& bt, uint64_t gstep);
   Batch* next();  // batch for step first_step + (number of previous calls)
 };
 

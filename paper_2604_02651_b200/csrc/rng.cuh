@@ -31,6 +31,12 @@ __host__ __device__ __forceinline__ bool element_keep(uint64_t row_key, uint64_t
   return (h >> 11) >= thresh;
 }
 
+/// detail::dropout_key (model.hpp:164-171).
+__host__ __device__ __forceinline__ uint64_t dropout_key(uint64_t seed, int dp, uint64_t gstep, int layer) {
+  return hash_combine(hash_combine(hash_combine(hash_combine(seed, 0xd509), static_cast<uint64_t>(dp)), gstep),
+                      static_cast<uint64_t>(layer));
+}
+
 /// rng.hpp:73-76 as a double.
 __host__ __device__ __forceinline__ double element_unit(uint64_t key, uint64_t i, uint64_t j) {
   const uint64_t h = splitmix64(hash_combine(hash_combine(key, i), j));

@@ -67,7 +67,9 @@ __device__ __forceinline__ void f4(const float4& a, float* v) {
   v[3] = a.w;
 }
 
+template <int J>  // chunks of 128 columns held per row
 __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
+  constexpr int kMaxJ = J;
   const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
   if (r >= p.rows) return;
@@ -107,8 +109,11 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
     for (int i = 0; i < 4; ++i) {
       const float y = p.gamma ? g[i] * x[j][i] * inv : x[j][i];
       float sc = y > 0.f ? 1.f : 0.f;
-      if (p.drop && sc != 0.f && c + i < p.cols)
+      if (p.drop && p.keep) {  // precomputed keep-bits (prefetcher)
+        sc = (sc != 0.f && ((p.keep[r * p.ldm + 4 * j + i] >> lane) & 1u)) ? p.keep_scale : 0.f;
+      } else if (p.drop && sc != 0.f && c + i < p.cols) {
         sc = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + c + i), p.thresh) ? p.keep_scale : 0.f;
+      }
       const unsigned bits = __ballot_sync(0xffffffffu, sc != 0.f && c + i < p.cols);
       if (lane == i) p.mask[r * p.ldm + 4 * j + i] = bits;
       o[i] = y * sc + res[i];
@@ -124,6 +129,26 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
       }
     }
   }
+}
+
+// Dropout keep-bits element_unit(key, row, col) >= rate (pmm.hpp:317-322) of
+// a block, in the row-kernel layout: one thread per (row, word), word 4j+i
+// holding bit l for column 128j + 4l + i. Pure integer work, independent of
+// the activations, so the prefetcher runs it ahead on its own stream.
+__global__ void k_dropout_keep(uint64_t key, int64_t rows, int64_t cols, int64_t row_g0, int64_t col_g0,
+                               uint64_t thresh, uint32_t* __restrict__ out, int64_t ldm) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows * ldm) return;
+  const int64_t r = t / ldm, w = t % ldm;
+  const int64_t j = w / 4, i = w % 4;
+  const uint64_t row_key = hash_combine(key, static_cast<uint64_t>(row_g0 + r));
+  uint32_t bits = 0;
+#pragma unroll 4
+  for (int l = 0; l < 32; ++l) {
+    const int64_t c = j * kRowChunk + 4 * l + i;
+    if (c < cols && element_keep(row_key, static_cast<uint64_t>(col_g0 + c), thresh)) bits |= 1u << l;
+  }
+  out[t] = bits;
 }
 
 // Row dot product s_r = sum_j dxn * gamma * x (the all-reduced input of the
@@ -154,7 +179,9 @@ __global__ void __launch_bounds__(kT) k_bwd_row_stats(BwdApply p) {
 // dx = gamma*dxn/r - x*s/(d r^3) (bf16 out); dgamma_j += dxn*x/r accumulated
 // per lane over the block's rows (grid-stride), then reduced across the
 // block's warps into dgamma_part[block][cols].
+template <int J>
 __global__ void __launch_bounds__(kT) k_bwd_row(BwdApply p) {
+  constexpr int kMaxJ = J;
   __shared__ float sh[kRowsPerBlock][kMaxJ * kRowChunk];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nj = static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
@@ -267,6 +294,64 @@ __global__ void __launch_bounds__(kT) k_ce_row(CeArgs p) {
   }
 }
 
+// Register-resident variant for narrow class blocks: LPR lanes per row (32/LPR
+// rows per warp), VPL logits per lane, one global read of the row.
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kT) k_ce_row_reg(CeArgs p) {
+  constexpr int RPW = 32 / LPR;
+  __shared__ float part[kRowsPerBlock];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, gl = lane % LPR;
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib) * RPW + lane / LPR;
+  const bool ok = r < p.rows;
+  float v[VPL];
+  float m = -3.402823466e38f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int64_t j = gl + static_cast<int64_t>(LPR) * k;
+    v[k] = (ok && j < p.cols) ? p.logits[r * p.ld + j] : -3.402823466e38f;
+    m = fmaxf(m, v[k]);
+  }
+#pragma unroll
+  for (int o = LPR / 2; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float z = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int64_t j = gl + static_cast<int64_t>(LPR) * k;
+    v[k] = (ok && j < p.cols) ? expf(v[k] - m) : 0.f;
+    z += v[k];
+  }
+#pragma unroll
+  for (int o = LPR / 2; o; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+  float contrib = 0.f;
+  if (ok) {
+    const int64_t y = p.labels[p.row_g0 + r];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int64_t j = gl + static_cast<int64_t>(LPR) * k;
+      if (j >= p.cols) continue;
+      float g = v[k] / z;
+      if (p.c0 + j == y) g -= 1.f;
+      const float d = g * p.invb;
+      if (p.dlog) p.dlog[r * p.lddlog + j] = d;
+      if (p.dlogb) p.dlogb[r * p.lddlogb + j] = __float2bfloat16_rn(d);
+    }
+    if (gl == 0) {
+      const float zy = (y >= p.c0 && y < p.c0 + p.cols) ? p.logits[r * p.ld + (y - p.c0)] : 0.f;
+      contrib = (m + logf(z)) - zy;
+    }
+  }
+  // warp total of the row contributions (lanes gl == 0 hold them)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, o);
+  if (lane == 0) part[wib] = contrib;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int k = 0; k < kRowsPerBlock; ++k) s += part[k];
+    p.loss_part[blockIdx.x] = s;
+  }
+}
+
 __global__ void k_sum_parts_row(const float* __restrict__ part, int64_t n, float* __restrict__ out) {
   __shared__ float sh[kT];
   float s = 0.f;
@@ -289,7 +374,12 @@ void fwd_apply(Ctx& ctx, const FwdApply& p) {
   require(p.cols <= kMaxJ * kRowChunk, "row kernels: at most 512 local feature columns");
   require(p.ldx % 4 == 0 && (!p.res || p.ldres % 4 == 0) && (!p.out || p.ldo % 4 == 0),
           "row kernels: fp32 rows must be 16-byte aligned");
-  k_fwd_row<<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
+  if (p.cols <= kRowChunk)
+    k_fwd_row<1><<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
+  else if (p.cols <= 2 * kRowChunk)
+    k_fwd_row<2><<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
+  else
+    k_fwd_row<kMaxJ><<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
@@ -303,22 +393,48 @@ void bwd_stats(Ctx& ctx, const BwdApply& p) {
 
 int bwd_apply_blocks(Ctx& ctx, int64_t rows, int64_t cols) {
   (void)cols;
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), 8 * ctx.num_sms)));
+  // few enough blocks that the dgamma partials reduce in microseconds, enough
+  // warps (2 blocks x 8 warps per SM, grid-stride) to saturate HBM
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), 4 * ctx.num_sms)));
 }
 
 void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks) {
   if (p.rows <= 0) return;
   require(p.cols <= kMaxJ * kRowChunk, "row kernels: at most 512 local feature columns");
   require(p.lddy % 4 == 0 && p.ldx % 4 == 0, "row kernels: fp32 rows must be 16-byte aligned");
-  k_bwd_row<<<blocks, kT, 0, ctx.stream>>>(p);
+  if (p.cols <= kRowChunk)
+    k_bwd_row<1><<<blocks, kT, 0, ctx.stream>>>(p);
+  else if (p.cols <= 2 * kRowChunk)
+    k_bwd_row<2><<<blocks, kT, 0, ctx.stream>>>(p);
+  else
+    k_bwd_row<kMaxJ><<<blocks, kT, 0, ctx.stream>>>(p);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+void dropout_keep(Ctx& ctx, uint64_t key, int64_t rows, int64_t cols, int64_t row_g0, int64_t col_g0,
+                  uint64_t thresh, uint32_t* out, int64_t ldm) {
+  if (rows <= 0) return;
+  k_dropout_keep<<<static_cast<unsigned>(ceil_div(rows * ldm, 128)), 128, 0, ctx.stream>>>(
+      key, rows, cols, row_g0, col_g0, thresh, out, ldm);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
 
 void ce_fused(Ctx& ctx, const CeArgs& p) {
-  const unsigned blocks = std::max(1u, row_blocks(p.rows));
+  // rows per block: 8 warps x (32 / lanes-per-row)
+  const int rpw = p.cols <= 64 ? 2 : 1;
+  const unsigned blocks = std::max<unsigned>(1u, static_cast<unsigned>(ceil_div(p.rows, kRowsPerBlock * rpw)));
+  require(static_cast<int64_t>(blocks) <= ce_grad_blocks(p.rows) + 1, "ce: partial buffer too small");
   if (p.rows > 0) {
-    k_ce_row<<<blocks, kT, 0, ctx.stream>>>(p);
+    if (p.cols <= 64)
+      k_ce_row_reg<16, 4><<<blocks, kT, 0, ctx.stream>>>(p);
+    else if (p.cols <= 128)
+      k_ce_row_reg<32, 4><<<blocks, kT, 0, ctx.stream>>>(p);
+    else if (p.cols <= 256)
+      k_ce_row_reg<32, 8><<<blocks, kT, 0, ctx.stream>>>(p);
+    else
+      k_ce_row<<<blocks, kT, 0, ctx.stream>>>(p);
     ctx.launches += 1;
   } else {
     GGB_CUDA(cudaMemsetAsync(p.loss_part, 0, sizeof(float), ctx.stream));

@@ -78,8 +78,17 @@ struct BatchCsr {
   DevBuf val64;    // double (exact reference values, for export)
 };
 
+/// Precomputed dropout keep-bits of one layer's output block (row-kernel
+/// layout, ops.hpp kRowChunk): element_unit(key, r0+i, c0+j) >= rate.
+struct DropMask {
+  uint64_t key = 0, thresh = 0;
+  int64_t r0 = 0, c0 = 0, rows = -1, cols = -1, ldm = 0;
+  DevBuf bits;  // uint32 [rows][ldm]
+};
+
 struct Batch {
   Ctx* ctx = nullptr;
+  std::vector<DropMask> masks;  // per layer, filled by the prefetcher
   int64_t b = 0, n = 0;
   int planes = 0;
   DevBuf sample;  // int64 [b], strictly increasing

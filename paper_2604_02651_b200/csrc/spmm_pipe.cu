@@ -1,0 +1,293 @@
+// Pipelined row-split SpMM (the production path of spmm, pmm.hpp:134-167).
+//
+// Each warp of a persistent grid (one CTA per SM) owns a contiguous range of
+// output rows and streams the nonzeros of that range in CSR order through a
+// private STAGES-deep ring in shared memory: for every nonzero the gathered
+// feature row (RB bytes: 256, 512 or 1024) is copied with cp.async (LDGSTS,
+// 16 B per lane), so rows in flight cost shared memory, not registers, and
+// the row_ptr -> col/val -> feature-row dependency chain is hidden behind
+// STAGES-1 stages of look-ahead. A stage is 4 KB = S = 4096/RB nonzeros; its
+// copies are issued by one unrolled loop of 8 warp-wide LDGSTS (every lane
+// copies one 16-byte chunk per iteration), so the issue side costs a few
+// instructions per nonzero. Column ids / values are loaded one stage ahead.
+// The consumer accumulates in fp32 registers (lane l owns 16-byte chunks l and
+// l+32 of the row) and flushes a row when the stream crosses its row_ptr
+// boundary; empty rows flush zeros.
+#include "runtime.hpp"
+
+namespace ggb {
+namespace {
+
+constexpr int kWarps = 16;
+constexpr int kStages = 3;
+constexpr int kStageBytes = 4096;  // per warp per stage
+
+struct PipeArgs {
+  int64_t rows;
+  const int64_t* rp;
+  const int32_t* col;
+  const float* val;
+  const uint8_t* F;  // feature rows
+  uint32_t ldf_bytes;
+  int vcpr;  // valid 16-byte chunks of a row (the rest of RB is not read)
+  int fcols;
+  float* out;
+  int64_t ldo;
+  bf16* outb;
+  bf16* outlo;
+  int64_t ldob;
+  int accumulate;
+};
+
+__device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// TIn: element type of F; RB: smem bytes per gathered row.
+template <class TIn, int RB>
+__global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) {
+  constexpr int EPC = 16 / static_cast<int>(sizeof(TIn));  // elements per 16-byte chunk
+  constexpr int CPR = RB / 16;                              // chunks per row slot
+  constexpr int S = kStageBytes / RB;                       // nonzeros per stage
+  constexpr int CPL = CPR > 32 ? 2 : 1;                     // chunks per lane (consumer)
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint8_t* ring = smem + static_cast<size_t>(wib) * kStages * kStageBytes;
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  float* meta_val = reinterpret_cast<float*>(smem + kWarps * kStages * kStageBytes) + wib * kStages * 32;
+
+  const int64_t total_warps = static_cast<int64_t>(gridDim.x) * kWarps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + wib;
+  const int64_t per = (a.rows + total_warps - 1) / total_warps;
+  const int64_t r_begin = imin(a.rows, gw * per), r_end = imin(a.rows, r_begin + per);
+  if (r_begin >= r_end) return;
+  const int64_t e_begin = a.rp[r_begin], e_end = a.rp[r_end];
+  const int64_t n_stages = (e_end - e_begin + S - 1) / S;
+
+  int32_t nx_col = 0;  // lane k < S: column id / value of entry k of the next stage to issue
+  float nx_val = 0.f;
+  auto load_meta = [&](int64_t t) {
+    const int64_t e = e_begin + t * S + lane;
+    nx_col = 0;
+    nx_val = 0.f;
+    if (lane < S && t < n_stages && e < e_end) {
+      nx_col = __ldg(a.col + e);
+      nx_val = __ldg(a.val + e);
+    }
+  };
+  auto issue = [&](int64_t t) {
+    if (t < n_stages) {
+      const int slot = static_cast<int>(t % kStages);
+      const int valid = static_cast<int>(imin(S, e_end - (e_begin + t * S)));
+      if (lane < S) meta_val[slot * 32 + lane] = nx_val;
+      const uint32_t dst0 = ring_s + slot * kStageBytes;
+#pragma unroll
+      for (int it = 0; it < kStageBytes / 512; ++it) {
+        const int idx = it * 32 + lane;  // chunk of the stage: entry k, chunk ch
+        const int k = idx / CPR, ch = idx % CPR;
+        const int32_t c = __shfl_sync(0xffffffffu, nx_col, k);
+        if (k < valid && ch < a.vcpr)
+          cp_async16(dst0 + idx * 16, a.F + static_cast<uint64_t>(static_cast<uint32_t>(c)) * a.ldf_bytes + ch * 16);
+      }
+    }
+    cp_commit();
+    load_meta(t + 1);
+  };
+
+  load_meta(0);
+#pragma unroll 1
+  for (int t = 0; t < kStages - 1; ++t) issue(t);
+
+  float acc[CPL][EPC];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int i = 0; i < EPC; ++i) acc[q][i] = 0.f;
+  int64_t row = r_begin;
+  int64_t row_end_e = a.rp[row + 1];
+
+  auto flush = [&]() {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int ch = lane + 32 * q;
+      const int64_t cc = static_cast<int64_t>(ch) * EPC;
+      if (ch < a.vcpr) {
+        const bool whole = cc + EPC <= a.fcols;
+        if (a.out) {
+          float* dst = a.out + row * a.ldo + cc;
+          if (whole && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int v = 0; v < EPC; v += 4) {
+              float4 o = make_float4(acc[q][v], acc[q][v + 1], acc[q][v + 2], acc[q][v + 3]);
+              if (a.accumulate) {
+                const float4 p = *reinterpret_cast<const float4*>(dst + v);
+                o.x += p.x;
+                o.y += p.y;
+                o.z += p.z;
+                o.w += p.w;
+                acc[q][v] = o.x;
+                acc[q][v + 1] = o.y;
+                acc[q][v + 2] = o.z;
+                acc[q][v + 3] = o.w;
+              }
+              *reinterpret_cast<float4*>(dst + v) = o;
+            }
+          } else {
+            for (int i = 0; i < EPC && cc + i < a.fcols; ++i) {
+              if (a.accumulate) acc[q][i] += dst[i];
+              dst[i] = acc[q][i];
+            }
+          }
+        }
+        if (a.outb) {
+          bf16* db = a.outb + row * a.ldob + cc;
+          bf16* dl = a.outlo ? a.outlo + row * a.ldob + cc : nullptr;
+          if (whole && (reinterpret_cast<uintptr_t>(db) & (EPC * 2 - 1)) == 0) {
+            uint32_t hi[EPC / 2], lo[EPC / 2];
+#pragma unroll
+            for (int v = 0; v < EPC; v += 2) {
+              hi[v / 2] = pack_bf16(acc[q][v], acc[q][v + 1]);
+              const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&hi[v / 2]);
+              const float2 hf = __bfloat1622float2(h);
+              lo[v / 2] = pack_bf16(acc[q][v] - hf.x, acc[q][v + 1] - hf.y);
+            }
+            if constexpr (EPC == 8) {
+              *reinterpret_cast<uint4*>(db) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+              if (dl) *reinterpret_cast<uint4*>(dl) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            } else {
+              *reinterpret_cast<uint2*>(db) = make_uint2(hi[0], hi[1]);
+              if (dl) *reinterpret_cast<uint2*>(dl) = make_uint2(lo[0], lo[1]);
+            }
+          } else {
+            for (int i = 0; i < EPC && cc + i < a.fcols; ++i) {
+              const bf16 h = __float2bfloat16_rn(acc[q][i]);
+              db[i] = h;
+              if (dl) dl[i] = __float2bfloat16_rn(acc[q][i] - __bfloat162float(h));
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < EPC; ++i) acc[q][i] = 0.f;
+    }
+  };
+
+#pragma unroll 1
+  for (int64_t t = 0; t < n_stages; ++t) {
+    issue(t + kStages - 1);
+    cp_wait<kStages - 1>();
+    __syncwarp();
+    const int slot = static_cast<int>(t % kStages);
+    const int64_t e0 = e_begin + t * S;
+    const int valid = static_cast<int>(imin(S, e_end - e0));
+    const uint8_t* base = ring + slot * kStageBytes;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      if (k < valid) {
+        while (e0 + k >= row_end_e) {  // crossed into the next row(s): flush; empty rows give zeros
+          flush();
+          ++row;
+          row_end_e = a.rp[row + 1];
+        }
+        const float v = meta_val[slot * 32 + k];
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          const int ch = lane + 32 * q;
+          if (ch < a.vcpr) {
+            const uint4 u = *reinterpret_cast<const uint4*>(base + k * RB + ch * 16);
+            if constexpr (sizeof(TIn) == 2) {
+              const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 f = __bfloat1622float2(h[i]);
+                acc[q][2 * i] = fmaf(v, f.x, acc[q][2 * i]);
+                acc[q][2 * i + 1] = fmaf(v, f.y, acc[q][2 * i + 1]);
+              }
+            } else {
+              acc[q][0] = fmaf(v, __uint_as_float(u.x), acc[q][0]);
+              acc[q][1] = fmaf(v, __uint_as_float(u.y), acc[q][1]);
+              acc[q][2] = fmaf(v, __uint_as_float(u.z), acc[q][2]);
+              acc[q][3] = fmaf(v, __uint_as_float(u.w), acc[q][3]);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();  // the slot is refilled by a later issue
+  }
+  cp_wait<0>();
+  while (row < r_end) {  // the last row and any trailing empty rows of the range
+    flush();
+    ++row;
+  }
+}
+
+template <class TIn, int RB>
+void launch_pipe(Ctx& ctx, const PipeArgs& a) {
+  const int smem = kWarps * kStages * kStageBytes + kWarps * kStages * 32 * 4;
+  static bool attr = false;
+  if (!attr) {
+    GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_spmm_pipe<TIn, RB><<<ctx.num_sms, kWarps * 32, smem, ctx.stream>>>(a);
+}
+
+}  // namespace
+
+// Row-split SpMM through the pipelined kernel when a gathered row fits a
+// 1 KB slot; returns false otherwise (the caller falls back).
+bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val, const void* f,
+               int esize, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb, bf16* outlo, int64_t ldob,
+               int accumulate) {
+  const int64_t row_bytes = round_up(fcols * esize, 16);
+  if (row_bytes > 1024 || rows <= 0 || fcols <= 0) return false;
+  if (ldf * esize >= (int64_t{1} << 32)) return false;
+  PipeArgs a{};
+  a.rows = rows;
+  a.rp = rp;
+  a.col = col;
+  a.val = val;
+  a.F = static_cast<const uint8_t*>(f);
+  a.ldf_bytes = static_cast<uint32_t>(ldf * esize);
+  a.vcpr = static_cast<int>(row_bytes / 16);
+  a.fcols = static_cast<int>(fcols);
+  a.out = out;
+  a.ldo = ldo;
+  a.outb = outb;
+  a.outlo = outlo;
+  a.ldob = ldob;
+  a.accumulate = accumulate;
+  if (esize == 2) {
+    if (row_bytes <= 256)
+      launch_pipe<bf16, 256>(ctx, a);
+    else if (row_bytes <= 512)
+      launch_pipe<bf16, 512>(ctx, a);
+    else
+      launch_pipe<bf16, 1024>(ctx, a);
+  } else {
+    if (row_bytes <= 256)
+      launch_pipe<float, 256>(ctx, a);
+    else if (row_bytes <= 512)
+      launch_pipe<float, 512>(ctx, a);
+    else
+      launch_pipe<float, 1024>(ctx, a);
+  }
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+  return true;
+}
+
+}  // namespace ggb

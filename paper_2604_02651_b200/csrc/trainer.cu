@@ -104,11 +104,6 @@ ReshardWork& reshard_work() {
 
 bool pmm_trivial(const Ctx& ctx) { return ctx.grid.dims[1] == 1 && ctx.grid.dims[2] == 1 && ctx.grid.dims[3] == 1; }
 
-uint64_t dropout_key(uint64_t seed, int dp, uint64_t gstep, int layer) {  // model.hpp:164-171
-  return hash_combine(hash_combine(hash_combine(hash_combine(seed, 0xd509), static_cast<uint64_t>(dp)), gstep),
-                      static_cast<uint64_t>(layer));
-}
-
 }  // namespace
 
 // ---- init_state (model.hpp:175-208) -------------------------------------------------
@@ -410,6 +405,13 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     fa.ldob = L.x.ldb;
     fa.mask = grow<uint32_t>(L.mask, xb.rows() * L.ldm);
     fa.ldm = L.ldm;
+    fa.keep = nullptr;  // keep-bits precomputed by the prefetcher for exactly this block?
+    if (drop && bt.masks.size() >= static_cast<size_t>(l)) {
+      const DropMask& dm = bt.masks[l - 1];
+      if (dm.key == fa.mask_key && dm.thresh == thresh && dm.r0 == xb.r0 && dm.c0 == xb.c0 &&
+          dm.rows == xb.rows() && dm.cols == xb.cols() && dm.ldm == L.ldm)
+        fa.keep = dm.bits.as<uint32_t>();
+    }
     {
       const double e = static_cast<double>(xb.rows()) * xb.cols();
       ProfScope ps(ctx, kProfElementwise, e * (4 + (res ? 4 : 0) + 4 + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0)) + e / 8);
@@ -501,6 +503,7 @@ void backward(State& st, const Batch& bt, int precision) {
   // dxh = dlogits . W_out^T -> (X_L.row, X_L.col), all-reduce logits.col
   Block db = XL.blk;
   float* dxh = grow<float>(st.dxh, db.rows() * ld8(db.cols()));
+  bool dxh_b_ready = false;  // bf16 copy of the final dxh already written
   {
     const ParamSlot& w = st.params[st.wout];
     ProfScope ps(ctx, kProfGemmDx, gemm_bytes(db.rows(), db.cols(), lb.cols(), 2, 2, 4),
@@ -599,9 +602,12 @@ void backward(State& st, const Batch& bt, int precision) {
     const bool inplace = pmm_trivial(ctx) && cfg.use_residual;
     ProfScope ps(ctx, kProfSpmmBwd, spmm_bytes(At.n_rows, At.nnz, hc, 2, inplace ? 8 : 4), 2.0 * At.nnz * hc);
     if (inplace) {
-      // dxh (== dres) += A_t . dhagg
+      // dxh (== dres) += A_t . dhagg; the first layer also emits the bf16
+      // copy that feeds dW_in (no separate cast pass)
+      bf16* outb = l == 1 ? grow<bf16>(st.dxh_b, F.rows() * ld8(F.cols())) : nullptr;
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
-               dxh, ld8(F.cols()), nullptr, 0, 1);
+               dxh, ld8(F.cols()), outb, ld8(F.cols()), 1);
+      dxh_b_ready = l == 1;
     } else {
       float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
@@ -619,7 +625,7 @@ void backward(State& st, const Batch& bt, int precision) {
     const int64_t rows = db.rows(), cols = db.cols();
     const int64_t ldb = ld8(cols);
     bf16* dxb = grow<bf16>(st.dxh_b, rows * ldb);
-    {
+    if (!dxh_b_ready) {
       ProfScope ps(ctx, kProfElementwise, static_cast<double>(rows) * cols * 6);
       cast_bf16(ctx, dxh, rows, cols, ld8(cols), dxb, ldb);
     }

@@ -356,10 +356,17 @@ class Prefetcher:
     model.hpp:556-581): a native producer thread samples step t+1 on its own
     stream while step t trains; next() returns the batch of the following step."""
 
-    def __init__(self, ctx: Context, graph: Graph, b: int, group_seed: int, first_step: int = 0):
+    def __init__(self, ctx: Context, graph: Graph, b: int, group_seed: int, first_step: int = 0,
+                 run_seed: int = 0, cfg: "ModelConfig | None" = None):
+        """With cfg (and its dropout on), the producer also evaluates the
+        dropout keep-bits of every layer for the step ahead (keyed by run_seed)."""
         self.ctx, self.graph = ctx, graph
+        layers = cfg.layers if (cfg is not None and cfg.use_dropout) else 0
+        rate = cfg.dropout_rate if cfg is not None else 0.0
+        d_h = cfg.d_h if cfg is not None else 0
         h = P()
-        check(lib().ggb_prefetch_create(ctx.h, graph.h, b, group_seed, first_step, C.byref(h)))
+        check(lib().ggb_prefetch_create(ctx.h, graph.h, b, group_seed, first_step, run_seed, layers, d_h, rate,
+                                        C.byref(h)))
         self.h = h
 
     def next(self) -> StepBatch:

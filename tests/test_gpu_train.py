@@ -172,7 +172,9 @@ def test_prefetch_is_transparent(gg, orc):
     cfg = gg.ModelConfig(layers=3, d_in=d_in, d_h=32, d_out=ncls, dropout_rate=0.2)
     gs = gg.hash_combine(seed, 0)
     st_a, st_b = gg.init_state(ctx, cfg, seed), gg.init_state(ctx, cfg, seed)
-    pf = gg.Prefetcher(ctx, g, b, gs, 0)
+    # the producer also precomputes the dropout keep-bits: equal losses prove
+    # they match the in-kernel hash bit for bit
+    pf = gg.Prefetcher(ctx, g, b, gs, 0, run_seed=seed, cfg=cfg)
     plain = None
     for t in range(6):
         pb = pf.next()
