@@ -1,0 +1,389 @@
+// gridgnn drop-in (header-only C++20) over the C ABI of libggb.so.
+//
+// Restores the reference's hot-path C++ surface (namespace gridgnn,
+// /root/reference/proj/include/gridgnn) on top of the B200 implementation:
+// the same names, by-value results and exception types
+//   std::invalid_argument  <- GGB_EINVAL
+//   gridgnn::CommContract  <- GGB_ECONTRACT   (comm.hpp:44-46)
+//   gridgnn::CommTimeout   <- GGB_ETIMEOUT    (comm.hpp:41-43)
+//   std::runtime_error     <- CUDA / NCCL failures
+// Device state lives behind RAII handles; host copies are materialized only
+// by the accessors (the reference's "parity mode" field access).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/ggb.h"
+
+namespace gridgnn {
+
+using index_t = std::int64_t;
+
+struct CommTimeout : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CommContract : std::logic_error {
+  using std::logic_error::logic_error;
+};
+
+enum class Precision { kFp32 = GGB_FP32, kBf16Roundtrip = GGB_BF16_WIRE };  // comm.hpp:22
+enum class Optimizer { kSgd = GGB_SGD, kAdam = GGB_ADAM };                 // model.hpp:45
+enum class Axis : int { D = 0, X = 1, Y = 2, Z = 3 };                       // grid.hpp:11
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == GGB_OK) return;
+  const std::string msg = ggb_last_error();
+  switch (rc) {
+    case GGB_EINVAL: throw std::invalid_argument(msg);
+    case GGB_ECONTRACT: throw CommContract(msg);
+    case GGB_ETIMEOUT: throw CommTimeout(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+}  // namespace detail
+
+/// grid.hpp:18-73 (lexicographic rank = ((d*gx + x)*gy + y)*gz + z).
+struct DeviceGrid {
+  std::int32_t dims[4] = {1, 1, 1, 1};
+  DeviceGrid() = default;
+  DeviceGrid(int gd, int gx, int gy, int gz) : dims{gd, gx, gy, gz} {
+    for (int d : dims)
+      if (d < 1) throw std::invalid_argument("DeviceGrid: dims must be >= 1");
+  }
+  int total() const { return dims[0] * dims[1] * dims[2] * dims[3]; }
+  int dim(Axis a) const { return dims[static_cast<int>(a)]; }
+  int dp_group(int rank) const { return rank / (dims[1] * dims[2] * dims[3]); }
+};
+
+/// sampling.hpp:13-19
+struct SampleSet {
+  std::vector<index_t> vertices;
+  index_t batch_size = 0, graph_size = 0;
+  std::uint64_t seed = 0, step = 0;
+};
+
+/// csr.hpp:13-24 (int64 indices, fp64 values)
+struct CsrMatrix {
+  index_t n_rows = 0, n_cols = 0;
+  std::vector<index_t> row_ptr{0};
+  std::vector<index_t> col_idx;
+  std::vector<double> values;
+  index_t nnz() const { return static_cast<index_t>(col_idx.size()); }
+  bool operator==(const CsrMatrix&) const = default;
+};
+
+/// model.hpp:26-43
+struct ModelConfig {
+  int layers = 2;
+  index_t d_in = 0, d_h = 64, d_out = 0;
+  double dropout_rate = 0.1;
+  bool use_rmsnorm = true, use_dropout = true, use_residual = true;
+  ggb_model_config c() const {
+    return {layers, d_in, d_h, d_out, dropout_rate, use_rmsnorm, use_dropout, use_residual};
+  }
+};
+
+inline std::vector<index_t> block_partition(index_t n, int g) {  // shardsample.cpp:8-17
+  if (g < 1) throw std::invalid_argument("block_partition: g must be >= 1");
+  std::vector<index_t> off(static_cast<size_t>(g) + 1, 0);
+  for (int k = 0; k < g; ++k) off[k + 1] = off[k] + n / g + (k < n % g ? 1 : 0);
+  return off;
+}
+
+inline index_t steps_per_epoch(index_t n, index_t b, int gd) {  // model.hpp:539-542
+  const index_t per = b * gd;
+  return (n + per - 1) / per;
+}
+
+/// One rank on one GPU (replaces Communicator + RankComm, comm.hpp:203-408).
+class RankComm {
+ public:
+  /// nccl_uid: 128 bytes from unique_id() on rank 0 (nullptr: virtual rank,
+  /// multi-rank collectives throw CommContract).
+  RankComm(const DeviceGrid& grid, int rank, int device = 0, const std::uint8_t* nccl_uid = nullptr,
+           void* stream = nullptr)
+      : grid_(grid), rank_(rank) {
+    detail::check(ggb_ctx_create(grid.dims, rank, device, nccl_uid, stream, &h_));
+  }
+  ~RankComm() {
+    if (h_) ggb_ctx_destroy(h_);
+  }
+  RankComm(const RankComm&) = delete;
+  RankComm& operator=(const RankComm&) = delete;
+  static std::vector<std::uint8_t> unique_id() {
+    std::vector<std::uint8_t> id(128);
+    detail::check(ggb_get_unique_id(id.data()));
+    return id;
+  }
+  int rank() const { return rank_; }
+  const DeviceGrid& grid() const { return grid_; }
+  void synchronize() { detail::check(ggb_ctx_synchronize(h_)); }
+  ggb_ctx_t handle() const { return h_; }
+
+ private:
+  DeviceGrid grid_;
+  int rank_;
+  ggb_ctx_t h_ = nullptr;
+};
+
+/// sampling.hpp:33 — sampled on the GPU, bit-exact with the reference.
+inline SampleSet sample_vertices(RankComm& rc, index_t n, index_t b, std::uint64_t seed, std::uint64_t step) {
+  SampleSet s;
+  if (b <= 0 || b > n) throw std::invalid_argument("sample_vertices: need 1 <= b <= n");
+  s.vertices.resize(static_cast<size_t>(b));
+  detail::check(ggb_sample_vertices(rc.handle(), n, b, seed, step, s.vertices.data()));
+  s.batch_size = b;
+  s.graph_size = n;
+  s.seed = seed;
+  s.step = step;
+  return s;
+}
+
+/// Dataset + RankContext resident in HBM (dataset.hpp:16-29, model.hpp:212-234).
+class DeviceDataset {
+ public:
+  DeviceDataset(RankComm& rc, const CsrMatrix& adjacency, index_t d_in, const std::vector<float>& features,
+                index_t n_classes, const std::vector<std::int32_t>& labels, int layers, bool symmetric = true) {
+    detail::check(ggb_graph_create(rc.handle(), adjacency.n_rows, adjacency.row_ptr.data(), adjacency.col_idx.data(),
+                                   adjacency.values.data(), symmetric, d_in, features.data(), n_classes, labels.data(),
+                                   layers, &h_));
+  }
+  /// generate_synthetic (dataset.cpp:85-131), built natively.
+  DeviceDataset(RankComm& rc, index_t n, double avg_degree, index_t d_in, index_t n_classes, std::uint64_t seed,
+                int layers) {
+    detail::check(ggb_graph_generate_synthetic(rc.handle(), n, avg_degree, d_in, n_classes, seed, layers, &h_));
+  }
+  ~DeviceDataset() {
+    if (h_) ggb_graph_destroy(h_);
+  }
+  DeviceDataset(const DeviceDataset&) = delete;
+  DeviceDataset& operator=(const DeviceDataset&) = delete;
+  ggb_graph_t handle() const { return h_; }
+  index_t n() const { return info(0); }
+  index_t nnz() const { return info(1); }
+
+ private:
+  index_t info(int k) const {
+    index_t v[6];
+    detail::check(ggb_graph_info(h_, v));
+    return v[k];
+  }
+  ggb_graph_t h_ = nullptr;
+};
+
+/// StepBatch (model.hpp:238-246) resident in HBM; accessors copy to the host.
+class StepBatch {
+ public:
+  StepBatch() = default;
+  ~StepBatch() {
+    if (h_ && own_) ggb_batch_destroy(h_);
+  }
+  StepBatch(const StepBatch&) = delete;
+  StepBatch& operator=(const StepBatch&) = delete;
+  StepBatch(StepBatch&& o) noexcept : h_(o.h_), own_(o.own_) { o.h_ = nullptr; }
+  StepBatch& operator=(StepBatch&& o) noexcept {
+    if (this != &o) {
+      if (h_ && own_) ggb_batch_destroy(h_);
+      h_ = o.h_;
+      own_ = o.own_;
+      o.h_ = nullptr;
+    }
+    return *this;
+  }
+  ggb_batch_t handle() const { return h_; }
+  ggb_batch_t* slot() { return &h_; }
+  static StepBatch borrow(ggb_batch_t h) {
+    StepBatch b;
+    b.h_ = h;
+    b.own_ = false;
+    return b;
+  }
+
+  SampleSet sample() const {
+    SampleSet s;
+    index_t info[9];
+    detail::check(ggb_batch_info(h_, info));
+    s.vertices.resize(static_cast<size_t>(info[0]));
+    detail::check(ggb_batch_sample(h_, s.vertices.data()));
+    s.batch_size = info[0];
+    s.graph_size = info[1];
+    return s;
+  }
+  std::vector<index_t> batch_off(Axis a) const {
+    std::vector<index_t> v(64);
+    detail::check(ggb_batch_offsets(h_, static_cast<int>(a), v.data()));
+    return v;
+  }
+  /// a[p] (transposed == false) or a_t[p]: local CSR block (MiniBatchShard a_loc / a_t_loc)
+  CsrMatrix plane(int p, bool transposed) const {
+    index_t dims[7];
+    detail::check(ggb_batch_plane(h_, p, transposed, dims, nullptr, nullptr, nullptr));
+    CsrMatrix m;
+    m.n_rows = dims[0];
+    m.n_cols = dims[1];
+    m.row_ptr.resize(static_cast<size_t>(dims[0] + 1));
+    m.col_idx.resize(static_cast<size_t>(dims[2]));
+    m.values.resize(static_cast<size_t>(dims[2]));
+    detail::check(ggb_batch_plane(h_, p, transposed, dims, m.row_ptr.data(), m.col_idx.data(), m.values.data()));
+    return m;
+  }
+  std::vector<std::int32_t> labels() const {
+    std::vector<std::int32_t> v(static_cast<size_t>(sample_size()));
+    detail::check(ggb_batch_labels(h_, v.data()));
+    return v;
+  }
+
+ private:
+  index_t sample_size() const {
+    index_t info[9];
+    detail::check(ggb_batch_info(h_, info));
+    return info[0];
+  }
+  ggb_batch_t h_ = nullptr;
+  bool own_ = true;
+};
+
+/// build_step_batch (model.hpp:250-309): communication-free. Reuses the
+/// batch's device buffers when passed back in.
+inline void build_step_batch(RankComm& rc, const DeviceDataset& ds, index_t b, std::uint64_t group_seed,
+                             std::uint64_t step, StepBatch& inout) {
+  detail::check(ggb_build_step_batch(rc.handle(), ds.handle(), b, group_seed, step, inout.slot()));
+}
+inline StepBatch build_step_batch(RankComm& rc, const DeviceDataset& ds, index_t b, std::uint64_t group_seed,
+                                  std::uint64_t step) {
+  StepBatch sb;
+  build_step_batch(rc, ds, b, group_seed, step, sb);
+  return sb;
+}
+
+/// ModelState (model.hpp:87-105) resident in HBM.
+class ModelState {
+ public:
+  ModelState(RankComm& rc, const ModelConfig& cfg, std::uint64_t seed) : cfg_(cfg) {  // init_state
+    const ggb_model_config c = cfg.c();
+    detail::check(ggb_state_create(rc.handle(), &c, seed, &h_));
+  }
+  ~ModelState() {
+    if (h_) ggb_state_destroy(h_);
+  }
+  ModelState(const ModelState&) = delete;
+  ModelState& operator=(const ModelState&) = delete;
+  ggb_state_t handle() const { return h_; }
+  const ModelConfig& cfg() const { return cfg_; }
+  int num_params() const { return ggb_state_num_params(h_); }
+  /// param_views order (model.hpp:107-133): which 0 weight, 1 grad, 2 m, 3 v
+  std::vector<float> param(int idx, int which = 0) const {
+    index_t info[6];
+    detail::check(ggb_state_param_info(h_, idx, info));
+    std::vector<float> v(static_cast<size_t>((info[3] - info[2]) * (info[5] - info[4])));
+    detail::check(ggb_state_param_get(h_, idx, which, v.data()));
+    return v;
+  }
+
+ private:
+  ModelConfig cfg_;
+  ggb_state_t h_ = nullptr;
+};
+
+inline ModelState init_state(RankComm& rc, const ModelConfig& cfg, std::uint64_t seed) { return {rc, cfg, seed}; }
+
+/// train_step (model.hpp:459-478): forward + cross-entropy + backward.
+inline float train_step(RankComm& rc, ModelState& st, const StepBatch& batch, Precision prec, std::uint64_t run_seed,
+                        std::uint64_t global_step, double rmsnorm_eps = 1e-6) {
+  float loss = 0.f;
+  detail::check(ggb_train_step(rc.handle(), st.handle(), batch.handle(), static_cast<int>(prec), run_seed,
+                               global_step, rmsnorm_eps, &loss));
+  return loss;
+}
+
+inline void dp_sync(RankComm& rc, ModelState& st) { detail::check(ggb_dp_sync(rc.handle(), st.handle())); }
+
+inline void optimizer_step(RankComm& rc, ModelState& st, Optimizer opt, double lr) {
+  detail::check(ggb_optimizer_step(rc.handle(), st.handle(), static_cast<int>(opt), lr));
+}
+
+/// The train_run producer thread + PrefetchQueue (model.hpp:556-581).
+class Prefetcher {
+ public:
+  Prefetcher(RankComm& rc, const DeviceDataset& ds, index_t b, std::uint64_t group_seed, std::uint64_t first_step,
+             std::uint64_t run_seed = 0, const ModelConfig* cfg = nullptr) {
+    const int layers = (cfg && cfg->use_dropout) ? cfg->layers : 0;
+    detail::check(ggb_prefetch_create(rc.handle(), ds.handle(), b, group_seed, first_step, run_seed, layers,
+                                      cfg ? cfg->d_h : 0, cfg ? cfg->dropout_rate : 0.0, &h_));
+  }
+  ~Prefetcher() {
+    if (h_) ggb_prefetch_destroy(h_);
+  }
+  Prefetcher(const Prefetcher&) = delete;
+  Prefetcher& operator=(const Prefetcher&) = delete;
+  StepBatch next() {
+    ggb_batch_t b = nullptr;
+    detail::check(ggb_prefetch_next(h_, &b));
+    return StepBatch::borrow(b);
+  }
+
+ private:
+  ggb_prefetch_t h_ = nullptr;
+};
+
+struct TrainConfig {  // model.hpp:47-58 (the fields of the step loop)
+  DeviceGrid grid;
+  index_t batch = 0;
+  int epochs = 1;
+  std::uint64_t seed = 0;
+  Precision precision = Precision::kFp32;
+  bool prefetch = false;
+  Optimizer optimizer = Optimizer::kAdam;
+  double lr = 1e-3;
+  double rmsnorm_eps = 1e-6;
+};
+
+/// The train_run step loop of one rank (model.hpp:643-691, without the
+/// per-epoch evaluation): S = steps_per_epoch steps per epoch, per step
+/// [batch -> train_step -> dp_sync -> optimizer_step]. Returns the per-step
+/// losses.
+inline std::vector<double> train_run(RankComm& rc, const DeviceDataset& ds, const ModelConfig& mcfg,
+                                     const TrainConfig& tcfg) {
+  if (tcfg.batch < 2 || tcfg.batch > ds.n()) throw std::invalid_argument("train_run: batch size must be in [2, N]");
+  if (tcfg.epochs < 1) throw std::invalid_argument("train_run: epochs must be >= 1");
+  const int dp = tcfg.grid.dp_group(rc.rank());
+  const std::uint64_t group_seed = [&] {  // rng::hash_combine(seed, dp) (model.hpp:620-621)
+    auto sm = [](std::uint64_t x) {
+      x += 0x9e3779b97f4a7c15ULL;
+      x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+      return x ^ (x >> 31);
+    };
+    const std::uint64_t b = static_cast<std::uint64_t>(dp);
+    return sm(tcfg.seed ^ (0x9e3779b97f4a7c15ULL + (b << 6) + (b >> 2)));
+  }();
+  const index_t S = steps_per_epoch(ds.n(), tcfg.batch, tcfg.grid.dims[0]);
+  ModelState st(rc, mcfg, tcfg.seed);
+  std::vector<double> losses;
+  std::unique_ptr<Prefetcher> pf;
+  if (tcfg.prefetch) pf = std::make_unique<Prefetcher>(rc, ds, tcfg.batch, group_seed, 0, tcfg.seed, &mcfg);
+  StepBatch batch;
+  std::uint64_t gstep = 0;
+  for (int epoch = 0; epoch < tcfg.epochs; ++epoch)
+    for (index_t s = 0; s < S; ++s, ++gstep) {
+      StepBatch borrowed;
+      const StepBatch* cur = &batch;
+      if (pf) {
+        borrowed = pf->next();
+        cur = &borrowed;
+      } else {
+        build_step_batch(rc, ds, tcfg.batch, group_seed, gstep, batch);
+      }
+      losses.push_back(train_step(rc, st, *cur, tcfg.precision, tcfg.seed, gstep, tcfg.rmsnorm_eps));
+      dp_sync(rc, st);
+      optimizer_step(rc, st, tcfg.optimizer, tcfg.lr);
+    }
+  return losses;
+}
+
+}  // namespace gridgnn

@@ -26,7 +26,8 @@ namespace {
 constexpr int kBM = 128;  // UMMA M (cta_group::1)
 constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16 along K
 constexpr int kThreads = 192;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 225 * 1024;         // dynamic smem per CTA (227 KB max on sm_100)
+constexpr int kEpiSmem = 4 * 32 * 17 * 4 + 256;  // barriers + epilogue transpose tiles
 
 // ---- PTX wrappers --------------------------------------------------------------
 
@@ -256,7 +257,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4
+    // Each 32-row x 16-column accumulator block goes TMEM -> registers (row
+    // per lane) -> padded smem tile -> registers (4 consecutive columns per
+    // lane), so the global stores are row-contiguous: 4 lanes cover 64 bytes
+    // of one row (fp32) and one store instruction writes 8 full row segments.
     const int q = warp & 3;
+    float* stile = reinterpret_cast<float*>(tmem_base_smem + 4) + (warp - 2) * (32 * 17);
     int lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int mt = t / args.n_tiles, nt = t % args.n_tiles;
@@ -264,40 +270,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (lt >> 1) & 1;
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;
-      const bool row_ok = row < args.M;
+      const int64_t row_base = static_cast<int64_t>(mt) * kBM + q * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
       for (int c16 = 0; c16 < BN; c16 += 16) {
         float v[16];
         tmem_ld16(taddr + c16, v);
         const int col0 = nt * BN + c16;
-        if (!row_ok || col0 >= args.N) continue;
-        const bool full16 = col0 + 16 <= args.N;
-        if (args.c) {
-          float* dst = args.c + row * args.ldc + col0;
-          if (full16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+        if (col0 >= args.N) continue;  // warp-uniform
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
-            for (int i = 0; i < 16 && col0 + i < args.N; ++i) dst[i] = v[i];
+        for (int i = 0; i < 16; ++i) stile[lane * 17 + i] = v[i];
+        __syncwarp();
+        const int cc = (lane & 3) * 4;  // column offset within the 16-column block
+        const int col = col0 + cc;
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rl = it * 8 + (lane >> 2);  // local row 0..31
+          const int64_t row = row_base + rl;
+          float o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o[i] = stile[rl * 17 + cc + i];
+          if (row >= args.M || col >= args.N) continue;
+          const bool full4 = col + 4 <= args.N;
+          if (args.c) {
+            float* dst = args.c + row * args.ldc + col;
+            if (full4 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+              *reinterpret_cast<float4*>(dst) = make_float4(o[0], o[1], o[2], o[3]);
+            else
+              for (int i = 0; i < 4 && col + i < args.N; ++i) dst[i] = o[i];
           }
-        }
-        if (args.cb) {
-          bf16* dst = args.cb + row * args.ldcb + col0;
-          if (full16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-            uint32_t pk[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+          if (args.cb) {
+            bf16* dst = args.cb + row * args.ldcb + col;
+            if (full4 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+              __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
+              *reinterpret_cast<uint2*>(dst) =
+                  make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+            } else {
+              for (int i = 0; i < 4 && col + i < args.N; ++i) dst[i] = __float2bfloat16_rn(o[i]);
             }
-            *reinterpret_cast<uint4*>(dst) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            *reinterpret_cast<uint4*>(dst + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          } else {
-            for (int i = 0; i < 16 && col0 + i < args.N; ++i) dst[i] = __float2bfloat16_rn(v[i]);
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -517,7 +529,7 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
   ga.BN = static_cast<int>(std::min<int64_t>(256, round_up(n, 16)));
   ga.n_tiles = static_cast<int>(ceil_div(n, ga.BN));
   const int stage_bytes = (1 + ga.split) * (kBM * kBK * 2 + ga.BN * kBK * 2);
-  ga.stages = std::min(8, (kSmemBudget - 1024 - 256) / stage_bytes);
+  ga.stages = std::min(8, (kSmemBudget - 1024 - kEpiSmem) / stage_bytes);
   require(ga.stages >= 2, "gemm: tile does not fit shared memory");
   ga.tmem_cols = tmem_cols_for(2 * ga.BN);
   ga.c = c;
@@ -528,7 +540,7 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
   const CUtensorMap tb = make_tmap(bt, n, k, ldb, kBK, ga.BN);
   const CUtensorMap tal = ga.split ? make_tmap(a_lo, m, k, lda, kBK, kBM) : ta;
   const CUtensorMap tbl = ga.split ? make_tmap(bt_lo, n, k, ldb, kBK, ga.BN) : tb;
-  const int smem = ga.stages * stage_bytes + 1024 + 256;
+  const int smem = ga.stages * stage_bytes + 1024 + kEpiSmem;
   static bool attr = false;
   if (!attr) {
     GGB_CUDA(cudaFuncSetAttribute(k_gemm_kmajor, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -190,20 +190,34 @@ __global__ void __launch_bounds__(kT) k_bwd_row(BwdApply p) {
   for (int j = 0; j < kMaxJ; ++j)
 #pragma unroll
     for (int i = 0; i < 4; ++i) dg[j][i] = 0.f;
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib; r < p.rows;
-       r += static_cast<int64_t>(gridDim.x) * kRowsPerBlock) {
-    float dxn[kMaxJ][4], x[kMaxJ][4];
-    const uint32_t* mrow = p.mask + r * p.ldm;
+  // two rows per iteration: both rows' loads are issued before either row's
+  // reductions, doubling the memory-level parallelism of the warp
+  constexpr int R = 2;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kRowsPerBlock;
+  for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib; r0 < p.rows; r0 += R * stride) {
+    float dxr[R][kMaxJ][4], xr[R][kMaxJ][4];
 #pragma unroll
-    for (int j = 0; j < kMaxJ; ++j) {
-      if (j >= nj) break;
-      const int64_t c = j * kRowChunk + 4 * lane;
-      float dy[4];
-      f4(ld4(p.dy + r * p.lddy, c, p.cols), dy);
-      f4(ld4(p.x + r * p.ldx, c, p.cols), x[j]);
+    for (int h = 0; h < R; ++h) {
+      const int64_t r = r0 + h * stride;
+      if (r >= p.rows) break;
+      const uint32_t* mrow = p.mask + r * p.ldm;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) dxn[j][i] = ((mrow[4 * j + i] >> lane) & 1u) ? dy[i] * p.keep_scale : 0.f;
+      for (int j = 0; j < kMaxJ; ++j) {
+        if (j >= nj) break;
+        const int64_t c = j * kRowChunk + 4 * lane;
+        float dy[4];
+        f4(ld4(p.dy + r * p.lddy, c, p.cols), dy);
+        f4(ld4(p.x + r * p.ldx, c, p.cols), xr[h][j]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dxr[h][j][i] = ((mrow[4 * j + i] >> lane) & 1u) ? dy[i] * p.keep_scale : 0.f;
+      }
     }
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+    const int64_t r = r0 + h * stride;
+    if (r >= p.rows) break;
+    float(&dxn)[kMaxJ][4] = dxr[h];
+    float(&x)[kMaxJ][4] = xr[h];
     float inv = 1.f, coef = 0.f;
     if (p.rms) {
       float s;
@@ -243,6 +257,7 @@ __global__ void __launch_bounds__(kT) k_bwd_row(BwdApply p) {
         for (int i = 0; i < 4; ++i) dx[i] = dxn[j][i];
       }
       st4_bf16(p.dxb + r * p.lddxb, c, p.cols, dx);
+    }
     }
   }
   if (!p.dgamma_part) return;
