@@ -168,7 +168,8 @@ def main():
     ap.add_argument("--grid", default=None, help="GdxGxxGyxGz (default: data-parallel Gd = N)")
     ap.add_argument("--compute", default="accurate", choices=["accurate", "fast"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prefetch", type=int, default=1, help="overlap sampling of step t+1 with step t")
+    ap.add_argument("--prefetch", type=int, default=1,
+                    help="1: sample step t+1 on a side stream during step t; 2: also its dropout masks; 0: off")
     ap.add_argument("--ref-steps", type=int, default=2)
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -215,7 +216,9 @@ def main():
         obj = [gg.get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
-    stream = torch.cuda.Stream()  # a real stream: libggb launches on it, torch events bracket it
+    # a real (high-priority) stream: libggb launches on it, torch events bracket
+    # it; the prefetcher's sampling stream runs at the lowest priority
+    stream = torch.cuda.Stream(priority=-1)
     torch.cuda.set_stream(stream)
     ctx = gg.Context(grid, rank, device=local_rank, nccl_uid=uid, stream=stream.cuda_stream)
 
@@ -232,7 +235,9 @@ def main():
     group_seed = gg.hash_combine(RUN_SEED, grid.dp_group(rank))
     batch = None
     # sampling of step t+1 overlaps training of step t (producer thread + own stream)
-    pf = gg.Prefetcher(ctx, graph, b, group_seed, 0, run_seed=RUN_SEED, cfg=mcfg) if args.prefetch else None
+    # (--prefetch 2 also hashes the next step's dropout masks on that stream)
+    pf = (gg.Prefetcher(ctx, graph, b, group_seed, 0, run_seed=RUN_SEED, cfg=mcfg if args.prefetch == 2 else None)
+          if args.prefetch else None)
 
     def step(gstep: int, sync_loss: bool):
         nonlocal batch
@@ -349,7 +354,7 @@ def main():
             "batch_per_dp_group": b, "steps_per_epoch": S, "grid": "x".join(map(str, dims)),
             "layers": cfg["layers"], "hidden": cfg["d_h"], "d_in": cfg["d_in"], "classes": cfg["n_classes"],
             "n_vertices": cfg["n"], "nnz": graph.nnz, "compute": args.compute,
-            "prefetch": bool(args.prefetch),
+            "prefetch": ["off", "sampling", "sampling+dropout masks"][args.prefetch],
             "l2": "inputs larger than L2 (graph %.1f GB + features resident in HBM; random gathers)" %
                   (graph.device_bytes / 1e9),
             "optimizer": "adam lr 1e-3", "dropout": DROPOUT, "eval": "excluded (per SURVEY 8d)",

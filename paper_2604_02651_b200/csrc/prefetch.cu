@@ -36,7 +36,11 @@ Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t see
   sctx.device = consumer->device;
   sctx.num_sms = consumer->num_sms;
   GGB_CUDA(cudaSetDevice(sctx.device));
-  GGB_CUDA(cudaStreamCreateWithFlags(&sctx.stream, cudaStreamNonBlocking));
+  // lowest scheduling priority: sampling and mask hashing fill idle SM slots
+  // without displacing the training stream's CTAs
+  int least = 0, greatest = 0;
+  GGB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  GGB_CUDA(cudaStreamCreateWithPriority(&sctx.stream, cudaStreamNonBlocking, least));
   sctx.own_stream = true;
   for (int s = 0; s < 2; ++s) {
     GGB_CUDA(cudaEventCreateWithFlags(&ready[s], cudaEventDisableTiming));

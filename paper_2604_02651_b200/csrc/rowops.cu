@@ -135,10 +135,13 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
 // a block, in the row-kernel layout: one thread per (row, word), word 4j+i
 // holding bit l for column 128j + 4l + i. Pure integer work, independent of
 // the activations, so the prefetcher runs it ahead on its own stream.
-__global__ void k_dropout_keep(uint64_t key, int64_t rows, int64_t cols, int64_t row_g0, int64_t col_g0,
-                               uint64_t thresh, uint32_t* __restrict__ out, int64_t ldm) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= rows * ldm) return;
+__global__ void __launch_bounds__(128) k_dropout_keep(uint64_t key, int64_t rows, int64_t cols, int64_t row_g0,
+                                                      int64_t col_g0, uint64_t thresh, uint32_t* __restrict__ out,
+                                                      int64_t ldm) {
+  // grid-stride over a small persistent grid: the kernel runs beside the
+  // training stream and must leave room for its CTAs
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < rows * ldm;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
   const int64_t r = t / ldm, w = t % ldm;
   const int64_t j = w / 4, i = w % 4;
   const uint64_t row_key = hash_combine(key, static_cast<uint64_t>(row_g0 + r));
@@ -149,6 +152,7 @@ __global__ void k_dropout_keep(uint64_t key, int64_t rows, int64_t cols, int64_t
     if (c < cols && element_keep(row_key, static_cast<uint64_t>(col_g0 + c), thresh)) bits |= 1u << l;
   }
   out[t] = bits;
+  }
 }
 
 // Row dot product s_r = sum_j dxn * gamma * x (the all-reduced input of the
@@ -430,7 +434,8 @@ void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks) {
 void dropout_keep(Ctx& ctx, uint64_t key, int64_t rows, int64_t cols, int64_t row_g0, int64_t col_g0,
                   uint64_t thresh, uint32_t* out, int64_t ldm) {
   if (rows <= 0) return;
-  k_dropout_keep<<<static_cast<unsigned>(ceil_div(rows * ldm, 128)), 128, 0, ctx.stream>>>(
+  const int64_t blocks = std::min<int64_t>(ceil_div(rows * ldm, 128), 2 * ctx.num_sms);
+  k_dropout_keep<<<static_cast<unsigned>(blocks), 128, 0, ctx.stream>>>(
       key, rows, cols, row_g0, col_g0, thresh, out, ldm);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;

@@ -1,0 +1,41 @@
+"""Multi-GPU parity (NCCL communicators inside libggb): sharded == serial on
+PMM grids, data-parallel training == the reference's DP run. Needs >= 2 GPUs
+(skipped otherwise); run with `gpurun --gpus 2|4`."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WORKER = os.path.join(ROOT, "tests", "mgpu_worker.py")
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+GRIDS = [("1x1x1x2", 0), ("1x2x1x1", 0), ("1x1x2x1", 1), ("2x1x1x1", 0), ("1x2x2x1", 0), ("1x1x2x2", 1),
+         ("2x1x1x2", 0), ("4x1x1x1", 0)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grid,prec", GRIDS)
+def test_sharded_matches_serial(grid, prec):
+    world = 1
+    for d in grid.split("x"):
+        world *= int(d)
+    if _ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29531", WORKER, grid, str(prec)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert res["ok"], res
