@@ -97,26 +97,76 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
     inv = 1.f / rms;
     if (lane == 0 && p.rms) p.rms[r] = rms;
   }
-  const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
+  // y = gamma * x / rms for every held element; residual loads issued early
+  float y[kMaxJ][4], res[kMaxJ][4];
+  uint32_t posm = 0;  // bit 4j+i: y > 0 and the column exists
 #pragma unroll
   for (int j = 0; j < kMaxJ; ++j) {
     if (j >= nj) break;
     const int64_t c = j * kRowChunk + 4 * lane;
-    float g[4] = {1.f, 1.f, 1.f, 1.f}, res[4] = {0.f, 0.f, 0.f, 0.f}, o[4];
+    float g[4] = {1.f, 1.f, 1.f, 1.f};
     if (p.gamma) f4(ld4(p.gamma, c, p.cols), g);
-    if (p.res) f4(ld4(p.res + r * p.ldres, c, p.cols), res);
+    if (p.res)
+      f4(ld4(p.res + r * p.ldres, c, p.cols), res[j]);
+    else
+      res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float y = p.gamma ? g[i] * x[j][i] * inv : x[j][i];
-      float sc = y > 0.f ? 1.f : 0.f;
-      if (p.drop && p.keep) {  // precomputed keep-bits (prefetcher)
-        sc = (sc != 0.f && ((p.keep[r * p.ldm + 4 * j + i] >> lane) & 1u)) ? p.keep_scale : 0.f;
-      } else if (p.drop && sc != 0.f && c + i < p.cols) {
-        sc = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + c + i), p.thresh) ? p.keep_scale : 0.f;
-      }
-      const unsigned bits = __ballot_sync(0xffffffffu, sc != 0.f && c + i < p.cols);
+      y[j][i] = p.gamma ? g[i] * x[j][i] * inv : x[j][i];
+      if (y[j][i] > 0.f && c + i < p.cols) posm |= 1u << (4 * j + i);
+    }
+  }
+  // keep bits (ReLU and dropout): only ReLU-active elements need the dropout
+  // hash, so the warp compacts them and every lane hashes an equal share
+  // (about half the elements of the row) instead of all of its own
+  uint32_t keepm = posm;
+  if (p.drop && p.keep) {  // precomputed keep-bits (prefetcher)
+    uint32_t kb = 0;
+#pragma unroll
+    for (int j = 0; j < kMaxJ; ++j)
+      if (j < nj)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) kb |= ((p.keep[r * p.ldm + 4 * j + i] >> lane) & 1u) << (4 * j + i);
+    keepm = posm & kb;
+  } else if (p.drop) {
+    __shared__ uint16_t s_list[kRowsPerBlock][32 * 4 * kMaxJ];
+    __shared__ uint32_t s_bits[kRowsPerBlock][32];
+    const int wib = threadIdx.x >> 5;
+    const int cnt = __popc(posm);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    int pos = incl - cnt;
+    for (uint32_t m = posm; m; m &= m - 1) s_list[wib][pos++] = static_cast<uint16_t>((lane << 8) | (__ffs(m) - 1));
+    s_bits[wib][lane] = 0;
+    __syncwarp();
+    const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
+    for (int k = lane; k < total; k += 32) {
+      const int e = s_list[wib][k];
+      const int owner = e >> 8, slot = e & 0xff;
+      const int64_t col = (slot >> 2) * kRowChunk + 4 * owner + (slot & 3);
+      if (element_keep(row_key, static_cast<uint64_t>(p.col_g0 + col), p.thresh))
+        atomicOr(&s_bits[wib][owner], 1u << slot);
+    }
+    __syncwarp();
+    keepm = s_bits[wib][lane];
+  }
+  const float sc_on = p.drop ? p.keep_scale : 1.f;
+#pragma unroll
+  for (int j = 0; j < kMaxJ; ++j) {
+    if (j >= nj) break;
+    const int64_t c = j * kRowChunk + 4 * lane;
+    float o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool on = (keepm >> (4 * j + i)) & 1u;
+      const unsigned bits = __ballot_sync(0xffffffffu, on);
       if (lane == i) p.mask[r * p.ldm + 4 * j + i] = bits;
-      o[i] = y * sc + res[i];
+      o[i] = y[j][i] * (on ? sc_on : 0.f) + res[j][i];
     }
     if (p.out) st4(p.out + r * p.ldo, c, p.cols, o);
     if (p.outb) {
