@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kT) k_bwd_row_stats(BwdApply p) {
 // per lane over the block's rows (grid-stride), then reduced across the
 // block's warps into dgamma_part[block][cols].
 template <int J>
-__global__ void __launch_bounds__(kT) k_bwd_row(BwdApply p) {
+__global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
   constexpr int kMaxJ = J;
   __shared__ float sh[kRowsPerBlock][kMaxJ * kRowChunk];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -244,9 +244,11 @@ __global__ void __launch_bounds__(kT) k_bwd_row(BwdApply p) {
   for (int j = 0; j < kMaxJ; ++j)
 #pragma unroll
     for (int i = 0; i < 4; ++i) dg[j][i] = 0.f;
-  // two rows per iteration: both rows' loads are issued before either row's
-  // reductions, doubling the memory-level parallelism of the warp
-  constexpr int R = 2;
+  // narrow rows: two rows per iteration (both rows' loads issued before either
+  // row's reductions) to double the warp's memory-level parallelism; wider
+  // rows already hold enough loads in flight and need the registers for
+  // occupancy
+  constexpr int R = J == 1 ? 2 : 1;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kRowsPerBlock;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib; r0 < p.rows; r0 += R * stride) {
     float dxr[R][kMaxJ][4], xr[R][kMaxJ][4];
@@ -461,10 +463,11 @@ void bwd_stats(Ctx& ctx, const BwdApply& p) {
 }
 
 int bwd_apply_blocks(Ctx& ctx, int64_t rows, int64_t cols) {
-  (void)cols;
-  // few enough blocks that the dgamma partials reduce in microseconds, enough
-  // warps (2 blocks x 8 warps per SM, grid-stride) to saturate HBM
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), 4 * ctx.num_sms)));
+  // one resident wave (4 blocks x 8 warps per SM up to 256 columns, 2 above),
+  // grid-stride: few enough blocks that the dgamma partials reduce in
+  // microseconds, enough warps in flight to saturate HBM
+  const int per_sm = cols <= 2 * kRowChunk ? 4 : 2;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(row_blocks(rows), per_sm * ctx.num_sms)));
 }
 
 void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks) {

@@ -1,9 +1,17 @@
-# Round profile capture: plain run, launch list, full capture of the top kernels (1 GPU).
+# Round profile capture: plain run, launch list, one full capture per hot kernel (1 GPU).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
+R=${ROUND:-r01}
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"
 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01.csv $CMD > gpurun_out/ncu_list.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv $CMD > gpurun_out/ncu_list.log 2>&1
 echo "list rc=$?" > gpurun_out/ncu_rc.txt
-ncu --set full --clock-control none --import-source on -k regex:"k_spmm_pipe|k_gemm_kmajor|k_fwd_row|k_bwd_row|k_gemm_wgrad|k_extract_fill|k_ce_row" -s 40 -c 16 -o gpurun_out/prof_r01 $CMD > gpurun_out/ncu_full.log 2>&1
-echo "full rc=$?" >> gpurun_out/ncu_rc.txt
+# skip the warm-up step's launches of each kernel, capture one of the timed ones
+for spec in "spmm_fwd:k_spmm_pipe<float:4" "spmm_bwd:k_spmm_pipe<__nv_bfloat16:4" "gemm:k_gemm_kmajor:12" \
+            "wgrad:k_gemm_wgrad:6" "fwd_row:k_fwd_row:4" "bwd_row:k_bwd_row:4" "extract:k_extract_fill:2" \
+            "gather:k_gather_x:2" "ce:k_ce_row:1"; do
+  name=${spec%%:*}; rest=${spec#*:}; kre=${rest%:*}; skip=${rest##*:}
+  ncu --set full --clock-control none --import-source on -k regex:"$kre" -s $skip -c 1 \
+      -o gpurun_out/prof_${R}_$name $CMD > gpurun_out/ncu_full_$name.log 2>&1
+  echo "$name rc=$?" >> gpurun_out/ncu_rc.txt
+done
