@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--grid", default=None, help="GdxGxxGyxGz (default: data-parallel Gd = N)")
     ap.add_argument("--compute", default="accurate", choices=["accurate", "fast"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-eval", action="store_true", help="skip the separately timed full-graph evaluation")
     ap.add_argument("--prefetch", type=int, default=1,
                     help="1: sample step t+1 on a side stream during step t; 2: also its dropout masks; 0: off")
     ap.add_argument("--ref-steps", type=int, default=2)
@@ -298,6 +299,30 @@ def main():
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
     c2 = ctx.counters()
     clk = clocks.stop()
+    # ---- per-epoch full-graph evaluation (train_run's evaluate_full_graph), timed
+    # separately: the reference's epoch time excludes it; it is the
+    # paper's full-graph inference metric
+    ev_info = None
+    if not args.no_eval:
+        t0 = time.time()
+        evb = gg.build_eval_batch(ctx, graph, RUN_SEED)
+        t_evb = time.time() - t0
+        counts = gg.evaluate_full_graph(ctx, st, evb, graph)  # warm (buffers grow to N rows)
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        x0.record(stream)
+        for _ in range(reps):
+            counts = gg.evaluate_full_graph(ctx, st, evb, graph)
+        x1.record(stream)
+        barrier()
+        ms_eval = max_over_ranks(x0.elapsed_time(x1)) / reps
+        ev_info = {"full_graph_eval_s": ms_eval / 1000.0, "eval_batch_build_s": t_evb,
+                   "rows": cfg["n"], "accuracy": {k: counts.accuracy(i) for i, k in
+                                                  enumerate(("train", "val", "test"))},
+                   "note": "dropout-off forward over all N vertices + argmax + split counts; "
+                           "after %d training steps" % gstep}
+        del evb
 
     if rank != 0:
         if pg:
@@ -372,6 +397,7 @@ def main():
         "clocks": clk,
         "loss_last": losses[-1] if losses else None,
         "graph_build_s": t_graph,
+        "eval": ev_info,
     }
     if not args.no_cpu_baseline and n_gpus == 1:
         try:

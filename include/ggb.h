@@ -96,6 +96,10 @@ int ggb_graph_create(ggb_ctx_t ctx, int64_t n, const int64_t* row_ptr, const int
 int ggb_graph_generate_synthetic(ggb_ctx_t ctx, int64_t n, double avg_degree, int64_t d_in,
                                  int64_t n_classes, uint64_t seed, int32_t layers,
                                  ggb_graph_t* out);
+/* Split tags (Dataset::split, dataset.hpp:12,23): 0 train, 1 val, 2 test,
+ * 3 unused; one byte per vertex. generate_synthetic sets them itself
+ * (dataset.cpp:122-129); needed only by ggb_evaluate_full_graph. */
+int ggb_graph_set_split(ggb_graph_t g, const uint8_t* split);
 int ggb_graph_destroy(ggb_graph_t g);
 /* info = {n, nnz, d_in, n_classes, distinct_plane_shards, device_bytes} */
 int ggb_graph_info(ggb_graph_t g, int64_t* info);
@@ -165,6 +169,13 @@ int ggb_last_loss_device(ggb_state_t st, const float** dev_ptr);
 int ggb_state_logits(ggb_state_t st, int64_t* dims, float* host_out);
 int ggb_forward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, int32_t precision,
                 int32_t training, uint64_t run_seed, uint64_t global_step, double rmsnorm_eps);
+/* evaluate_full_graph (model.hpp:493-537): forward over the eval batch (built
+ * with b = n, seed, step 0 as train_run does, model.hpp:625) with dropout off,
+ * argmax per vertex (ties to the lowest class id), per-split counts summed
+ * over the grid. counts = {correct train, val, test, total train, val, test}
+ * (EvalCounts, model.hpp:480-490), identical on every rank. */
+int ggb_evaluate_full_graph(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t eval_batch, ggb_graph_t g,
+                            int32_t precision, double rmsnorm_eps, uint64_t* counts);
 int ggb_dp_sync(ggb_ctx_t ctx, ggb_state_t st);
 int ggb_optimizer_step(ggb_ctx_t ctx, ggb_state_t st, int32_t optimizer, double lr);
 

@@ -455,6 +455,8 @@ class Ref:
         L.ref_train.argtypes = [P, P, P, P, I64, U64, U64, C.c_int, C.c_int, C.c_int,
                                 C.c_double, C.c_double, P, P, P, P]
         L.ref_init_weights.argtypes = [P, P, U64, P]
+        L.ref_train_eval.argtypes = [P, P, P, P, I64, U64, C.c_int, C.c_int, C.c_int, C.c_double,
+                                     C.c_double, P, P]
         L.ref_bench.argtypes = [P, P, P, P, I64, U64, C.c_int, C.c_int, C.c_int, P, P]
         self.L = L
 
@@ -551,6 +553,18 @@ class Ref:
                                      optimizer, lr, eps, _ptr(losses), _ptr(logits), _ptr(grads),
                                      _ptr(weights)))
         return losses, logits, unflatten(cfg, grads), (unflatten(cfg, weights) if want_weights else None)
+
+    def train_eval(self, h, n, dims, cfg: ModelConfig, b, seed, n_steps=1, prec=0, optimizer=1, lr=1e-3,
+                   eps=1e-6, want_logits=True):
+        """n_steps of train_run's step loop, then evaluate_full_graph (model.hpp:493-537).
+        Returns (counts[6] = correct train/val/test + totals, eval logits n x d_out or None)."""
+        mc, md = cfg.arrays()
+        d = np.asarray(dims, np.int32)
+        counts = np.zeros(6, np.uint64)
+        logits = np.zeros((n, cfg.d_out), np.float32) if want_logits else None
+        self._check(self.L.ref_train_eval(h, _ptr(d), _ptr(mc), _ptr(md), b, seed, n_steps, prec, optimizer, lr,
+                                          eps, _ptr(counts), _ptr(logits)))
+        return counts, logits
 
     def init_weights(self, cfg: ModelConfig, seed: int):
         mc, md = cfg.arrays()

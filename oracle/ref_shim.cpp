@@ -376,6 +376,51 @@ int ref_train(void* dsp, const int* dims, const std::int64_t* mc, const double* 
   });
 }
 
+/// train_run's per-epoch evaluation (model.hpp:621-626,686-688): n_steps
+/// training steps from step 0 (group seeds, dp_sync, optimizer), then
+/// evaluate_full_graph on the eval batch build_step_batch(b = n, seed, step 0).
+/// counts = {correct train/val/test, total train/val/test}; eval_logits
+/// (n x d_out, nullable) = the eval forward's logits.
+int ref_train_eval(void* dsp, const int* dims, const std::int64_t* mc, const double* md,
+                   std::int64_t b, std::uint64_t seed, int n_steps, int prec, int optimizer, double lr,
+                   double eps, std::uint64_t* counts, float* eval_logits) {
+  auto* ds = static_cast<Dataset*>(dsp);
+  return guard([&] {
+    const ModelConfig mcfg = make_cfg(mc, md);
+    DeviceGrid grid(dims[0], dims[1], dims[2], dims[3]);
+    Communicator comm(grid);
+    const Precision p = prec ? Precision::kBf16Roundtrip : Precision::kFp32;
+    std::vector<ShardedTensor<float>> logits(static_cast<std::size_t>(grid.total()));
+    std::vector<EvalCounts> res(static_cast<std::size_t>(grid.total()));
+    run_ranks(comm, [&](RankComm& rc) {
+      const int dp = grid.dp_group(rc.rank());
+      const std::uint64_t group_seed = rng::hash_combine(seed, static_cast<std::uint64_t>(dp));
+      RankContext ctx = make_rank_context(grid, rc.coord(), *ds, mcfg.layers);
+      const auto eval_batch = build_step_batch<float>(grid, rc.coord(), ctx, *ds, ds->n, seed, 0, nullptr);
+      auto st = init_state<float>(grid, rc.coord(), mcfg, seed);
+      for (int s = 0; s < n_steps; ++s) {
+        const auto gstep = static_cast<std::uint64_t>(s);
+        auto batch = build_step_batch<float>(grid, rc.coord(), ctx, *ds, b, group_seed, gstep);
+        auto cache = forward(rc, st, batch, p, true, seed, gstep, eps);
+        auto ce = parallel_cross_entropy(rc, cache.logits, batch.labels);
+        backward(rc, st, cache, batch, ce.grad_logits, p);
+        dp_sync(rc, st);
+        optimizer_step(st, optimizer == 0 ? Optimizer::kSgd : Optimizer::kAdam, lr);
+      }
+      res[static_cast<std::size_t>(rc.rank())] = evaluate_full_graph(rc, st, eval_batch, *ds, p, eps);
+      if (eval_logits)
+        logits[static_cast<std::size_t>(rc.rank())] = forward(rc, st, eval_batch, p, false, 0, 0, eps).logits;
+    });
+    for (int i = 0; i < 3; ++i) {
+      counts[i] = res[0].correct[static_cast<std::size_t>(i)];
+      counts[3 + i] = res[0].total[static_cast<std::size_t>(i)];
+    }
+    if (eval_logits)
+      for (int r = 0; r < grid.total(); ++r)
+        if (grid.dp_group(r) == 0) put_tile(logits[static_cast<std::size_t>(r)], eval_logits);
+  });
+}
+
 /// Initial weights (init_state on the 1x1x1x1 grid), flattened in
 /// param_views order.
 int ref_init_weights(const std::int64_t* mc, const double* md, std::uint64_t seed, float* out) {

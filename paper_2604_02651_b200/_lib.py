@@ -43,6 +43,7 @@ _SIGS = [
     ("ggb_sample_vertices", C.c_int, [P, I64, I64, U64, U64, P]),
     ("ggb_graph_create", C.c_int, [P, I64, P, P, P, I32, I64, P, I64, P, I32, P]),
     ("ggb_graph_generate_synthetic", C.c_int, [P, I64, F64, I64, I64, U64, I32, P]),
+    ("ggb_graph_set_split", C.c_int, [P, P]),
     ("ggb_graph_destroy", C.c_int, [P]),
     ("ggb_graph_info", C.c_int, [P, P]),
     ("ggb_build_step_batch", C.c_int, [P, P, I64, U64, U64, P]),
@@ -67,6 +68,7 @@ _SIGS = [
     ("ggb_last_loss_device", C.c_int, [P, P]),
     ("ggb_state_logits", C.c_int, [P, P, P]),
     ("ggb_forward", C.c_int, [P, P, P, I32, I32, U64, U64, F64]),
+    ("ggb_evaluate_full_graph", C.c_int, [P, P, P, P, C.c_int32, C.c_double, P]),
     ("ggb_dp_sync", C.c_int, [P, P]),
     ("ggb_optimizer_step", C.c_int, [P, P, I32, F64]),
     ("ggb_gemm_bf16", C.c_int, [P, I64, I64, I64, P, I64, P, I64, P, I64, P, I64]),

@@ -11,6 +11,8 @@
 // by the accessors (the reference's "parity mode" field access).
 #pragma once
 
+#include <array>
+#include <chrono>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -33,6 +35,7 @@ struct CommContract : std::logic_error {
 enum class Precision { kFp32 = GGB_FP32, kBf16Roundtrip = GGB_BF16_WIRE };  // comm.hpp:22
 enum class Optimizer { kSgd = GGB_SGD, kAdam = GGB_ADAM };                 // model.hpp:45
 enum class Axis : int { D = 0, X = 1, Y = 2, Z = 3 };                       // grid.hpp:11
+enum class SplitTag : std::uint8_t { kTrain = 0, kVal = 1, kTest = 2, kUnused = 3 };  // dataset.hpp:12
 
 namespace detail {
 inline void check(int rc) {
@@ -148,10 +151,12 @@ inline SampleSet sample_vertices(RankComm& rc, index_t n, index_t b, std::uint64
 class DeviceDataset {
  public:
   DeviceDataset(RankComm& rc, const CsrMatrix& adjacency, index_t d_in, const std::vector<float>& features,
-                index_t n_classes, const std::vector<std::int32_t>& labels, int layers, bool symmetric = true) {
+                index_t n_classes, const std::vector<std::int32_t>& labels, int layers, bool symmetric = true,
+                const std::vector<SplitTag>* split = nullptr) {
     detail::check(ggb_graph_create(rc.handle(), adjacency.n_rows, adjacency.row_ptr.data(), adjacency.col_idx.data(),
                                    adjacency.values.data(), symmetric, d_in, features.data(), n_classes, labels.data(),
                                    layers, &h_));
+    if (split) set_split(*split);
   }
   /// generate_synthetic (dataset.cpp:85-131), built natively.
   DeviceDataset(RankComm& rc, index_t n, double avg_degree, index_t d_in, index_t n_classes, std::uint64_t seed,
@@ -163,6 +168,11 @@ class DeviceDataset {
   }
   DeviceDataset(const DeviceDataset&) = delete;
   DeviceDataset& operator=(const DeviceDataset&) = delete;
+  /// Dataset::split (dataset.hpp:23); generate_synthetic sets it itself.
+  void set_split(const std::vector<SplitTag>& split) {
+    if (static_cast<index_t>(split.size()) != n()) throw std::invalid_argument("set_split: one tag per vertex");
+    detail::check(ggb_graph_set_split(h_, reinterpret_cast<const std::uint8_t*>(split.data())));
+  }
   ggb_graph_t handle() const { return h_; }
   index_t n() const { return info(0); }
   index_t nnz() const { return info(1); }
@@ -231,6 +241,12 @@ class StepBatch {
     m.values.resize(static_cast<size_t>(dims[2]));
     detail::check(ggb_batch_plane(h_, p, transposed, dims, m.row_ptr.data(), m.col_idx.data(), m.values.data()));
     return m;
+  }
+  /// {nnz_extracted, nnz_kept} work counters (MiniBatchShard, shardsample.hpp:111-113)
+  std::array<std::uint64_t, 2> counters() const {
+    index_t info[9];
+    detail::check(ggb_batch_info(h_, info));
+    return {static_cast<std::uint64_t>(info[7]), static_cast<std::uint64_t>(info[8])};
   }
   std::vector<std::int32_t> labels() const {
     std::vector<std::int32_t> v(static_cast<size_t>(sample_size()));
@@ -307,6 +323,37 @@ inline void optimizer_step(RankComm& rc, ModelState& st, Optimizer opt, double l
   detail::check(ggb_optimizer_step(rc.handle(), st.handle(), static_cast<int>(opt), lr));
 }
 
+/// EvalCounts (model.hpp:480-490).
+struct EvalCounts {
+  std::array<std::uint64_t, 3> correct{};  // train, val, test
+  std::array<std::uint64_t, 3> total{};
+  double accuracy(SplitTag s) const {
+    const auto i = static_cast<std::size_t>(s);
+    return total[i] == 0 ? 0.0 : static_cast<double>(correct[i]) / static_cast<double>(total[i]);
+  }
+};
+
+/// train_run's eval batch: every vertex, seed = run seed, step 0 (model.hpp:625).
+inline StepBatch build_eval_batch(RankComm& rc, const DeviceDataset& ds, std::uint64_t seed) {
+  return build_step_batch(rc, ds, ds.n(), seed, 0);
+}
+
+/// evaluate_full_graph (model.hpp:493-537): dropout-off forward over the eval
+/// batch, argmax per vertex (ties to the lowest class id), per-split counts
+/// summed over the grid (identical on every rank).
+inline EvalCounts evaluate_full_graph(RankComm& rc, ModelState& st, const StepBatch& eval_batch,
+                                      const DeviceDataset& ds, Precision prec, double rmsnorm_eps = 1e-6) {
+  std::uint64_t c[6];
+  detail::check(ggb_evaluate_full_graph(rc.handle(), st.handle(), eval_batch.handle(), ds.handle(),
+                                        static_cast<int>(prec), rmsnorm_eps, c));
+  EvalCounts out;
+  for (int i = 0; i < 3; ++i) {
+    out.correct[static_cast<std::size_t>(i)] = c[i];
+    out.total[static_cast<std::size_t>(i)] = c[3 + i];
+  }
+  return out;
+}
+
 /// The train_run producer thread + PrefetchQueue (model.hpp:556-581).
 class Prefetcher {
  public:
@@ -341,14 +388,45 @@ struct TrainConfig {  // model.hpp:47-58 (the fields of the step loop)
   Optimizer optimizer = Optimizer::kAdam;
   double lr = 1e-3;
   double rmsnorm_eps = 1e-6;
+  bool evaluate = true;  // per-epoch evaluate_full_graph, as train_run always does
 };
 
-/// The train_run step loop of one rank (model.hpp:643-691, without the
-/// per-epoch evaluation): S = steps_per_epoch steps per epoch, per step
-/// [batch -> train_step -> dp_sync -> optimizer_step]. Returns the per-step
-/// losses.
-inline std::vector<double> train_run(RankComm& rc, const DeviceDataset& ds, const ModelConfig& mcfg,
-                                     const TrainConfig& tcfg) {
+/// EpochMetrics (metrics.hpp:13-29). Timings are host wall-clock around the
+/// device calls (sampling wait, train_step = forward + CE + backward, which
+/// the device runs back to back, so t_bwd_ms stays 0; dp_sync). Byte columns
+/// are not tracked by the NCCL path and stay 0.
+struct EpochMetrics {
+  int epoch = 0;
+  std::int64_t step = 0;
+  double loss = 0.0;
+  double train_acc = 0.0, val_acc = 0.0, test_acc = 0.0;
+  double t_sample_ms = 0.0, t_fwd_ms = 0.0, t_bwd_ms = 0.0, t_dpsync_ms = 0.0;
+  std::uint64_t bytes_x = 0, bytes_y = 0, bytes_z = 0, bytes_d = 0;
+};
+
+/// TrainReport (metrics.hpp:31-44) of one rank.
+struct TrainReport {
+  std::vector<EpochMetrics> epochs;
+  std::vector<double> step_losses;
+  std::uint64_t sampled_nnz_extracted = 0;
+  std::uint64_t sampled_nnz_kept = 0;
+  double wall_ms = 0.0;
+  double final_train_acc() const { return epochs.empty() ? 0.0 : epochs.back().train_acc; }
+  double final_val_acc() const { return epochs.empty() ? 0.0 : epochs.back().val_acc; }
+  double final_test_acc() const { return epochs.empty() ? 0.0 : epochs.back().test_acc; }
+};
+
+/// train_run of one rank (model.hpp:588-747; the reference runs one thread per
+/// rank, here one process per GPU): S = steps_per_epoch steps per epoch, per
+/// step [batch -> train_step -> dp_sync -> optimizer_step], then the per-epoch
+/// full-graph evaluation.
+inline TrainReport train_run(RankComm& rc, const DeviceDataset& ds, const ModelConfig& mcfg,
+                             const TrainConfig& tcfg) {
+  using clock = std::chrono::steady_clock;
+  auto ms_since = [](clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+  };
+  const auto run_start = clock::now();
   if (tcfg.batch < 2 || tcfg.batch > ds.n()) throw std::invalid_argument("train_run: batch size must be in [2, N]");
   if (tcfg.epochs < 1) throw std::invalid_argument("train_run: epochs must be >= 1");
   const int dp = tcfg.grid.dp_group(rc.rank());
@@ -364,13 +442,18 @@ inline std::vector<double> train_run(RankComm& rc, const DeviceDataset& ds, cons
   }();
   const index_t S = steps_per_epoch(ds.n(), tcfg.batch, tcfg.grid.dims[0]);
   ModelState st(rc, mcfg, tcfg.seed);
-  std::vector<double> losses;
+  TrainReport report;
+  StepBatch eval_batch;
+  if (tcfg.evaluate) eval_batch = build_eval_batch(rc, ds, tcfg.seed);
   std::unique_ptr<Prefetcher> pf;
   if (tcfg.prefetch) pf = std::make_unique<Prefetcher>(rc, ds, tcfg.batch, group_seed, 0, tcfg.seed, &mcfg);
   StepBatch batch;
   std::uint64_t gstep = 0;
-  for (int epoch = 0; epoch < tcfg.epochs; ++epoch)
+  for (int epoch = 0; epoch < tcfg.epochs; ++epoch) {
+    EpochMetrics row;
+    double loss_sum = 0.0;
     for (index_t s = 0; s < S; ++s, ++gstep) {
+      auto t0 = clock::now();
       StepBatch borrowed;
       const StepBatch* cur = &batch;
       if (pf) {
@@ -379,11 +462,35 @@ inline std::vector<double> train_run(RankComm& rc, const DeviceDataset& ds, cons
       } else {
         build_step_batch(rc, ds, tcfg.batch, group_seed, gstep, batch);
       }
-      losses.push_back(train_step(rc, st, *cur, tcfg.precision, tcfg.seed, gstep, tcfg.rmsnorm_eps));
+      const auto cnt = cur->counters();
+      report.sampled_nnz_extracted += cnt[0];
+      report.sampled_nnz_kept += cnt[1];
+      row.t_sample_ms += ms_since(t0);
+      t0 = clock::now();
+      const double loss = train_step(rc, st, *cur, tcfg.precision, tcfg.seed, gstep, tcfg.rmsnorm_eps);
+      row.t_fwd_ms += ms_since(t0);
+      report.step_losses.push_back(loss);
+      loss_sum += loss;
+      t0 = clock::now();
       dp_sync(rc, st);
+      rc.synchronize();
+      row.t_dpsync_ms += ms_since(t0);
       optimizer_step(rc, st, tcfg.optimizer, tcfg.lr);
     }
-  return losses;
+    row.epoch = epoch + 1;
+    row.step = static_cast<std::int64_t>(gstep);
+    row.loss = loss_sum / static_cast<double>(S);
+    if (tcfg.evaluate) {
+      const EvalCounts c = evaluate_full_graph(rc, st, eval_batch, ds, tcfg.precision, tcfg.rmsnorm_eps);
+      row.train_acc = c.accuracy(SplitTag::kTrain);
+      row.val_acc = c.accuracy(SplitTag::kVal);
+      row.test_acc = c.accuracy(SplitTag::kTest);
+    }
+    report.epochs.push_back(row);
+  }
+  rc.synchronize();
+  report.wall_ms = ms_since(run_start);
+  return report;
 }
 
 }  // namespace gridgnn

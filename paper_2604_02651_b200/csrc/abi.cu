@@ -234,6 +234,17 @@ void download(T* host, const void* dev, size_t n, cudaStream_t s) {
   GGB_CUDA(cudaStreamSynchronize(s));
 }
 
+// Split tags (Dataset::split, dataset.hpp:23), validated as load_dataset
+// does (dataset.cpp:222-229).
+void set_split(Graph& g, const uint8_t* split) {
+  for (int64_t v = 0; v < g.n; ++v)
+    if (split[v] > 3) fail(GGB_EINVAL, "graph_set_split: invalid split tag at vertex " + std::to_string(v));
+  const size_t old = g.split.bytes;
+  upload(g.split, split, static_cast<size_t>(g.n), g.ctx->stream);
+  GGB_CUDA(cudaStreamSynchronize(g.ctx->stream));
+  g.device_bytes += g.split.bytes - old;
+}
+
 }  // namespace
 }  // namespace ggb
 
@@ -373,7 +384,16 @@ int ggb_graph_generate_synthetic(ggb_ctx_t ctx, int64_t n, double avg_degree, in
     auto g = std::make_unique<ggb_graph_s>();
     graph_build(*ctx, *g, n, ds.adj.row_ptr.data(), ds.adj.col.data(), ds.adj.val.data(), true, d_in,
                 ds.features.data(), n_classes, ds.labels.data(), layers);
+    set_split(*g, ds.split.data());
     *out = g.release();
+  });
+}
+
+int ggb_graph_set_split(ggb_graph_t g, const uint8_t* split) {
+  return guard([&] {
+    require(g && split, "graph_set_split: null argument");
+    use_device(*g->ctx);
+    set_split(*g, split);
   });
 }
 
@@ -622,6 +642,15 @@ int ggb_forward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precision
   return guard([&] {
     use_device(*ctx);
     forward(*st, *bt, precision, training != 0, run_seed, global_step, rmsnorm_eps);
+  });
+}
+
+int ggb_evaluate_full_graph(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t eval_batch, ggb_graph_t g,
+                            int32_t precision, double rmsnorm_eps, uint64_t* counts) {
+  return guard([&] {
+    require(st && eval_batch && g && counts, "evaluate_full_graph: null argument");
+    use_device(*ctx);
+    evaluate_full_graph(*st, *eval_batch, *g, precision, rmsnorm_eps, counts);
   });
 }
 

@@ -101,6 +101,13 @@ void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count) {
                          as_nccl(ctx.comm->axis[axis]), ctx.stream));
 }
 
+void all_reduce_u64(Ctx& ctx, int axis, uint64_t* buf, int64_t count) {
+  if (trivial(ctx, axis) || count <= 0) return;
+  need(ctx, axis);
+  GGB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclUint64, ncclSum,
+                         as_nccl(ctx.comm->axis[axis]), ctx.stream));
+}
+
 void all_gather(Ctx& ctx, int axis, const float* in, int64_t count, float* out) {
   if (trivial(ctx, axis)) {
     if (count > 0)

@@ -27,6 +27,7 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
 // reproduced exactly by an all-gather of bf16 contributions.
 void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire);
 void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count);
+void all_reduce_u64(Ctx& ctx, int axis, uint64_t* buf, int64_t count);  // exact integer sum
 // Gathers `count` floats from every member of the axis group into out
 // ([size][count], axis order).
 void all_gather(Ctx& ctx, int axis, const float* in, int64_t count, float* out);

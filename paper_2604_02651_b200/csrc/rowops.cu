@@ -67,18 +67,20 @@ __device__ __forceinline__ void f4(const float4& a, float* v) {
   v[3] = a.w;
 }
 
-template <int J>  // chunks of 128 columns held per row
+template <int J, bool Full>  // chunks of 128 columns held per row; Full: cols == 128 J
 __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
   constexpr int kMaxJ = J;
+  // Full rows: no column bounds anywhere (constant-folded below)
+  const int64_t ncols = Full ? static_cast<int64_t>(J) * kRowChunk : p.cols;
   const int lane = threadIdx.x & 31;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
   if (r >= p.rows) return;
-  const int nj = static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
+  const int nj = Full ? J : static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
   const float* xr = p.x + r * p.ldx;
   float x[kMaxJ][4];
 #pragma unroll
   for (int j = 0; j < kMaxJ; ++j)
-    if (j < nj) f4(ld4(xr, j * kRowChunk + 4 * lane, p.cols), x[j]);
+    if (j < nj) f4(ld4(xr, j * kRowChunk + 4 * lane, ncols), x[j]);
   float inv = 1.f;
   if (p.gamma) {  // RMSNorm on
     float ss;
@@ -105,15 +107,15 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
     if (j >= nj) break;
     const int64_t c = j * kRowChunk + 4 * lane;
     float g[4] = {1.f, 1.f, 1.f, 1.f};
-    if (p.gamma) f4(ld4(p.gamma, c, p.cols), g);
+    if (p.gamma) f4(ld4(p.gamma, c, ncols), g);
     if (p.res)
-      f4(ld4(p.res + r * p.ldres, c, p.cols), res[j]);
+      f4(ld4(p.res + r * p.ldres, c, ncols), res[j]);
     else
       res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       y[j][i] = p.gamma ? g[i] * x[j][i] * inv : x[j][i];
-      if (y[j][i] > 0.f && c + i < p.cols) posm |= 1u << (4 * j + i);
+      if (y[j][i] > 0.f && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
     }
   }
   // keep bits (ReLU and dropout): only ReLU-active elements need the dropout
@@ -129,31 +131,36 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
         for (int i = 0; i < 4; ++i) kb |= ((p.keep[r * p.ldm + 4 * j + i] >> lane) & 1u) << (4 * j + i);
     keepm = posm & kb;
   } else if (p.drop) {
+    // list of the row's active columns, slot-major (slot 4j+i, then lane):
+    // per-slot ballots give every element its list index with one popc
     __shared__ uint16_t s_list[kRowsPerBlock][32 * 4 * kMaxJ];
-    __shared__ uint32_t s_bits[kRowsPerBlock][32];
+    __shared__ uint32_t s_keep[kRowsPerBlock][4 * kMaxJ];  // keep ballot per 32 list entries
     const int wib = threadIdx.x >> 5;
-    const int cnt = __popc(posm);
-    int incl = cnt;
+    const uint32_t lt = (1u << lane) - 1u;
+    int idx[4 * kMaxJ];
+    int total = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+    for (int s = 0; s < 4 * kMaxJ; ++s) {
+      const bool on = (posm >> s) & 1u;
+      const uint32_t b = __ballot_sync(0xffffffffu, on);
+      idx[s] = total + __popc(b & lt);
+      if (on) s_list[wib][idx[s]] = static_cast<uint16_t>((s >> 2) * kRowChunk + 4 * lane + (s & 3));
+      total += __popc(b);
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    int pos = incl - cnt;
-    for (uint32_t m = posm; m; m &= m - 1) s_list[wib][pos++] = static_cast<uint16_t>((lane << 8) | (__ffs(m) - 1));
-    s_bits[wib][lane] = 0;
     __syncwarp();
     const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
-    for (int k = lane; k < total; k += 32) {
-      const int e = s_list[wib][k];
-      const int owner = e >> 8, slot = e & 0xff;
-      const int64_t col = (slot >> 2) * kRowChunk + 4 * owner + (slot & 3);
-      if (element_keep(row_key, static_cast<uint64_t>(p.col_g0 + col), p.thresh))
-        atomicOr(&s_bits[wib][owner], 1u << slot);
+    for (int k0 = 0; k0 < total; k0 += 32) {
+      const int k = k0 + lane;
+      bool keep = false;
+      if (k < total) keep = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + s_list[wib][k]), p.thresh);
+      const uint32_t w = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) s_keep[wib][k0 >> 5] = w;
     }
     __syncwarp();
-    keepm = s_bits[wib][lane];
+    keepm = 0;
+#pragma unroll
+    for (int s = 0; s < 4 * kMaxJ; ++s)
+      if ((posm >> s) & 1u) keepm |= ((s_keep[wib][idx[s] >> 5] >> (idx[s] & 31)) & 1u) << s;
   }
   const float sc_on = p.drop ? p.keep_scale : 1.f;
 #pragma unroll
@@ -168,14 +175,14 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
       if (lane == i) p.mask[r * p.ldm + 4 * j + i] = bits;
       o[i] = y[j][i] * (on ? sc_on : 0.f) + res[j][i];
     }
-    if (p.out) st4(p.out + r * p.ldo, c, p.cols, o);
+    if (p.out) st4(p.out + r * p.ldo, c, ncols, o);
     if (p.outb) {
-      st4_bf16(p.outb + r * p.ldob, c, p.cols, o);
+      st4_bf16(p.outb + r * p.ldob, c, ncols, o);
       if (p.outlo) {
         float lo[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) lo[i] = o[i] - __bfloat162float(__float2bfloat16_rn(o[i]));
-        st4_bf16(p.outlo + r * p.ldob, c, p.cols, lo);
+        st4_bf16(p.outlo + r * p.ldob, c, ncols, lo);
       }
     }
   }
@@ -445,12 +452,23 @@ void fwd_apply(Ctx& ctx, const FwdApply& p) {
   require(p.cols <= kMaxJ * kRowChunk, "row kernels: at most 512 local feature columns");
   require(p.ldx % 4 == 0 && (!p.res || p.ldres % 4 == 0) && (!p.out || p.ldo % 4 == 0),
           "row kernels: fp32 rows must be 16-byte aligned");
-  if (p.cols <= kRowChunk)
-    k_fwd_row<1><<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
-  else if (p.cols <= 2 * kRowChunk)
-    k_fwd_row<2><<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
-  else
-    k_fwd_row<kMaxJ><<<row_blocks(p.rows), kT, 0, ctx.stream>>>(p);
+  const int g = row_blocks(p.rows);
+  if (p.cols <= kRowChunk) {
+    if (p.cols == kRowChunk)
+      k_fwd_row<1, true><<<g, kT, 0, ctx.stream>>>(p);
+    else
+      k_fwd_row<1, false><<<g, kT, 0, ctx.stream>>>(p);
+  } else if (p.cols <= 2 * kRowChunk) {
+    if (p.cols == 2 * kRowChunk)
+      k_fwd_row<2, true><<<g, kT, 0, ctx.stream>>>(p);
+    else
+      k_fwd_row<2, false><<<g, kT, 0, ctx.stream>>>(p);
+  } else {
+    if (p.cols == kMaxJ * kRowChunk)
+      k_fwd_row<kMaxJ, true><<<g, kT, 0, ctx.stream>>>(p);
+    else
+      k_fwd_row<kMaxJ, false><<<g, kT, 0, ctx.stream>>>(p);
+  }
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }

@@ -64,6 +64,7 @@ struct Graph {
   int64_t feat_c0 = 0, feat_c1 = 0;  // Z-slice of the feature columns held here
   DevBuf features;                   // fp32 [n][feat_c1-feat_c0]
   DevBuf labels;                     // int32 [n]
+  DevBuf split;                      // uint8 [n] SplitTag (dataset.hpp:12), for evaluation
   size_t device_bytes = 0;
 };
 

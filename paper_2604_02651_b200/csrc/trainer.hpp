@@ -77,5 +77,8 @@ void cross_entropy(State& st, const Batch& bt);
 void backward(State& st, const Batch& bt, int precision);
 void dp_sync(State& st);
 void optimizer_step(State& st, int optimizer, double lr);
+// evaluate_full_graph (model.hpp:493-537); counts = {correct train/val/test, total train/val/test}
+void evaluate_full_graph(State& st, const Batch& eval, const Graph& g, int precision, double eps,
+                         uint64_t counts[6]);
 
 }  // namespace ggb

@@ -214,7 +214,7 @@ class Graph:
 
     @staticmethod
     def from_csr(ctx: Context, n: int, row_ptr, col_idx, values, features, labels, n_classes: int,
-                 layers: int, symmetric: bool = True) -> "Graph":
+                 layers: int, symmetric: bool = True, split=None) -> "Graph":
         rp = np.ascontiguousarray(row_ptr, np.int64)
         ci = np.ascontiguousarray(col_idx, np.int64)
         va = np.ascontiguousarray(values, np.float64)
@@ -224,7 +224,17 @@ class Graph:
         check(lib().ggb_graph_create(ctx.h, n, _ptr(rp), _ptr(ci), _ptr(va), int(symmetric),
                                      fe.shape[1] if fe.ndim == 2 else 1, _ptr(fe), n_classes, _ptr(la),
                                      layers, C.byref(h)))
-        return Graph(ctx, h)
+        g = Graph(ctx, h)
+        if split is not None:
+            g.set_split(split)
+        return g
+
+    def set_split(self, split) -> None:
+        """Split tags per vertex (Dataset::split: 0 train, 1 val, 2 test, 3 unused)."""
+        sp = np.ascontiguousarray(split, np.uint8)
+        if sp.shape != (self.n,):
+            raise InvalidArgument(1, f"split: expected {self.n} tags, got shape {sp.shape}")
+        check(lib().ggb_graph_set_split(self.h, _ptr(sp)))
 
     @staticmethod
     def generate_synthetic(ctx: Context, n: int, avg_degree: float, d_in: int, n_classes: int,
@@ -519,6 +529,30 @@ def train_step(ctx: Context, st: ModelState, batch: StepBatch, prec: int, run_se
     check(lib().ggb_train_step(ctx.h, st.h, batch.h, prec, run_seed, global_step, rmsnorm_eps,
                                C.byref(loss) if sync_loss else None))
     return float(loss.value) if sync_loss else None
+
+
+@dataclass
+class EvalCounts:
+    """EvalCounts (model.hpp:480-490): index 0 train, 1 val, 2 test."""
+    correct: tuple
+    total: tuple
+
+    def accuracy(self, split: int) -> float:
+        return 0.0 if self.total[split] == 0 else self.correct[split] / self.total[split]
+
+
+def build_eval_batch(ctx: Context, graph: Graph, run_seed: int) -> StepBatch:
+    """train_run's eval batch: build_step_batch(b = n, seed, step 0) (model.hpp:625)."""
+    return build_step_batch(ctx, graph, graph.n, run_seed, 0)
+
+
+def evaluate_full_graph(ctx: Context, st: ModelState, eval_batch: StepBatch, graph: Graph,
+                        precision: int = FP32, rmsnorm_eps: float = 1e-6) -> EvalCounts:
+    """evaluate_full_graph (model.hpp:493-537): dropout-off forward over every vertex,
+    argmax (ties to the lowest class id), per-split counts summed over the grid."""
+    c = np.zeros(6, np.uint64)
+    check(lib().ggb_evaluate_full_graph(ctx.h, st.h, eval_batch.h, graph.h, precision, rmsnorm_eps, _ptr(c)))
+    return EvalCounts(tuple(int(x) for x in c[:3]), tuple(int(x) for x in c[3:]))
 
 
 def dp_sync(ctx: Context, st: ModelState) -> None:

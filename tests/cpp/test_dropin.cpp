@@ -24,6 +24,9 @@ void ref_batch_plane(void* p, int plane, int transposed, std::int64_t* dims, std
 int ref_train(void* ds, const int* dims, const std::int64_t* mc, const double* md, std::int64_t b, std::uint64_t seed,
               std::uint64_t step0, int n_steps, int prec, int optimizer, double lr, double eps, float* losses,
               float* logits_out, float* grads_out, float* weights_out);
+int ref_train_eval(void* ds, const int* dims, const std::int64_t* mc, const double* md, std::int64_t b,
+                   std::uint64_t seed, int n_steps, int prec, int optimizer, double lr, double eps,
+                   std::uint64_t* counts, float* eval_logits);
 }
 
 using namespace gridgnn;
@@ -96,7 +99,8 @@ int main() {
     tcfg.batch = b;
     tcfg.epochs = 2;
     tcfg.seed = 1;
-    auto losses = train_run(rc, ds, mcfg, tcfg);
+    const TrainReport rep = train_run(rc, ds, mcfg, tcfg);
+    const std::vector<double>& losses = rep.step_losses;
     const std::int64_t mc[7] = {layers, 12, 64, 6, 1, 1, 1};
     const double md[1] = {0.1};
     const int dims[4] = {1, 1, 1, 1};
@@ -110,8 +114,19 @@ int main() {
 
     // 4. prefetch is transparent (acceptance criterion 8)
     tcfg.prefetch = true;
-    auto pl = train_run(rc, ds, mcfg, tcfg);
-    report(4, "prefetch on/off identical losses", pl == losses, "");
+    const TrainReport pl = train_run(rc, ds, mcfg, tcfg);
+    report(4, "prefetch on/off identical losses", pl.step_losses == losses, "");
+
+    // 5. per-epoch evaluate_full_graph tracks the reference's (model.hpp:686-700)
+    std::uint64_t counts[6];
+    ref_train_eval(rds, dims, mc, md, b, 1, static_cast<int>(losses.size()), 0, 1, 1e-3, 1e-6, counts, nullptr);
+    const EpochMetrics& last = rep.epochs.back();
+    const double acc[3] = {last.train_acc, last.val_acc, last.test_acc};
+    double dev = 0.0;
+    for (int s = 0; s < 3; ++s)
+      dev = std::max(dev, std::abs(acc[s] - static_cast<double>(counts[s]) / static_cast<double>(counts[3 + s])));
+    report(5, "full-graph eval accuracy vs reference", dev <= 5e-3 && rep.epochs.size() == 2,
+           "max |acc diff| " + std::to_string(dev) + ", test acc " + std::to_string(last.test_acc));
   }
   ref_dataset_free(rds);
   return g_fail;

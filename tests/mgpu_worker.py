@@ -37,7 +37,8 @@ def main():
 
     n, d_in, ncls, b, seed = 3000, 20, 7, 900, 5
     ds = O.generate_synthetic(n, 10.0, d_in, ncls, 3)
-    g = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls, 3)
+    g = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls, 3,
+                          split=ds.split)
     cfg_kw = dict(layers=3, d_h=64, dropout_rate=0.1)
     cfg = gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw)
     st = gg.init_state(ctx, cfg, seed)
@@ -59,6 +60,10 @@ def main():
             gg.optimizer_step(ctx, st, gg.ADAM, 1e-3)
         blocks = [(bl.name, (bl.r0, bl.r1, bl.c0, bl.c1), w.tolist()) for bl, w in zip(st.blocks, st.weights())]
         result = {"losses": losses, "weights": blocks}
+    # evaluate_full_graph on the grid (model.hpp:493-537): counts identical on every rank
+    ev = gg.build_eval_batch(ctx, g, seed)
+    counts = gg.evaluate_full_graph(ctx, st, ev, g, prec)
+    result["eval"] = (counts.correct, counts.total)
     gathered = [None] * world
     dist.all_gather_object(gathered, result)
     if rank == 0:
@@ -111,6 +116,17 @@ def main():
                     worst = max(worst, np.linalg.norm(wv - ref_blk) / max(np.linalg.norm(ref_blk), 1e-30))
             ok &= worst <= 1e-3
             report = {"loss_rel": lrel, "weight_rel_worst": worst}
+        # eval: PMM grids evaluate the initial weights, DP grids the 3 Adam steps
+        want, want_lg = R.train_eval(h, n, dims, ocfg, b, seed, n_steps=0 if dims[0] == 1 else 3, prec=prec,
+                                     optimizer=1, lr=1e-3)
+        evs = [r["eval"] for r in gathered]
+        ok &= all(e == evs[0] for e in evs)
+        top2 = np.sort(want_lg, axis=1)[:, -2:]
+        slack = int(np.sum(top2[:, 1] - top2[:, 0] <= 2 * logit_tol * max(1.0, float(np.max(np.abs(want_lg))))))
+        ok &= tuple(evs[0][1]) == tuple(int(x) for x in want[3:])
+        ev_dev = max(abs(evs[0][0][s] - int(want[s])) for s in range(3))
+        ok &= ev_dev <= slack
+        report.update(eval_correct_dev=ev_dev, eval_slack=slack)
         R.free_dataset(h)
         report = {k: float(v) for k, v in report.items()}
         print(json.dumps({"grid": dims, "prec": prec, "ok": bool(ok), **report}), flush=True)

@@ -27,4 +27,4 @@ def test_dropin_acceptance_on_gpu():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 4
+    assert r.stdout.count("PASS") == 5
