@@ -119,6 +119,47 @@ void all_gather(Ctx& ctx, int axis, const float* in, int64_t count, float* out) 
                          as_nccl(ctx.comm->axis[axis]), ctx.stream));
 }
 
+void exchange_blocks(Ctx& ctx, const std::vector<BlockXfer>& sends, const std::vector<BlockXfer>& recvs) {
+  if (sends.empty() && recvs.empty()) return;
+  if (!ctx.comm) fail(GGB_ECONTRACT, "block exchange on a context without communicators");
+  Comm& c = *ctx.comm;
+  int64_t ns = 0, nr = 0;
+  for (const auto& x : sends) ns += x.rows * x.cols;
+  for (const auto& x : recvs) nr += x.rows * x.cols;
+  float* sbuf = c.wire.reserve_n<float>(static_cast<size_t>(std::max<int64_t>(ns, 1)));
+  float* rbuf = c.gather.reserve_n<float>(static_cast<size_t>(std::max<int64_t>(nr, 1)));
+  int64_t off = 0;
+  for (const auto& x : sends) {
+    if (x.rows * x.cols == 0) continue;
+    GGB_CUDA(cudaMemcpy2DAsync(sbuf + off, x.cols * 4, x.ptr, x.ld * 4, x.cols * 4, x.rows,
+                               cudaMemcpyDeviceToDevice, ctx.stream));
+    off += x.rows * x.cols;
+  }
+  GGB_NCCL(ncclGroupStart());
+  off = 0;
+  for (const auto& x : sends) {
+    const int64_t n = x.rows * x.cols;
+    if (n == 0) continue;
+    GGB_NCCL(ncclSend(sbuf + off, static_cast<size_t>(n), ncclFloat32, x.peer, as_nccl(c.world), ctx.stream));
+    off += n;
+  }
+  off = 0;
+  for (const auto& x : recvs) {
+    const int64_t n = x.rows * x.cols;
+    if (n == 0) continue;
+    GGB_NCCL(ncclRecv(rbuf + off, static_cast<size_t>(n), ncclFloat32, x.peer, as_nccl(c.world), ctx.stream));
+    off += n;
+  }
+  GGB_NCCL(ncclGroupEnd());
+  off = 0;
+  for (const auto& x : recvs) {
+    if (x.rows * x.cols == 0) continue;
+    GGB_CUDA(cudaMemcpy2DAsync(x.ptr, x.ld * 4, rbuf + off, x.cols * 4, x.cols * 4, x.rows,
+                               cudaMemcpyDeviceToDevice, ctx.stream));
+    off += x.rows * x.cols;
+  }
+}
+
 void barrier(Ctx& ctx) {
   if (ctx.grid.total() == 1) return;
   if (!ctx.comm) fail(GGB_ECONTRACT, "barrier on a context without communicators");

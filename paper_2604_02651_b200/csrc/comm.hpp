@@ -31,6 +31,15 @@ void all_reduce_u64(Ctx& ctx, int axis, uint64_t* buf, int64_t count);  // exact
 // Gathers `count` floats from every member of the axis group into out
 // ([size][count], axis order).
 void all_gather(Ctx& ctx, int axis, const float* in, int64_t count, float* out);
+// Point-to-point block exchange on the world communicator (one NCCL group):
+// every send is a (rows x cols) fp32 sub-block at ptr with leading dimension
+// ld, packed, sent to world rank `peer`; every recv unpacks into its block.
+struct BlockXfer {
+  int peer;
+  float* ptr;
+  int64_t ld, rows, cols;
+};
+void exchange_blocks(Ctx& ctx, const std::vector<BlockXfer>& sends, const std::vector<BlockXfer>& recvs);
 void barrier(Ctx& ctx);
 inline bool trivial(const Ctx& ctx, int axis) { return ctx.grid.dims[axis] == 1; }
 

@@ -38,68 +38,60 @@ T* grow(DevBuf& b, int64_t n) {
 
 std::vector<int64_t> hoff(const Ctx& ctx, int64_t d, int axis) { return block_partition(d, ctx.grid.dims[axis]); }
 
-// ---- reshard (pmm.hpp:171-204): gather the full matrix, slice the new block ---------
-__global__ void k_slice(const float* __restrict__ full, int gr, int64_t maxr, int64_t maxc,
-                        const int64_t* __restrict__ roff, int gc, const int64_t* __restrict__ coff,
-                        int64_t R0, int64_t C0, int64_t rows, int64_t cols, float* __restrict__ out,
-                        int64_t ldo) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= rows * cols) return;
-  const int64_t i = R0 + t / cols, j = C0 + t % cols;
-  int kr = 0, kc = 0;
-  while (kr + 1 < gr && roff[kr + 1] <= i) ++kr;
-  while (kc + 1 < gc && coff[kc + 1] <= j) ++kc;
-  const int64_t li = i - roff[kr], lj = j - coff[kc];
-  out[(t / cols) * ldo + (t % cols)] = full[((static_cast<int64_t>(kc) * gr + kr) * maxr + li) * maxc + lj];
-}
-
-__global__ void k_pad_copy(const float* __restrict__ in, int64_t ld, int64_t rows, int64_t cols,
-                           float* __restrict__ out, int64_t maxc) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= rows * cols) return;
-  out[(t / cols) * maxc + t % cols] = in[(t / cols) * ld + t % cols];
-}
-
-struct ReshardWork {
-  DevBuf pad, stage1, full, offs;
-  PinnedBuf hoffs;
+// ---- reshard (pmm.hpp:171-204) as a block permutation -----------------------------
+// The reference all-gathers the full matrix along both source axes and slices
+// the new block. Here every destination rank receives exactly the pieces of
+// its new block, each from one provider: the rank holding that source block
+// whose coordinate on the source layout's replica axis equals the receiver's
+// (so replicas of a source block share the sending). Pure data movement, hence
+// bit-exact; about g^2 times fewer bytes than the gather.
+struct Span {
+  int64_t lo, hi;
 };
+inline Span meet(int64_t a0, int64_t a1, int64_t b0, int64_t b1) { return {std::max(a0, b0), std::min(a1, b1)}; }
 
-// dst block of the same global matrix under another layout / partition.
-void reshard(Ctx& ctx, ReshardWork& w, const Block& sb, const std::vector<int64_t>& s_roff,
-             const std::vector<int64_t>& s_coff, const float* src, int64_t lds, const Block& db,
-             float* dst, int64_t ldd) {
-  const int gr = static_cast<int>(s_roff.size()) - 1, gc = static_cast<int>(s_coff.size()) - 1;
-  int64_t maxr = 1, maxc = 1;
-  for (int k = 0; k < gr; ++k) maxr = std::max(maxr, s_roff[k + 1] - s_roff[k]);
-  for (int k = 0; k < gc; ++k) maxc = std::max(maxc, s_coff[k + 1] - s_coff[k]);
-  const int64_t blk = maxr * maxc;
-  float* pad = w.pad.reserve_n<float>(blk);
-  GGB_CUDA(cudaMemsetAsync(pad, 0, blk * 4, ctx.stream));
-  if (sb.rows() * sb.cols() > 0)
-    k_pad_copy<<<static_cast<unsigned>(ceil_div(sb.rows() * sb.cols(), 256)), 256, 0, ctx.stream>>>(
-        src, lds, sb.rows(), sb.cols(), pad, maxc);
-  float* s1 = w.stage1.reserve_n<float>(blk * gr);
-  all_gather(ctx, sb.lay.row, pad, blk, s1);
-  float* full = w.full.reserve_n<float>(blk * gr * gc);
-  all_gather(ctx, sb.lay.col, s1, blk * gr, full);
-  int64_t* ho = static_cast<int64_t*>(w.hoffs.reserve((gr + gc + 2) * 8));
-  std::copy(s_roff.begin(), s_roff.end(), ho);
-  std::copy(s_coff.begin(), s_coff.end(), ho + gr + 1);
-  int64_t* doffs = w.offs.reserve_n<int64_t>(gr + gc + 2);
-  GGB_CUDA(cudaMemcpyAsync(doffs, ho, (gr + gc + 2) * 8, cudaMemcpyHostToDevice, ctx.stream));
-  const int64_t n = db.rows() * db.cols();
-  if (n > 0)
-    k_slice<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, ctx.stream>>>(
-        full, gr, maxr, maxc, doffs, gc, doffs + gr + 1, db.r0, db.c0, db.rows(), db.cols(), dst, ldd);
-  GGB_CUDA(cudaStreamSynchronize(ctx.stream));  // pinned offsets are reused
-  GGB_LAUNCH_CHECK();
-  ctx.launches += 3;
-}
-
-ReshardWork& reshard_work() {
-  static thread_local ReshardWork w;
-  return w;
+void reshard(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff, const std::vector<int64_t>& s_coff,
+             const float* src, int64_t lds, const Block& db, const std::vector<int64_t>& d_roff,
+             const std::vector<int64_t>& d_coff, float* dst, int64_t ldd) {
+  const Grid& G = ctx.grid;
+  const int me = ctx.rank;
+  int mc[4];
+  G.coord_of(me, mc);
+  const Layout sl = sb.lay, dl = db.lay;
+  const int s_rep = third_axis(sl);
+  std::vector<BlockXfer> sends, recvs;
+  // receives: pieces of my destination block
+  for (int i = 0; i + 1 < static_cast<int>(s_roff.size()); ++i)
+    for (int j = 0; j + 1 < static_cast<int>(s_coff.size()); ++j) {
+      const Span r = meet(s_roff[i], s_roff[i + 1], db.r0, db.r1), c = meet(s_coff[j], s_coff[j + 1], db.c0, db.c1);
+      if (r.lo >= r.hi || c.lo >= c.hi) continue;
+      int pc[4] = {mc[0], mc[1], mc[2], mc[3]};
+      pc[sl.row] = i;
+      pc[sl.col] = j;
+      pc[s_rep] = mc[s_rep];
+      const int p = G.rank_of(pc);
+      float* out = dst + (r.lo - db.r0) * ldd + (c.lo - db.c0);
+      if (p == me) {  // local piece
+        GGB_CUDA(cudaMemcpy2DAsync(out, ldd * 4, src + (r.lo - sb.r0) * lds + (c.lo - sb.c0), lds * 4,
+                                   (c.hi - c.lo) * 4, r.hi - r.lo, cudaMemcpyDeviceToDevice, ctx.stream));
+      } else {
+        recvs.push_back({p, out, ldd, r.hi - r.lo, c.hi - c.lo});
+      }
+    }
+  // sends: for every rank q of my DP group that takes its piece from me
+  for (int q = 0; q < G.total(); ++q) {
+    if (q == me) continue;
+    int qc[4];
+    G.coord_of(q, qc);
+    if (qc[0] != mc[0] || qc[s_rep] != mc[s_rep]) continue;  // other DP group / other provider
+    const int64_t q_r0 = d_roff[qc[dl.row]], q_r1 = d_roff[qc[dl.row] + 1];
+    const int64_t q_c0 = d_coff[qc[dl.col]], q_c1 = d_coff[qc[dl.col] + 1];
+    const Span r = meet(sb.r0, sb.r1, q_r0, q_r1), c = meet(sb.c0, sb.c1, q_c0, q_c1);
+    if (r.lo >= r.hi || c.lo >= c.hi) continue;
+    sends.push_back({q, const_cast<float*>(src) + (r.lo - sb.r0) * lds + (c.lo - sb.c0), lds, r.hi - r.lo,
+                     c.hi - c.lo});
+  }
+  exchange_blocks(ctx, sends, recvs);
 }
 
 bool pmm_trivial(const Ctx& ctx) { return ctx.grid.dims[1] == 1 && ctx.grid.dims[2] == 1 && ctx.grid.dims[3] == 1; }
@@ -362,8 +354,8 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
         ldres = prev->ldf;
       } else {
         float* r = grow<float>(st.dres, rb.rows() * ld8(rb.cols()));
-        reshard(ctx, reshard_work(), F, bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), prev->f, prev->ldf, rb,
-                r, ld8(rb.cols()));
+        reshard(ctx, F, bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), prev->f, prev->ldf, rb,
+                bt.batch_off[out.row], hoff(ctx, H, out.col), r, ld8(rb.cols()));
         res = r;
         ldres = ld8(rb.cols());
       }
@@ -525,8 +517,8 @@ void backward(State& st, const Batch& bt, int precision) {
         dres = dxh;  // identical block; the SpMM below accumulates into it
       } else {
         dres = grow<float>(st.dres, F.rows() * ld8(F.cols()));
-        reshard(ctx, reshard_work(), db, bt.batch_off[db.lay.row], hoff(ctx, H, db.lay.col), dxh, ld8(db.cols()), F, dres,
-                ld8(F.cols()));
+        reshard(ctx, db, bt.batch_off[db.lay.row], hoff(ctx, H, db.lay.col), dxh, ld8(db.cols()), F,
+                bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), dres, ld8(F.cols()));
       }
     }
     // fused element-wise backward + RMSNorm backward -> dxw (bf16), dgamma

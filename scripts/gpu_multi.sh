@@ -11,3 +11,7 @@ for gp in 2x1x1x1:0 1x1x1x2:0 1x2x1x1:0 1x1x2x1:1 1x2x2x1:0 1x1x2x2:1 2x1x1x2:0 
     tests/mgpu_worker.py $g $p > gpurun_out/mg_$g.log 2>&1
   echo "$g prec=$p rc=$? $(grep '^{' gpurun_out/mg_$g.log | tail -1)" >> gpurun_out/mg_rc.txt
 done
+# the driver's scaling run: bench.py under torchrun on all GPUs of the box (default DP grid)
+timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1 --master-port=29534 \
+  bench.py --gpus $N --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err
+echo "bench n=$N rc=$?" >> gpurun_out/mg_rc.txt

@@ -122,7 +122,7 @@ def main():
         evs = [r["eval"] for r in gathered]
         ok &= all(e == evs[0] for e in evs)
         top2 = np.sort(want_lg, axis=1)[:, -2:]
-        slack = int(np.sum(top2[:, 1] - top2[:, 0] <= 2 * logit_tol * max(1.0, float(np.max(np.abs(want_lg))))))
+        slack = int(np.sum(top2[:, 1] - top2[:, 0] <= 2 * (1e-3 if prec == 0 else logit_tol) * max(1.0, float(np.max(np.abs(want_lg))))))
         ok &= tuple(evs[0][1]) == tuple(int(x) for x in want[3:])
         ev_dev = max(abs(evs[0][0][s] - int(want[s])) for s in range(3))
         ok &= ev_dev <= slack
