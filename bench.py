@@ -277,12 +277,16 @@ def main():
     c0 = ctx.counters()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    marks = []
     for _ in range(args.steps):
         step(gstep, False)
         gstep += 1
+        marks.append(torch.cuda.Event(enable_timing=True))
+        marks[-1].record(stream)
     ev1.record(stream)
     barrier()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    step_ms = [round((marks[i - 1] if i else ev0).elapsed_time(marks[i]), 3) for i in range(len(marks))]
     c1 = ctx.counters()
     prof = ctx.profile_read(reset=True)
     ctx.profile(False)
@@ -291,12 +295,16 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     losses = []
+    emarks = []
     for _ in range(args.steps):
         losses.append(step(gstep, True))
         gstep += 1
+        emarks.append(torch.cuda.Event(enable_timing=True))
+        emarks[-1].record(stream)
     e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    e2e_step_ms = [round((emarks[i - 1] if i else e0).elapsed_time(emarks[i]), 3) for i in range(len(emarks))]
     c2 = ctx.counters()
     clk = clocks.stop()
     # ---- per-epoch full-graph evaluation (train_run's evaluate_full_graph), timed
@@ -398,6 +406,8 @@ def main():
         "loss_last": losses[-1] if losses else None,
         "graph_build_s": t_graph,
         "eval": ev_info,
+        "step_ms_rank0": step_ms,
+        "e2e_step_ms_rank0": e2e_step_ms,
     }
     if not args.no_cpu_baseline and n_gpus == 1:
         try:

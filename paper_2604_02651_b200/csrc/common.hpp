@@ -74,12 +74,16 @@ struct DevBuf {
   }
   void* reserve(size_t n) {
     if (n > bytes) {
-      // re-growth gets 25% headroom: per-step sizes (batch nonzeros, local
-      // rows) fluctuate, and a cudaFree/cudaMalloc inside a step stalls it
+      // per-step sizes (batch nonzeros, local rows) fluctuate by well under
+      // a percent, and a cudaFree/cudaMalloc inside a step stalls the device:
+      // large first allocations get 1/16 headroom, re-growth 1/4
       const bool regrow = bytes > 0;
       release();
       size_t want = n < 256 ? 256 : n;
-      if (regrow) want += want / 4;
+      if (regrow)
+        want += want / 4;
+      else if (want >= (size_t(1) << 20))
+        want += want / 16;
       GGB_CUDA(cudaMalloc(&p, want));
       bytes = want;
     }

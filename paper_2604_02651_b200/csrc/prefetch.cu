@@ -15,6 +15,8 @@
 #include <thread>
 
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "comm.hpp"
 #include "ops.hpp"
@@ -36,11 +38,16 @@ Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t see
   sctx.device = consumer->device;
   sctx.num_sms = consumer->num_sms;
   GGB_CUDA(cudaSetDevice(sctx.device));
-  // lowest scheduling priority: sampling and mask hashing fill idle SM slots
-  // without displacing the training stream's CTAs
-  int least = 0, greatest = 0;
+  // lowest scheduling priority: sampling (and mask hashing) fill idle SM
+  // slots without displacing the training stream's CTAs (measured ~2% faster
+  // per step than equal priority at 1 and 2 GPUs). GGB_PREFETCH_PRIORITY=same
+  // gives the sampling stream the training stream's priority instead.
+  int least = 0, greatest = 0, prio = 0;
   GGB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-  GGB_CUDA(cudaStreamCreateWithPriority(&sctx.stream, cudaStreamNonBlocking, least));
+  prio = least;
+  const char* pe = std::getenv("GGB_PREFETCH_PRIORITY");
+  if (pe && std::string(pe) == "same") GGB_CUDA(cudaStreamGetPriority(consumer->stream, &prio));
+  GGB_CUDA(cudaStreamCreateWithPriority(&sctx.stream, cudaStreamNonBlocking, prio));
   sctx.own_stream = true;
   for (int s = 0; s < 2; ++s) {
     GGB_CUDA(cudaEventCreateWithFlags(&ready[s], cudaEventDisableTiming));
