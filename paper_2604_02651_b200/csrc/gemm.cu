@@ -25,9 +25,11 @@ namespace {
 
 constexpr int kBM = 128;  // UMMA M (cta_group::1)
 constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16 along K
-constexpr int kThreads = 192;
-constexpr int kSmemBudget = 225 * 1024;         // dynamic smem per CTA (227 KB max on sm_100)
-constexpr int kEpiSmem = 4 * 32 * 17 * 4 + 256;  // barriers + epilogue transpose tiles
+constexpr int kEpiWarps = 8;  // 2 per TMEM lane quarter, each on half of the tile's columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kWgradThreads = 192;
+constexpr int kSmemBudget = 225 * 1024;                 // dynamic smem per CTA (227 KB max on sm_100)
+constexpr int kEpiSmem = kEpiWarps * 32 * 17 * 4 + 256;  // barriers + epilogue transpose tiles
 
 // ---- PTX wrappers --------------------------------------------------------------
 
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, 4);
+      mbar_init(tempty + a, kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -256,12 +258,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncwarp();
-  } else {  // ---- epilogue: warps 2..5, TMEM lane quarter = warp % 4
+  } else {  // ---- epilogue: warps 2..9, TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
     // Each 32-row x 16-column accumulator block goes TMEM -> registers (row
     // per lane) -> padded smem tile -> registers (4 consecutive columns per
     // lane), so the global stores are row-contiguous: 4 lanes cover 64 bytes
     // of one row (fp32) and one store instruction writes 8 full row segments.
     const int q = warp & 3;
+    const int half = (warp - 2) / 4;
     float* stile = reinterpret_cast<float*>(tmem_base_smem + 4) + (warp - 2) * (32 * 17);
     int lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
@@ -272,7 +275,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int64_t row_base = static_cast<int64_t>(mt) * kBM + q * 32;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-      for (int c16 = 0; c16 < BN; c16 += 16) {
+      const int cspan = ((BN / 16 + 1) / 2) * 16;  // columns of this warp's half (multiple of 16)
+      const int cbeg = half * cspan, cend = min(BN, cbeg + cspan);
+      for (int c16 = cbeg; c16 < cend; c16 += 16) {
         float v[16];
         tmem_ld16(taddr + c16, v);
         const int col0 = nt * BN + c16;
@@ -332,7 +337,7 @@ struct WgradArgs {
   float* part;  // [splits][KW][NW]
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kWgradThreads, 1)
     k_gemm_wgrad(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
                  const WgradArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -600,7 +605,7 @@ void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x,
     attr = true;
   }
   dim3 grid(tiles, wa.splits);
-  k_gemm_wgrad<<<grid, kThreads, smem, ctx.stream>>>(tx, td, wa);
+  k_gemm_wgrad<<<grid, kWgradThreads, smem, ctx.stream>>>(tx, td, wa);
   const int64_t total = kw * nw;
   k_reduce_partials<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, ctx.stream>>>(
       wa.part, wa.splits, kw, nw, dw, lddw);
