@@ -356,14 +356,18 @@ def main():
     roof["peak_source"] = peak_kind
     roof["bytes_per_launch"] = dom["bytes"] / dom["launches"]
     roof["ms_per_launch"] = per_launch_ms
-    traffic = None
+    # dram__bytes_read.sum + dram__bytes_write.sum per launch of the same kernel,
+    # from the committed ncu --set full capture (profiles/ncu_traffic.json)
+    roof["traffic"] = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        traffic = tr.get(dom_name)
+            tr = json.load(f).get(dom_name)
+        if tr:
+            roof["traffic"] = tr["bytes"]
+            roof["traffic_over_algorithmic"] = tr["bytes"] / roof["bytes_per_launch"]
+            roof["traffic_source"] = {k: tr[k] for k in ("kernel", "us", "dram_TBps", "source")}
     except Exception:
         pass
-    roof["traffic"] = traffic
     breakdown = {k: {"ms_per_step": v["ms"] / args.steps,
                      "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
                      "TFLOP_per_s": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None,
