@@ -77,10 +77,24 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
   if (r >= p.rows) return;
   const int nj = Full ? J : static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
   const float* xr = p.x + r * p.ldx;
-  float x[kMaxJ][4];
+  // every load of the row (xw, gamma, residual) is issued up front: one
+  // memory round trip per row instead of one before and one after the
+  // row reduction
+  float x[kMaxJ][4], g[kMaxJ][4], res[kMaxJ][4];
 #pragma unroll
-  for (int j = 0; j < kMaxJ; ++j)
-    if (j < nj) f4(ld4(xr, j * kRowChunk + 4 * lane, ncols), x[j]);
+  for (int j = 0; j < kMaxJ; ++j) {
+    if (j >= nj) break;
+    const int64_t c = j * kRowChunk + 4 * lane;
+    f4(ld4(xr, c, ncols), x[j]);
+    if (p.gamma)
+      f4(ld4(p.gamma, c, ncols), g[j]);
+    else
+      g[j][0] = g[j][1] = g[j][2] = g[j][3] = 1.f;
+    if (p.res)
+      f4(ld4(p.res + r * p.ldres, c, ncols), res[j]);
+    else
+      res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
+  }
   float inv = 1.f;
   if (p.gamma) {  // RMSNorm on
     float ss;
@@ -99,22 +113,16 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
     inv = 1.f / rms;
     if (lane == 0 && p.rms) p.rms[r] = rms;
   }
-  // y = gamma * x / rms for every held element; residual loads issued early
-  float y[kMaxJ][4], res[kMaxJ][4];
+  // y = gamma * x / rms for every held element
+  float y[kMaxJ][4];
   uint32_t posm = 0;  // bit 4j+i: y > 0 and the column exists
 #pragma unroll
   for (int j = 0; j < kMaxJ; ++j) {
     if (j >= nj) break;
     const int64_t c = j * kRowChunk + 4 * lane;
-    float g[4] = {1.f, 1.f, 1.f, 1.f};
-    if (p.gamma) f4(ld4(p.gamma, c, ncols), g);
-    if (p.res)
-      f4(ld4(p.res + r * p.ldres, c, ncols), res[j]);
-    else
-      res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      y[j][i] = p.gamma ? g[i] * x[j][i] * inv : x[j][i];
+      y[j][i] = p.gamma ? g[j][i] * x[j][i] * inv : x[j][i];
       if (y[j][i] > 0.f && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
     }
   }
