@@ -149,6 +149,7 @@ struct GemmArgs {
   float* c;
   int64_t ldc;
   bf16* cb;
+  bf16* cl;  // optional lo residual of the bf16 output: c == cb + cl to ~2^-16
   int64_t ldcb;
 };
 
@@ -305,12 +306,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (args.cb) {
             bf16* dst = args.cb + row * args.ldcb + col;
+            bf16* dl = args.cl ? args.cl + row * args.ldcb + col : nullptr;
             if (full4 && (reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
               __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
               *reinterpret_cast<uint2*>(dst) =
                   make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+              if (dl) {
+                const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+                __nv_bfloat162 l0 = __floats2bfloat162_rn(o[0] - f0.x, o[1] - f0.y),
+                               l1 = __floats2bfloat162_rn(o[2] - f1.x, o[3] - f1.y);
+                *reinterpret_cast<uint2*>(dl) =
+                    make_uint2(*reinterpret_cast<uint32_t*>(&l0), *reinterpret_cast<uint32_t*>(&l1));
+              }
             } else {
-              for (int i = 0; i < 4 && col + i < args.N; ++i) dst[i] = __float2bfloat16_rn(o[i]);
+              for (int i = 0; i < 4 && col + i < args.N; ++i) {
+                const bf16 h = __float2bfloat16_rn(o[i]);
+                dst[i] = h;
+                if (dl) dl[i] = __float2bfloat16_rn(o[i] - __bfloat162float(h));
+              }
             }
           }
         }
@@ -450,13 +463,14 @@ __global__ void __launch_bounds__(kWgradThreads, 1)
 }
 
 __global__ void k_reduce_partials(const float* __restrict__ part, int splits, int64_t kw, int64_t nw,
-                                  float* __restrict__ out, int64_t ldo) {
+                                  float* __restrict__ out, int64_t ldo, int accumulate) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t total = kw * nw;
   if (i >= total) return;
   float s = 0.f;
   for (int k = 0; k < splits; ++k) s += part[k * total + i];
-  out[(i / nw) * ldo + (i % nw)] = s;
+  float* o = out + (i / nw) * ldo + (i % nw);
+  *o = accumulate ? *o + s : s;
 }
 
 // ---- host: TMA descriptors through the driver entry point ---------------------------
@@ -521,7 +535,8 @@ int sm_count() {
 // C[m x n] = A[m x k] . Bt[n x k]^T; with a_lo/bt_lo (same layouts) the
 // operands are fp32 values carried as bf16 hi + lo pairs (split-bf16).
 void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, const bf16* a_lo, int64_t lda,
-                    const bf16* bt, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb) {
+                    const bf16* bt, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb,
+                    bf16* cl = nullptr) {
   if (m <= 0 || n <= 0) return;
   require(k > 0, "gemm: k must be positive");
   require(m < (int64_t{1} << 31) && n < (int64_t{1} << 31) && k < (int64_t{1} << 31), "gemm: dims");
@@ -540,6 +555,7 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
   ga.c = c;
   ga.ldc = ldc;
   ga.cb = cb;
+  ga.cl = cb ? cl : nullptr;
   ga.ldcb = ldcb;
   const CUtensorMap ta = make_tmap(a, m, k, lda, kBK, kBM);
   const CUtensorMap tb = make_tmap(bt, n, k, ldb, kBK, ga.BN);
@@ -565,15 +581,17 @@ void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t
 }
 
 void gemm_split(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a_hi, const bf16* a_lo, int64_t lda,
-                const bf16* bt_hi, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb) {
-  gemm_bf16_impl(ctx, m, n, k, a_hi, a_lo, lda, bt_hi, bt_lo, ldb, c, ldc, cb, ldcb);
+                const bf16* bt_hi, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb,
+                bf16* cl) {
+  gemm_bf16_impl(ctx, m, n, k, a_hi, a_lo, lda, bt_hi, bt_lo, ldb, c, ldc, cb, ldcb, cl);
 }
 
 // DW[kw x nw] = X[m x kw]^T . DY[m x nw]; ws: scratch
 void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x, int64_t ldx,
-                     const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws) {
+                     const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws, int accumulate) {
   if (kw <= 0 || nw <= 0) return;
   if (m <= 0) {
+    if (accumulate) return;
     for (int64_t r = 0; r < kw; ++r)
       GGB_CUDA(cudaMemsetAsync(dw + r * lddw, 0, nw * 4, ctx.stream));
     return;
@@ -608,7 +626,7 @@ void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x,
   k_gemm_wgrad<<<grid, kWgradThreads, smem, ctx.stream>>>(tx, td, wa);
   const int64_t total = kw * nw;
   k_reduce_partials<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, ctx.stream>>>(
-      wa.part, wa.splits, kw, nw, dw, lddw);
+      wa.part, wa.splits, kw, nw, dw, lddw, accumulate);
   GGB_LAUNCH_CHECK();
   ctx.launches += 2;
 }

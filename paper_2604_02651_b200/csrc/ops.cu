@@ -9,6 +9,7 @@
 // element_unit(key, global_row, global_col) >= rate (pmm.hpp:317-322),
 // evaluated in the forward pass and kept as one bit per element for the
 // backward pass instead of the reference's fp32 `scale` matrix.
+#include <algorithm>
 #include <cmath>
 
 #include "ops.hpp"
@@ -19,6 +20,10 @@ namespace {
 
 constexpr int kT = 256;
 inline unsigned nb(int64_t n, int t = kT) { return static_cast<unsigned>(ceil_div(n, t)); }
+// warp-per-row kernels: enough 256-thread blocks for every row, capped at 8 waves of 8 blocks per SM
+inline unsigned row_blocks(const Ctx& ctx, int64_t rows) {
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, kT / 32), ctx.num_sms * 64)));
+}
 
 __global__ void k_init_weight(float* __restrict__ w, int64_t rows, int64_t cols, int64_t r0, int64_t c0,
                               uint64_t key, double lim) {
@@ -46,34 +51,67 @@ __global__ void k_weight_bf16(const float* __restrict__ w, int64_t rows, int64_t
   if (wtl) wtl[c * ldt + r] = __float2bfloat16_rn(w[i] - __bfloat162float(v));
 }
 
-__global__ void k_cast_split(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
-                             bf16* __restrict__ hi, bf16* __restrict__ lo, int64_t ldy) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows * cols) return;
-  const int64_t r = i / cols, c = i % cols;
-  const float v = x[r * ldx + c];
-  const bf16 h = __float2bfloat16_rn(v);
-  hi[r * ldy + c] = h;
-  lo[r * ldy + c] = __float2bfloat16_rn(v - __bfloat162float(h));
+// Row-blocked element-wise kernels over padded row-major matrices: one warp
+// per row (grid-stride over rows), lanes over 4-column quads, 16-byte loads
+// where the rows allow it. No index division.
+__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+__device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
+  __nv_bfloat162 h0 = __floats2bfloat162_rn(a, b), h1 = __floats2bfloat162_rn(c, d);
+  return make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
 }
 
-__global__ void k_cast_bf16(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
-                            bf16* __restrict__ y, int64_t ldy) {
-  const int64_t r = blockIdx.y * static_cast<int64_t>(gridDim.x) + blockIdx.x;
-  (void)r;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows * cols) return;
-  const int64_t rr = i / cols, cc = i % cols;
-  y[rr * ldy + cc] = __float2bfloat16_rn(x[rr * ldx + cc]);
+__device__ __forceinline__ float lo_of(float v) { return v - __bfloat162float(__float2bfloat16_rn(v)); }
+
+template <bool Split>
+__global__ void k_cast_rows(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                            bf16* __restrict__ hi, bf16* __restrict__ lo, int64_t ldy) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool vec = (cols & 3) == 0 && (ldx & 3) == 0 && (ldy & 3) == 0 && al16(x) && ((reinterpret_cast<uintptr_t>(hi) & 7) == 0) &&
+                   (!Split || (reinterpret_cast<uintptr_t>(lo) & 7) == 0);
+  for (int64_t r = w0; r < rows; r += nw) {
+    const float* xr = x + r * ldx;
+    if (vec) {
+      for (int64_t c = lane * 4; c < cols; c += 128) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + c);
+        *reinterpret_cast<uint2*>(hi + r * ldy + c) = pack4_bf16(v.x, v.y, v.z, v.w);
+        if (Split) *reinterpret_cast<uint2*>(lo + r * ldy + c) = pack4_bf16(lo_of(v.x), lo_of(v.y), lo_of(v.z), lo_of(v.w));
+      }
+    } else {
+      for (int64_t c = lane; c < cols; c += 32) {
+        const float v = xr[c];
+        hi[r * ldy + c] = __float2bfloat16_rn(v);
+        if (Split) lo[r * ldy + c] = __float2bfloat16_rn(lo_of(v));
+      }
+    }
+  }
 }
 
-__global__ void k_add(float* __restrict__ a, int64_t lda, const float* __restrict__ b, int64_t ldb,
-                      int64_t rows, int64_t cols) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= rows * cols) return;
-  const int64_t r = i / cols, c = i % cols;
-  a[r * lda + c] += b[r * ldb + c];
+__global__ void k_add_rows(float* __restrict__ a, int64_t lda, const float* __restrict__ b, int64_t ldb,
+                           int64_t rows, int64_t cols) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool vec = (cols & 3) == 0 && (lda & 3) == 0 && (ldb & 3) == 0 && al16(a) && al16(b);
+  for (int64_t r = w0; r < rows; r += nw) {
+    if (vec) {
+      for (int64_t c = lane * 4; c < cols; c += 128) {
+        float4 u = *reinterpret_cast<float4*>(a + r * lda + c);
+        const float4 v = *reinterpret_cast<const float4*>(b + r * ldb + c);
+        u.x += v.x;
+        u.y += v.y;
+        u.z += v.z;
+        u.w += v.w;
+        *reinterpret_cast<float4*>(a + r * lda + c) = u;
+      }
+    } else {
+      for (int64_t c = lane; c < cols; c += 32) a[r * lda + c] += b[r * ldb + c];
+    }
+  }
 }
+
 
 // warp per row: ss[r] = sum_j x[r][j]^2 (pmm.hpp:220-228)
 __global__ void k_rowsumsq(const float* __restrict__ x, int64_t ldx, int64_t rows, int64_t cols,
@@ -234,21 +272,21 @@ void weight_bf16(Ctx& ctx, const float* w, int64_t rows, int64_t cols, bf16* wb,
 
 void cast_bf16(Ctx& ctx, const float* x, int64_t rows, int64_t cols, int64_t ldx, bf16* y, int64_t ldy) {
   if (rows * cols <= 0) return;
-  k_cast_bf16<<<nb(rows * cols), kT, 0, ctx.stream>>>(x, rows, cols, ldx, y, ldy);
+  k_cast_rows<false><<<row_blocks(ctx, rows), kT, 0, ctx.stream>>>(x, rows, cols, ldx, y, nullptr, ldy);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
 
 void cast_split(Ctx& ctx, const float* x, int64_t rows, int64_t cols, int64_t ldx, bf16* hi, bf16* lo, int64_t ldy) {
   if (rows * cols <= 0) return;
-  k_cast_split<<<nb(rows * cols), kT, 0, ctx.stream>>>(x, rows, cols, ldx, hi, lo, ldy);
+  k_cast_rows<true><<<row_blocks(ctx, rows), kT, 0, ctx.stream>>>(x, rows, cols, ldx, hi, lo, ldy);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
 
 void add_inplace(Ctx& ctx, float* a, int64_t lda, const float* b, int64_t ldb, int64_t rows, int64_t cols) {
   if (rows * cols <= 0) return;
-  k_add<<<nb(rows * cols), kT, 0, ctx.stream>>>(a, lda, b, ldb, rows, cols);
+  k_add_rows<<<row_blocks(ctx, rows), kT, 0, ctx.stream>>>(a, lda, b, ldb, rows, cols);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }

@@ -108,9 +108,10 @@ void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t
                int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb);
 // split-bf16: fp32 operands carried as (hi, lo) bf16 pairs; 3 tcgen05 MMAs per k-step
 void gemm_split(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a_hi, const bf16* a_lo, int64_t lda,
-                const bf16* bt_hi, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb);
+                const bf16* bt_hi, const bf16* bt_lo, int64_t ldb, float* c, int64_t ldc, bf16* cb, int64_t ldcb,
+                bf16* cl = nullptr);
 void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x, int64_t ldx,
-                     const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws);
+                     const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws, int accumulate = 0);
 // spmm.cu
 void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
               const bf16* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb,

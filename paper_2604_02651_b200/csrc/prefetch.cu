@@ -23,6 +23,7 @@
 #include "prefetch.hpp"
 #include "prof.hpp"
 #include "rng.cuh"
+#include "trainer.hpp"
 
 namespace ggb {
 
@@ -37,6 +38,10 @@ Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t see
   for (int a = 0; a < 4; ++a) sctx.coord[a] = consumer->coord[a];
   sctx.device = consumer->device;
   sctx.num_sms = consumer->num_sms;
+  {
+    const char* e = std::getenv("GGB_SIDE_SMALL");
+    sctx.side_stream = !(e && e[0] == '0');
+  }
   GGB_CUDA(cudaSetDevice(sctx.device));
   // lowest scheduling priority: sampling (and mask hashing) fill idle SM
   // slots without displacing the training stream's CTAs (measured ~2% faster
@@ -83,7 +88,9 @@ void Prefetcher::run() {
         if (stop) return;
       }
       if (k >= 2) GGB_CUDA(cudaStreamWaitEvent(sctx.stream, released[slot], 0));
-      build_step_batch(sctx, *g, b, seed, step0 + static_cast<uint64_t>(k), slots[slot]);
+      const bool pre = preagg_enabled() && preagg_in_prefetch();
+      build_step_batch(sctx, *g, b, seed, step0 + static_cast<uint64_t>(k), slots[slot], pre);
+      if (pre && preagg_eligible(sctx, slots[slot])) preaggregate(sctx, slots[slot]);
       if (drop_layers > 0) make_masks(slots[slot], step0 + static_cast<uint64_t>(k));
       GGB_CUDA(cudaEventRecord(ready[slot], sctx.stream));
       {

@@ -40,6 +40,9 @@ struct Ctx {
   uint64_t launches = 0;              // kernels this library launched
   uint64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of the step path
   int num_sms = 148;
+  // side-stream context (the prefetcher): launch short non-persistent grids,
+  // so compute-stream persistent kernels (one CTA per SM) are not held back
+  bool side_stream = false;
   std::unique_ptr<Prof> prof;
   ~Ctx();
 };
@@ -101,15 +104,22 @@ struct Batch {
   DevBuf x_in;    // bf16 [x_r1-x_r0][x_ld], zero padded (hi of the split pair)
   DevBuf x_in_lo; // bf16 lo residual: x == hi + lo to ~2^-16
   DevBuf labels;  // int32 [b]
+  // first-layer pre-aggregation P = A_0 . x_in (sampler.cu preaggregate): fp32
+  // x_in rows, P as split bf16 [A_0 rows][x_ld]; a cache of the batch, hence mutable
+  mutable DevBuf x_f, p_in, p_in_lo;
+  mutable bool p_ready = false, x_f_ready = false;
   uint64_t nnz_extracted = 0, nnz_kept = 0;
   const Graph* graph = nullptr;
 };
 
 // sampler.cu
 void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* d_sample);
+// want_xf: also keep the fp32 x_in rows for preaggregate() (same gather)
 void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
-                      Batch& out);
+                      Batch& out, bool want_xf = false);
 void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out);
+bool preagg_eligible(const Ctx& ctx, const Batch& bt);
+void preaggregate(Ctx& ctx, const Batch& bt);
 
 // scan.cu: out[0..n] = exclusive prefix sums of in[0..n), out[n] = total.
 void exclusive_scan_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, DevBuf& tmp,

@@ -31,6 +31,7 @@
 // stable csr_transpose order.
 #include <cmath>
 
+#include "ops.hpp"
 #include "prof.hpp"
 #include "rng.cuh"
 #include "runtime.hpp"
@@ -221,21 +222,46 @@ __global__ void k_extract_fill(int64_t nr, const int64_t* __restrict__ sample, i
   }
 }
 
-// x_in rows: bf16 hi (+ lo residual for the split-bf16 GEMM) and/or exact fp32
+// x_in rows: bf16 hi (+ lo residual for the split-bf16 GEMM) and/or exact
+// fp32, zero padded to the row stride. One warp per gathered row (grid-stride),
+// 16-byte loads when the feature rows are 16-byte aligned.
+__device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
+  __nv_bfloat162 h0 = __floats2bfloat162_rn(a, b), h1 = __floats2bfloat162_rn(c, d);
+  return make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+}
+__device__ __forceinline__ float lo_of(float v) { return v - __bfloat162float(__float2bfloat16_rn(v)); }
+
 __global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t* __restrict__ sample,
                            int64_t row_lo, const float* __restrict__ feats, int64_t fld,
-                           bf16* __restrict__ xb, bf16* __restrict__ xl, float* __restrict__ xf) {
-  // one warp per gathered row (coalesced over the row's columns)
-  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (r >= rows) return;
-  const float* src = feats + sample[row_lo + r] * fld;
-  for (int64_t c = threadIdx.x & 31; c < ld; c += 32) {
-    const float x = c < cols ? src[c] : 0.0f;
-    const bf16 h = __float2bfloat16_rn(x);
-    if (xb) xb[r * ld + c] = h;
-    if (xl) xl[r * ld + c] = __float2bfloat16_rn(x - __bfloat162float(h));
-    if (xf && c < cols) xf[r * cols + c] = x;
+                           bf16* __restrict__ xb, bf16* __restrict__ xl, float* __restrict__ xf, int64_t xfld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool vec = (cols & 3) == 0 && (fld & 3) == 0 && (ld & 3) == 0 && (!xf || (xfld & 3) == 0);
+  for (int64_t r = w0; r < rows; r += nw) {
+    const float* src = feats + sample[row_lo + r] * fld;
+    if (vec) {
+      for (int64_t c = lane * 4; c < ld; c += 128) {
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < cols) x = __ldg(reinterpret_cast<const float4*>(src + c));
+        if (xb) *reinterpret_cast<uint2*>(xb + r * ld + c) = pack4_bf16(x.x, x.y, x.z, x.w);
+        if (xl) *reinterpret_cast<uint2*>(xl + r * ld + c) = pack4_bf16(lo_of(x.x), lo_of(x.y), lo_of(x.z), lo_of(x.w));
+        if (xf && c < xfld) *reinterpret_cast<float4*>(xf + r * xfld + c) = x;
+      }
+    } else {
+      for (int64_t c = lane; c < ld; c += 32) {
+        const float x = c < cols ? src[c] : 0.0f;
+        const bf16 h = __float2bfloat16_rn(x);
+        if (xb) xb[r * ld + c] = h;
+        if (xl) xl[r * ld + c] = __float2bfloat16_rn(x - __bfloat162float(h));
+        if (xf && c < xfld) xf[r * xfld + c] = x;
+      }
+    }
   }
+}
+
+inline unsigned gather_blocks(const Ctx& ctx, int64_t rows) {
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8), ctx.num_sms * 64)));
 }
 
 __global__ void k_gather_labels(int64_t b, const int64_t* __restrict__ sample,
@@ -325,7 +351,7 @@ void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t
 }  // namespace
 
 void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
-                      Batch& bt) {
+                      Batch& bt, bool want_xf) {
   require(b >= 2 && b <= g.n, "build_local_minibatch: need 2 <= b <= N");
   ProfScope prof(ctx, kProfSample);
   cudaStream_t s = ctx.stream;
@@ -428,6 +454,7 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
   for (size_t k = 0; k < nk; ++k)
     fill_block(ctx, g.shards[keys[k].shard], d_sample, keys[k].rl, keys[k].cl, b, g.n, bt.csrs[k]);
 
+  bt.p_ready = false;
   // x_in (X,Z) = features[S rows of this X block, Z column block] (model.hpp:293-303)
   {
     const auto& xo = bt.batch_off[kInputFeatureLayout.row];
@@ -441,9 +468,12 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     const int64_t rows = bt.x_r1 - bt.x_r0;
     bf16* xb = bt.x_in.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
     bf16* xl = bt.x_in_lo.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
+    // fp32 rows too when the first layer will be pre-aggregated (one gather)
+    bt.x_f_ready = want_xf && preagg_eligible(ctx, bt);
+    float* xf = bt.x_f_ready ? bt.x_f.reserve_n<float>(std::max<int64_t>(rows, 1) * bt.x_ld) : nullptr;
     if (rows > 0) {
-      k_gather_x<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, s>>>(rows, cols, bt.x_ld, d_sample, bt.x_r0,
-                                                            g.features.as<float>(), cols, xb, xl, nullptr);
+      k_gather_x<<<gather_blocks(ctx, rows), 256, 0, s>>>(rows, cols, bt.x_ld, d_sample, bt.x_r0,
+                                                          g.features.as<float>(), cols, xb, xl, xf, bt.x_ld);
       ctx.launches += 1;
     }
   }
@@ -467,11 +497,49 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
 void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out) {
   const int64_t rows = bt.x_r1 - bt.x_r0, cols = bt.x_c1 - bt.x_c0;
   if (rows <= 0 || cols <= 0) return;
-  k_gather_x<<<static_cast<unsigned>(ceil_div(rows, 8)), 256, 0, ctx.stream>>>(
+  k_gather_x<<<gather_blocks(ctx, rows), 256, 0, ctx.stream>>>(
       rows, cols, cols, bt.sample.as<int64_t>(), bt.x_r0, bt.graph->features.as<float>(), cols,
-      nullptr, nullptr, d_out);
+      nullptr, nullptr, d_out, cols);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
+}
+
+// Pre-aggregated input features of the first layer, P = A_0 . x_in.
+// The reference's first layer computes A_0 . (x_in . W_in) (model.hpp:346-351);
+// with d_in < H the association (A_0 . x_in) . W_in gathers d_in-wide rows
+// instead of H-wide ones, and P depends on the batch only (no weights), so it
+// is built with the batch, on the sampling stream when prefetched. Valid when
+// plane 0's column axis (X) and x_in's column axis (Z) are unsplit, i.e. the
+// X- and Z-partial sums of the two contractions need no all-reduce.
+bool preagg_eligible(const Ctx& ctx, const Batch& bt) {
+  return bt.planes >= 1 && ctx.grid.dims[kX] == 1 && ctx.grid.dims[kZ] == 1 && bt.x_c1 > bt.x_c0;
+}
+
+void preaggregate(Ctx& ctx, const Batch& bt) {
+  require(preagg_eligible(ctx, bt), "preaggregate: grid splits the first layer's contractions");
+  const BatchCsr& A = bt.csrs[bt.csr_of[0]];
+  const int64_t xrows = bt.x_r1 - bt.x_r0, cols = bt.x_c1 - bt.x_c0;
+  contract(A.c0 == bt.x_r0 && A.c1 == bt.x_r1, "preaggregate: A_0 columns differ from the x_in rows");
+  float* xf = bt.x_f.reserve_n<float>(std::max<int64_t>(xrows, 1) * bt.x_ld);
+  const bool gather = !bt.x_f_ready;
+  bf16* ph = bt.p_in.reserve_n<bf16>(std::max<int64_t>(A.n_rows, 1) * bt.x_ld);
+  bf16* pl = bt.p_in_lo.reserve_n<bf16>(std::max<int64_t>(A.n_rows, 1) * bt.x_ld);
+  if (xrows > 0 && gather) {
+    k_gather_x<<<gather_blocks(ctx, xrows), 256, 0, ctx.stream>>>(
+        xrows, cols, bt.x_ld, bt.sample.as<int64_t>(), bt.x_r0, bt.graph->features.as<float>(), cols, nullptr,
+        nullptr, xf, bt.x_ld);
+    GGB_LAUNCH_CHECK();
+    ctx.launches += 1;
+  }
+  if (A.n_rows > 0) {
+    // padding columns of P stay zero (the GEMM reads K up to x_ld)
+    GGB_CUDA(cudaMemsetAsync(ph, 0, static_cast<size_t>(A.n_rows) * bt.x_ld * 2, ctx.stream));
+    GGB_CUDA(cudaMemsetAsync(pl, 0, static_cast<size_t>(A.n_rows) * bt.x_ld * 2, ctx.stream));
+    spmm_csr_f32(ctx, A.n_rows, A.row_ptr.as<int64_t>(), A.col.as<int32_t>(), A.val.as<float>(), xf, bt.x_ld, cols,
+                 nullptr, 0, ph, pl, bt.x_ld, 0);
+  }
+  bt.x_f_ready = true;
+  bt.p_ready = true;
 }
 
 }  // namespace ggb

@@ -230,7 +230,7 @@ void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, con
   require(!(accumulate && !out), "spmm: accumulate needs an fp32 output");
   require(ldf % 8 == 0 && (reinterpret_cast<uintptr_t>(f) & 15) == 0,
           "spmm: feature operand needs 16-byte aligned rows of 8-element multiples");
-  if (spmm_kernel_choice() == 0 &&
+  if (spmm_kernel_choice() == 0 && !ctx.side_stream &&
       spmm_pipe(ctx, rows, rp, col, val, f, 2, ldf, fcols, out, ldo, outb, nullptr, ldob, accumulate))
     return;
   dispatch<bf16>(ctx, rows, rp, col, val, f, ldf, fcols, out, ldo, outb, nullptr, ldob, accumulate);
@@ -243,7 +243,7 @@ void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col,
   require(!(accumulate && !out), "spmm: accumulate needs an fp32 output");
   require(ldf % 8 == 0 && (reinterpret_cast<uintptr_t>(f) & 15) == 0,
           "spmm: feature operand needs 16-byte aligned rows of 8-element multiples");
-  if (spmm_kernel_choice() == 0 &&
+  if (spmm_kernel_choice() == 0 && !ctx.side_stream &&
       spmm_pipe(ctx, rows, rp, col, val, f, 4, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate))
     return;
   dispatch<float>(ctx, rows, rp, col, val, f, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate);

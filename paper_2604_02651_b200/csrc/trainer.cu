@@ -201,17 +201,27 @@ double gemm_bytes(int64_t m, int64_t n, int64_t k, int ea, int eb, int ec) {
 
 // C = A . W (forward contract): split-bf16 in the accurate mode, bf16 otherwise.
 void fwd_gemm(State& st, int64_t m, int64_t n, int64_t k, const Tensor& a, const ParamSlot& w, float* c,
-              int64_t ldc, bf16* cb, int64_t ldcb) {
+              int64_t ldc, bf16* cb, int64_t ldcb, bf16* cl = nullptr) {
   const int e = st.compute == kAccurate ? 4 : 2;
-  ProfScope ps(*st.ctx, kProfGemmFwd, gemm_bytes(m, n, k, e, e, 4 + (cb ? 2 : 0)),
+  ProfScope ps(*st.ctx, kProfGemmFwd, gemm_bytes(m, n, k, e, e, (c ? 4 : 0) + (cb ? 2 : 0) + (cl ? 2 : 0)),
                2.0 * m * n * k * (st.compute == kAccurate ? 3 : 1));
   if (st.compute == kAccurate)
-    gemm_split(*st.ctx, m, n, k, a.b, a.lo, a.ldb, w.wt.as<bf16>(), w.wtl.as<bf16>(), w.ldt, c, ldc, cb, ldcb);
+    gemm_split(*st.ctx, m, n, k, a.b, a.lo, a.ldb, w.wt.as<bf16>(), w.wtl.as<bf16>(), w.ldt, c, ldc, cb, ldcb, cl);
   else
     gemm_bf16(*st.ctx, m, n, k, a.b, a.ldb, w.wt.as<bf16>(), w.ldt, c, ldc, cb, ldcb);
 }
 
 }  // namespace
+
+bool preagg_enabled() {
+  const char* e = std::getenv("GGB_PREAGG");
+  return !(e && e[0] == '0');
+}
+
+bool preagg_in_prefetch() {
+  const char* e = std::getenv("GGB_PREAGG_PF");
+  return !(e && e[0] == '0');
+}
 
 // ---- forward (model.hpp:335-376) ----------------------------------------------------
 void forward(State& st, const Batch& bt, int precision, bool training, uint64_t run_seed, uint64_t global_step,
@@ -258,6 +268,8 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
   st.fwd_keep_scale = drop ? static_cast<float>(1.0 / (1.0 - rate)) : 1.0f;
   const uint64_t thresh = drop ? static_cast<uint64_t>(std::ceil(rate * 0x1.0p53)) : 0;
 
+  // layer 1 as (A_0 . x_in) . W_in: same product, d_in-wide instead of H-wide gathers
+  st.preagg = preagg_enabled() && preagg_eligible(ctx, bt);
   const Tensor* prev = &st.x0;
   for (int l = 1; l <= cfg.layers; ++l) {
     LayerBufs& L = st.layers[l - 1];
@@ -281,6 +293,19 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.hagg.lo = accurate ? grow<bf16>(L.hagg_lo, hb.rows() * L.hagg.ldb) : nullptr;
     const bool ar_h = !trivial(ctx, alay.col);
     const int64_t* arp = A.row_ptr.as<int64_t>();
+    if (l == 1 && st.preagg) {
+      // hagg_1 = P . W_in with P = A_0 . x_in (built with the batch); X and Z
+      // unsplit, so neither product needs an all-reduce
+      if (!bt.p_ready) preaggregate(ctx, bt);
+      const ParamSlot& wi = st.params[st.win];
+      contract(wi.blk.c0 == hb.c0 && wi.blk.c1 == hb.c1 && wi.blk.rows() == bt.x_c1 - bt.x_c0,
+               "contract: inner partitions differ");
+      Tensor pt;
+      pt.b = bt.p_in.as<bf16>();
+      pt.lo = bt.p_in_lo.as<bf16>();
+      pt.ldb = bt.x_ld;
+      fwd_gemm(st, A.n_rows, hb.cols(), wi.blk.rows(), pt, wi, nullptr, 0, L.hagg.b, L.hagg.ldb, L.hagg.lo);
+    } else {
     const int32_t* acol = A.col.as<int32_t>();
     const float* aval = A.val.as<float>();
     {
@@ -305,6 +330,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
                    L.hagg.ldb, 0);
     } else {
       spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
+    }
     }
     }
     // xw = hagg . W_l -> (A.row, third), all-reduce F.col
@@ -504,6 +530,9 @@ void backward(State& st, const Batch& bt, int precision) {
               ld8(db.cols()), nullptr, 0);
     all_reduce_sum(ctx, lb.lay.col, dxh, db.rows() * ld8(db.cols()), wire);
   }
+  const bf16* pre_dhb = nullptr;  // layer 1 under pre-aggregation: dhagg_1 (bf16) and the residual gradient
+  int64_t pre_ldhb = 0;
+  const float* pre_dres = nullptr;
   for (int l = cfg.layers; l >= 1; --l) {
     LayerBufs& L = st.layers[l - 1];
     const Block& xb = L.xw_t.blk;  // == db
@@ -585,6 +614,15 @@ void backward(State& st, const Batch& bt, int precision) {
       gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, nullptr, 0, dhb, ldhb);
     }
     }
+    if (l == 1 && st.preagg) {
+      // layer 1 was (A_0 . x_in) . W_in: dX_0 is not formed; dW_in takes
+      // P^T . dhagg_1 plus the residual term x_in^T . dres (below)
+      pre_dhb = dhb;
+      pre_ldhb = ldhb;
+      pre_dres = dres;
+      db = F;
+      break;
+    }
     // dxh = A_t . dhagg (+ dres) -> (A.col, hagg.col) = F's layout, all-reduce A.row
     const int p = (l - 1) % 3;
     const BatchCsr& At = bt.csrs[bt.csrt_of[p]];
@@ -596,10 +634,12 @@ void backward(State& st, const Batch& bt, int precision) {
     if (inplace) {
       // dxh (== dres) += A_t . dhagg; the first layer also emits the bf16
       // copy that feeds dW_in (no separate cast pass)
-      bf16* outb = l == 1 ? grow<bf16>(st.dxh_b, F.rows() * ld8(F.cols())) : nullptr;
+      // (under pre-aggregation layer 2 emits it: its dX_1 is layer 1's residual gradient)
+      const bool emit_b = st.preagg ? l == 2 : l == 1;
+      bf16* outb = emit_b ? grow<bf16>(st.dxh_b, F.rows() * ld8(F.cols())) : nullptr;
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
                dxh, ld8(F.cols()), outb, ld8(F.cols()), 1);
-      dxh_b_ready = l == 1;
+      dxh_b_ready = emit_b;
     } else {
       float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
@@ -610,6 +650,27 @@ void backward(State& st, const Batch& bt, int precision) {
       dxh = nd;
     }
     db = F;
+  }
+  if (st.preagg) {
+    // dW_in = x_in^T . dres + P^T . dhagg_1 (= x_in^T . (dres + A_0^T . dhagg_1)); X, Z unsplit
+    const ParamSlot& w = st.params[st.win];
+    const int64_t rows = db.rows(), cols = db.cols();
+    const int64_t kin = bt.x_c1 - bt.x_c0;
+    const BatchCsr& A0 = bt.csrs[bt.csr_of[0]];
+    contract(rows == bt.x_r1 - bt.x_r0 && A0.n_rows == rows, "backward: first-layer blocks differ");
+    ProfScope ps(ctx, kProfGemmWgrad, gemm_bytes(kin, cols, rows, 2, 2, 4) * (pre_dres ? 2 : 1),
+                 2.0 * rows * kin * cols * (pre_dres ? 2 : 1));
+    if (pre_dres) {
+      const int64_t ldb = ld8(cols);
+      bf16* drb = grow<bf16>(st.dxh_b, rows * ldb);
+      if (!(dxh_b_ready && pre_dres == dxh)) cast_bf16(ctx, pre_dres, rows, cols, ld8(cols), drb, ldb);
+      gemm_wgrad_bf16(ctx, rows, kin, cols, bt.x_in.as<bf16>(), bt.x_ld, drb, ldb, G + w.off, w.blk.cols(),
+                      st.ws_wgrad, 0);
+    }
+    gemm_wgrad_bf16(ctx, rows, kin, cols, bt.p_in.as<bf16>(), bt.x_ld, pre_dhb, pre_ldhb, G + w.off, w.blk.cols(),
+                    st.ws_wgrad, pre_dres ? 1 : 0);
+    all_reduce_sum(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
+    return;
   }
   // dW_in = x_in^T . dxh, all-reduce x_in.row (X)
   {

@@ -67,7 +67,14 @@ struct State {
   bool fwd_drop = false;
   float fwd_keep_scale = 1.f;
   bool have_forward = false;
+  bool preagg = false;  // the last forward computed layer 1 as (A_0 . x_in) . W_in
 };
+
+/// First-layer pre-aggregation switch (GGB_PREAGG=0 turns it off); applied
+/// where preagg_eligible() holds.
+bool preagg_enabled();
+/// ... computed by the prefetcher with the batch (GGB_PREAGG_PF=0: lazily by forward)
+bool preagg_in_prefetch();
 
 void state_init(Ctx& ctx, State& st, const ggb_model_config& cfg, uint64_t seed);
 void refresh_bf16(State& st);

@@ -41,8 +41,12 @@ CFGS = [
 ]
 
 
+# preagg "1": the first layer as (A_0 . x_in) . W_in (default on this grid);
+# "0": the reference's association A_0 . (x_in . W_in)
+@pytest.mark.parametrize("preagg", ["1", "0"])
 @pytest.mark.parametrize("cfg_kw", CFGS)
-def test_train_step_matches_reference(gg, orc, ref, cfg_kw):
+def test_train_step_matches_reference(gg, orc, ref, cfg_kw, preagg, monkeypatch):
+    monkeypatch.setenv("GGB_PREAGG", preagg)
     n, d_in, ncls, b, seed, step = 4000, 24, 7, 1000, 7, 4
     ds, h, ctx, g = _setup(gg, orc, ref, n, 10.0, d_in, ncls, 3, cfg_kw["layers"])
     try:
@@ -70,8 +74,10 @@ def test_train_step_matches_reference(gg, orc, ref, cfg_kw):
 FAST_GRAD_RTOL = 6e-2
 
 
+@pytest.mark.parametrize("preagg", ["1", "0"])
 @pytest.mark.parametrize("cfg_kw", CFGS[:2] + CFGS[5:])
-def test_train_step_fast_mode(gg, orc, ref, cfg_kw):
+def test_train_step_fast_mode(gg, orc, ref, cfg_kw, preagg, monkeypatch):
+    monkeypatch.setenv("GGB_PREAGG", preagg)
     n, d_in, ncls, b, seed, step = 4000, 24, 7, 1000, 7, 4
     ds, h, ctx, g = _setup(gg, orc, ref, n, 10.0, d_in, ncls, 3, cfg_kw["layers"])
     try:
