@@ -290,22 +290,6 @@ def main():
     c1 = ctx.counters()
     prof = ctx.profile_read(reset=True)
     ctx.profile(False)
-    # ---- e2e: the reference-facing call pattern, the loss read back to the host every step
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    losses = []
-    emarks = []
-    for _ in range(args.steps):
-        losses.append(step(gstep, True))
-        gstep += 1
-        emarks.append(torch.cuda.Event(enable_timing=True))
-        emarks[-1].record(stream)
-    e1.record(stream)
-    barrier()
-    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
-    e2e_step_ms = [round((emarks[i - 1] if i else e0).elapsed_time(emarks[i]), 3) for i in range(len(emarks))]
-    c2 = ctx.counters()
     clk = clocks.stop()
     # ---- per-epoch full-graph evaluation (train_run's evaluate_full_graph), timed
     # separately: the reference's epoch time excludes it; it is the
@@ -331,6 +315,41 @@ def main():
                    "note": "dropout-off forward over all N vertices + argmax + split counts; "
                            "after %d training steps" % gstep}
         del evb
+
+    # ---- e2e: the reference-facing call pattern through the C ABI with the
+    # reference's data placement: the feature matrix lives in (pinned) host
+    # memory, as the reference's Dataset does, so every batch build gathers its
+    # x_in rows over PCIe (zero-copy, on the prefetcher's sampling stream), and
+    # the loss is read back to the host every step. The graph structure (the
+    # RankContext plane shards, a one-time setup in the reference too) stays
+    # resident.
+    if pf:
+        pf.close()
+    graph.features_to_host()
+    pf = (gg.Prefetcher(ctx, graph, b, group_seed, gstep, run_seed=RUN_SEED, cfg=mcfg if args.prefetch == 2 else None)
+          if args.prefetch else None)
+    batch = None
+    for _ in range(args.warmup):
+        step(gstep, True)
+        gstep += 1
+    barrier()
+    c1e = ctx.counters()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    losses = []
+    emarks = []
+    for _ in range(args.steps):
+        losses.append(step(gstep, True))
+        gstep += 1
+        emarks.append(torch.cuda.Event(enable_timing=True))
+        emarks[-1].record(stream)
+    e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    e2e_step_ms = [round((emarks[i - 1] if i else e0).elapsed_time(emarks[i]), 3) for i in range(len(emarks))]
+    c2 = ctx.counters()
+    if pf:
+        pf.close()
 
     if rank != 0:
         if pg:
@@ -401,10 +420,12 @@ def main():
         "roofline": roof,
         "kernels": breakdown,
         "e2e": {"value": S * ms_e2e / args.steps / 1000.0, "unit": "s",
-                "h2d_bytes_per_step": (c2["h2d_bytes"] - c1["h2d_bytes"]) / args.steps,
-                "d2h_bytes_per_step": (c2["d2h_bytes"] - c1["d2h_bytes"]) / args.steps,
+                "h2d_bytes_per_step": (c2["h2d_bytes"] - c1e["h2d_bytes"]) / args.steps,
+                "d2h_bytes_per_step": (c2["d2h_bytes"] - c1e["d2h_bytes"]) / args.steps,
                 "ms_per_step": ms_e2e / args.steps,
-                "note": "C-ABI loop with the loss read back to the host each step; graph/features uploaded once"},
+                "note": "C-ABI loop (build/prefetch -> train_step -> dp_sync -> Adam) with the features in pinned "
+                        "host memory, each batch's x_in rows gathered over PCIe, and the loss read back to the "
+                        "host every step; the graph structure is resident (one-time setup)"},
         "gpu_launches": c1["launches"] - c0["launches"],
         "clocks": clk,
         "loss_last": losses[-1] if losses else None,

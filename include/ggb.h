@@ -101,7 +101,14 @@ int ggb_graph_generate_synthetic(ggb_ctx_t ctx, int64_t n, double avg_degree, in
  * (dataset.cpp:122-129); needed only by ggb_evaluate_full_graph. */
 int ggb_graph_set_split(ggb_graph_t g, const uint8_t* split);
 int ggb_graph_destroy(ggb_graph_t g);
-/* info = {n, nnz, d_in, n_classes, distinct_plane_shards, device_bytes} */
+/* Keep the feature slice in host memory instead of HBM, as the reference's
+ * Dataset does (build_step_batch reads ds.features rows per step,
+ * model.hpp:293-303): the slice moves to mapped pinned host memory and every
+ * batch build gathers its x_in rows over PCIe (zero-copy loads on the
+ * sampling stream; counted in the context's h2d bytes). Not reversible. */
+int ggb_graph_features_to_host(ggb_graph_t g);
+/* info = {n, nnz, d_in, n_classes, distinct_plane_shards, device_bytes, features_on_host}
+ * (7 entries) */
 int ggb_graph_info(ggb_graph_t g, int64_t* info);
 
 /* ---- batches: build_step_batch (model.hpp:250-309) / build_local_minibatch

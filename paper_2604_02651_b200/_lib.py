@@ -46,6 +46,7 @@ _SIGS = [
     ("ggb_graph_set_split", C.c_int, [P, P]),
     ("ggb_graph_destroy", C.c_int, [P]),
     ("ggb_graph_info", C.c_int, [P, P]),
+    ("ggb_graph_features_to_host", C.c_int, [P]),
     ("ggb_build_step_batch", C.c_int, [P, P, I64, U64, U64, P]),
     ("ggb_batch_destroy", C.c_int, [P]),
     ("ggb_prefetch_create", C.c_int, [P, P, I64, U64, U64, U64, I32, I64, F64, P]),

@@ -223,6 +223,7 @@ void graph_build(Ctx& ctx, Graph& g, int64_t n, const int64_t* rp, const int64_t
   }
   upload(g.labels, labels, static_cast<size_t>(n), ctx.stream);
   GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+  g.feat_ptr = g.features.as<float>();
   g.device_bytes = g.features.bytes + g.labels.bytes;
   for (auto& s : g.shards) g.device_bytes += s.row_ptr.bytes + s.col.bytes + s.val.bytes;
 }
@@ -404,6 +405,26 @@ int ggb_graph_destroy(ggb_graph_t g) {
   });
 }
 
+int ggb_graph_features_to_host(ggb_graph_t g) {
+  return guard([&] {
+    require(g != nullptr, "graph_features_to_host: null graph");
+    use_device(*g->ctx);
+    if (g->features_on_host()) return;
+    const size_t bytes = g->features.bytes ? static_cast<size_t>(g->n) * (g->feat_c1 - g->feat_c0) * 4 : 0;
+    require(bytes > 0, "graph_features_to_host: no device features");
+    PinnedBuf& h = g->features_host;
+    GGB_CUDA(cudaHostAlloc(&h.p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    h.bytes = bytes;
+    GGB_CUDA(cudaMemcpyAsync(h.p, g->features.p, bytes, cudaMemcpyDeviceToHost, g->ctx->stream));
+    GGB_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    void* dp = nullptr;
+    GGB_CUDA(cudaHostGetDevicePointer(&dp, h.p, 0));
+    g->feat_ptr = static_cast<const float*>(dp);
+    g->device_bytes -= g->features.bytes;
+    g->features.release();
+  });
+}
+
 int ggb_graph_info(ggb_graph_t g, int64_t* info) {
   return guard([&] {
     info[0] = g->n;
@@ -412,6 +433,7 @@ int ggb_graph_info(ggb_graph_t g, int64_t* info) {
     info[3] = g->n_classes;
     info[4] = static_cast<int64_t>(g->shards.size());
     info[5] = static_cast<int64_t>(g->device_bytes);
+    info[6] = g->features_on_host() ? 1 : 0;
   });
 }
 

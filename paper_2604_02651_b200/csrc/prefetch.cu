@@ -142,6 +142,7 @@ Batch* Prefetcher::next() {
   if (failed && produced <= consumed) std::rethrow_exception(err);
   const int slot = static_cast<int>(consumed & 1);
   GGB_CUDA(cudaStreamWaitEvent(consumer->stream, ready[slot], 0));
+  consumer->h2d_bytes += slots[slot].h2d_bytes;  // the batch's PCIe feature reads count for the consumer
   ++consumed;
   return &slots[slot];
 }

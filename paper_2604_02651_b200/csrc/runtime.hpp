@@ -65,7 +65,10 @@ struct Graph {
   std::vector<int> fwd_of, tr_of;
   std::vector<PlaneShard> shards;
   int64_t feat_c0 = 0, feat_c1 = 0;  // Z-slice of the feature columns held here
-  DevBuf features;                   // fp32 [n][feat_c1-feat_c0]
+  DevBuf features;                   // fp32 [n][feat_c1-feat_c0] in HBM, or empty when host-resident
+  PinnedBuf features_host;           // the same slice in mapped pinned host memory (ggb_graph_features_to_host)
+  const float* feat_ptr = nullptr;   // device-accessible feature rows (HBM or the host mapping)
+  bool features_on_host() const { return features_host.p != nullptr; }
   DevBuf labels;                     // int32 [n]
   DevBuf split;                      // uint8 [n] SplitTag (dataset.hpp:12), for evaluation
   size_t device_bytes = 0;
@@ -109,6 +112,7 @@ struct Batch {
   mutable DevBuf x_f, p_in, p_in_lo;
   mutable bool p_ready = false, x_f_ready = false;
   uint64_t nnz_extracted = 0, nnz_kept = 0;
+  uint64_t h2d_bytes = 0;  // feature bytes this build read over PCIe (host-resident features)
   const Graph* graph = nullptr;
 };
 

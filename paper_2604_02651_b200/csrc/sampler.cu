@@ -34,6 +34,7 @@
 #include "ops.hpp"
 #include "prof.hpp"
 #include "rng.cuh"
+#include "trainer.hpp"
 #include "runtime.hpp"
 
 namespace ggb {
@@ -231,37 +232,85 @@ __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) 
 }
 __device__ __forceinline__ float lo_of(float v) { return v - __bfloat162float(__float2bfloat16_rn(v)); }
 
+template <int U>  // rows in flight per warp (U > 1 for the PCIe-latency-bound host gather)
 __global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t* __restrict__ sample,
                            int64_t row_lo, const float* __restrict__ feats, int64_t fld,
                            bf16* __restrict__ xb, bf16* __restrict__ xl, float* __restrict__ xf, int64_t xfld) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const bool vec = (cols & 3) == 0 && (fld & 3) == 0 && (ld & 3) == 0 && (!xf || (xfld & 3) == 0);
+  const bool vec = (cols & 3) == 0 && (fld & 3) == 0 && (ld & 3) == 0 && (!xf || (xfld & 3) == 0) && ld <= 128 * 4;
+  if (vec) {
+    constexpr int Q = 4;  // up to 4 quads per lane: rows of <= 512 floats
+    for (int64_t rb = w0; rb < rows; rb += nw * U) {
+      float4 x[U][Q];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = rb + u * nw;
+        const float* src = r < rows ? feats + sample[row_lo + r] * fld : nullptr;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int64_t c = lane * 4 + q * 128;
+          x[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (src && c < cols) x[u][q] = __ldg(reinterpret_cast<const float4*>(src + c));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = rb + u * nw;
+        if (r >= rows) break;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int64_t c = lane * 4 + q * 128;
+          if (c >= ld) break;
+          const float4 v = x[u][q];
+          if (xb) *reinterpret_cast<uint2*>(xb + r * ld + c) = pack4_bf16(v.x, v.y, v.z, v.w);
+          if (xl) *reinterpret_cast<uint2*>(xl + r * ld + c) = pack4_bf16(lo_of(v.x), lo_of(v.y), lo_of(v.z), lo_of(v.w));
+          if (xf && c < xfld) *reinterpret_cast<float4*>(xf + r * xfld + c) = v;
+        }
+      }
+    }
+    return;
+  }
   for (int64_t r = w0; r < rows; r += nw) {
     const float* src = feats + sample[row_lo + r] * fld;
-    if (vec) {
-      for (int64_t c = lane * 4; c < ld; c += 128) {
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c < cols) x = __ldg(reinterpret_cast<const float4*>(src + c));
-        if (xb) *reinterpret_cast<uint2*>(xb + r * ld + c) = pack4_bf16(x.x, x.y, x.z, x.w);
-        if (xl) *reinterpret_cast<uint2*>(xl + r * ld + c) = pack4_bf16(lo_of(x.x), lo_of(x.y), lo_of(x.z), lo_of(x.w));
-        if (xf && c < xfld) *reinterpret_cast<float4*>(xf + r * xfld + c) = x;
-      }
-    } else {
-      for (int64_t c = lane; c < ld; c += 32) {
-        const float x = c < cols ? src[c] : 0.0f;
-        const bf16 h = __float2bfloat16_rn(x);
-        if (xb) xb[r * ld + c] = h;
-        if (xl) xl[r * ld + c] = __float2bfloat16_rn(x - __bfloat162float(h));
-        if (xf && c < xfld) xf[r * xfld + c] = x;
-      }
+    for (int64_t c = lane; c < ld; c += 32) {
+      const float x = c < cols ? src[c] : 0.0f;
+      const bf16 h = __float2bfloat16_rn(x);
+      if (xb) xb[r * ld + c] = h;
+      if (xl) xl[r * ld + c] = __float2bfloat16_rn(x - __bfloat162float(h));
+      if (xf && c < xfld) xf[r * xfld + c] = x;
     }
   }
 }
 
-inline unsigned gather_blocks(const Ctx& ctx, int64_t rows) {
-  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8), ctx.num_sms * 64)));
+// Host-resident features are read over PCIe by a small grid with several
+// rows in flight per warp, so the gather, which runs for milliseconds on the
+// sampling stream, holds only part of a few SMs while keeping enough reads
+// outstanding for the link (measured at C2: 245 MB in ~5 ms, ~49 GB/s, the
+// same from 32 to 296 blocks).
+int host_gather_blocks() {
+  static int v = [] {
+    const char* e = std::getenv("GGB_HOST_GATHER_BLOCKS");
+    const int b = e ? std::atoi(e) : 32;
+    return b > 0 ? b : 32;
+  }();
+  return v;
+}
+
+void launch_gather_x(const Ctx& ctx, cudaStream_t s, bool host, int64_t rows, int64_t cols, int64_t ld,
+                     const int64_t* sample, int64_t row_lo, const float* feats, int64_t fld, bf16* xb, bf16* xl,
+                     float* xf, int64_t xfld) {
+  if (rows <= 0) return;
+  if (host) {
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 8 * 4), host_gather_blocks()));
+    k_gather_x<4><<<std::max(blocks, 1u), 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+  } else {
+    const unsigned blocks =
+        static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8), ctx.num_sms * 64)));
+    k_gather_x<1><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+  }
+  GGB_LAUNCH_CHECK();
 }
 
 __global__ void k_gather_labels(int64_t b, const int64_t* __restrict__ sample,
@@ -469,13 +518,16 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     bf16* xb = bt.x_in.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
     bf16* xl = bt.x_in_lo.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
     // fp32 rows too when the first layer will be pre-aggregated (one gather)
-    bt.x_f_ready = want_xf && preagg_eligible(ctx, bt);
+    // (host-resident features: always, so the rows cross PCIe once)
+    bt.x_f_ready = (want_xf || g.features_on_host()) && preagg_enabled() && preagg_eligible(ctx, bt);
     float* xf = bt.x_f_ready ? bt.x_f.reserve_n<float>(std::max<int64_t>(rows, 1) * bt.x_ld) : nullptr;
     if (rows > 0) {
-      k_gather_x<<<gather_blocks(ctx, rows), 256, 0, s>>>(rows, cols, bt.x_ld, d_sample, bt.x_r0,
-                                                          g.features.as<float>(), cols, xb, xl, xf, bt.x_ld);
+      launch_gather_x(ctx, s, g.features_on_host(), rows, cols, bt.x_ld, d_sample, bt.x_r0, g.feat_ptr, cols, xb,
+                      xl, xf, bt.x_ld);
       ctx.launches += 1;
     }
+    bt.h2d_bytes = g.features_on_host() ? static_cast<uint64_t>(rows) * cols * 4 : 0;
+    ctx.h2d_bytes += bt.h2d_bytes;
   }
   int32_t* lab = bt.labels.reserve_n<int32_t>(b);
   k_gather_labels<<<blocks(b), kThreads, 0, s>>>(b, d_sample, g.labels.as<int32_t>(), lab);
@@ -497,10 +549,8 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
 void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out) {
   const int64_t rows = bt.x_r1 - bt.x_r0, cols = bt.x_c1 - bt.x_c0;
   if (rows <= 0 || cols <= 0) return;
-  k_gather_x<<<gather_blocks(ctx, rows), 256, 0, ctx.stream>>>(
-      rows, cols, cols, bt.sample.as<int64_t>(), bt.x_r0, bt.graph->features.as<float>(), cols,
-      nullptr, nullptr, d_out, cols);
-  GGB_LAUNCH_CHECK();
+  launch_gather_x(ctx, ctx.stream, bt.graph->features_on_host(), rows, cols, cols, bt.sample.as<int64_t>(), bt.x_r0,
+                  bt.graph->feat_ptr, cols, nullptr, nullptr, d_out, cols);
   ctx.launches += 1;
 }
 
@@ -525,10 +575,8 @@ void preaggregate(Ctx& ctx, const Batch& bt) {
   bf16* ph = bt.p_in.reserve_n<bf16>(std::max<int64_t>(A.n_rows, 1) * bt.x_ld);
   bf16* pl = bt.p_in_lo.reserve_n<bf16>(std::max<int64_t>(A.n_rows, 1) * bt.x_ld);
   if (xrows > 0 && gather) {
-    k_gather_x<<<gather_blocks(ctx, xrows), 256, 0, ctx.stream>>>(
-        xrows, cols, bt.x_ld, bt.sample.as<int64_t>(), bt.x_r0, bt.graph->features.as<float>(), cols, nullptr,
-        nullptr, xf, bt.x_ld);
-    GGB_LAUNCH_CHECK();
+    launch_gather_x(ctx, ctx.stream, bt.graph->features_on_host(), xrows, cols, bt.x_ld, bt.sample.as<int64_t>(),
+                    bt.x_r0, bt.graph->feat_ptr, cols, nullptr, nullptr, xf, bt.x_ld);
     ctx.launches += 1;
   }
   if (A.n_rows > 0) {

@@ -207,10 +207,20 @@ class Graph:
     def __init__(self, ctx: Context, h):
         self.ctx = ctx
         self.h = h
-        info = np.zeros(6, np.int64)
-        check(lib().ggb_graph_info(h, _ptr(info)))
-        self.n, self.nnz, self.d_in, self.n_classes, self.distinct_shards, self.device_bytes = (
-            int(x) for x in info)
+        self._info()
+
+    def _info(self):
+        info = np.zeros(7, np.int64)
+        check(lib().ggb_graph_info(self.h, _ptr(info)))
+        (self.n, self.nnz, self.d_in, self.n_classes, self.distinct_shards, self.device_bytes,
+         host) = (int(x) for x in info)
+        self.features_on_host = bool(host)
+
+    def features_to_host(self) -> None:
+        """Move the feature slice to mapped pinned host memory (the reference's
+        host-resident Dataset); batch builds then gather x_in rows over PCIe."""
+        check(lib().ggb_graph_features_to_host(self.h))
+        self._info()
 
     @staticmethod
     def from_csr(ctx: Context, n: int, row_ptr, col_idx, values, features, labels, n_classes: int,
