@@ -28,8 +28,11 @@ constexpr int kBK = 64;   // one 128-byte swizzle atom of bf16 along K
 constexpr int kEpiWarps = 8;  // 2 per TMEM lane quarter, each on half of the tile's columns
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kWgradThreads = 192;
-constexpr int kSmemBudget = 225 * 1024;                 // dynamic smem per CTA (227 KB max on sm_100)
-constexpr int kEpiSmem = kEpiWarps * 32 * 17 * 4 + 256;  // barriers + epilogue transpose tiles
+constexpr int kSmemBudget = 227 * 1024;  // dynamic smem per CTA (the sm_100 maximum)
+// epilogue staging, one 4 KB buffer per epilogue warp (32 rows x 16 columns:
+// fp32 2 KB, bf16 1 KB, bf16 lo 1 KB), then the barriers
+constexpr int kEpiBuf = 4096;
+constexpr int kEpiSmem = kEpiWarps * kEpiBuf + 256;
 
 // ---- PTX wrappers --------------------------------------------------------------
 
@@ -69,6 +72,26 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA store of a shared-memory box; bulk-group completion
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t pack2_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t pack2_lo(float a, float b) {
+  return pack2_bf16(a - __bfloat162float(__float2bfloat16_rn(a)), b - __bfloat162float(__float2bfloat16_rn(b)));
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -144,6 +167,8 @@ struct GemmArgs {
   int split;    // 1: operands given as bf16 hi + lo pairs, D += Ah.Bh + Ah.Bl + Al.Bh
   int BN;       // MMA N of one tile (multiple of 16, <= 256)
   int n_tiles;  // ceil(N / BN)
+  int b_res;    // 1: B loaded once per CTA and kept in shared memory (n_tiles == 1)
+  int tma_out;  // 1: outputs leave through TMA stores (16-byte aligned rows)
   int stages;
   uint32_t tmem_cols;
   float* c;
@@ -156,24 +181,32 @@ struct GemmArgs {
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_kmajor(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmBl,
-                  const GemmArgs args) {
+                  const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCb,
+                  const __grid_constant__ CUtensorMap tmCl, const GemmArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by pointer arithmetic on the shared array, so every
+  // derived pointer stays in the shared window (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = args.stages, BN = args.BN;
   const int parts = args.split ? 2 : 1;
+  const int k_chunks = (args.K + kBK - 1) / kBK;
   const uint32_t bytes_a = kBM * kBK * 2, bytes_b = static_cast<uint32_t>(BN) * kBK * 2;
-  // stage: [A hi][A lo]?[B hi][B lo]?
-  const uint32_t stage_bytes = parts * (bytes_a + bytes_b);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
+  // streamed stage: [A hi][A lo]?[B hi][B lo]? -- or, with B resident (one
+  // n-tile: the whole B is loaded once per CTA), [A hi][A lo]? only
+  const uint32_t stage_bytes = parts * (bytes_a + (args.b_res ? 0u : bytes_b));
+  uint8_t* bres = smem + S * stage_bytes;  // [k chunk][hi, lo?] when b_res
+  const uint32_t bres_bytes = args.b_res ? static_cast<uint32_t>(k_chunks) * parts * bytes_b : 0u;
+  uint8_t* epi = bres + bres_bytes;  // kEpiWarps x kEpiBuf, 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + kEpiWarps * kEpiBuf);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;  // [2]
   uint64_t* tempty = tfull + 2;  // [2]
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;  // B resident loaded
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (args.M + kBM - 1) / kBM;
   const int num_tiles = m_tiles * args.n_tiles;
-  const int k_chunks = (args.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -190,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, kEpiWarps);
     }
+    mbar_init(bfull, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_base_smem, args.tmem_cols);
@@ -202,6 +236,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ---- TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      if (args.b_res) {  // the whole B (single n-tile), once
+        mbar_expect_tx(bfull, bres_bytes);
+        for (int kc = 0; kc < k_chunks; ++kc) {
+          uint8_t* sb = bres + kc * parts * bytes_b;
+          tma_load_2d(sb, &tmB, bfull, kc * kBK, 0);
+          if (args.split) tma_load_2d(sb + bytes_b, &tmBl, bfull, kc * kBK, 0);
+        }
+      }
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int mt = t / args.n_tiles, nt = t % args.n_tiles;
         for (int kc = 0; kc < k_chunks; ++kc) {
@@ -210,10 +252,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* sb = sa + parts * bytes_a;
           mbar_expect_tx(full + stage, stage_bytes);
           tma_load_2d(sa, &tmA, full + stage, kc * kBK, mt * kBM);
-          tma_load_2d(sb, &tmB, full + stage, kc * kBK, nt * BN);
+          if (!args.b_res) tma_load_2d(sb, &tmB, full + stage, kc * kBK, nt * BN);
           if (args.split) {
             tma_load_2d(sa + bytes_a, &tmAl, full + stage, kc * kBK, mt * kBM);
-            tma_load_2d(sb + bytes_b, &tmBl, full + stage, kc * kBK, nt * BN);
+            if (!args.b_res) tma_load_2d(sb + bytes_b, &tmBl, full + stage, kc * kBK, nt * BN);
           }
           if (++stage == S) {
             stage = 0;
@@ -229,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
+      if (args.b_res) mbar_wait(bfull, 0);
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
         const int acc = lt & 1;
         const uint32_t acc_phase = (lt >> 1) & 1;
@@ -239,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * stage_bytes);
-          const uint32_t sb = sa + parts * bytes_a;
+          const uint32_t sb = args.b_res ? smem_u32(bres + kc * parts * bytes_b) : sa + parts * bytes_a;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ah = sdesc(sa + k * 32, 16, 1024), bh = sdesc(sb + k * 32, 16, 1024);
@@ -266,7 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // of one row (fp32) and one store instruction writes 8 full row segments.
     const int q = warp & 3;
     const int half = (warp - 2) / 4;
-    float* stile = reinterpret_cast<float*>(tmem_base_smem + 4) + (warp - 2) * (32 * 17);
+    uint8_t* ebuf = epi + (warp - 2) * kEpiBuf;
+    float* stile = reinterpret_cast<float*>(ebuf);  // 32 x 17 padded transpose tile (store fallback)
     int lt = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
       const int mt = t / args.n_tiles, nt = t % args.n_tiles;
@@ -283,6 +327,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld16(taddr + c16, v);
         const int col0 = nt * BN + c16;
         if (col0 >= args.N) continue;  // warp-uniform
+        if (args.tma_out) {
+          // lane = row: its 16 columns go to the staging boxes in the TMA
+          // swizzle (fp32 64 B rows: SWIZZLE_64B; bf16 32 B rows: SWIZZLE_32B,
+          // conflict-free 16-byte stores), then one lane issues the stores
+          if (lane == 0) bulk_wait_read0();  // the previous block's stores have read the buffer
+          __syncwarp();
+          if (args.c) {
+            float4* rowp = reinterpret_cast<float4*>(ebuf + lane * 64);
+            const int sw = (lane >> 1) & 3;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+              rowp[ch ^ sw] = make_float4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+          }
+          if (args.cb) {
+            const int sw = (lane >> 2) & 1;
+            uint4* rowb = reinterpret_cast<uint4*>(ebuf + 2048 + lane * 32);
+#pragma unroll
+            for (int ch = 0; ch < 2; ++ch)
+              rowb[ch ^ sw] = make_uint4(pack2_bf16(v[8 * ch], v[8 * ch + 1]), pack2_bf16(v[8 * ch + 2], v[8 * ch + 3]),
+                                         pack2_bf16(v[8 * ch + 4], v[8 * ch + 5]),
+                                         pack2_bf16(v[8 * ch + 6], v[8 * ch + 7]));
+            if (args.cl) {
+              uint4* rowl = reinterpret_cast<uint4*>(ebuf + 3072 + lane * 32);
+#pragma unroll
+              for (int ch = 0; ch < 2; ++ch)
+                rowl[ch ^ sw] = make_uint4(pack2_lo(v[8 * ch], v[8 * ch + 1]), pack2_lo(v[8 * ch + 2], v[8 * ch + 3]),
+                                           pack2_lo(v[8 * ch + 4], v[8 * ch + 5]),
+                                           pack2_lo(v[8 * ch + 6], v[8 * ch + 7]));
+            }
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            const int r0 = mt * kBM + q * 32;
+            if (args.c) tma_store_2d(&tmC, ebuf, col0, r0);
+            if (args.cb) tma_store_2d(&tmCb, ebuf + 2048, col0, r0);
+            if (args.cl) tma_store_2d(&tmCl, ebuf + 3072, col0, r0);
+            bulk_commit();
+          }
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) stile[lane * 17 + i] = v[i];
         __syncwarp();
@@ -333,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
     }
+    if (args.tma_out && lane == 0) bulk_wait0();
   }
   __syncthreads();
   if (warp == 1) {
@@ -513,10 +599,45 @@ CUtensorMap make_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, 
   return m;
 }
 
+// Output map for TMA stores: [rows][cols] with row stride ld elements of
+// esize bytes, box {16 columns, 32 rows}, swizzle matching the 16-column row
+// bytes (fp32 64 B, bf16 32 B). Out-of-bounds parts of a box are not written.
+CUtensorMap make_out_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int esize) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esize)};
+  cuuint32_t box[2] = {16, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           esize == 4 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(GGB_ECUDA, "cuTensorMapEncodeTiled (output) failed: " + std::to_string(r));
+  return m;
+}
+
+bool tma_store_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("GGB_GEMM_TMA_STORE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 uint32_t tmem_cols_for(int n) {
   uint32_t c = 32;
   while (c < static_cast<uint32_t>(n)) c <<= 1;
   return c;
+}
+
+bool b_resident_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("GGB_GEMM_BRES");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 int sm_count() {
@@ -548,8 +669,17 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
   require((a_lo != nullptr) == (bt_lo != nullptr), "gemm: split mode needs both lo operands");
   ga.BN = static_cast<int>(std::min<int64_t>(256, round_up(n, 16)));
   ga.n_tiles = static_cast<int>(ceil_div(n, ga.BN));
-  const int stage_bytes = (1 + ga.split) * (kBM * kBK * 2 + ga.BN * kBK * 2);
-  ga.stages = std::min(8, (kSmemBudget - 1024 - kEpiSmem) / stage_bytes);
+  // B resident when it is a single n-tile and fits beside >= 2 A stages
+  // (every tile then streams only A: the dX products, the out-head and the
+  // K = d_in products); otherwise A and B stream together per stage
+  const int parts = 1 + ga.split;
+  const int64_t kch = ceil_div(k, kBK);
+  const int64_t bres_bytes = kch * parts * ga.BN * kBK * 2;
+  const int fixed = 1024 + kEpiSmem;
+  const int a_stage = parts * kBM * kBK * 2;
+  ga.b_res = (ga.n_tiles == 1 && b_resident_enabled() && fixed + bres_bytes + 2 * a_stage <= kSmemBudget) ? 1 : 0;
+  const int stage_bytes = ga.b_res ? a_stage : parts * (kBM * kBK * 2 + ga.BN * kBK * 2);
+  ga.stages = std::min<int64_t>(8, (kSmemBudget - fixed - (ga.b_res ? bres_bytes : 0)) / stage_bytes);
   require(ga.stages >= 2, "gemm: tile does not fit shared memory");
   ga.tmem_cols = tmem_cols_for(2 * ga.BN);
   ga.c = c;
@@ -561,16 +691,26 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
   const CUtensorMap tb = make_tmap(bt, n, k, ldb, kBK, ga.BN);
   const CUtensorMap tal = ga.split ? make_tmap(a_lo, m, k, lda, kBK, kBM) : ta;
   const CUtensorMap tbl = ga.split ? make_tmap(bt_lo, n, k, ldb, kBK, ga.BN) : tb;
-  const int smem = ga.stages * stage_bytes + 1024 + kEpiSmem;
+  auto al16 = [](const void* p, int64_t ld, int es) {
+    return p == nullptr || ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * es) % 16 == 0);
+  };
+  ga.tma_out = tma_store_enabled() && al16(c, ldc, 4) && al16(cb, ldcb, 2) && al16(ga.cl, ldcb, 2) ? 1 : 0;
+  CUtensorMap tc = ta, tcb = ta, tcl = ta;  // unused placeholders unless tma_out
+  if (ga.tma_out) {
+    if (c) tc = make_out_tmap(c, m, n, ldc, 4);
+    if (cb) tcb = make_out_tmap(cb, m, n, ldcb, 2);
+    if (ga.cl) tcl = make_out_tmap(ga.cl, m, n, ldcb, 2);
+  }
+  const int smem = ga.stages * stage_bytes + static_cast<int>(ga.b_res ? bres_bytes : 0) + 1024 + kEpiSmem;
   static bool attr = false;
   if (!attr) {
     GGB_CUDA(cudaFuncSetAttribute(k_gemm_kmajor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBudget + 1024));
+                                  kSmemBudget));
     attr = true;
   }
   const int64_t tiles = ceil_div(m, kBM) * ga.n_tiles;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
-  k_gemm_kmajor<<<grid, kThreads, smem, ctx.stream>>>(ta, tb, tal, tbl, ga);
+  k_gemm_kmajor<<<grid, kThreads, smem, ctx.stream>>>(ta, tb, tal, tbl, tc, tcb, tcl, ga);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
@@ -619,7 +759,7 @@ void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x,
   static bool attr = false;
   if (!attr) {
     GGB_CUDA(cudaFuncSetAttribute(k_gemm_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBudget + 1024));
+                                  kSmemBudget));
     attr = true;
   }
   dim3 grid(tiles, wa.splits);
