@@ -71,9 +71,10 @@ int ggb_ctx_synchronize(ggb_ctx_t ctx);
 int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters);
 /* Per-kernel-class timing with CUDA events on the ctx stream. Classes:
  * 0 sampling, 1 SpMM fwd, 2 SpMM bwd, 3 GEMM fwd, 4 GEMM dX, 5 GEMM dW,
- * 6 element-wise (RMSNorm/ReLU/dropout/CE), 7 optimizer, 8 collectives.
+ * 6 other element-wise passes, 7 optimizer, 8 collectives, 9 fused
+ * RMSNorm/ReLU/dropout/residual forward, 10 its backward, 11 cross-entropy.
  * read: totals since the last reset of time (ms), algorithmic bytes, flops
- * and launch counts (arrays of 9). */
+ * and launch counts (arrays of 12). */
 int ggb_ctx_profile(ggb_ctx_t ctx, int32_t enable);
 int ggb_ctx_profile_read(ggb_ctx_t ctx, double* ms, double* bytes, double* flops, int64_t* counts,
                          int32_t reset);

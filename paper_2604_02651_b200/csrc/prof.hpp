@@ -16,9 +16,12 @@ enum ProfCat : int {
   kProfGemmFwd,
   kProfGemmDx,
   kProfGemmWgrad,
-  kProfElementwise,  // RMSNorm / fused element-wise / cross-entropy
+  kProfElementwise,  // other element-wise passes (casts, split row statistics)
   kProfOptimizer,
   kProfComm,
+  kProfFwdRow,  // fused RMSNorm + ReLU + dropout + residual (k_fwd_row)
+  kProfBwdRow,  // fused element-wise + RMSNorm backward (k_bwd_row)
+  kProfCe,      // cross-entropy
   kProfCats
 };
 

@@ -11,6 +11,8 @@
 //              gradient in one pass over the logits row.
 // When the row is split over the grid's column axis the same kernels run in
 // two phases around the fp32 all-reduce of the row statistic.
+#include <algorithm>
+
 #include "ops.hpp"
 #include "rng.cuh"
 
@@ -69,130 +71,140 @@ __device__ __forceinline__ void f4(const float4& a, float* v) {
 
 template <int J, bool Full>  // chunks of 128 columns held per row; Full: cols == 128 J
 __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
-  constexpr int kMaxJ = J;
-  // Full rows: no column bounds anywhere (constant-folded below)
+  // Warp per row (grid-stride, so a capped grid also works), gamma and the
+  // per-lane constants held across rows.
   const int64_t ncols = Full ? static_cast<int64_t>(J) * kRowChunk : p.cols;
-  const int lane = threadIdx.x & 31;
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + (threadIdx.x >> 5);
-  if (r >= p.rows) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nj = Full ? J : static_cast<int>((p.cols + kRowChunk - 1) / kRowChunk);
-  const float* xr = p.x + r * p.ldx;
-  // every load of the row (xw, gamma, residual) is issued up front: one
-  // memory round trip per row instead of one before and one after the
-  // row reduction
-  float x[kMaxJ][4], g[kMaxJ][4], res[kMaxJ][4];
+  const int64_t w0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kRowsPerBlock;
+  float g[J][4];
 #pragma unroll
-  for (int j = 0; j < kMaxJ; ++j) {
+  for (int j = 0; j < J; ++j) {
     if (j >= nj) break;
-    const int64_t c = j * kRowChunk + 4 * lane;
-    f4(ld4(xr, c, ncols), x[j]);
     if (p.gamma)
-      f4(ld4(p.gamma, c, ncols), g[j]);
+      f4(ld4(p.gamma, j * kRowChunk + 4 * lane, ncols), g[j]);
     else
       g[j][0] = g[j][1] = g[j][2] = g[j][3] = 1.f;
-    if (p.res)
-      f4(ld4(p.res + r * p.ldres, c, ncols), res[j]);
-    else
-      res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
   }
-  float inv = 1.f;
-  if (p.gamma) {  // RMSNorm on
-    float ss;
-    if (p.fuse_ss) {
-      float s = 0.f;
-#pragma unroll
-      for (int j = 0; j < kMaxJ; ++j)
-        if (j < nj)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) s = fmaf(x[j][i], x[j][i], s);
-      ss = warp_sum(s);
-    } else {
-      ss = p.ss[r];
-    }
-    const float rms = sqrtf(ss / p.d + p.eps);
-    inv = 1.f / rms;
-    if (lane == 0 && p.rms) p.rms[r] = rms;
-  }
-  // y = gamma * x / rms for every held element
-  float y[kMaxJ][4];
-  uint32_t posm = 0;  // bit 4j+i: y > 0 and the column exists
-#pragma unroll
-  for (int j = 0; j < kMaxJ; ++j) {
-    if (j >= nj) break;
-    const int64_t c = j * kRowChunk + 4 * lane;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      y[j][i] = p.gamma ? g[j][i] * x[j][i] * inv : x[j][i];
-      if (y[j][i] > 0.f && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
-    }
-  }
-  // keep bits (ReLU and dropout): only ReLU-active elements need the dropout
-  // hash, so the warp compacts them and every lane hashes an equal share
-  // (about half the elements of the row) instead of all of its own
-  uint32_t keepm = posm;
-  if (p.drop && p.keep) {  // precomputed keep-bits (prefetcher)
-    uint32_t kb = 0;
-#pragma unroll
-    for (int j = 0; j < kMaxJ; ++j)
-      if (j < nj)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) kb |= ((p.keep[r * p.ldm + 4 * j + i] >> lane) & 1u) << (4 * j + i);
-    keepm = posm & kb;
-  } else if (p.drop) {
-    // list of the row's active columns, slot-major (slot 4j+i, then lane):
-    // per-slot ballots give every element its list index with one popc
-    __shared__ uint16_t s_list[kRowsPerBlock][32 * 4 * kMaxJ];
-    __shared__ uint32_t s_keep[kRowsPerBlock][4 * kMaxJ];  // keep ballot per 32 list entries
-    const int wib = threadIdx.x >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
-    int idx[4 * kMaxJ];
-    int total = 0;
-#pragma unroll
-    for (int s = 0; s < 4 * kMaxJ; ++s) {
-      const bool on = (posm >> s) & 1u;
-      const uint32_t b = __ballot_sync(0xffffffffu, on);
-      idx[s] = total + __popc(b & lt);
-      if (on) s_list[wib][idx[s]] = static_cast<uint16_t>((s >> 2) * kRowChunk + 4 * lane + (s & 3));
-      total += __popc(b);
-    }
-    __syncwarp();
-    const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
-    for (int k0 = 0; k0 < total; k0 += 32) {
-      const int k = k0 + lane;
-      bool keep = false;
-      if (k < total) keep = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + s_list[wib][k]), p.thresh);
-      const uint32_t w = __ballot_sync(0xffffffffu, keep);
-      if (lane == 0) s_keep[wib][k0 >> 5] = w;
-    }
-    __syncwarp();
-    keepm = 0;
-#pragma unroll
-    for (int s = 0; s < 4 * kMaxJ; ++s)
-      if ((posm >> s) & 1u) keepm |= ((s_keep[wib][idx[s] >> 5] >> (idx[s] & 31)) & 1u) << s;
-  }
+  const uint32_t lt = (1u << lane) - 1u;
   const float sc_on = p.drop ? p.keep_scale : 1.f;
+  const bool hash = p.drop && !p.keep;
+  // row's ReLU-active columns (compacted), and one keep byte per column
+  __shared__ uint16_t s_list[kRowsPerBlock][32 * 4 * J];
+  __shared__ __align__(16) uint8_t s_kb[kRowsPerBlock][kRowChunk * J];
+
+#pragma unroll 1
+  for (int64_t r = w0; r < p.rows; r += nw) {
+    const float* xr = p.x + r * p.ldx;
+    // every load of the row is issued up front: one memory round trip per row
+    float x[J][4], res[J][4];
 #pragma unroll
-  for (int j = 0; j < kMaxJ; ++j) {
-    if (j >= nj) break;
-    const int64_t c = j * kRowChunk + 4 * lane;
-    float o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const bool on = (keepm >> (4 * j + i)) & 1u;
-      const unsigned bits = __ballot_sync(0xffffffffu, on);
-      if (lane == i) p.mask[r * p.ldm + 4 * j + i] = bits;
-      o[i] = y[j][i] * (on ? sc_on : 0.f) + res[j][i];
+    for (int j = 0; j < J; ++j) {
+      if (j >= nj) break;
+      const int64_t c = j * kRowChunk + 4 * lane;
+      f4(ld4(xr, c, ncols), x[j]);
+      if (p.res)
+        f4(ld4(p.res + r * p.ldres, c, ncols), res[j]);
+      else
+        res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
     }
-    if (p.out) st4(p.out + r * p.ldo, c, ncols, o);
-    if (p.outb) {
-      st4_bf16(p.outb + r * p.ldob, c, ncols, o);
-      if (p.outlo) {
-        float lo[4];
+    float inv = 1.f;
+    if (p.gamma) {  // RMSNorm on
+      float ss;
+      if (p.fuse_ss) {
+        float s = 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) lo[i] = o[i] - __bfloat162float(__float2bfloat16_rn(o[i]));
-        st4_bf16(p.outlo + r * p.ldob, c, ncols, lo);
+        for (int j = 0; j < J; ++j)
+          if (j < nj)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) s = fmaf(x[j][i], x[j][i], s);
+        ss = warp_sum(s);
+      } else {
+        ss = p.ss[r];
+      }
+      const float rms = sqrtf(ss / p.d + p.eps);
+      inv = 1.f / rms;
+      if (lane == 0 && p.rms) p.rms[r] = rms;
+    }
+    // y = gamma * x / rms; bit 4j+i of posm: y > 0 and the column exists
+    float y[J][4];
+    uint32_t posm = 0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (j >= nj) break;
+      const int64_t c = j * kRowChunk + 4 * lane;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        y[j][i] = p.gamma ? g[j][i] * x[j][i] * inv : x[j][i];
+        if (y[j][i] > 0.f && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
       }
     }
+    uint32_t keepm = posm;
+    if (p.drop && p.keep) {  // precomputed keep-bits (prefetcher)
+      uint32_t kb = 0;
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        if (j < nj)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) kb |= ((p.keep[r * p.ldm + 4 * j + i] >> lane) & 1u) << (4 * j + i);
+      keepm = posm & kb;
+    } else if (hash) {
+      // only ReLU-active elements need the dropout hash: the warp lists them
+      // (per-slot ballots give each its list index) and every lane hashes an
+      // equal share; the hashing lane writes the element's keep byte
+      int total = 0;
+#pragma unroll
+      for (int sl = 0; sl < 4 * J; ++sl) {
+        const bool on = (posm >> sl) & 1u;
+        const uint32_t bl = __ballot_sync(0xffffffffu, on);
+        if (on) s_list[wib][total + __popc(bl & lt)] = static_cast<uint16_t>((sl >> 2) * kRowChunk + 4 * lane + (sl & 3));
+        total += __popc(bl);
+      }
+      __syncwarp();
+      const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
+      for (int k = lane; k < total; k += 32) {
+        const int col = s_list[wib][k];
+        s_kb[wib][col] = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + col), p.thresh) ? 1 : 0;
+      }
+      __syncwarp();
+      // the lane's 4 keep bytes per chunk in one load (bytes of inactive
+      // columns are stale and masked by posm)
+      uint32_t kb = 0;
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        if (j < nj) {
+          const uint32_t w4 = *reinterpret_cast<const uint32_t*>(&s_kb[wib][j * kRowChunk + 4 * lane]);
+          kb |= ((w4 & 1u) | ((w4 >> 7) & 2u) | ((w4 >> 14) & 4u) | ((w4 >> 21) & 8u)) << (4 * j);
+        }
+      keepm = posm & kb;
+      __syncwarp();  // s_list / s_kb are rewritten by the next row
+    }
+    uint32_t myword = 0;  // lane s < 4 nj stores keep word s of the row
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      if (j >= nj) break;
+      const int64_t c = j * kRowChunk + 4 * lane;
+      float o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool on = (keepm >> (4 * j + i)) & 1u;
+        const uint32_t bits = __ballot_sync(0xffffffffu, on);
+        if (lane == 4 * j + i) myword = bits;
+        o[i] = y[j][i] * (on ? sc_on : 0.f) + res[j][i];
+      }
+      if (p.out) st4(p.out + r * p.ldo, c, ncols, o);
+      if (p.outb) {
+        st4_bf16(p.outb + r * p.ldob, c, ncols, o);
+        if (p.outlo) {
+          float lo[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) lo[i] = o[i] - __bfloat162float(__float2bfloat16_rn(o[i]));
+          st4_bf16(p.outlo + r * p.ldob, c, ncols, lo);
+        }
+      }
+    }
+    if (lane < 4 * nj) p.mask[r * p.ldm + lane] = myword;
   }
 }
 
@@ -455,27 +467,34 @@ inline unsigned row_blocks(int64_t rows) { return static_cast<unsigned>(ceil_div
 
 }  // namespace
 
+template <int J, bool Full>
+void launch_fwd_row(Ctx& ctx, const FwdApply& p) {
+  // a warp per row (the kernel also strides, for capped grids): the dropout
+  // hashing needs every resident warp it can get to hide its latency
+  const unsigned g = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(p.rows, kRowsPerBlock)));
+  k_fwd_row<J, Full><<<g, kT, 0, ctx.stream>>>(p);
+}
+
 void fwd_apply(Ctx& ctx, const FwdApply& p) {
   if (p.rows <= 0) return;
   require(p.cols <= kMaxJ * kRowChunk, "row kernels: at most 512 local feature columns");
   require(p.ldx % 4 == 0 && (!p.res || p.ldres % 4 == 0) && (!p.out || p.ldo % 4 == 0),
           "row kernels: fp32 rows must be 16-byte aligned");
-  const int g = row_blocks(p.rows);
   if (p.cols <= kRowChunk) {
     if (p.cols == kRowChunk)
-      k_fwd_row<1, true><<<g, kT, 0, ctx.stream>>>(p);
+      launch_fwd_row<1, true>(ctx, p);
     else
-      k_fwd_row<1, false><<<g, kT, 0, ctx.stream>>>(p);
+      launch_fwd_row<1, false>(ctx, p);
   } else if (p.cols <= 2 * kRowChunk) {
     if (p.cols == 2 * kRowChunk)
-      k_fwd_row<2, true><<<g, kT, 0, ctx.stream>>>(p);
+      launch_fwd_row<2, true>(ctx, p);
     else
-      k_fwd_row<2, false><<<g, kT, 0, ctx.stream>>>(p);
+      launch_fwd_row<2, false>(ctx, p);
   } else {
     if (p.cols == kMaxJ * kRowChunk)
-      k_fwd_row<kMaxJ, true><<<g, kT, 0, ctx.stream>>>(p);
+      launch_fwd_row<kMaxJ, true>(ctx, p);
     else
-      k_fwd_row<kMaxJ, false><<<g, kT, 0, ctx.stream>>>(p);
+      launch_fwd_row<kMaxJ, false>(ctx, p);
   }
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;

@@ -432,7 +432,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     }
     {
       const double e = static_cast<double>(xb.rows()) * xb.cols();
-      ProfScope ps(ctx, kProfElementwise, e * (4 + (res ? 4 : 0) + 4 + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0)) + e / 8);
+      ProfScope ps(ctx, kProfFwdRow, e * (4 + (res ? 4 : 0) + 4 + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0)) + e / 8);
       fwd_apply(ctx, fa);
     }
     prev = &L.x;
@@ -478,10 +478,10 @@ void cross_entropy(State& st, const Batch& bt) {
   c.loss_part = grow<float>(st.ce_part, ce_grad_blocks(c.rows) + 1);
   c.loss_acc = grow<float>(st.loss_acc, 1);
   if (trivial(ctx, lb.lay.col)) {  // class block complete here: one pass per row
-    ProfScope ps(ctx, kProfElementwise, static_cast<double>(c.rows) * c.cols * (4 + 2));
+    ProfScope ps(ctx, kProfCe, static_cast<double>(c.rows) * c.cols * (4 + 2));
     ce_fused(ctx, c);
   } else {
-    ProfScope ps(ctx, kProfElementwise, static_cast<double>(c.rows) * c.cols * (3 * 4 + 2));
+    ProfScope ps(ctx, kProfCe, static_cast<double>(c.rows) * c.cols * (3 * 4 + 2));
     ce_rowmax(ctx, c);
     all_reduce_max(ctx, lb.lay.col, c.mx, c.rows);
     ce_rowsum(ctx, c);
@@ -569,7 +569,7 @@ void backward(State& st, const Batch& bt, int precision) {
     ba.lddxb = lddxw;
     {
     // reads dy + xw twice (stats, apply) + mask, writes dxw bf16
-    ProfScope ps(ctx, kProfElementwise, static_cast<double>(rows) * cols * (2 * 8 + 2) + rows * cols / 4.0);
+    ProfScope ps(ctx, kProfBwdRow, static_cast<double>(rows) * cols * (2 * 8 + 2) + rows * cols / 4.0);
     if (cfg.use_rmsnorm) {
       const ParamSlot& gp = st.params[st.gamma[l - 1]];
       ba.gamma = W + gp.off;

@@ -146,7 +146,7 @@ class Context:
         return self.counters()["launches"]
 
     PROF_CLASSES = ["sampling", "spmm_fwd", "spmm_bwd", "gemm_fwd", "gemm_dx", "gemm_wgrad", "elementwise",
-                    "optimizer", "collectives"]
+                    "optimizer", "collectives", "fwd_row", "bwd_row", "cross_entropy"]
 
     def profile(self, enable: bool):
         """Per-kernel-class CUDA-event timing on the context's stream."""
