@@ -184,7 +184,7 @@ def main():
             return
         # each reference step is a bounded sample (seconds of CPU work); cap the count
         # so the whole run stays within a few minutes
-        steps_run, warm_run = max(1, min(args.steps, 3)), min(args.warmup, 1)
+        steps_run, warm_run = max(1, min(args.steps, 3)), min(args.warmup, 3)
         rb = reference_baseline(cfg, steps_run, warm_run)
         S = math.ceil(cfg["n"] / cfg["batch"])
         v = rb["epoch_time_s"]
