@@ -46,6 +46,13 @@ CONFIGS = {
     "C3": dict(workload="Reddit-shaped synthetic (233K vertices, 114.6M edges, 602 feat, 41 classes), "
                         "3-layer GCN hidden 256",
                n=232_965, avg_degree=492.5, d_in=602, n_classes=41, layers=3, d_h=256, batch=58_242),
+    # BASELINE configs[3]: ogbn-papers100M-shaped, 1.6G undirected edge draws (~3.3G nonzeros with
+    # self-loops); global batch ceil(N/16). Device-built graph; the reference CPU path
+    # cannot hold it (no CPU baseline).
+    "C4": dict(workload="ogbn-papers100M-shaped synthetic (111M vertices, 1.6B edges, 128 feat, 172 classes), "
+                        "3-layer GCN hidden 256",
+               n=111_059_956, avg_degree=28.8133, d_in=128, n_classes=172, layers=3, d_h=256, batch=6_941_248,
+               no_reference=True),
 }
 DATA_SEED, RUN_SEED, LR, DROPOUT = 7, 1, 1e-3, 0.1
 
@@ -172,6 +179,8 @@ def main():
     ap.add_argument("--prefetch", type=int, default=1,
                     help="1: sample step t+1 on a side stream during step t; 2: also its dropout masks; 0: off")
     ap.add_argument("--ref-steps", type=int, default=2)
+    ap.add_argument("--host-features", action="store_true",
+                    help="keep the features in pinned host memory for the timed loop too (papers100M-scale HBM budget)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -181,6 +190,10 @@ def main():
 
     if args.impl == "reference":
         if rank != 0:
+            return
+        if cfg.get("no_reference"):
+            print(json.dumps({"impl": "reference", "unavailable": "the reference CPU path cannot hold the "
+                              f"{args.config} graph in host memory (SURVEY §6.2)"}), flush=True)
             return
         # each reference step is a bounded sample (seconds of CPU work); cap the count
         # so the whole run stays within a few minutes
@@ -224,8 +237,12 @@ def main():
     ctx = gg.Context(grid, rank, device=local_rank, nccl_uid=uid, stream=stream.cuda_stream)
 
     t0 = time.time()
-    graph = gg.Graph.generate_synthetic(ctx, cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"], DATA_SEED,
-                                        cfg["layers"])
+    # generate_synthetic on the device (CSR, labels, split bit-identical to the
+    # reference generator, features to within one fp32 ulp in rare elements)
+    graph = gg.Graph.generate_synthetic_device(ctx, cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"],
+                                               DATA_SEED, cfg["layers"])
+    if args.host_features:
+        graph.features_to_host()
     t_graph = time.time() - t0
     gd = dims[0]
     b = cfg["batch"] // gd  # per data-parallel group: the global batch stays fixed
@@ -295,7 +312,7 @@ def main():
     # separately: the reference's epoch time excludes it; it is the
     # paper's full-graph inference metric
     ev_info = None
-    if not args.no_eval:
+    if not args.no_eval and not cfg.get("no_reference"):  # an N-row eval batch of C4 exceeds HBM
         t0 = time.time()
         evb = gg.build_eval_batch(ctx, graph, RUN_SEED)
         t_evb = time.time() - t0
@@ -434,7 +451,11 @@ def main():
         "step_ms_rank0": step_ms,
         "e2e_step_ms_rank0": e2e_step_ms,
     }
-    if not args.no_cpu_baseline and n_gpus == 1:
+    if cfg.get("no_reference"):
+        out["cpu_baseline"] = {"value": None, "unit": "s", "cores": None, "kind": "reference",
+                               "sample": "unavailable: the reference CPU path cannot hold this graph in host memory "
+                                         "(SURVEY §6.2)"}
+    elif not args.no_cpu_baseline and n_gpus == 1:
         try:
             rb = reference_baseline(cfg, args.ref_steps, 1)
             out["cpu_baseline"] = {"value": rb["epoch_time_s"], "unit": "s", "cores": rb["cores"],

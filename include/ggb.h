@@ -97,6 +97,20 @@ int ggb_graph_create(ggb_ctx_t ctx, int64_t n, const int64_t* row_ptr, const int
 int ggb_graph_generate_synthetic(ggb_ctx_t ctx, int64_t n, double avg_degree, int64_t d_in,
                                  int64_t n_classes, uint64_t seed, int32_t layers,
                                  ggb_graph_t* out);
+/* The same dataset generated on the device: edges, the
+ * normalized CSR, labels and split tags are bit-identical to
+ * generate_synthetic (dataset.cpp:85-150); features follow the same polar
+ * sequence with CUDA's fp64 log (a value may differ by one fp32 ulp in rare
+ * cases). No host pass, so papers100M-scale graphs build in seconds. */
+int ggb_graph_generate_synthetic_device(ggb_ctx_t ctx, int64_t n, double avg_degree, int64_t d_in,
+                                        int64_t n_classes, uint64_t seed, int32_t layers,
+                                        ggb_graph_t* out);
+/* Host copies of a graph's dataset (tests): the full normalized CSR (needs
+ * a full-matrix shard on this rank, i.e. a 1x1x1 grid), features (full
+ * device copy only), labels, split; any pointer may be NULL. col_idx is
+ * int64 like the reference's CsrMatrix. */
+int ggb_graph_export(ggb_graph_t g, int64_t* row_ptr, int64_t* col_idx, double* values, float* features,
+                     int32_t* labels, uint8_t* split);
 /* Split tags (Dataset::split, dataset.hpp:12,23): 0 train, 1 val, 2 test,
  * 3 unused; one byte per vertex. generate_synthetic sets them itself
  * (dataset.cpp:122-129); needed only by ggb_evaluate_full_graph. */

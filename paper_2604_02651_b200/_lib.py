@@ -43,6 +43,8 @@ _SIGS = [
     ("ggb_sample_vertices", C.c_int, [P, I64, I64, U64, U64, P]),
     ("ggb_graph_create", C.c_int, [P, I64, P, P, P, I32, I64, P, I64, P, I32, P]),
     ("ggb_graph_generate_synthetic", C.c_int, [P, I64, F64, I64, I64, U64, I32, P]),
+    ("ggb_graph_generate_synthetic_device", C.c_int, [P, I64, F64, I64, I64, U64, I32, P]),
+    ("ggb_graph_export", C.c_int, [P, P, P, P, P, P, P]),
     ("ggb_graph_set_split", C.c_int, [P, P]),
     ("ggb_graph_destroy", C.c_int, [P]),
     ("ggb_graph_info", C.c_int, [P, P]),

@@ -7,6 +7,7 @@
 #include <thread>
 
 #include "comm.hpp"
+#include "gendata.hpp"
 #include "dataset.hpp"
 #include "prefetch.hpp"
 #include "prof.hpp"
@@ -228,6 +229,80 @@ void graph_build(Ctx& ctx, Graph& g, int64_t n, const int64_t* rp, const int64_t
   for (auto& s : g.shards) g.device_bytes += s.row_ptr.bytes + s.col.bytes + s.val.bytes;
 }
 
+// graph_build from a device-generated dataset (gendata.cu): the plane
+// shards are cut on the device; a full-matrix shard takes the CSR buffers
+// over, so a 1x1x1 grid holds exactly one copy of the adjacency.
+void graph_build_device(Ctx& ctx, Graph& g, DevDataset& ds, int layers) {
+  const int64_t n = ds.n;
+  require(layers >= 1, "graph: layers must be >= 1");
+  g.ctx = &ctx;
+  g.n = n;
+  g.nnz = ds.nnz;
+  g.d_in = ds.d_in;
+  g.n_classes = ds.n_classes;
+  g.layers = layers;
+  g.planes = std::min(layers, 3);
+  g.shards.clear();
+  g.fwd_of.assign(g.planes, -1);
+  g.tr_of.assign(g.planes, -1);
+  struct Key {
+    int64_t r0, r1, c0, c1;
+  };
+  std::vector<Key> keys;
+  auto get = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {  // A == A^T: one key space
+    for (size_t k = 0; k < keys.size(); ++k)
+      if (keys[k].r0 == r0 && keys[k].r1 == r1 && keys[k].c0 == c0 && keys[k].c1 == c1) return static_cast<int>(k);
+    keys.push_back({r0, r1, c0, c1});
+    return static_cast<int>(keys.size() - 1);
+  };
+  for (int p = 0; p < g.planes; ++p) {
+    const Layout lay = adjacency_layout(p + 1);
+    const auto ro = block_partition(n, ctx.grid.dims[lay.row]);
+    const auto co = block_partition(n, ctx.grid.dims[lay.col]);
+    const int64_t r0 = ro[ctx.coord[lay.row]], r1 = ro[ctx.coord[lay.row] + 1];
+    const int64_t c0 = co[ctx.coord[lay.col]], c1 = co[ctx.coord[lay.col] + 1];
+    g.fwd_of[p] = get(r0, r1, c0, c1);
+    g.tr_of[p] = get(c0, c1, r0, r1);
+  }
+  g.shards.resize(keys.size());
+  int full = -1;
+  for (size_t k = 0; k < keys.size(); ++k) {
+    const Key& kk = keys[k];
+    if (kk.r0 == 0 && kk.r1 == n && kk.c0 == 0 && kk.c1 == n) {
+      full = static_cast<int>(k);
+      continue;
+    }
+    build_shard_device(ctx, n, ds, kk.r0, kk.r1, kk.c0, kk.c1, g.shards[k]);
+  }
+  if (full >= 0) {
+    PlaneShard& sh = g.shards[full];
+    sh.r0 = sh.c0 = 0;
+    sh.r1 = sh.c1 = n;
+    sh.nnz = ds.nnz;
+    sh.row_ptr = std::move(ds.row_ptr);
+    sh.col = std::move(ds.col);
+    sh.val = std::move(ds.val);
+  }
+  const auto fo = block_partition(ds.d_in, ctx.grid.dims[kInputFeatureLayout.col]);
+  g.feat_c0 = fo[ctx.coord[kInputFeatureLayout.col]];
+  g.feat_c1 = fo[ctx.coord[kInputFeatureLayout.col] + 1];
+  const int64_t fw = g.feat_c1 - g.feat_c0;
+  if (fw == ds.d_in) {
+    g.features = std::move(ds.features);
+  } else {
+    float* dst = g.features.reserve_n<float>(static_cast<size_t>(std::max<int64_t>(n * fw, 1)));
+    GGB_CUDA(cudaMemcpy2DAsync(dst, fw * 4, ds.features.as<float>() + g.feat_c0, ds.d_in * 4, fw * 4, n,
+                               cudaMemcpyDeviceToDevice, ctx.stream));
+    GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+    ds.features.release();
+  }
+  g.labels = std::move(ds.labels);
+  g.split = std::move(ds.split);
+  g.feat_ptr = g.features.as<float>();
+  g.device_bytes = g.features.bytes + g.labels.bytes + g.split.bytes;
+  for (auto& s : g.shards) g.device_bytes += s.row_ptr.bytes + s.col.bytes + s.val.bytes;
+}
+
 template <class T>
 void download(T* host, const void* dev, size_t n, cudaStream_t s) {
   if (n == 0 || !host) return;
@@ -387,6 +462,53 @@ int ggb_graph_generate_synthetic(ggb_ctx_t ctx, int64_t n, double avg_degree, in
                 ds.features.data(), n_classes, ds.labels.data(), layers);
     set_split(*g, ds.split.data());
     *out = g.release();
+  });
+}
+
+int ggb_graph_generate_synthetic_device(ggb_ctx_t ctx, int64_t n, double avg_degree, int64_t d_in,
+                                        int64_t n_classes, uint64_t seed, int32_t layers, ggb_graph_t* out) {
+  return guard([&] {
+    require(out != nullptr, "graph: null handle slot");
+    use_device(*ctx);
+    auto g = std::make_unique<ggb_graph_s>();
+    {
+      DevDataset ds;
+      generate_synthetic_device(*ctx, n, avg_degree, d_in, n_classes, seed, ds);
+      graph_build_device(*ctx, *g, ds, layers);
+    }
+    *out = g.release();
+  });
+}
+
+int ggb_graph_export(ggb_graph_t g, int64_t* row_ptr, int64_t* col_idx, double* values, float* features,
+                     int32_t* labels, uint8_t* split) {
+  return guard([&] {
+    require(g != nullptr, "graph_export: null graph");
+    use_device(*g->ctx);
+    cudaStream_t s = g->ctx->stream;
+    const PlaneShard* full = nullptr;
+    for (const auto& sh : g->shards)
+      if (sh.r0 == 0 && sh.r1 == g->n && sh.c0 == 0 && sh.c1 == g->n) full = &sh;
+    if (row_ptr || col_idx || values) {
+      require(full != nullptr, "graph_export: no full-matrix shard on this rank (1x1x1 grids only)");
+      download(row_ptr, full->row_ptr.p, static_cast<size_t>(g->n) + 1, s);
+      if (col_idx) {
+        std::vector<int32_t> c(static_cast<size_t>(full->nnz));
+        download(c.data(), full->col.p, c.size(), s);
+        std::copy(c.begin(), c.end(), col_idx);
+      }
+      download(values, full->val.p, static_cast<size_t>(full->nnz), s);
+    }
+    if (features) {
+      require(!g->features_on_host() && g->feat_c0 == 0 && g->feat_c1 == g->d_in,
+              "graph_export: features are not a full device copy on this rank");
+      download(features, g->features.p, static_cast<size_t>(g->n * g->d_in), s);
+    }
+    download(labels, g->labels.p, static_cast<size_t>(g->n), s);
+    if (split) {
+      require(g->split.bytes >= static_cast<size_t>(g->n), "graph_export: no split tags");
+      download(split, g->split.p, static_cast<size_t>(g->n), s);
+    }
   });
 }
 

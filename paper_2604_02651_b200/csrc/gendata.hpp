@@ -1,0 +1,23 @@
+// Device-built synthetic dataset (gendata.cu): the reference's
+// generate_synthetic (dataset.cpp:85-131) on the GPU.
+#pragma once
+
+#include "runtime.hpp"
+
+namespace ggb {
+
+/// Dataset (dataset.hpp:16-29) resident in HBM: the normalized adjacency as a
+/// column-sorted CSR (int64 row_ptr, int32 col, fp64 val), fp32 features
+/// [n][d_in], int32 labels, uint8 split tags.
+struct DevDataset {
+  int64_t n = 0, d_in = 0, n_classes = 0, nnz = 0;
+  DevBuf row_ptr, col, val, features, labels, split;
+};
+
+void generate_synthetic_device(Ctx& ctx, int64_t n, double avg_degree, int64_t d_in, int64_t n_classes,
+                               uint64_t seed, DevDataset& ds);
+/// make_csr_shard (shardsample.cpp:19-45) of the device CSR.
+void build_shard_device(Ctx& ctx, int64_t n, const DevDataset& ds, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                        PlaneShard& sh);
+
+}  // namespace ggb

@@ -255,6 +255,29 @@ class Graph:
                                                  C.byref(h)))
         return Graph(ctx, h)
 
+    @staticmethod
+    def generate_synthetic_device(ctx: Context, n: int, avg_degree: float, d_in: int, n_classes: int,
+                                  seed: int, layers: int) -> "Graph":
+        """generate_synthetic built on the GPU (edges, CSR, labels, split bit-identical)."""
+        h = P()
+        check(lib().ggb_graph_generate_synthetic_device(ctx.h, n, avg_degree, d_in, n_classes, seed, layers,
+                                                        C.byref(h)))
+        return Graph(ctx, h)
+
+    def export(self, csr: bool = True, features: bool = True):
+        """Host copies: (row_ptr, col_idx, values) | None, features | None, labels, split."""
+        rp = ci = va = fe = None
+        if csr:
+            rp = np.empty(self.n + 1, np.int64)
+            ci = np.empty(self.nnz, np.int64)
+            va = np.empty(self.nnz, np.float64)
+        if features:
+            fe = np.empty((self.n, self.d_in), np.float32)
+        la = np.empty(self.n, np.int32)
+        sp = np.empty(self.n, np.uint8)
+        check(lib().ggb_graph_export(self.h, _ptr(rp), _ptr(ci), _ptr(va), _ptr(fe), _ptr(la), _ptr(sp)))
+        return ((rp, ci, va) if csr else None), fe, la, sp
+
     def close(self):
         if getattr(self, "h", None):
             lib().ggb_graph_destroy(self.h)

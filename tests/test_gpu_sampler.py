@@ -191,3 +191,45 @@ def test_native_generator_matches_reference(gg, ref):
         assert np.array_equal(batch.labels, want.labels)
     finally:
         ref.free_dataset(h)
+
+
+# ---- the dataset generated on the device -----------------------------
+@pytest.mark.parametrize("n,deg,d_in,ncls,seed", [(2, 1.0, 3, 2, 7), (50, 0.0, 4, 3, 1), (3000, 9.5, 17, 5, 7),
+                                                  (65536, 30.52, 64, 16, 7)])
+def test_device_generated_dataset_matches_generator(gg, orc, n, deg, d_in, ncls, seed):
+    """generate_synthetic (dataset.cpp:85-150) on the GPU: normalized CSR
+    (row_ptr, col_idx, fp64 values), labels and split tags bit-identical to
+    the generator pinned to the reference; features the same polar sequence
+    (fp64 log from CUDA: at most one fp32 ulp, in rare elements)."""
+    ds = orc.generate_synthetic(n, deg, d_in, ncls, seed)
+    ctx = gg.Context()
+    g = gg.Graph.generate_synthetic_device(ctx, n, deg, d_in, ncls, seed, 3)
+    (rp, ci, va), fe, la, sp = g.export()
+    assert np.array_equal(rp, ds.adj.row_ptr) and np.array_equal(ci, ds.adj.col_idx)
+    assert np.array_equal(va.view(np.uint64), ds.adj.values.view(np.uint64))
+    assert np.array_equal(la, ds.labels) and np.array_equal(sp, ds.split)
+    a, b = fe.view(np.int32).astype(np.int64), ds.features.view(np.int32).astype(np.int64)
+    assert np.max(np.abs(a - b)) <= 1
+    assert np.count_nonzero(a != b) <= max(1, a.size // 10000)
+
+
+def test_device_generated_graph_trains_like_host_graph(gg, orc):
+    """A device-built graph gives the same batches and losses as the host-built one."""
+    n, deg, d_in, ncls, b, seed = 6000, 12.0, 24, 6, 1500, 3
+    ctx = gg.Context()
+    gh = gg.Graph.generate_synthetic(ctx, n, deg, d_in, ncls, seed, 3)
+    gd = gg.Graph.generate_synthetic_device(ctx, n, deg, d_in, ncls, seed, 3)
+    assert gd.nnz == gh.nnz
+    cfg = gg.ModelConfig(layers=3, d_in=d_in, d_h=32, d_out=ncls, dropout_rate=0.1)
+    sa, sb = gg.init_state(ctx, cfg, 1), gg.init_state(ctx, cfg, 1)
+    for t in range(2):
+        ba = gg.build_step_batch(ctx, gh, b, 5, t)
+        bb = gg.build_step_batch(ctx, gd, b, 5, t)
+        for p in range(3):
+            x, y = ba.a(p), bb.a(p)
+            assert np.array_equal(x.row_ptr, y.row_ptr) and np.array_equal(x.col_idx, y.col_idx)
+            assert np.array_equal(x.values.view(np.uint64), y.values.view(np.uint64))
+        assert np.array_equal(ba.labels, bb.labels)
+        la = gg.train_step(ctx, sa, ba, gg.FP32, 1, t)
+        lb = gg.train_step(ctx, sb, bb, gg.FP32, 1, t)
+        assert abs(la - lb) <= 1e-5 * abs(la)
