@@ -38,7 +38,8 @@ enum ggb_precision { GGB_FP32 = 0, GGB_BF16_WIRE = 1 }; /* comm.hpp:22 Precision
 enum ggb_optimizer { GGB_SGD = 0, GGB_ADAM = 1 };       /* model.hpp:45 Optimizer */
 
 typedef struct ggb_ctx_s* ggb_ctx_t;     /* one per (process, GPU): grid coords, streams, comms, sampler */
-typedef struct ggb_graph_s* ggb_graph_t; /* Dataset + RankContext plane shards resident in HBM */
+typedef struct ggb_graph_s* ggb_graph_t;
+typedef struct ggb_dataset_s* ggb_dataset_t; /* host Dataset (dataset.hpp:16-29) + its raw edge list */ /* Dataset + RankContext plane shards resident in HBM */
 typedef struct ggb_batch_s* ggb_batch_t; /* StepBatch resident in HBM (model.hpp:238-246) */
 typedef struct ggb_state_s* ggb_state_t; /* ModelState resident in HBM (model.hpp:87-105) */
 
@@ -111,6 +112,31 @@ int ggb_graph_generate_synthetic_device(ggb_ctx_t ctx, int64_t n, double avg_deg
  * int64 like the reference's CsrMatrix. */
 int ggb_graph_export(ggb_graph_t g, int64_t* row_ptr, int64_t* col_idx, double* values, float* features,
                      int32_t* labels, uint8_t* split);
+/* ---- host datasets and files. No GPU needed except for
+ * ggb_graph_from_dataset. Formats and validation messages are the
+ * reference's (dataset.cpp:152-280): text edge list ("u v" per line, '#'
+ * comments), SGNF (features), SGNL (labels), SGNS (split tags).
+ * load_dataset (dataset.cpp:178-239); errors -> GGB_EINVAL with the
+ * reference's message (std::invalid_argument there). */
+int ggb_dataset_load(const char* edges, const char* features, const char* labels, const char* split,
+                     ggb_dataset_t* out);
+/* generate_synthetic + synthetic_edges (dataset.cpp:85-150), host native. */
+int ggb_dataset_generate_synthetic(int64_t n, double avg_degree, int64_t d_in, int64_t n_classes,
+                                   uint64_t seed, ggb_dataset_t* out);
+/* info = {n, nnz, d_in, n_classes, raw_edges} (5 entries) */
+int ggb_dataset_info(ggb_dataset_t d, int64_t* info);
+/* any pointer may be NULL; col_idx int64 (CsrMatrix), edges_uv = 2 x raw_edges */
+int ggb_dataset_export(ggb_dataset_t d, int64_t* row_ptr, int64_t* col_idx, double* values, float* features,
+                       int32_t* labels, uint8_t* split, int64_t* edges_uv);
+/* save_edge_list / save_features / save_labels / save_split (dataset.cpp:241-280),
+ * byte-identical to the reference's CLI `gen` output (gridgnn_main.cpp:313-324);
+ * a NULL path skips that file. */
+int ggb_dataset_save(ggb_dataset_t d, const char* edges, const char* features, const char* labels,
+                     const char* split);
+/* ggb_graph_create + ggb_graph_set_split from a host dataset (make_rank_context). */
+int ggb_graph_from_dataset(ggb_ctx_t ctx, ggb_dataset_t d, int32_t layers, ggb_graph_t* out);
+int ggb_dataset_destroy(ggb_dataset_t d);
+
 /* Split tags (Dataset::split, dataset.hpp:12,23): 0 train, 1 val, 2 test,
  * 3 unused; one byte per vertex. generate_synthetic sets them itself
  * (dataset.cpp:122-129); needed only by ggb_evaluate_full_graph. */

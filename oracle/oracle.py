@@ -436,6 +436,9 @@ class Ref:
         L.ref_dataset_from_edges.restype = P
         L.ref_dataset_from_edges.argtypes = [I64, P, I64, I64, P, I64, P, P]
         L.ref_dataset_free.argtypes = [P]
+        L.ref_dataset_load.restype = P
+        L.ref_dataset_load.argtypes = [C.c_char_p] * 4
+        L.ref_save_synthetic.argtypes = [I64, C.c_double, I64, I64, U64] + [C.c_char_p] * 4
         L.ref_dataset_info.argtypes = [P, P]
         L.ref_dataset_export.argtypes = [P, P, P, P, P, P, P]
         L.ref_synthetic_edges.restype = I64
@@ -476,6 +479,56 @@ class Ref:
         if not h:
             raise ValueError(self.L.ref_last_error().decode())
         return h
+
+    def load_files(self, edges, features, labels, split):
+        """load_dataset (dataset.cpp:178-239) in a numpy-free child interpreter
+        (see save_synthetic): ((row_ptr, col_idx, values), features, labels,
+        split, n_classes); raises ValueError with the reference's message."""
+        import tempfile
+        with tempfile.TemporaryDirectory() as td:
+            code = ("import ctypes as C, sys, os\n"
+                    f"L = C.CDLL({_LIBREF!r})\n"
+                    "L.ref_last_error.restype = C.c_char_p\n"
+                    "L.ref_dataset_load.restype = C.c_void_p\n"
+                    "L.ref_dataset_load.argtypes = [C.c_char_p] * 4\n"
+                    "L.ref_dataset_info.argtypes = [C.c_void_p, C.c_void_p]\n"
+                    "L.ref_dataset_export.argtypes = [C.c_void_p] * 7\n"
+                    f"h = L.ref_dataset_load(*[a.encode() for a in {[str(x) for x in (edges, features, labels, split)]!r}])\n"
+                    "if not h:\n"
+                    "    sys.stderr.write(L.ref_last_error().decode()); sys.exit(1)\n"
+                    "info = (C.c_int64 * 4)(); L.ref_dataset_info(h, info)\n"
+                    "n, nnz, d, k = info\n"
+                    "bufs = [(C.c_int64 * (n + 1))(), (C.c_int64 * nnz)(), (C.c_double * nnz)(),"
+                    " (C.c_float * (n * d))(), (C.c_int32 * n)(), (C.c_uint8 * n)()]\n"
+                    "L.ref_dataset_export(h, *[C.addressof(b) for b in bufs])\n"
+                    f"td = {td!r}\n"
+                    "open(os.path.join(td, 'info'), 'w').write('%d %d %d %d' % (n, nnz, d, k))\n"
+                    "for i, b in enumerate(bufs): open(os.path.join(td, 'a%d' % i), 'wb').write(bytes(b))\n")
+            r = subprocess.run(["python3", "-c", code], capture_output=True, text=True)
+            if r.returncode != 0:
+                raise (ValueError if r.returncode == 1 else RuntimeError)(r.stderr.strip())
+            n, nnz, d, k = (int(x) for x in open(os.path.join(td, "info")).read().split())
+            rd = lambda i, dt: np.fromfile(os.path.join(td, "a%d" % i), dt)
+            return ((rd(0, np.int64), rd(1, np.int64), rd(2, np.float64)), rd(3, np.float32).reshape(n, d),
+                    rd(4, np.int32), rd(5, np.uint8), k)
+
+    def save_synthetic(self, n, avg_degree, d_in, n_classes, seed, edges, features, labels, split):
+        """The CLI's gen command (gridgnn_main.cpp:313-324). Run in a child
+        interpreter that never imports numpy: with numpy loaded, the
+        reference's std::ofstream writers crash in this image (the readers and
+        everything else are unaffected)."""
+        code = ("import ctypes as C, sys\n"
+                f"L = C.CDLL({_LIBREF!r})\n"
+                "L.ref_last_error.restype = C.c_char_p\n"
+                "L.ref_save_synthetic.argtypes = [C.c_int64, C.c_double, C.c_int64, C.c_int64, C.c_uint64]"
+                " + [C.c_char_p] * 4\n"
+                f"rc = L.ref_save_synthetic({int(n)}, {float(avg_degree)!r}, {int(d_in)}, {int(n_classes)}, "
+                f"{int(seed)}, *[a.encode() for a in {[str(x) for x in (edges, features, labels, split)]!r}])\n"
+                "sys.stderr.write(L.ref_last_error().decode())\n"
+                "sys.exit(rc)\n")
+        r = subprocess.run(["python3", "-c", code], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise (ValueError if r.returncode == 1 else RuntimeError)(r.stderr.strip())
 
     def dataset_from(self, ds: Dataset, uv: np.ndarray):
         uv = np.ascontiguousarray(uv, np.int64)

@@ -203,6 +203,28 @@ void* ref_dataset_from_edges(std::int64_t n, const std::int64_t* uv, std::int64_
   return out;
 }
 
+/// load_dataset (dataset.cpp:178-239): the reference's own readers.
+void* ref_dataset_load(const char* edges, const char* features, const char* labels, const char* split) {
+  Dataset* out = nullptr;
+  if (guard([&] { out = new Dataset(load_dataset(edges, features, labels, split)); }) != 0) return nullptr;
+  return out;
+}
+
+/// The CLI's `gen` command (gridgnn_main.cpp:313-324): synthetic_edges +
+/// generate_synthetic written with the reference's save_* (dataset.cpp:241-280).
+int ref_save_synthetic(std::int64_t n, double avg_degree, std::int64_t d_in, std::int64_t n_classes,
+                       std::uint64_t seed, const char* edges_path, const char* features_path,
+                       const char* labels_path, const char* split_path) {
+  return guard([&] {
+    const auto edges = synthetic_edges(n, avg_degree, seed);
+    const Dataset ds = generate_synthetic(n, avg_degree, d_in, n_classes, seed);
+    save_edge_list(edges_path, edges);
+    save_features(features_path, ds.n, ds.d_in, ds.features);
+    save_labels(labels_path, ds.n, ds.n_classes, ds.labels);
+    save_split(split_path, ds.split);
+  });
+}
+
 void ref_dataset_free(void* ds) { delete static_cast<Dataset*>(ds); }
 
 void ref_dataset_info(void* p, std::int64_t* out) {

@@ -45,6 +45,13 @@ _SIGS = [
     ("ggb_graph_generate_synthetic", C.c_int, [P, I64, F64, I64, I64, U64, I32, P]),
     ("ggb_graph_generate_synthetic_device", C.c_int, [P, I64, F64, I64, I64, U64, I32, P]),
     ("ggb_graph_export", C.c_int, [P, P, P, P, P, P, P]),
+    ("ggb_dataset_load", C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, P]),
+    ("ggb_dataset_generate_synthetic", C.c_int, [I64, F64, I64, I64, U64, P]),
+    ("ggb_dataset_info", C.c_int, [P, P]),
+    ("ggb_dataset_export", C.c_int, [P, P, P, P, P, P, P, P]),
+    ("ggb_dataset_save", C.c_int, [P, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p]),
+    ("ggb_graph_from_dataset", C.c_int, [P, P, I32, P]),
+    ("ggb_dataset_destroy", C.c_int, [P]),
     ("ggb_graph_set_split", C.c_int, [P, P]),
     ("ggb_graph_destroy", C.c_int, [P]),
     ("ggb_graph_info", C.c_int, [P, P]),

@@ -9,12 +9,16 @@
 #include "comm.hpp"
 #include "gendata.hpp"
 #include "dataset.hpp"
+#include "dsio.hpp"
 #include "prefetch.hpp"
 #include "prof.hpp"
 #include "trainer.hpp"
 
 struct ggb_ctx_s : ggb::Ctx {};
 struct ggb_graph_s : ggb::Graph {};
+struct ggb_dataset_s : ggb::HostDataset {
+  std::vector<int64_t> uv;  // the raw edge list the adjacency was normalized from
+};
 struct ggb_batch_s : ggb::Batch {};
 struct ggb_state_s : ggb::State {};
 struct ggb_prefetch_s : ggb::Prefetcher {
@@ -510,6 +514,83 @@ int ggb_graph_export(ggb_graph_t g, int64_t* row_ptr, int64_t* col_idx, double* 
       download(split, g->split.p, static_cast<size_t>(g->n), s);
     }
   });
+}
+
+// ---- host datasets and their files (dataset.cpp:152-280) --------------
+int ggb_dataset_load(const char* edges, const char* features, const char* labels, const char* split,
+                     ggb_dataset_t* out) {
+  return guard([&] {
+    require(edges && features && labels && split && out, "dataset_load: null argument");
+    auto d = std::make_unique<ggb_dataset_s>();
+    static_cast<HostDataset&>(*d) = load_dataset(edges, features, labels, split, &d->uv);
+    *out = d.release();
+  });
+}
+
+int ggb_dataset_generate_synthetic(int64_t n, double avg_degree, int64_t d_in, int64_t n_classes, uint64_t seed,
+                                   ggb_dataset_t* out) {
+  return guard([&] {
+    require(out != nullptr, "dataset: null handle slot");
+    auto d = std::make_unique<ggb_dataset_s>();
+    static_cast<HostDataset&>(*d) = generate_synthetic(n, avg_degree, d_in, n_classes, seed);
+    d->uv = synthetic_edges(n, avg_degree, seed);
+    *out = d.release();
+  });
+}
+
+int ggb_dataset_info(ggb_dataset_t d, int64_t* info) {
+  return guard([&] {
+    require(d && info, "dataset_info: null argument");
+    info[0] = d->n;
+    info[1] = static_cast<int64_t>(d->adj.col.size());
+    info[2] = d->d_in;
+    info[3] = d->n_classes;
+    info[4] = static_cast<int64_t>(d->uv.size() / 2);
+  });
+}
+
+int ggb_dataset_export(ggb_dataset_t d, int64_t* row_ptr, int64_t* col_idx, double* values, float* features,
+                       int32_t* labels, uint8_t* split, int64_t* edges_uv) {
+  return guard([&] {
+    require(d != nullptr, "dataset_export: null dataset");
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst) std::copy(v.begin(), v.end(), dst);
+    };
+    cp(row_ptr, d->adj.row_ptr);
+    cp(col_idx, d->adj.col);
+    cp(values, d->adj.val);
+    cp(features, d->features);
+    cp(labels, d->labels);
+    cp(split, d->split);
+    cp(edges_uv, d->uv);
+  });
+}
+
+int ggb_dataset_save(ggb_dataset_t d, const char* edges, const char* features, const char* labels,
+                     const char* split) {
+  return guard([&] {
+    require(d != nullptr, "dataset_save: null dataset");
+    if (edges) save_edge_list(edges, d->uv.data(), static_cast<int64_t>(d->uv.size() / 2));
+    if (features) save_features(features, d->n, d->d_in, d->features.data());
+    if (labels) save_labels(labels, d->n, d->n_classes, d->labels.data());
+    if (split) save_split(split, d->n, d->split.data());
+  });
+}
+
+int ggb_graph_from_dataset(ggb_ctx_t ctx, ggb_dataset_t d, int32_t layers, ggb_graph_t* out) {
+  return guard([&] {
+    require(d && out, "graph_from_dataset: null argument");
+    use_device(*ctx);
+    auto g = std::make_unique<ggb_graph_s>();
+    graph_build(*ctx, *g, d->n, d->adj.row_ptr.data(), d->adj.col.data(), d->adj.val.data(), true, d->d_in,
+                d->features.data(), d->n_classes, d->labels.data(), layers);
+    set_split(*g, d->split.data());
+    *out = g.release();
+  });
+}
+
+int ggb_dataset_destroy(ggb_dataset_t d) {
+  return guard([&] { delete d; });
 }
 
 int ggb_graph_set_split(ggb_graph_t g, const uint8_t* split) {

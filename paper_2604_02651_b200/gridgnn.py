@@ -291,6 +291,58 @@ class Graph:
 
 
 @dataclass
+class Dataset:
+    """Host Dataset (dataset.hpp:16-29) with its raw edge list: the reference's
+    file formats (load_dataset / save_*, dataset.cpp:152-280) and generator.
+    No GPU needed except for to_graph."""
+
+    def __init__(self, h):
+        self.h = h
+        info = np.zeros(5, np.int64)
+        check(lib().ggb_dataset_info(h, _ptr(info)))
+        self.n, self.nnz, self.d_in, self.n_classes, self.n_edges = (int(x) for x in info)
+
+    @staticmethod
+    def load(edges, features, labels, split) -> "Dataset":
+        h = P()
+        check(lib().ggb_dataset_load(*(str(x).encode() for x in (edges, features, labels, split)), C.byref(h)))
+        return Dataset(h)
+
+    @staticmethod
+    def generate_synthetic(n: int, avg_degree: float, d_in: int, n_classes: int, seed: int) -> "Dataset":
+        h = P()
+        check(lib().ggb_dataset_generate_synthetic(n, avg_degree, d_in, n_classes, seed, C.byref(h)))
+        return Dataset(h)
+
+    def save(self, edges=None, features=None, labels=None, split=None) -> None:
+        enc = lambda x: None if x is None else str(x).encode()
+        check(lib().ggb_dataset_save(self.h, enc(edges), enc(features), enc(labels), enc(split)))
+
+    def arrays(self):
+        """((row_ptr, col_idx, values), features, labels, split, edges_uv)"""
+        rp, ci, va = np.empty(self.n + 1, np.int64), np.empty(self.nnz, np.int64), np.empty(self.nnz, np.float64)
+        fe, la, sp = np.empty((self.n, self.d_in), np.float32), np.empty(self.n, np.int32), np.empty(self.n, np.uint8)
+        uv = np.empty((self.n_edges, 2), np.int64)
+        check(lib().ggb_dataset_export(self.h, _ptr(rp), _ptr(ci), _ptr(va), _ptr(fe), _ptr(la), _ptr(sp), _ptr(uv)))
+        return (rp, ci, va), fe, la, sp, uv
+
+    def to_graph(self, ctx: "Context", layers: int) -> "Graph":
+        h = P()
+        check(lib().ggb_graph_from_dataset(ctx.h, self.h, layers, C.byref(h)))
+        return Graph(ctx, h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().ggb_dataset_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Csr:
     n_rows: int
     n_cols: int

@@ -233,3 +233,19 @@ def test_device_generated_graph_trains_like_host_graph(gg, orc):
         la = gg.train_step(ctx, sa, ba, gg.FP32, 1, t)
         lb = gg.train_step(ctx, sb, bb, gg.FP32, 1, t)
         assert abs(la - lb) <= 1e-5 * abs(la)
+
+
+def test_graph_from_dataset_files(gg, orc, tmp_path):
+    """a graph built from the reference's files (load_dataset)
+    samples the same batches as one built from the in-memory dataset."""
+    n, deg, d_in, ncls, seed = 4000, 8.0, 12, 5, 9
+    p = [tmp_path / f"d.{e}" for e in ("edges", "sgnf", "sgnl", "sgns")]
+    gg.Dataset.generate_synthetic(n, deg, d_in, ncls, seed).save(*p)
+    ctx = gg.Context()
+    g_file = gg.Dataset.load(*p).to_graph(ctx, 3)
+    ds = orc.generate_synthetic(n, deg, d_in, ncls, seed)
+    g_mem = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls, 3)
+    a, b = gg.build_step_batch(ctx, g_file, 1000, 3, 2), gg.build_step_batch(ctx, g_mem, 1000, 3, 2)
+    assert np.array_equal(a.a(0).col_idx, b.a(0).col_idx)
+    assert np.array_equal(a.a(0).values.view(np.uint64), b.a(0).values.view(np.uint64))
+    assert np.array_equal(a.x_in[1], b.x_in[1]) and np.array_equal(a.labels, b.labels)
