@@ -290,7 +290,6 @@ class Graph:
             pass
 
 
-@dataclass
 class Dataset:
     """Host Dataset (dataset.hpp:16-29) with its raw edge list: the reference's
     file formats (load_dataset / save_*, dataset.cpp:152-280) and generator.
@@ -343,6 +342,7 @@ class Dataset:
             pass
 
 
+@dataclass
 class Csr:
     n_rows: int
     n_cols: int
