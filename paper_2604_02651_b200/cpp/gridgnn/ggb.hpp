@@ -147,9 +147,69 @@ inline SampleSet sample_vertices(RankComm& rc, index_t n, index_t b, std::uint64
   return s;
 }
 
+/// Host Dataset (dataset.hpp:16-29) with the reference's file formats
+/// (load_dataset / save_*, dataset.cpp:152-280) and generator; no GPU needed.
+class Dataset {
+ public:
+  explicit Dataset(ggb_dataset_t h) : h_(h) {}
+  Dataset(Dataset&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  Dataset(const Dataset&) = delete;
+  Dataset& operator=(const Dataset&) = delete;
+  ~Dataset() {
+    if (h_) ggb_dataset_destroy(h_);
+  }
+  /// save_edge_list + save_features + save_labels + save_split (the CLI's gen output)
+  void save(const std::string& edges, const std::string& features, const std::string& labels,
+            const std::string& split) const {
+    detail::check(ggb_dataset_save(h_, edges.c_str(), features.c_str(), labels.c_str(), split.c_str()));
+  }
+  index_t n() const { return info(0); }
+  index_t nnz() const { return info(1); }
+  index_t d_in() const { return info(2); }
+  index_t n_classes() const { return info(3); }
+  ggb_dataset_t handle() const { return h_; }
+
+ private:
+  index_t info(int k) const {
+    index_t v[5];
+    detail::check(ggb_dataset_info(h_, v));
+    return v[k];
+  }
+  ggb_dataset_t h_ = nullptr;
+};
+
+/// load_dataset (dataset.cpp:178-239): the same files, validation and messages.
+inline Dataset load_dataset(const std::string& graph_path, const std::string& feature_path,
+                            const std::string& label_path, const std::string& split_path) {
+  ggb_dataset_t h = nullptr;
+  detail::check(ggb_dataset_load(graph_path.c_str(), feature_path.c_str(), label_path.c_str(), split_path.c_str(), &h));
+  return Dataset(h);
+}
+
+/// generate_synthetic (dataset.cpp:85-131) on the host, bit-identical.
+inline Dataset generate_synthetic(index_t n, double avg_degree, index_t d_in, index_t n_classes, std::uint64_t seed) {
+  ggb_dataset_t h = nullptr;
+  detail::check(ggb_dataset_generate_synthetic(n, avg_degree, d_in, n_classes, seed, &h));
+  return Dataset(h);
+}
+
 /// Dataset + RankContext resident in HBM (dataset.hpp:16-29, model.hpp:212-234).
 class DeviceDataset {
  public:
+  /// make_rank_context from a host Dataset (its split tags included).
+  DeviceDataset(RankComm& rc, const Dataset& ds, int layers) {
+    detail::check(ggb_graph_from_dataset(rc.handle(), ds.handle(), layers, &h_));
+  }
+  /// generate_synthetic built on the GPU.
+  static DeviceDataset generate_on_device(RankComm& rc, index_t n, double avg_degree, index_t d_in,
+                                          index_t n_classes, std::uint64_t seed, int layers) {
+    ggb_graph_t h = nullptr;
+    detail::check(ggb_graph_generate_synthetic_device(rc.handle(), n, avg_degree, d_in, n_classes, seed, layers, &h));
+    return DeviceDataset(h);
+  }
+  DeviceDataset(DeviceDataset&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  /// keep the features in host memory, as the reference's Dataset does
+  void features_to_host() { detail::check(ggb_graph_features_to_host(h_)); }
   DeviceDataset(RankComm& rc, const CsrMatrix& adjacency, index_t d_in, const std::vector<float>& features,
                 index_t n_classes, const std::vector<std::int32_t>& labels, int layers, bool symmetric = true,
                 const std::vector<SplitTag>* split = nullptr) {
@@ -178,8 +238,9 @@ class DeviceDataset {
   index_t nnz() const { return info(1); }
 
  private:
+  explicit DeviceDataset(ggb_graph_t h) : h_(h) {}
   index_t info(int k) const {
-    index_t v[6];
+    index_t v[7];
     detail::check(ggb_graph_info(h_, v));
     return v[k];
   }

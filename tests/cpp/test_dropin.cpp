@@ -64,11 +64,13 @@ int main() {
   {
     bool ok = true;
     const int dims[4] = {1, 2, 2, 2};
-    for (int rank = 0; rank < 8; ++rank) {
-      RankComm vr(DeviceGrid(1, 2, 2, 2), rank);
-      DeviceDataset ds(vr, n, 16.0, 12, 6, 7, layers);  // native generator, bit-identical
+    for (int rank = 0; rank < 16; ++rank) {
+      RankComm vr(DeviceGrid(1, 2, 2, 2), rank % 8);
+      // ranks 0-7: native host generator; 8-15: built on the GPU with device shard cuts
+      DeviceDataset ds = rank < 8 ? DeviceDataset(vr, n, 16.0, 12, 6, 7, layers)
+                                  : DeviceDataset::generate_on_device(vr, n, 16.0, 12, 6, 7, layers);
       StepBatch sb = build_step_batch(vr, ds, b, 11, 3);
-      void* rb = ref_step_batch(rds, dims, rank, layers, b, 11, 3);
+      void* rb = ref_step_batch(rds, dims, rank % 8, layers, b, 11, 3);
       for (int p = 0; p < 3; ++p)
         for (int t = 0; t < 2; ++t) {
           index_t d[7];
@@ -84,7 +86,8 @@ int main() {
         }
       ref_batch_free(rb);
     }
-    report(2, "shard assembly bit-exact (2x2x2, 8 ranks)", ok, "a_loc and a_t_loc, fp64 values");
+    report(2, "shard assembly bit-exact (2x2x2, 8 ranks)", ok,
+           "a_loc and a_t_loc, fp64 values; host- and device-built graphs");
   }
 
   // 3. train_run losses track the reference (1x1x1x1, Adam, 6 steps)
