@@ -14,6 +14,7 @@
 #include <array>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -476,6 +477,34 @@ struct TrainReport {
   double final_val_acc() const { return epochs.empty() ? 0.0 : epochs.back().val_acc; }
   double final_test_acc() const { return epochs.empty() ? 0.0 : epochs.back().test_acc; }
 };
+
+/// metrics_csv_string / write_metrics_csv (metrics.cpp:10-32): the same
+/// fixed columns and exact (%.17g) number formatting.
+inline std::string metrics_csv_string(const TrainReport& report) {
+  std::string out =
+      "epoch,step,loss,train_acc,val_acc,test_acc,t_sample_ms,t_fwd_ms,t_bwd_ms,"
+      "t_dpsync_ms,bytes_x,bytes_y,bytes_z,bytes_d\n";
+  char buf[512];
+  for (const auto& e : report.epochs) {
+    std::snprintf(buf, sizeof(buf),
+                  "%d,%lld,%.17g,%.17g,%.17g,%.17g,%.3f,%.3f,%.3f,%.3f,%llu,%llu,%llu,%llu\n", e.epoch,
+                  static_cast<long long>(e.step), e.loss, e.train_acc, e.val_acc, e.test_acc, e.t_sample_ms,
+                  e.t_fwd_ms, e.t_bwd_ms, e.t_dpsync_ms, static_cast<unsigned long long>(e.bytes_x),
+                  static_cast<unsigned long long>(e.bytes_y), static_cast<unsigned long long>(e.bytes_z),
+                  static_cast<unsigned long long>(e.bytes_d));
+    out += buf;
+  }
+  return out;
+}
+
+inline void write_metrics_csv(const std::string& path, const TrainReport& report) {
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw std::runtime_error("cannot open metrics file for writing: " + path);
+  const std::string s = metrics_csv_string(report);
+  const bool ok = std::fwrite(s.data(), 1, s.size(), f) == s.size();
+  std::fclose(f);
+  if (!ok) throw std::runtime_error("failed writing metrics file: " + path);
+}
 
 /// train_run of one rank (model.hpp:588-747; the reference runs one thread per
 /// rank, here one process per GPU): S = steps_per_epoch steps per epoch, per

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Acceptance-style checks of the C++ drop-in (paper_2604_02651_b200/cpp/gridgnn/ggb.hpp),
 // written like the reference's acceptance.cpp: one PASS/FAIL line per
 // check, exit status = number of failures. The reference-side answers come
@@ -128,7 +129,11 @@ int main() {
     double dev = 0.0;
     for (int s = 0; s < 3; ++s)
       dev = std::max(dev, std::abs(acc[s] - static_cast<double>(counts[s]) / static_cast<double>(counts[3 + s])));
-    report(5, "full-graph eval accuracy vs reference", dev <= 5e-3 && rep.epochs.size() == 2,
+    // metrics.cpp:10-32 format: header + one row per epoch
+    const std::string csv = metrics_csv_string(rep);
+    const bool csv_ok = csv.rfind("epoch,step,loss,train_acc,val_acc,test_acc,", 0) == 0 &&
+                        std::count(csv.begin(), csv.end(), '\n') == 3;
+    report(5, "full-graph eval accuracy vs reference", dev <= 5e-3 && rep.epochs.size() == 2 && csv_ok,
            "max |acc diff| " + std::to_string(dev) + ", test acc " + std::to_string(last.test_acc));
   }
   ref_dataset_free(rds);
