@@ -284,13 +284,12 @@ def main():
     for _ in range(args.warmup):
         step(gstep, False)
         gstep += 1
-    # ---- timed region: device-resident inputs, loss stays on the device
+    # ---- timed region: device-resident inputs, loss stays on the device; no
+    # per-kernel event timing inside it (host-bound configurations would pay for it)
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.1)
     barrier()
-    ctx.profile(True)
-    ctx.profile_read(reset=True)
     c0 = ctx.counters()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -305,9 +304,19 @@ def main():
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     step_ms = [round((marks[i - 1] if i else ev0).elapsed_time(marks[i]), 3) for i in range(len(marks))]
     c1 = ctx.counters()
+    clk = clocks.stop()
+    # ---- the same steps again with the library's per-kernel-class CUDA events
+    # (live roofline and breakdown; the breakdown steps are not in `value`)
+    prof_steps = max(2, min(args.steps, 10))
+    barrier()
+    ctx.profile(True)
+    ctx.profile_read(reset=True)
+    for _ in range(prof_steps):
+        step(gstep, False)
+        gstep += 1
+    barrier()
     prof = ctx.profile_read(reset=True)
     ctx.profile(False)
-    clk = clocks.stop()
     # ---- per-epoch full-graph evaluation (train_run's evaluate_full_graph), timed
     # separately: the reference's epoch time excludes it; it is the
     # paper's full-graph inference metric
@@ -404,10 +413,10 @@ def main():
             roof["traffic_source"] = {k: tr[k] for k in ("kernel", "us", "dram_TBps", "source")}
     except Exception:
         pass
-    breakdown = {k: {"ms_per_step": v["ms"] / args.steps,
+    breakdown = {k: {"ms_per_step": v["ms"] / prof_steps,
                      "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
                      "TFLOP_per_s": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None,
-                     "launches_per_step": v["launches"] / args.steps}
+                     "launches_per_step": v["launches"] / prof_steps}
                  for k, v in kernels.items()}
     out = {
         "metric": "epoch_time_s",
@@ -436,6 +445,8 @@ def main():
         "sampled_vertices_per_s": b * gd * 1000.0 / ms_step,
         "roofline": roof,
         "kernels": breakdown,
+        "kernels_note": f"per-kernel-class CUDA events over {prof_steps} further steps run after the timed "
+                        "region (the timed steps carry no per-kernel events)",
         "e2e": {"value": S * ms_e2e / args.steps / 1000.0, "unit": "s",
                 "h2d_bytes_per_step": (c2["h2d_bytes"] - c1e["h2d_bytes"]) / args.steps,
                 "d2h_bytes_per_step": (c2["d2h_bytes"] - c1e["d2h_bytes"]) / args.steps,
