@@ -174,6 +174,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--grid", default=None, help="GdxGxxGyxGz (default: data-parallel Gd = N)")
     ap.add_argument("--compute", default="accurate", choices=["accurate", "fast"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16comm"],
+                    help="PMM all-reduce wire: the reference's Precision::kFp32 or kBf16Roundtrip (comm.hpp:22)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-eval", action="store_true", help="skip the separately timed full-graph evaluation")
     ap.add_argument("--prefetch", type=int, default=1,
@@ -251,6 +253,7 @@ def main():
                           dropout_rate=DROPOUT)
     st = gg.init_state(ctx, mcfg, RUN_SEED, gg.COMPUTE_ACCURATE if args.compute == "accurate" else gg.COMPUTE_FAST)
     group_seed = gg.hash_combine(RUN_SEED, grid.dp_group(rank))
+    prec = gg.FP32 if args.precision == "fp32" else gg.BF16_WIRE
     batch = None
     # sampling of step t+1 overlaps training of step t (producer thread + own stream)
     # (--prefetch 2 also hashes the next step's dropout masks on that stream)
@@ -263,7 +266,7 @@ def main():
             batch = pf.next()
         else:
             batch = gg.build_step_batch(ctx, graph, b, group_seed, gstep, reuse=batch)
-        loss = gg.train_step(ctx, st, batch, gg.FP32, RUN_SEED, gstep, sync_loss=sync_loss)
+        loss = gg.train_step(ctx, st, batch, prec, RUN_SEED, gstep, sync_loss=sync_loss)
         gg.dp_sync(ctx, st)
         gg.optimizer_step(ctx, st, gg.ADAM, LR)
         return loss
@@ -435,7 +438,7 @@ def main():
             "workload": cfg["workload"], "config_id": args.config, "global_batch": cfg["batch"],
             "batch_per_dp_group": b, "steps_per_epoch": S, "grid": "x".join(map(str, dims)),
             "layers": cfg["layers"], "hidden": cfg["d_h"], "d_in": cfg["d_in"], "classes": cfg["n_classes"],
-            "n_vertices": cfg["n"], "nnz": graph.nnz, "compute": args.compute,
+            "n_vertices": cfg["n"], "nnz": graph.nnz, "compute": args.compute, "precision": args.precision,
             "prefetch": ["off", "sampling", "sampling+dropout masks"][args.prefetch],
             "l2": "inputs larger than L2 (graph %.1f GB + features resident in HBM; random gathers)" %
                   (graph.device_bytes / 1e9),

@@ -1,4 +1,5 @@
 #include "comm.hpp"
+#include "prof.hpp"
 
 #include <nccl.h>
 
@@ -70,6 +71,25 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
     GGB_NCCL(ncclCommSplit(world, colour, co[a], &sub, nullptr));
     if (grid.dims[a] > 1) c->axis[a] = sub;
   }
+  // NCCL connects point-to-point peers lazily, on their first send/recv; the
+  // reshard's block permutation meets new peer pairs in later steps, so one
+  // tiny exchange with every peer here keeps that setup (tens of ms) out of
+  // the training steps
+  const int n = grid.total();
+  if (n > 1) {
+    float* buf = nullptr;
+    GGB_CUDA(cudaMalloc(&buf, sizeof(float) * 2 * n));
+    GGB_CUDA(cudaMemset(buf, 0, sizeof(float) * 2 * n));
+    GGB_NCCL(ncclGroupStart());
+    for (int p = 0; p < n; ++p) {
+      if (p == rank) continue;
+      GGB_NCCL(ncclSend(buf + p, 1, ncclFloat32, p, world, nullptr));
+      GGB_NCCL(ncclRecv(buf + n + p, 1, ncclFloat32, p, world, nullptr));
+    }
+    GGB_NCCL(ncclGroupEnd());
+    GGB_CUDA(cudaDeviceSynchronize());
+    GGB_CUDA(cudaFree(buf));
+  }
   return c;
 }
 
@@ -77,6 +97,9 @@ void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wir
   if (trivial(ctx, axis) || count <= 0) return;
   need(ctx, axis);
   Comm& c = *ctx.comm;
+  const int gg = c.size[axis];
+  // bytes one rank sends: ring all-reduce 2(g-1)/g of the fp32 buffer; bf16 wire: its bf16 contribution to g-1 peers
+  ProfScope ps(ctx, kProfComm, bf16_wire ? 2.0 * count * (gg - 1) : 2.0 * (gg - 1) / gg * count * 4);
   if (!bf16_wire) {
     GGB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum,
                            as_nccl(c.axis[axis]), ctx.stream));
@@ -126,6 +149,7 @@ void exchange_blocks(Ctx& ctx, const std::vector<BlockXfer>& sends, const std::v
   int64_t ns = 0, nr = 0;
   for (const auto& x : sends) ns += x.rows * x.cols;
   for (const auto& x : recvs) nr += x.rows * x.cols;
+  ProfScope ps(ctx, kProfComm, 4.0 * ns);
   float* sbuf = c.wire.reserve_n<float>(static_cast<size_t>(std::max<int64_t>(ns, 1)));
   float* rbuf = c.gather.reserve_n<float>(static_cast<size_t>(std::max<int64_t>(nr, 1)));
   int64_t off = 0;

@@ -70,12 +70,15 @@ struct ProfScope {
     a = p->get();
     GGB_CUDA(cudaEventRecord(a, ctx.stream));
   }
-  ~ProfScope() {
+  /// close the timed range early (e.g. before a collective timed on its own)
+  void end() {
     if (!p) return;
     cudaEvent_t b = p->get();
     cudaEventRecord(b, ctx.stream);
     p->marks.push_back({cat, a, b, bytes, flops});
+    p = nullptr;
   }
+  ~ProfScope() { end(); }
 };
 
 // Synchronizes the stream and folds the recorded marks into the totals.

@@ -320,6 +320,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
                      nullptr, 0, 0);
       else
         spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), L.hagg.f, L.hagg.ldf, nullptr, 0, 0);
+      ps.end();
       all_reduce_sum(ctx, alay.col, L.hagg.f, hb.rows() * L.hagg.ldf, wire);
       if (accurate)
         cast_split(ctx, L.hagg.f, hb.rows(), hb.cols(), L.hagg.ldf, L.hagg.b, L.hagg.lo, L.hagg.ldb);
@@ -608,6 +609,7 @@ void backward(State& st, const Batch& bt, int precision) {
     if (ar_d) {
       float* dhf = grow<float>(st.dhagg_f, rows * hc);
       gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, dhf, hc, nullptr, 0);
+      ps.end();
       all_reduce_sum(ctx, xb.lay.col, dhf, rows * hc, wire);
       cast_bf16(ctx, dhf, rows, hc, hc, dhb, ldhb);
     } else {
@@ -644,6 +646,7 @@ void backward(State& st, const Batch& bt, int precision) {
       float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
                nd, ld8(F.cols()), nullptr, 0, 0);
+      ps.end();
       if (ar_s) all_reduce_sum(ctx, alay.row, nd, F.rows() * ld8(F.cols()), wire);
       if (dres) add_inplace(ctx, nd, ld8(F.cols()), dres, ld8(F.cols()), F.rows(), F.cols());
       std::swap(st.dxh, st.dxh2);
@@ -694,7 +697,6 @@ void backward(State& st, const Batch& bt, int precision) {
 void dp_sync(State& st) {
   Ctx& ctx = *st.ctx;
   const int gd = ctx.grid.dims[0];
-  ProfScope ps(ctx, kProfComm, gd > 1 ? 2.0 * (gd - 1) / gd * st.total * 4 : 0.0);
   all_reduce_sum(ctx, kD, st.G.as<float>(), st.total, false);
   if (gd > 1) scale(ctx, st.G.as<float>(), st.total, 1.0f / static_cast<float>(gd));
 }
