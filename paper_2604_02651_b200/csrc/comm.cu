@@ -3,6 +3,8 @@
 
 #include <nccl.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace ggb {
@@ -32,6 +34,25 @@ __global__ void k_ordered_sum_bf16(const bf16* __restrict__ parts, int g, int64_
 
 ncclComm_t as_nccl(void* p) { return static_cast<ncclComm_t>(p); }
 
+// CTAs of an axis collective = SMs the persistent kernels leave it while overlapped
+int comm_ctas() {
+  static int v = [] {
+    const char* e = std::getenv("GGB_COMM_CTAS");
+    const int c = e ? std::atoi(e) : 16;
+    return c >= 1 && c <= 64 ? c : 16;
+  }();
+  return v;
+}
+
+int comm_chunks() {
+  static int v = [] {
+    const char* e = std::getenv("GGB_COMM_CHUNKS");
+    const int c = e ? std::atoi(e) : 1;
+    return c >= 1 && c <= 16 ? c : 1;
+  }();
+  return v;
+}
+
 void need(const Ctx& ctx, int axis) {
   if (!ctx.comm || !ctx.comm->axis[axis])
     fail(GGB_ECONTRACT, "collective over a multi-rank group on a context without communicators");
@@ -40,6 +61,8 @@ void need(const Ctx& ctx, int axis) {
 }  // namespace
 
 Comm::~Comm() {
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (cstream) cudaStreamDestroy(cstream);
   for (auto& a : axis)
     if (a) ncclCommDestroy(as_nccl(a));
   if (world) ncclCommDestroy(as_nccl(world));
@@ -68,7 +91,11 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
     // every rank takes part in every split (ncclCommSplit is collective on world)
     ncclComm_t sub = nullptr;
     const int colour = grid.dims[a] > 1 ? grid.group_id(a, rank) : NCCL_SPLIT_NOCOLOR;
-    GGB_NCCL(ncclCommSplit(world, colour, co[a], &sub, nullptr));
+    // axis collectives run beside the persistent kernels (pipelined_all_reduce):
+    // a bounded CTA count, matching the SMs those kernels leave free
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    if (comm_chunks() > 1) cfg.maxCTAs = comm_ctas();
+    GGB_NCCL(ncclCommSplit(world, colour, co[a], &sub, &cfg));
     if (grid.dims[a] > 1) c->axis[a] = sub;
   }
   // NCCL connects point-to-point peers lazily, on their first send/recv; the
@@ -93,28 +120,75 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
   return c;
 }
 
-void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire) {
-  if (trivial(ctx, axis) || count <= 0) return;
-  need(ctx, axis);
+namespace {
+void all_reduce_sum_on(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire, cudaStream_t s, DevBuf& wire,
+                       DevBuf& gather) {
   Comm& c = *ctx.comm;
   const int gg = c.size[axis];
   // bytes one rank sends: ring all-reduce 2(g-1)/g of the fp32 buffer; bf16 wire: its bf16 contribution to g-1 peers
-  ProfScope ps(ctx, kProfComm, bf16_wire ? 2.0 * count * (gg - 1) : 2.0 * (gg - 1) / gg * count * 4);
+  ProfScope ps(ctx, kProfComm, bf16_wire ? 2.0 * count * (gg - 1) : 2.0 * (gg - 1) / gg * count * 4, 0, s);
   if (!bf16_wire) {
-    GGB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum,
-                           as_nccl(c.axis[axis]), ctx.stream));
+    GGB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum, as_nccl(c.axis[axis]), s));
     return;
   }
-  const int g = c.size[axis];
-  bf16* mine = c.wire.reserve_n<bf16>(static_cast<size_t>(count));
-  bf16* all = c.gather.reserve_n<bf16>(static_cast<size_t>(count) * g);
+  bf16* mine = wire.reserve_n<bf16>(static_cast<size_t>(count));
+  bf16* all = gather.reserve_n<bf16>(static_cast<size_t>(count) * gg);
   const unsigned blocks = static_cast<unsigned>(ceil_div(count, 256));
-  k_to_bf16<<<blocks, 256, 0, ctx.stream>>>(buf, count, mine);
-  GGB_NCCL(ncclAllGather(mine, all, static_cast<size_t>(count), ncclBfloat16, as_nccl(c.axis[axis]),
-                         ctx.stream));
-  k_ordered_sum_bf16<<<blocks, 256, 0, ctx.stream>>>(all, g, count, buf);
+  k_to_bf16<<<blocks, 256, 0, s>>>(buf, count, mine);
+  GGB_NCCL(ncclAllGather(mine, all, static_cast<size_t>(count), ncclBfloat16, as_nccl(c.axis[axis]), s));
+  k_ordered_sum_bf16<<<blocks, 256, 0, s>>>(all, gg, count, buf);
   GGB_LAUNCH_CHECK();
   ctx.launches += 2;
+}
+}  // namespace
+
+void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire) {
+  if (trivial(ctx, axis) || count <= 0) return;
+  need(ctx, axis);
+  all_reduce_sum_on(ctx, axis, buf, count, bf16_wire, ctx.stream, ctx.comm->wire, ctx.comm->gather);
+}
+
+void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, float* buf, int64_t ld, bool bf16_wire,
+                          const std::function<void(int64_t, int64_t)>& produce,
+                          const std::function<void(int64_t, int64_t)>& after) {
+  const int K = comm_chunks();
+  if (trivial(ctx, axis) || rows <= 0 || K <= 1 || rows < 2 * quantum) {
+    produce(0, rows);
+    all_reduce_sum(ctx, axis, buf, rows * ld, bf16_wire);
+    if (after) after(0, rows);
+    return;
+  }
+  need(ctx, axis);
+  Comm& c = *ctx.comm;
+  if (!c.cstream) {
+    int lo = 0, hi = 0;
+    GGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GGB_CUDA(cudaStreamCreateWithPriority(&c.cstream, cudaStreamNonBlocking, hi));
+  }
+  while (static_cast<int>(c.ev.size()) < K + 1) {
+    cudaEvent_t e;
+    GGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.ev.push_back(e);
+  }
+  const int64_t per = round_up(ceil_div(rows, K), quantum);
+  ctx.sm_reserve = comm_ctas();
+  int k = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += per, ++k) {
+    const int64_t r1 = std::min(rows, r0 + per);
+    produce(r0, r1);
+    GGB_CUDA(cudaEventRecord(c.ev[k], ctx.stream));
+    GGB_CUDA(cudaStreamWaitEvent(c.cstream, c.ev[k], 0));
+    all_reduce_sum_on(ctx, axis, buf + r0 * ld, (r1 - r0) * ld, bf16_wire, c.cstream, c.wire2, c.gather2);
+    if (after) {
+      cudaStream_t saved = ctx.stream;  // the post-processing runs on the communication stream
+      ctx.stream = c.cstream;
+      after(r0, r1);
+      ctx.stream = saved;
+    }
+  }
+  ctx.sm_reserve = 0;
+  GGB_CUDA(cudaEventRecord(c.ev[K], c.cstream));
+  GGB_CUDA(cudaStreamWaitEvent(ctx.stream, c.ev[K], 0));
 }
 
 void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count) {

@@ -4,6 +4,8 @@
 // comm.hpp:209-214). Singleton groups are free and need no communicator.
 #pragma once
 
+#include <functional>
+
 #include "runtime.hpp"
 
 namespace ggb {
@@ -15,6 +17,10 @@ struct Comm {
   int pos[4] = {0, 0, 0, 0};  // coordinate on the axis
   DevBuf gather;             // all-gather staging
   DevBuf wire;               // bf16 wire staging
+  // pipelined collectives: their own stream, staging and events
+  cudaStream_t cstream = nullptr;
+  DevBuf gather2, wire2;
+  std::vector<cudaEvent_t> ev;
   ~Comm();
 };
 
@@ -27,6 +33,20 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
 // reproduced exactly by an all-gather of bf16 contributions.
 void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire);
 void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count);
+// Row-chunked overlap of a producer and its all-reduce: chunk k
+// of `rows` rows (row stride ld floats of buf) is produced on the compute
+// stream by produce(r0, r1), then all-reduced along `axis` on the
+// communication stream — and post-processed there by after(r0, r1) — while
+// chunk k+1 is produced. Chunk bounds are multiples of `quantum` rows. The
+// persistent kernels leave SMs free for the collective meanwhile. The compute
+// stream waits for the last chunk before returning. Same result as producing
+// everything, then one all-reduce (per-element sums are unchanged).
+// GGB_COMM_CHUNKS (default 1: produce everything, then one all-reduce) sets
+// the chunk count; measured on 4 B200 at C3 the chunked form is slower
+// (DESIGN.md), so it is off by default.
+void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, float* buf, int64_t ld, bool bf16_wire,
+                          const std::function<void(int64_t, int64_t)>& produce,
+                          const std::function<void(int64_t, int64_t)>& after = {});
 void all_reduce_u64(Ctx& ctx, int axis, uint64_t* buf, int64_t count);  // exact integer sum
 // Gathers `count` floats from every member of the axis group into out
 // ([size][count], axis order).

@@ -709,7 +709,7 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
     attr = true;
   }
   const int64_t tiles = ceil_div(m, kBM) * ga.n_tiles;
-  const int grid = static_cast<int>(std::min<int64_t>(tiles, sm_count()));
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, std::min(sm_count(), ctx.persistent_sms())));
   k_gemm_kmajor<<<grid, kThreads, smem, ctx.stream>>>(ta, tb, tal, tbl, tc, tcb, tcl, ga);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;

@@ -63,18 +63,20 @@ struct ProfScope {
   int cat;
   cudaEvent_t a = nullptr;
   double bytes, flops;
-  ProfScope(Ctx& c, int cat_, double bytes_ = 0, double flops_ = 0) : ctx(c), cat(cat_), bytes(bytes_), flops(flops_) {
+  cudaStream_t s;  // the stream the range is timed on (the context's unless given)
+  ProfScope(Ctx& c, int cat_, double bytes_ = 0, double flops_ = 0, cudaStream_t stream = nullptr)
+      : ctx(c), cat(cat_), bytes(bytes_), flops(flops_), s(stream ? stream : c.stream) {
     Prof& pr = prof_of(ctx);
     if (!pr.on) return;
     p = &pr;
     a = p->get();
-    GGB_CUDA(cudaEventRecord(a, ctx.stream));
+    GGB_CUDA(cudaEventRecord(a, s));
   }
   /// close the timed range early (e.g. before a collective timed on its own)
   void end() {
     if (!p) return;
     cudaEvent_t b = p->get();
-    cudaEventRecord(b, ctx.stream);
+    cudaEventRecord(b, s);
     p->marks.push_back({cat, a, b, bytes, flops});
     p = nullptr;
   }

@@ -43,6 +43,10 @@ struct Ctx {
   // side-stream context (the prefetcher): launch short non-persistent grids,
   // so compute-stream persistent kernels (one CTA per SM) are not held back
   bool side_stream = false;
+  // SMs left free by the persistent kernels (SpMM pipe, GEMM) while a
+  // collective runs beside them on the communication stream
+  int sm_reserve = 0;
+  int persistent_sms() const { return num_sms - sm_reserve > 0 ? num_sms - sm_reserve : 1; }
   std::unique_ptr<Prof> prof;
   ~Ctx();
 };

@@ -242,7 +242,7 @@ void launch_pipe(Ctx& ctx, const PipeArgs& a) {
     GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  k_spmm_pipe<TIn, RB><<<ctx.num_sms, kWarps * 32, smem, ctx.stream>>>(a);
+  k_spmm_pipe<TIn, RB><<<ctx.persistent_sms(), kWarps * 32, smem, ctx.stream>>>(a);
 }
 
 }  // namespace

@@ -308,25 +308,36 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     } else {
     const int32_t* acol = A.col.as<int32_t>();
     const float* aval = A.val.as<float>();
-    {
-    ProfScope ps(ctx, kProfSpmmFwd,
-                 spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, ar_h ? 4 : (accurate ? 4 : 2)),
-                 2.0 * A.nnz * F.cols());
     if (ar_h) {
+      // partial sums over A's column blocks: row chunks of the SpMM pipelined
+      // with their all-reduce (and the bf16 split of the reduced rows)
       L.hagg.ldf = ld8(hb.cols());
       L.hagg.f = grow<float>(L.hagg_f, hb.rows() * L.hagg.ldf);
-      if (accurate)
-        spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), L.hagg.f, L.hagg.ldf, nullptr,
-                     nullptr, 0, 0);
-      else
-        spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), L.hagg.f, L.hagg.ldf, nullptr, 0, 0);
-      ps.end();
-      all_reduce_sum(ctx, alay.col, L.hagg.f, hb.rows() * L.hagg.ldf, wire);
-      if (accurate)
-        cast_split(ctx, L.hagg.f, hb.rows(), hb.cols(), L.hagg.ldf, L.hagg.b, L.hagg.lo, L.hagg.ldb);
-      else
-        cast_bf16(ctx, L.hagg.f, hb.rows(), hb.cols(), L.hagg.ldf, L.hagg.b, L.hagg.ldb);
-    } else if (accurate) {
+      const int64_t ldf = L.hagg.ldf, ldb = L.hagg.ldb;
+      pipelined_all_reduce(
+          ctx, alay.col, A.n_rows, 128, L.hagg.f, ldf, wire,
+          [&](int64_t r0, int64_t r1) {
+            const double frac = static_cast<double>(r1 - r0) / std::max<int64_t>(A.n_rows, 1);
+            ProfScope ps(ctx, kProfSpmmFwd, frac * spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, 4),
+                         frac * 2.0 * A.nnz * F.cols());
+            if (accurate)
+              spmm_csr_f32(ctx, r1 - r0, arp + r0, acol, aval, prev->f, prev->ldf, F.cols(), L.hagg.f + r0 * ldf,
+                           ldf, nullptr, nullptr, 0, 0);
+            else
+              spmm_csr(ctx, r1 - r0, arp + r0, acol, aval, prev->b, prev->ldb, F.cols(), L.hagg.f + r0 * ldf, ldf,
+                       nullptr, 0, 0);
+          },
+          [&](int64_t r0, int64_t r1) {
+            if (accurate)
+              cast_split(ctx, L.hagg.f + r0 * ldf, r1 - r0, hb.cols(), ldf, L.hagg.b + r0 * ldb, L.hagg.lo + r0 * ldb,
+                         ldb);
+            else
+              cast_bf16(ctx, L.hagg.f + r0 * ldf, r1 - r0, hb.cols(), ldf, L.hagg.b + r0 * ldb, ldb);
+          });
+    } else {
+    ProfScope ps(ctx, kProfSpmmFwd, spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, accurate ? 4 : 2),
+                 2.0 * A.nnz * F.cols());
+    if (accurate) {
       spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), nullptr, 0, L.hagg.b, L.hagg.lo,
                    L.hagg.ldb, 0);
     } else {
@@ -349,8 +360,12 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.xw_t.blk = xb;
     L.xw_t.ldf = ld8(xb.cols());
     L.xw_t.f = grow<float>(L.xw, xb.rows() * L.xw_t.ldf);
-    fwd_gemm(st, xb.rows(), xb.cols(), hb.cols(), L.hagg, w, L.xw_t.f, L.xw_t.ldf, nullptr, 0);
-    all_reduce_sum(ctx, hb.lay.col, L.xw_t.f, xb.rows() * L.xw_t.ldf, wire);
+    pipelined_all_reduce(ctx, hb.lay.col, xb.rows(), 128, L.xw_t.f, L.xw_t.ldf, wire, [&](int64_t r0, int64_t r1) {
+      Tensor sub = L.hagg;
+      sub.b = L.hagg.b + r0 * L.hagg.ldb;
+      sub.lo = L.hagg.lo ? L.hagg.lo + r0 * L.hagg.ldb : nullptr;
+      fwd_gemm(st, r1 - r0, xb.cols(), hb.cols(), sub, w, L.xw_t.f + r0 * L.xw_t.ldf, L.xw_t.ldf, nullptr, 0);
+    });
     // RMSNorm statistics: row sum of squares, all-reduce along the column axis (fp32)
     float* ss = nullptr;
     float* rms = nullptr;
@@ -607,11 +622,16 @@ void backward(State& st, const Batch& bt, int precision) {
     {
     ProfScope ps(ctx, kProfGemmDx, gemm_bytes(rows, hc, cols, 2, 2, ar_d ? 4 : 2), 2.0 * rows * hc * cols);
     if (ar_d) {
-      float* dhf = grow<float>(st.dhagg_f, rows * hc);
-      gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, dhf, hc, nullptr, 0);
       ps.end();
-      all_reduce_sum(ctx, xb.lay.col, dhf, rows * hc, wire);
-      cast_bf16(ctx, dhf, rows, hc, hc, dhb, ldhb);
+      float* dhf = grow<float>(st.dhagg_f, rows * hc);
+      pipelined_all_reduce(
+          ctx, xb.lay.col, rows, 128, dhf, hc, wire,
+          [&](int64_t r0, int64_t r1) {
+            ProfScope pc(ctx, kProfGemmDx, gemm_bytes(r1 - r0, hc, cols, 2, 2, 4), 2.0 * (r1 - r0) * hc * cols);
+            gemm_bf16(ctx, r1 - r0, hc, cols, ba.dxb + r0 * lddxw, lddxw, w.wb.as<bf16>(), w.ldb, dhf + r0 * hc, hc,
+                      nullptr, 0);
+          },
+          [&](int64_t r0, int64_t r1) { cast_bf16(ctx, dhf + r0 * hc, r1 - r0, hc, hc, dhb + r0 * ldhb, ldhb); });
     } else {
       gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, nullptr, 0, dhb, ldhb);
     }
@@ -643,12 +663,22 @@ void backward(State& st, const Batch& bt, int precision) {
                dxh, ld8(F.cols()), outb, ld8(F.cols()), 1);
       dxh_b_ready = emit_b;
     } else {
-      float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
-      spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
-               nd, ld8(F.cols()), nullptr, 0, 0);
       ps.end();
-      if (ar_s) all_reduce_sum(ctx, alay.row, nd, F.rows() * ld8(F.cols()), wire);
-      if (dres) add_inplace(ctx, nd, ld8(F.cols()), dres, ld8(F.cols()), F.rows(), F.cols());
+      float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
+      const int64_t ldn = ld8(F.cols());
+      const int64_t* trp = At.row_ptr.as<int64_t>();
+      // row chunks of the SpMM pipelined with their all-reduce along A.row and the residual add
+      pipelined_all_reduce(
+          ctx, alay.row, At.n_rows, 128, nd, ldn, wire,
+          [&](int64_t r0, int64_t r1) {
+            const double frac = static_cast<double>(r1 - r0) / std::max<int64_t>(At.n_rows, 1);
+            ProfScope pc(ctx, kProfSpmmBwd, frac * spmm_bytes(At.n_rows, At.nnz, hc, 2, 4), frac * 2.0 * At.nnz * hc);
+            spmm_csr(ctx, r1 - r0, trp + r0, At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc, nd + r0 * ldn,
+                     ldn, nullptr, 0, 0);
+          },
+          [&](int64_t r0, int64_t r1) {
+            if (dres) add_inplace(ctx, nd + r0 * ldn, ldn, dres + r0 * ldn, ldn, r1 - r0, F.cols());
+          });
       std::swap(st.dxh, st.dxh2);
       dxh = nd;
     }
