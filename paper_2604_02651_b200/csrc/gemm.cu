@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 struct WgradArgs {
   int M, KW, NW;
   int BN;  // multiple of 64, <= 256
+  int MT;  // m-tiles (128 KW rows each) per CTA: 2 when KW <= 256 (the DY chunk is loaded once for both)
   int n_tiles, m_tiles, splits, chunks_per_split;
   int stages;
   uint32_t tmem_cols;
@@ -440,10 +441,10 @@ __global__ void __launch_bounds__(kWgradThreads, 1)
     k_gemm_wgrad(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmD,
                  const WgradArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = args.stages, BN = args.BN;
-  // A' tile: 128 (KW) x 64 (rows): two 64-col boxes of 64 rows x 128 B
-  const uint32_t bytes_a = kBM * kBK * 2, bytes_b = static_cast<uint32_t>(BN) * kBK * 2;
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int S = args.stages, BN = args.BN, MT = args.MT;
+  // A' tile: MT x 128 (KW) x 64 (rows): 2 MT 64-col boxes of 64 rows x 128 B
+  const uint32_t bytes_a = MT * kBM * kBK * 2, bytes_b = static_cast<uint32_t>(BN) * kBK * 2;
   const uint32_t stage_bytes = bytes_a + bytes_b;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(kWgradThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, split = blockIdx.y;
-  const int mt = tile / args.n_tiles, nt = tile % args.n_tiles;
+  const int mt = (tile / args.n_tiles) * MT, nt = tile % args.n_tiles;  // first m-tile of this CTA
   const int total_chunks = (args.M + kBK - 1) / kBK;
   const int c_begin = split * args.chunks_per_split;
   const int c_end = min(total_chunks, c_begin + args.chunks_per_split);
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(kWgradThreads, 1)
         uint8_t* sa = smem + stage * stage_bytes;
         uint8_t* sb = sa + bytes_a;
         mbar_expect_tx(full + stage, stage_bytes);
-        for (int h = 0; h < kBM / 64; ++h)
+        for (int h = 0; h < MT * kBM / 64; ++h)
           tma_load_2d(sa + h * 8192, &tmX, full + stage, mt * kBM + h * 64, c * kBK);
         for (int h = 0; h < BN / 64; ++h)
           tma_load_2d(sb + h * 8192, &tmD, full + stage, nt * BN + h * 64, c * kBK);
@@ -505,8 +506,9 @@ __global__ void __launch_bounds__(kWgradThreads, 1)
         const uint32_t sb = sa + bytes_a;
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k)  // 16 K-rows = 2 groups of 8 rows x 128 B
-          umma_bf16(tmem_base, sdesc(sa + k * 2048, 8192, 1024), sdesc(sb + k * 2048, 8192, 1024),
-                    idesc, (c != c_begin || k != 0));
+          for (int t = 0; t < MT; ++t)      // m-tile t: accumulator columns [t BN, (t + 1) BN)
+            umma_bf16(tmem_base + static_cast<uint32_t>(t * BN), sdesc(sa + t * 16384 + k * 2048, 8192, 1024),
+                      sdesc(sb + k * 2048, 8192, 1024), idesc, (c != c_begin || k != 0));
         umma_commit(empty + stage);
         if (++stage == S) {
           stage = 0;
@@ -523,21 +525,29 @@ __global__ void __launch_bounds__(kWgradThreads, 1)
       mbar_wait(tfull, 0);
       tc_fence_after();
     }
-    const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;  // KW index
-    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
     float* dst_base = args.part + static_cast<int64_t>(split) * args.KW * args.NW;
-    for (int c16 = 0; c16 < BN; c16 += 16) {
-      float v[16];
-      if (any) {
-        tmem_ld16(taddr + c16, v);
-      } else {
+    for (int t = 0; t < MT; ++t) {
+      const int64_t row = static_cast<int64_t>(mt + t) * kBM + q * 32 + lane;  // KW index
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(t * BN);
+      for (int c16 = 0; c16 < BN; c16 += 16) {
+        float v[16];
+        if (any) {
+          tmem_ld16(taddr + c16, v);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        const int col0 = nt * BN + c16;
+        if (row >= args.KW || col0 >= args.NW) continue;
+        float* dst = dst_base + row * args.NW + col0;
+        if (col0 + 16 <= args.NW && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch)
+            reinterpret_cast<float4*>(dst)[ch] = make_float4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+        } else {
+          for (int i = 0; i < 16 && col0 + i < args.NW; ++i) dst[i] = v[i];
+        }
       }
-      const int col0 = nt * BN + c16;
-      if (row >= args.KW || col0 >= args.NW) continue;
-      float* dst = dst_base + row * args.NW + col0;
-      for (int i = 0; i < 16 && col0 + i < args.NW; ++i) dst[i] = v[i];
     }
     tc_fence_before();
   }
@@ -743,15 +753,19 @@ void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x,
   wa.BN = static_cast<int>(std::min<int64_t>(256, round_up(nw, 64)));
   wa.n_tiles = static_cast<int>(ceil_div(nw, wa.BN));
   wa.m_tiles = static_cast<int>(ceil_div(kw, kBM));
-  const int tiles = wa.m_tiles * wa.n_tiles;
+  wa.MT = wa.m_tiles == 2 ? 2 : 1;  // both m-tiles in one CTA: the DY chunk is read once
+  const int tiles = (wa.m_tiles / wa.MT) * wa.n_tiles;
   const int total_chunks = static_cast<int>(ceil_div(m, kBK));
   int splits = std::max(1, sm_count() / tiles);
   splits = std::min(splits, std::max(1, total_chunks / 4));
+  // the fp32 partials (written, then reduced) stay within a quarter of the operand bytes
+  const double operand_bytes = static_cast<double>(m) * (kw + nw) * 2;
+  splits = std::min<int>(splits, std::max(1, static_cast<int>(operand_bytes / (4.0 * kw * nw * 4))));
   wa.chunks_per_split = static_cast<int>(ceil_div(total_chunks, splits));
   wa.splits = static_cast<int>(ceil_div(total_chunks, wa.chunks_per_split));
-  const int stage_bytes = kBM * kBK * 2 + wa.BN * kBK * 2;
+  const int stage_bytes = wa.MT * kBM * kBK * 2 + wa.BN * kBK * 2;
   wa.stages = std::min(8, (kSmemBudget - 1024 - 256) / stage_bytes);
-  wa.tmem_cols = tmem_cols_for(wa.BN);
+  wa.tmem_cols = tmem_cols_for(wa.MT * wa.BN);
   wa.part = ws.reserve_n<float>(static_cast<size_t>(wa.splits) * kw * nw);
   const CUtensorMap tx = make_tmap(x, m, kw, ldx, 64, kBK);
   const CUtensorMap td = make_tmap(dy, m, nw, lddy, 64, kBK);

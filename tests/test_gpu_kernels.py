@@ -78,6 +78,7 @@ def test_gemm_split_bf16_is_fp32_accurate(env, gg, m, n, k):
 
 
 @pytest.mark.parametrize("m,kw,nw", [(128, 128, 256), (10000, 256, 256), (612, 100, 256), (5000, 256, 47),
+                                     (20000, 200, 256), (153000, 256, 256), (3000, 129, 64),
                                      (333, 16, 16), (64, 8, 5), (20000, 301, 128), (1, 64, 64)])
 def test_gemm_wgrad(env, gg, m, kw, nw):
     ctx, torch = env
