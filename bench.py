@@ -181,6 +181,8 @@ def main():
     ap.add_argument("--prefetch", type=int, default=1,
                     help="1: sample step t+1 on a side stream during step t; 2: also its dropout masks; 0: off")
     ap.add_argument("--ref-steps", type=int, default=2)
+    ap.add_argument("--e2e-device-features", action="store_true",
+                    help="diagnostic: run the e2e loop with the features still in HBM")
     ap.add_argument("--host-features", action="store_true",
                     help="keep the features in pinned host memory for the timed loop too (papers100M-scale HBM budget)")
     args = ap.parse_args()
@@ -354,7 +356,8 @@ def main():
     # resident.
     if pf:
         pf.close()
-    graph.features_to_host()
+    if not args.e2e_device_features:
+        graph.features_to_host()
     pf = (gg.Prefetcher(ctx, graph, b, group_seed, gstep, run_seed=RUN_SEED, cfg=mcfg if args.prefetch == 2 else None)
           if args.prefetch else None)
     batch = None

@@ -171,7 +171,8 @@ void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, flo
     c.ev.push_back(e);
   }
   const int64_t per = round_up(ceil_div(rows, K), quantum);
-  ctx.sm_reserve = comm_ctas();
+  const int saved_reserve = ctx.sm_reserve;
+  ctx.sm_reserve = std::max(saved_reserve, comm_ctas());
   int k = 0;
   for (int64_t r0 = 0; r0 < rows; r0 += per, ++k) {
     const int64_t r1 = std::min(rows, r0 + per);
@@ -186,7 +187,7 @@ void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, flo
       ctx.stream = saved;
     }
   }
-  ctx.sm_reserve = 0;
+  ctx.sm_reserve = saved_reserve;
   GGB_CUDA(cudaEventRecord(c.ev[K], c.cstream));
   GGB_CUDA(cudaStreamWaitEvent(ctx.stream, c.ev[K], 0));
 }
