@@ -174,8 +174,9 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--grid", default=None, help="GdxGxxGyxGz (default: data-parallel Gd = N)")
     ap.add_argument("--compute", default="accurate", choices=["accurate", "fast"])
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16comm"],
-                    help="PMM all-reduce wire: the reference's Precision::kFp32 or kBf16Roundtrip (comm.hpp:22)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "bf16comm", "bf16sum"],
+                    help="PMM all-reduce wire: the reference's Precision::kFp32 or kBf16Roundtrip (comm.hpp:22), "
+                         "or bf16 payloads summed by NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-eval", action="store_true", help="skip the separately timed full-graph evaluation")
     ap.add_argument("--prefetch", type=int, default=1,
@@ -255,7 +256,7 @@ def main():
                           dropout_rate=DROPOUT)
     st = gg.init_state(ctx, mcfg, RUN_SEED, gg.COMPUTE_ACCURATE if args.compute == "accurate" else gg.COMPUTE_FAST)
     group_seed = gg.hash_combine(RUN_SEED, grid.dp_group(rank))
-    prec = gg.FP32 if args.precision == "fp32" else gg.BF16_WIRE
+    prec = {"fp32": gg.FP32, "bf16comm": gg.BF16_WIRE, "bf16sum": gg.BF16_SUM}[args.precision]
     batch = None
     # sampling of step t+1 overlaps training of step t (producer thread + own stream)
     # (--prefetch 2 also hashes the next step's dropout masks on that stream)

@@ -34,7 +34,12 @@ enum ggb_status {
   GGB_EINTERNAL = 9
 };
 
-enum ggb_precision { GGB_FP32 = 0, GGB_BF16_WIRE = 1 }; /* comm.hpp:22 Precision */
+/* comm.hpp:22 Precision: GGB_FP32 = kFp32; GGB_BF16_WIRE = kBf16Roundtrip
+ * reproduced exactly (each contribution rounded to bf16, fp32 sum in axis
+ * order: an all-gather of bf16); GGB_BF16_SUM = bf16 payloads summed by NCCL
+ * (half the bytes of kFp32 with one ring all-reduce; rounding differs from
+ * kBf16Roundtrip within the bf16-communication tolerance). */
+enum ggb_precision { GGB_FP32 = 0, GGB_BF16_WIRE = 1, GGB_BF16_SUM = 2 };
 enum ggb_optimizer { GGB_SGD = 0, GGB_ADAM = 1 };       /* model.hpp:45 Optimizer */
 
 typedef struct ggb_ctx_s* ggb_ctx_t;     /* one per (process, GPU): grid coords, streams, comms, sampler */

@@ -15,7 +15,7 @@ LIBPATH = os.path.join(HERE, "libggb.so")
 I32, I64, U64, F64, P = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
 
 GGB_OK, GGB_EINVAL, GGB_ECONTRACT, GGB_ETIMEOUT, GGB_ECUDA, GGB_ENCCL = 0, 1, 2, 3, 4, 5
-FP32, BF16_WIRE = 0, 1
+FP32, BF16_WIRE, BF16_SUM = 0, 1, 2
 SGD, ADAM = 0, 1
 COMPUTE_ACCURATE, COMPUTE_FAST = 0, 1
 

@@ -22,6 +22,10 @@ __global__ void k_to_bf16(const float* __restrict__ in, int64_t n, bf16* __restr
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __float2bfloat16_rn(in[i]);
 }
+__global__ void k_from_bf16(const bf16* __restrict__ in, int64_t n, float* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __bfloat162float(in[i]);
+}
 
 // out[i] = 0 + c_0[i] + c_1[i] + ... in ascending member order (comm.hpp:282-295)
 __global__ void k_ordered_sum_bf16(const bf16* __restrict__ parts, int g, int64_t n, float* __restrict__ out) {
@@ -121,14 +125,26 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
 }
 
 namespace {
-void all_reduce_sum_on(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire, cudaStream_t s, DevBuf& wire,
+void all_reduce_sum_on(Ctx& ctx, int axis, float* buf, int64_t count, int mode, cudaStream_t s, DevBuf& wire,
                        DevBuf& gather) {
   Comm& c = *ctx.comm;
   const int gg = c.size[axis];
-  // bytes one rank sends: ring all-reduce 2(g-1)/g of the fp32 buffer; bf16 wire: its bf16 contribution to g-1 peers
-  ProfScope ps(ctx, kProfComm, bf16_wire ? 2.0 * count * (gg - 1) : 2.0 * (gg - 1) / gg * count * 4, 0, s);
-  if (!bf16_wire) {
+  // bytes one rank sends: ring all-reduce 2(g-1)/g of the buffer (fp32 or bf16); exact bf16 wire: its bf16
+  // contribution to g-1 peers
+  const double sent = mode == 1 ? 2.0 * count * (gg - 1) : 2.0 * (gg - 1) / gg * count * (mode == 2 ? 2 : 4);
+  ProfScope ps(ctx, kProfComm, sent, 0, s);
+  if (mode == 0) {
     GGB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclSum, as_nccl(c.axis[axis]), s));
+    return;
+  }
+  if (mode == 2) {
+    bf16* w = wire.reserve_n<bf16>(static_cast<size_t>(count));
+    const unsigned blocks = static_cast<unsigned>(ceil_div(count, 256));
+    k_to_bf16<<<blocks, 256, 0, s>>>(buf, count, w);
+    GGB_NCCL(ncclAllReduce(w, w, static_cast<size_t>(count), ncclBfloat16, ncclSum, as_nccl(c.axis[axis]), s));
+    k_from_bf16<<<blocks, 256, 0, s>>>(w, count, buf);
+    GGB_LAUNCH_CHECK();
+    ctx.launches += 2;
     return;
   }
   bf16* mine = wire.reserve_n<bf16>(static_cast<size_t>(count));
@@ -142,13 +158,13 @@ void all_reduce_sum_on(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_
 }
 }  // namespace
 
-void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire) {
+void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, int wire) {
   if (trivial(ctx, axis) || count <= 0) return;
   need(ctx, axis);
-  all_reduce_sum_on(ctx, axis, buf, count, bf16_wire, ctx.stream, ctx.comm->wire, ctx.comm->gather);
+  all_reduce_sum_on(ctx, axis, buf, count, wire, ctx.stream, ctx.comm->wire, ctx.comm->gather);
 }
 
-void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, float* buf, int64_t ld, bool bf16_wire,
+void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, float* buf, int64_t ld, int bf16_wire,
                           const std::function<void(int64_t, int64_t)>& produce,
                           const std::function<void(int64_t, int64_t)>& after) {
   const int K = comm_chunks();

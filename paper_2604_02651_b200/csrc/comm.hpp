@@ -27,11 +27,12 @@ struct Comm {
 int comm_get_unique_id(uint8_t out[128]);
 std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid);
 
-// In-place sum over the rank's group along `axis`. bf16_wire: each member's
-// contribution is rounded to bf16 (RNE) and the fp32 sum taken in ascending
-// axis order — the reference's Precision::kBf16Roundtrip (comm.hpp:271-303)
-// reproduced exactly by an all-gather of bf16 contributions.
-void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, bool bf16_wire);
+// In-place sum over the rank's group along `axis`. wire (ggb_precision):
+// 0 fp32; 1 each member's contribution rounded to bf16 (RNE) and the fp32 sum
+// taken in ascending axis order — the reference's Precision::kBf16Roundtrip
+// (comm.hpp:271-303) reproduced exactly by an all-gather of bf16
+// contributions; 2 bf16 payloads summed by one NCCL all-reduce.
+void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, int wire);
 void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count);
 // Row-chunked overlap of a producer and its all-reduce: chunk k
 // of `rows` rows (row stride ld floats of buf) is produced on the compute
@@ -44,7 +45,7 @@ void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count);
 // GGB_COMM_CHUNKS (default 1: produce everything, then one all-reduce) sets
 // the chunk count; measured on 4 B200 at C3 the chunked form is slower
 // (DESIGN.md), so it is off by default.
-void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, float* buf, int64_t ld, bool bf16_wire,
+void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, float* buf, int64_t ld, int wire,
                           const std::function<void(int64_t, int64_t)>& produce,
                           const std::function<void(int64_t, int64_t)>& after = {});
 void all_reduce_u64(Ctx& ctx, int axis, uint64_t* buf, int64_t count);  // exact integer sum

@@ -228,7 +228,8 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
              double eps) {
   Ctx& ctx = *st.ctx;
   const auto& cfg = st.cfg;
-  const bool wire = precision == GGB_BF16_WIRE;
+  require(precision >= GGB_FP32 && precision <= GGB_BF16_SUM, "forward: unknown precision");
+  const int wire = precision;  // ggb_precision: the all-reduce wire mode
   const int64_t H = cfg.d_h;
   const int dp = ctx.coord[0];
   contract(bt.planes == std::min(cfg.layers, 3), "forward: batch planes do not match the model layers");
@@ -514,7 +515,7 @@ void backward(State& st, const Batch& bt, int precision) {
   const auto& cfg = st.cfg;
   contract(st.have_forward && st.layers.size() >= static_cast<size_t>(cfg.layers),
            "backward: cache does not match the model");
-  const bool wire = precision == GGB_BF16_WIRE;
+  const int wire = precision;  // ggb_precision: the all-reduce wire mode
   const int64_t H = cfg.d_h;
   float* W = st.W.as<float>();
   float* G = st.G.as<float>();

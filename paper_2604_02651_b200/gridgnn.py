@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (ADAM, BF16_WIRE, COMPUTE_ACCURATE, COMPUTE_FAST, FP32, SGD, CommContract, CommTimeout, GgbError,  # noqa: F401
+from ._lib import (ADAM, BF16_SUM, BF16_WIRE, COMPUTE_ACCURATE, COMPUTE_FAST, FP32, SGD, CommContract, CommTimeout, GgbError,  # noqa: F401
                    InvalidArgument, ModelConfigC, check, lib)
 
 P = C.c_void_p

@@ -3,7 +3,7 @@ mkdir -p gpurun_out
 export GGB_WATCHDOG_S=120
 N=$(nvidia-smi -L | wc -l)
 rm -f gpurun_out/mg_rc.txt
-for gp in 2x1x1x1:0 1x1x1x2:0 1x2x1x1:0 1x1x2x1:1 1x2x2x1:0 1x1x2x2:1 2x1x1x2:0 4x1x1x1:0 1x2x2x2:0 2x2x2x1:0; do
+for gp in ${MG_GRIDS:-2x1x1x1:0 1x1x1x2:0 1x2x1x1:0 1x1x2x1:1 1x2x2x1:0 1x1x2x2:1 2x1x1x2:0 4x1x1x1:0 1x2x1x1:2 1x2x2x1:2 1x2x2x2:0 2x2x2x1:0}; do
   g=${gp%%:*}; p=${gp##*:}
   W=$(echo $g | tr 'x' '\n' | awk 'BEGIN{p=1}{p*=$1}END{print p}')
   if [ $W -gt $N ]; then continue; fi

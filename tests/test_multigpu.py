@@ -21,7 +21,7 @@ def _ngpus():
 
 
 GRIDS = [("1x1x1x2", 0), ("1x2x1x1", 0), ("1x1x2x1", 1), ("2x1x1x1", 0), ("1x2x2x1", 0), ("1x1x2x2", 1),
-         ("2x1x1x2", 0), ("4x1x1x1", 0)]
+         ("2x1x1x2", 0), ("4x1x1x1", 0), ("1x2x1x1", 2), ("1x2x2x1", 2)]
 
 
 @pytest.mark.gpu
