@@ -182,12 +182,16 @@ def main():
     ap.add_argument("--prefetch", type=int, default=1,
                     help="1: sample step t+1 on a side stream during step t; 2: also its dropout masks; 0: off")
     ap.add_argument("--ref-steps", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=None,
+                    help="diagnostic: override the configuration's global batch")
     ap.add_argument("--e2e-device-features", action="store_true",
                     help="diagnostic: run the e2e loop with the features still in HBM")
     ap.add_argument("--host-features", action="store_true",
                     help="keep the features in pinned host memory for the timed loop too (papers100M-scale HBM budget)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["batch"] = args.batch
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

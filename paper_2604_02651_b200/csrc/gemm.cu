@@ -17,6 +17,7 @@
 #include <cuda.h>
 
 #include <mutex>
+#include <unordered_map>
 
 #include "runtime.hpp"
 
@@ -592,8 +593,44 @@ EncodeFn encode_fn() {
 
 // 2D bf16 row-major tensor [rows][cols] with row stride ld (elements); box
 // {box_inner (cols), box_outer (rows)}; 128-byte swizzle; OOB -> zeros.
-CUtensorMap make_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_inner,
-                      int box_outer) {
+// Tensor maps are a pure function of (address, shape, stride, box, kind):
+// encoded once per distinct key (per host thread) instead of on every launch,
+// which keeps the host ahead of the GPU for small batches.
+struct TmapKey {
+  const void* base;
+  int64_t rows, cols, ld;
+  int a, b;  // box (operand maps) or element size (output maps, a = -esize)
+  bool operator==(const TmapKey& o) const {
+    return base == o.base && rows == o.rows && cols == o.cols && ld == o.ld && a == o.a && b == o.b;
+  }
+};
+struct TmapKeyHash {
+  size_t operator()(const TmapKey& k) const {
+    size_t h = std::hash<const void*>()(k.base);
+    for (int64_t v : {k.rows, k.cols, k.ld, static_cast<int64_t>(k.a), static_cast<int64_t>(k.b)})
+      h = h * 1000003u ^ std::hash<int64_t>()(v);
+    return h;
+  }
+};
+std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash>& tmap_cache() {
+  thread_local std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> c;
+  if (c.size() > 4096) c.clear();
+  return c;
+}
+
+CUtensorMap encode_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_inner, int box_outer);
+CUtensorMap make_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_inner, int box_outer) {
+  const TmapKey k{base, rows, cols, ld, box_inner, box_outer};
+  auto& c = tmap_cache();
+  auto it = c.find(k);
+  if (it != c.end()) return it->second;
+  const CUtensorMap m = encode_tmap(base, rows, cols, ld, box_inner, box_outer);
+  c.emplace(k, m);
+  return m;
+}
+
+CUtensorMap encode_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_inner,
+                        int box_outer) {
   require((reinterpret_cast<uintptr_t>(base) & 15) == 0, "gemm: operand must be 16-byte aligned");
   require((ld * 2) % 16 == 0, "gemm: leading dimension must be a multiple of 8 elements");
   CUtensorMap m;
@@ -612,7 +649,18 @@ CUtensorMap make_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, 
 // Output map for TMA stores: [rows][cols] with row stride ld elements of
 // esize bytes, box {16 columns, 32 rows}, swizzle matching the 16-column row
 // bytes (fp32 64 B, bf16 32 B). Out-of-bounds parts of a box are not written.
+CUtensorMap encode_out_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int esize);
 CUtensorMap make_out_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int esize) {
+  const TmapKey k{base, rows, cols, ld, -esize, 0};
+  auto& c = tmap_cache();
+  auto it = c.find(k);
+  if (it != c.end()) return it->second;
+  const CUtensorMap m = encode_out_tmap(base, rows, cols, ld, esize);
+  c.emplace(k, m);
+  return m;
+}
+
+CUtensorMap encode_out_tmap(const void* base, int64_t rows, int64_t cols, int64_t ld, int esize) {
   CUtensorMap m;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * esize)};
