@@ -243,3 +243,37 @@ def test_contract_errors(gg, orc):
     batch = gg.build_step_batch(ctx, g, 100, 1, 0)  # 2 planes for a 3-layer model
     with pytest.raises(gg.CommContract):
         gg.train_step(ctx, st, batch, gg.FP32, 1, 0)
+
+
+def test_c1_config_step_matches_reference(gg, orc, ref):
+    """BASELINE configs[0] at full size (2^16 vertices, ~1M edges, 64 features,
+    3-layer GCN hidden 128, batch N/4; the reference's own CPU-runnable case):
+    three Adam steps of train_run's loop — losses and final weights — and the
+    first step's batch bit-exact, against the reference compiled in place."""
+    n, deg, d_in, ncls, b, seed = 65536, 30.52, 64, 16, 16384, 1
+    cfg_kw = dict(layers=3, d_h=128, dropout_rate=0.1)
+    ds = orc.generate_synthetic(n, deg, d_in, ncls, 7)
+    h = ref.dataset_from(ds, orc.synthetic_edges(n, deg, 7))
+    try:
+        ctx = gg.Context()
+        g = gg.Graph.generate_synthetic_device(ctx, n, deg, d_in, ncls, 7, 3)
+        st = gg.init_state(ctx, gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), seed)
+        gs = gg.hash_combine(seed, 0)
+        got, batch = [], None
+        for t in range(3):
+            batch = gg.build_step_batch(ctx, g, b, gs, t, reuse=batch)
+            if t == 0:
+                lb = orc.local_minibatch(ds.adj, 0, n, 0, n, b, gs, 0)
+                a = batch.a(0)
+                assert np.array_equal(a.row_ptr, lb.a.row_ptr) and np.array_equal(a.col_idx, lb.a.col_idx)
+                assert np.array_equal(a.values.view(np.uint64), lb.a.values.view(np.uint64))
+            got.append(gg.train_step(ctx, st, batch, gg.FP32, seed, t))
+            gg.dp_sync(ctx, st)
+            gg.optimizer_step(ctx, st, gg.ADAM, 1e-3)
+        losses, _, _, W = ref.train(h, (1, 1, 1, 1), orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), b, seed, 0, 3,
+                                    optimizer=1, want_logits=False, want_weights=True)
+        assert np.all(np.abs(np.array(got) - losses) <= LOSS_RTOL * np.abs(losses)), (got, losses)
+        for mine, want in zip(st.weights(), W):
+            assert _rel(mine, want) <= 1e-3
+    finally:
+        ref.free_dataset(h)
