@@ -249,3 +249,45 @@ def test_graph_from_dataset_files(gg, orc, tmp_path):
     assert np.array_equal(a.a(0).col_idx, b.a(0).col_idx)
     assert np.array_equal(a.a(0).values.view(np.uint64), b.a(0).values.view(np.uint64))
     assert np.array_equal(a.x_in[1], b.x_in[1]) and np.array_equal(a.labels, b.labels)
+
+
+def test_c2_batch_properties_at_full_size(gg):
+    """BASELINE configs[1] at full size (2.45M vertices, 126M nonzeros, batch
+    612,500): properties of the induced, rescaled batch adjacency that hold at
+    any size — sorted distinct sample, canonical CSR, every self-loop kept,
+    A == A^T bit for bit, nnz at its expectation, off-diagonal values
+    = static value / p (fp64, exact) against the static CSR."""
+    n, deg, b = 2_450_000, 50.53, 612_500
+    ctx = gg.Context()
+    g = gg.Graph.generate_synthetic_device(ctx, n, deg, 100, 47, 7, 3)
+    (rp, ci, va), _, _, _ = g.export(features=False)
+    bt = gg.build_step_batch(ctx, g, b, gg.hash_combine(1, 0), 3)
+    s = bt.sample
+    assert len(s) == b and s[0] >= 0 and s[-1] < n and np.all(np.diff(s) > 0)
+    a = bt.a(0)
+    assert a.row_ptr[0] == 0 and np.all(np.diff(a.row_ptr) >= 1)  # every row keeps its self-loop
+    rows = np.repeat(np.arange(b), np.diff(a.row_ptr))
+    cols = a.col_idx
+    starts = a.row_ptr[:-1]
+    first = np.zeros(len(cols), bool)
+    first[starts] = True
+    assert np.all((np.diff(cols) > 0) | first[1:])  # strictly increasing within rows
+    nnz = len(cols)
+    expect = b + (g.nnz - n) * (b / n) * ((b - 1) / (n - 1))
+    assert abs(nnz - expect) <= 0.01 * expect
+    # symmetric, values bit-identical: sort the transposed triples
+    key = rows.astype(np.int64) * b + cols
+    tkey = cols.astype(np.int64) * b + rows
+    order = np.argsort(tkey, kind="stable")
+    assert np.array_equal(key, tkey[order])
+    assert np.array_equal(a.values.view(np.uint64), a.values[order].view(np.uint64))
+    # rescale: off-diagonal entries = static value / p, diagonal unchanged
+    p = (b - 1) / (n - 1)
+    rng = np.random.default_rng(0)
+    for k in rng.integers(0, nnz, 2000):
+        u, v = int(s[rows[k]]), int(s[cols[k]])
+        lo, hi = rp[u], rp[u + 1]
+        pos = lo + np.searchsorted(ci[lo:hi], v)
+        assert ci[pos] == v
+        want = va[pos] if u == v else va[pos] / p
+        assert np.float64(want).view(np.uint64) == np.float64(a.values[k]).view(np.uint64)
