@@ -564,8 +564,18 @@ __global__ void k_reduce_partials(const float* __restrict__ part, int splits, in
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t total = kw * nw;
   if (i >= total) return;
-  float s = 0.f;
-  for (int k = 0; k < splits; ++k) s += part[k * total + i];
+  // four independent chains over the splits (short dependent-load chains),
+  // combined in a fixed order: deterministic
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int k = 0;
+  for (; k + 4 <= splits; k += 4) {
+    s0 += part[k * total + i];
+    s1 += part[(k + 1) * total + i];
+    s2 += part[(k + 2) * total + i];
+    s3 += part[(k + 3) * total + i];
+  }
+  for (; k < splits; ++k) s0 += part[k * total + i];
+  const float s = (s0 + s1) + (s2 + s3);
   float* o = out + (i / nw) * ldo + (i % nw);
   *o = accumulate ? *o + s : s;
 }

@@ -131,18 +131,22 @@ __global__ void k_rowsumsq(const float* __restrict__ x, int64_t ldx, int64_t row
 
 // out[c] = sum_k part[k][c]; a block owns 32 columns, its 8 warps split the
 // parts, then a fixed-order combine (deterministic).
-__global__ void k_reduce_rows(const float* __restrict__ part, int parts, int64_t cols, float* __restrict__ out) {
-  __shared__ float sh[8][33];
+// column sums of `parts` partial rows: 32 warps per 32 columns, each warp
+// summing every 32nd partial, then the warps' sums in order
+__global__ void __launch_bounds__(1024) k_reduce_rows(const float* __restrict__ part, int parts, int64_t cols,
+                                                     float* __restrict__ out) {
+  __shared__ float sh[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
   float s = 0.f;
   if (c < cols)
-    for (int k = w; k < parts; k += 8) s += part[k * cols + c];
+    for (int k = w; k < parts; k += 32) s += part[k * cols + c];
   sh[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < cols) {
     float t = 0.f;
-    for (int k = 0; k < 8; ++k) t += sh[k][lane];
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) t += sh[k][lane];
     out[c] = t;
   }
 }
@@ -300,7 +304,7 @@ void rowsumsq(Ctx& ctx, const float* x, int64_t ldx, int64_t rows, int64_t cols,
 
 void reduce_rows(Ctx& ctx, const float* part, int parts, int64_t cols, float* out) {
   if (cols <= 0) return;
-  k_reduce_rows<<<static_cast<unsigned>(ceil_div(cols, 32)), 256, 0, ctx.stream>>>(part, parts, cols, out);
+  k_reduce_rows<<<static_cast<unsigned>(ceil_div(cols, 32)), 1024, 0, ctx.stream>>>(part, parts, cols, out);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
