@@ -75,6 +75,19 @@ int ggb_ctx_synchronize(ggb_ctx_t ctx);
 /* counters = {kernels launched on ctx since creation, host->device bytes,
  * device->host bytes} */
 int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters);
+/* CommStats (reference comm.hpp:75-117, 385-403): the reference's accounting
+ * of every logical collective of the step, charged at its call sites —
+ * all-reduce: count * elem_bytes * (g-1)/g (elem_bytes 2 on the bf16 wires),
+ * all-gather: the whole gathered payload, nothing in a singleton group.
+ * out[GGB_COMM_STATS_LEN] = bytes[axis][phase] (axis D,X,Y,Z; phase sampling,
+ * forward, backward, dp_sync, other; 20 entries), then all-reduce calls per
+ * axis (4), then all-gather calls per axis (4). grid_total != 0 sums over
+ * every rank of the grid (Communicator::snapshot; collective: every rank
+ * calls it); reset != 0 zeroes this rank's counters after reading.
+ * Phases: train_step's forward + loss (forward) and backward (backward),
+ * dp_sync (dp_sync), anything else (other). */
+#define GGB_COMM_STATS_LEN 28
+int ggb_ctx_comm_stats(ggb_ctx_t ctx, int32_t grid_total, int32_t reset, uint64_t* out);
 /* Per-kernel-class timing with CUDA events on the ctx stream. Classes:
  * 0 sampling, 1 SpMM fwd, 2 SpMM bwd, 3 GEMM fwd, 4 GEMM dX, 5 GEMM dW,
  * 6 other element-wise passes, 7 optimizer, 8 collectives, 9 fused

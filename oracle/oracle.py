@@ -461,6 +461,7 @@ class Ref:
         L.ref_train_eval.argtypes = [P, P, P, P, I64, U64, C.c_int, C.c_int, C.c_int, C.c_double,
                                      C.c_double, P, P]
         L.ref_bench.argtypes = [P, P, P, P, I64, U64, C.c_int, C.c_int, C.c_int, P, P]
+        L.ref_comm_stats.argtypes = [P, P, P, P, I64, U64, C.c_int, C.c_int, C.c_int, P]
         self.L = L
 
     def _check(self, rc: int):
@@ -618,6 +619,21 @@ class Ref:
         self._check(self.L.ref_train_eval(h, _ptr(d), _ptr(mc), _ptr(md), b, seed, n_steps, prec, optimizer, lr,
                                           eps, _ptr(counts), _ptr(logits)))
         return counts, logits
+
+    def comm_stats(self, h, dims, cfg: ModelConfig, b, seed, n_steps, prec=0, evaluate=False):
+        """The reference's CommStats snapshot after n_steps of the train_run
+        loop (+ one evaluate_full_graph), in the layout of Ctx.comm_stats."""
+        mc, md = cfg.arrays()
+        d = np.asarray(dims, np.int32)
+        out = np.zeros(28, np.uint64)
+        self._check(self.L.ref_comm_stats(h, _ptr(d), _ptr(mc), _ptr(md), b, seed, n_steps, prec,
+                                          int(evaluate), _ptr(out)))
+        axes, phases = ("D", "X", "Y", "Z"), ("sampling", "forward", "backward", "dp_sync", "other")
+        return {
+            "bytes": {a: {p: int(out[i * 5 + j]) for j, p in enumerate(phases)} for i, a in enumerate(axes)},
+            "allreduce_calls": {a: int(out[20 + i]) for i, a in enumerate(axes)},
+            "allgather_calls": {a: int(out[24 + i]) for i, a in enumerate(axes)},
+        }
 
     def init_weights(self, cfg: ModelConfig, seed: int):
         mc, md = cfg.arrays()

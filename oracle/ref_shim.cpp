@@ -443,6 +443,49 @@ int ref_train_eval(void* dsp, const int* dims, const std::int64_t* mc, const dou
   });
 }
 
+/// CommStats of the train_run step loop (model.hpp:646-685): n_steps of
+/// [build_step_batch -> train_step (forward/backward phases) -> dp_sync ->
+/// optimizer_step], then (eval != 0) evaluate_full_graph on the b = n eval
+/// batch outside any phase. out[28] = Communicator::snapshot(): bytes[axis]
+/// [phase] (20), all-reduce calls (4), all-gather calls (4), axes D,X,Y,Z.
+int ref_comm_stats(void* dsp, const int* dims, const std::int64_t* mc, const double* md, std::int64_t b,
+                   std::uint64_t seed, int n_steps, int prec, int eval, std::uint64_t* out) {
+  auto* ds = static_cast<Dataset*>(dsp);
+  return guard([&] {
+    const ModelConfig mcfg = make_cfg(mc, md);
+    DeviceGrid grid(dims[0], dims[1], dims[2], dims[3]);
+    Communicator comm(grid);
+    const Precision p = prec ? Precision::kBf16Roundtrip : Precision::kFp32;
+    run_ranks(comm, [&](RankComm& rc) {
+      const int dp = grid.dp_group(rc.rank());
+      const std::uint64_t group_seed = rng::hash_combine(seed, static_cast<std::uint64_t>(dp));
+      RankContext ctx = make_rank_context(grid, rc.coord(), *ds, mcfg.layers);
+      auto st = init_state<float>(grid, rc.coord(), mcfg, seed);
+      for (int s = 0; s < n_steps; ++s) {
+        const auto gstep = static_cast<std::uint64_t>(s);
+        StepBatch<float> batch;
+        {
+          PhaseScope ps(rc, Phase::kSampling);
+          batch = build_step_batch<float>(grid, rc.coord(), ctx, *ds, b, group_seed, gstep, &rc.stats());
+        }
+        train_step(rc, st, batch, p, seed, gstep, 1e-6);
+        dp_sync(rc, st);
+        optimizer_step(st, Optimizer::kAdam, 1e-3);
+      }
+      if (eval) {
+        const auto eval_batch = build_step_batch<float>(grid, rc.coord(), ctx, *ds, ds->n, seed, 0, nullptr);
+        evaluate_full_graph(rc, st, eval_batch, *ds, p, 1e-6);
+      }
+    });
+    const CommStats snap = comm.snapshot();
+    for (int a = 0; a < 4; ++a) {
+      for (int q = 0; q < kNumPhases; ++q) out[a * kNumPhases + q] = snap.bytes[a][q];
+      out[20 + a] = snap.allreduce_calls[a];
+      out[24 + a] = snap.allgather_calls[a];
+    }
+  });
+}
+
 /// Initial weights (init_state on the 1x1x1x1 grid), flattened in
 /// param_views order.
 int ref_init_weights(const std::int64_t* mc, const double* md, std::uint64_t seed, float* out) {

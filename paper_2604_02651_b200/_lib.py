@@ -38,6 +38,7 @@ _SIGS = [
     ("ggb_ctx_set_stream", C.c_int, [P, P]),
     ("ggb_ctx_synchronize", C.c_int, [P]),
     ("ggb_ctx_counters", C.c_int, [P, P]),
+    ("ggb_ctx_comm_stats", C.c_int, [P, I32, I32, P]),
     ("ggb_ctx_profile", C.c_int, [P, I32]),
     ("ggb_ctx_profile_read", C.c_int, [P, P, P, P, P, I32]),
     ("ggb_sample_vertices", C.c_int, [P, I64, I64, U64, U64, P]),

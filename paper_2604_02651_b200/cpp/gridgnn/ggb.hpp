@@ -104,6 +104,44 @@ inline index_t steps_per_epoch(index_t n, index_t b, int gd) {  // model.hpp:539
   return (n + per - 1) / per;
 }
 
+enum class Phase : int { kSampling = 0, kForward, kBackward, kDpSync, kOther };  // comm.hpp:24
+inline constexpr int kNumPhases = 5;
+
+/// CommStats (comm.hpp:94-117): the reference's byte accounting of the
+/// logical collectives (ring-equivalent all-reduce volume, full all-gather
+/// payload, singleton groups free).
+struct CommStats {
+  std::array<std::array<std::uint64_t, kNumPhases>, 4> bytes{};
+  std::array<std::uint64_t, 4> allreduce_calls{};
+  std::array<std::uint64_t, 4> allgather_calls{};
+  std::uint64_t bytes_on(Axis a) const {
+    std::uint64_t s = 0;
+    for (auto b : bytes[static_cast<std::size_t>(static_cast<int>(a))]) s += b;
+    return s;
+  }
+  std::uint64_t phase_bytes(Phase p) const {
+    std::uint64_t s = 0;
+    for (const auto& ax : bytes) s += ax[static_cast<std::size_t>(static_cast<int>(p))];
+    return s;
+  }
+  std::uint64_t sampling_bytes() const { return phase_bytes(Phase::kSampling); }
+  std::uint64_t total_bytes() const {
+    std::uint64_t s = 0;
+    for (const auto& ax : bytes)
+      for (auto b : ax) s += b;
+    return s;
+  }
+  CommStats operator-(const CommStats& o) const {
+    CommStats d;
+    for (int a = 0; a < 4; ++a) {
+      for (int p = 0; p < kNumPhases; ++p) d.bytes[a][p] = bytes[a][p] - o.bytes[a][p];
+      d.allreduce_calls[a] = allreduce_calls[a] - o.allreduce_calls[a];
+      d.allgather_calls[a] = allgather_calls[a] - o.allgather_calls[a];
+    }
+    return d;
+  }
+};
+
 /// One rank on one GPU (replaces Communicator + RankComm, comm.hpp:203-408).
 class RankComm {
  public:
@@ -128,6 +166,20 @@ class RankComm {
   const DeviceGrid& grid() const { return grid_; }
   void synchronize() { detail::check(ggb_ctx_synchronize(h_)); }
   ggb_ctx_t handle() const { return h_; }
+  /// This rank's counters (RankStats), or with grid_total the sum over the
+  /// grid (Communicator::snapshot; collective, every rank calls it).
+  CommStats comm_stats(bool grid_total = false, bool reset = false) {
+    std::uint64_t v[GGB_COMM_STATS_LEN];
+    detail::check(ggb_ctx_comm_stats(h_, grid_total ? 1 : 0, reset ? 1 : 0, v));
+    CommStats s;
+    for (int a = 0; a < 4; ++a) {
+      for (int p = 0; p < kNumPhases; ++p) s.bytes[a][p] = v[a * kNumPhases + p];
+      s.allreduce_calls[a] = v[20 + a];
+      s.allgather_calls[a] = v[24 + a];
+    }
+    return s;
+  }
+  CommStats snapshot() { return comm_stats(true); }
 
  private:
   DeviceGrid grid_;
@@ -455,8 +507,8 @@ struct TrainConfig {  // model.hpp:47-58 (the fields of the step loop)
 
 /// EpochMetrics (metrics.hpp:13-29). Timings are host wall-clock around the
 /// device calls (sampling wait, train_step = forward + CE + backward, which
-/// the device runs back to back, so t_bwd_ms stays 0; dp_sync). Byte columns
-/// are not tracked by the NCCL path and stay 0.
+/// the device runs back to back, so t_bwd_ms stays 0; dp_sync). Byte columns:
+/// the epoch's CommStats delta summed over the grid (model.hpp:706-716).
 struct EpochMetrics {
   int epoch = 0;
   std::int64_t step = 0;
@@ -472,6 +524,7 @@ struct TrainReport {
   std::vector<double> step_losses;
   std::uint64_t sampled_nnz_extracted = 0;
   std::uint64_t sampled_nnz_kept = 0;
+  CommStats comm_total;  // grid total at the end of the run
   double wall_ms = 0.0;
   double final_train_acc() const { return epochs.empty() ? 0.0 : epochs.back().train_acc; }
   double final_val_acc() const { return epochs.empty() ? 0.0 : epochs.back().val_acc; }
@@ -539,6 +592,8 @@ inline TrainReport train_run(RankComm& rc, const DeviceDataset& ds, const ModelC
   if (tcfg.prefetch) pf = std::make_unique<Prefetcher>(rc, ds, tcfg.batch, group_seed, 0, tcfg.seed, &mcfg);
   StepBatch batch;
   std::uint64_t gstep = 0;
+  const CommStats run_start_stats = rc.snapshot();  // the reference's Communicator starts at zero
+  CommStats prev_snapshot = run_start_stats;
   for (int epoch = 0; epoch < tcfg.epochs; ++epoch) {
     EpochMetrics row;
     double loss_sum = 0.0;
@@ -576,9 +631,16 @@ inline TrainReport train_run(RankComm& rc, const DeviceDataset& ds, const ModelC
       row.val_acc = c.accuracy(SplitTag::kVal);
       row.test_acc = c.accuracy(SplitTag::kTest);
     }
+    const CommStats snap = rc.snapshot();
+    row.bytes_x = snap.bytes_on(Axis::X) - prev_snapshot.bytes_on(Axis::X);
+    row.bytes_y = snap.bytes_on(Axis::Y) - prev_snapshot.bytes_on(Axis::Y);
+    row.bytes_z = snap.bytes_on(Axis::Z) - prev_snapshot.bytes_on(Axis::Z);
+    row.bytes_d = snap.bytes_on(Axis::D) - prev_snapshot.bytes_on(Axis::D);
+    prev_snapshot = snap;
     report.epochs.push_back(row);
   }
   rc.synchronize();
+  report.comm_total = prev_snapshot - run_start_stats;
   report.wall_ms = ms_since(run_start);
   return report;
 }

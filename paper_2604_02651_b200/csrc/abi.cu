@@ -407,6 +407,30 @@ int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters) {
   });
 }
 
+int ggb_ctx_comm_stats(ggb_ctx_t ctx, int32_t grid_total, int32_t reset, uint64_t* out) {
+  return guard([&] {
+    require(out != nullptr, "comm_stats: null output");
+    const CommStats& cs = ctx->stats;
+    uint64_t v[GGB_COMM_STATS_LEN];
+    for (int a = 0; a < 4; ++a) {
+      for (int p = 0; p < kNumPhases; ++p) v[a * kNumPhases + p] = cs.bytes[a][p];
+      v[4 * kNumPhases + a] = cs.allreduce_calls[a];
+      v[4 * kNumPhases + 4 + a] = cs.allgather_calls[a];
+    }
+    if (grid_total) {  // Communicator::snapshot (comm.hpp:224-236): the sum over every rank of the grid
+      use_device(*ctx);
+      DevBuf tmp;
+      uint64_t* d = tmp.reserve_n<uint64_t>(GGB_COMM_STATS_LEN);
+      GGB_CUDA(cudaMemcpyAsync(d, v, sizeof(v), cudaMemcpyHostToDevice, ctx->stream));
+      for (int a = 0; a < 4; ++a) all_reduce_u64(*ctx, a, d, GGB_COMM_STATS_LEN);
+      GGB_CUDA(cudaMemcpyAsync(v, d, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream));
+      GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    for (int i = 0; i < GGB_COMM_STATS_LEN; ++i) out[i] = v[i];
+    if (reset) ctx->stats = CommStats{};
+  });
+}
+
 int ggb_ctx_profile(ggb_ctx_t ctx, int32_t enable) {
   return guard([&] {
     use_device(*ctx);
@@ -832,9 +856,15 @@ int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precis
     use_device(*ctx);
     contract(st->ctx == ctx && bt->ctx && bt->ctx->device == ctx->device && bt->ctx->rank == ctx->rank,
              "train_step: handles belong to another rank");
-    forward(*st, *bt, precision, true, run_seed, global_step, rmsnorm_eps);
-    cross_entropy(*st, *bt);
-    backward(*st, *bt, precision);
+    {  // train_step's phases (model.hpp:466-476)
+      PhaseScope ps(*ctx, kPhaseForward);
+      forward(*st, *bt, precision, true, run_seed, global_step, rmsnorm_eps);
+      cross_entropy(*st, *bt);
+    }
+    {
+      PhaseScope ps(*ctx, kPhaseBackward);
+      backward(*st, *bt, precision);
+    }
     if (loss_out) {
       download(loss_out, st->loss.p, 1, ctx->stream);
       ctx->d2h_bytes += sizeof(float);

@@ -91,6 +91,11 @@ void evaluate_full_graph(State& st, const Batch& eval, const Graph& g, int preci
   const int64_t rows = lb.rows();
   const int col_axis = lb.lay.col, row_axis = lb.lay.row;
   const int parts = ctx.grid.dims[col_axis];
+  // the reference gathers (value, index) as two all-gathers (fp32, int64) and
+  // all-reduces six u64 counters (model.hpp:508-509, 533)
+  charge_all_gather(ctx, col_axis, static_cast<uint64_t>(rows) * parts * 4);
+  charge_all_gather(ctx, col_axis, static_cast<uint64_t>(rows) * parts * 8);
+  charge_all_reduce(ctx, row_axis, 6, 8);
   DevBuf& wk = st.tmp;
   // [best pairs: rows] [gathered: parts x rows] [counts: 6 u64]
   const size_t pair_bytes = static_cast<size_t>(rows) * sizeof(float2);

@@ -12,6 +12,21 @@ namespace ggb {
 struct Comm;  // comm.cu (NCCL per-axis communicators)
 struct Prof;  // prof.hpp (per-kernel-class event timing)
 
+/// CommStats accounting (comm.hpp:24-25, 75-117, 385-403): every logical
+/// collective of the reference's step is charged to (axis, phase) with the
+/// reference's model: an all-reduce charges count * elem_bytes * (g-1)/g, an
+/// all-gather the whole gathered payload, nothing in a singleton group; call
+/// counters always advance. Charged at the reference's call sites whether or
+/// not this implementation moves those bytes (it fuses, skips or replaces some
+/// of them), so the byte columns of the metrics match the reference's.
+enum Phase : int { kPhaseSampling = 0, kPhaseForward = 1, kPhaseBackward = 2, kPhaseDpSync = 3, kPhaseOther = 4 };
+constexpr int kNumPhases = 5;
+struct CommStats {
+  uint64_t bytes[4][kNumPhases] = {};
+  uint64_t allreduce_calls[4] = {};
+  uint64_t allgather_calls[4] = {};
+};
+
 /// Sampler scratch, reused across steps (one build at a time per context).
 struct SamplerWork {
   DevBuf head;      // uint64 [n]: step-tagged (tag<<32 | step index) list heads
@@ -48,8 +63,30 @@ struct Ctx {
   int sm_reserve = 0;
   int persistent_sms() const { return num_sms - sm_reserve > 0 ? num_sms - sm_reserve : 1; }
   std::unique_ptr<Prof> prof;
+  CommStats stats;
+  int phase = kPhaseOther;
   ~Ctx();
 };
+
+/// PhaseScope (comm.hpp:411-421).
+struct PhaseScope {
+  Ctx& ctx;
+  int prev;
+  PhaseScope(Ctx& c, int p) : ctx(c), prev(c.phase) { ctx.phase = p; }
+  ~PhaseScope() { ctx.phase = prev; }
+  PhaseScope(const PhaseScope&) = delete;
+  PhaseScope& operator=(const PhaseScope&) = delete;
+};
+
+inline void charge_all_reduce(Ctx& ctx, int axis, int64_t count, int ebytes) {
+  const uint64_t g = static_cast<uint64_t>(ctx.grid.dims[axis]);
+  if (g > 1) ctx.stats.bytes[axis][ctx.phase] += static_cast<uint64_t>(count) * static_cast<uint64_t>(ebytes) * (g - 1) / g;
+  ctx.stats.allreduce_calls[axis] += 1;
+}
+inline void charge_all_gather(Ctx& ctx, int axis, uint64_t payload_bytes) {
+  if (ctx.grid.dims[axis] > 1) ctx.stats.bytes[axis][ctx.phase] += payload_bytes;
+  ctx.stats.allgather_calls[axis] += 1;
+}
 
 /// One static plane shard (shardsample.hpp:18-25): rows [r0,r1) with local
 /// row ids, global column ids restricted to [c0,c1).

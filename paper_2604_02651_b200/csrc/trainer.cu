@@ -94,6 +94,17 @@ void reshard(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff, cons
   exchange_blocks(ctx, sends, recvs);
 }
 
+// reshard's accounting (pmm.hpp:171-204): a layout change runs gather_full,
+// an all-gather of the column strip (g_rows x local cols) along the row axis,
+// then of the whole matrix along the column axis; an unchanged layout is free
+void charge_reshard(Ctx& ctx, const Block& t, Layout to) {
+  if (t.lay == to) return;
+  charge_all_gather(ctx, t.lay.row, static_cast<uint64_t>(t.g_rows) * t.cols() * 4);
+  charge_all_gather(ctx, t.lay.col, static_cast<uint64_t>(t.g_rows) * t.g_cols * 4);
+}
+
+inline int wire_bytes(int wire) { return wire == GGB_FP32 ? 4 : 2; }  // RankComm::elem_bytes (comm.hpp:266-270)
+
 bool pmm_trivial(const Ctx& ctx) { return ctx.grid.dims[1] == 1 && ctx.grid.dims[2] == 1 && ctx.grid.dims[3] == 1; }
 
 }  // namespace
@@ -250,6 +261,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     // accurate: X0 stays fp32 (the next SpMM gathers fp32); fast: + bf16 operand copy
     const bool want_b = st.compute != kAccurate;
     const bool ar = !trivial(ctx, kInputFeatureLayout.col);
+    charge_all_reduce(ctx, kInputFeatureLayout.col, ob.rows() * ob.cols(), wire_bytes(wire));
     Tensor xin;
     xin.b = bt.x_in.as<bf16>();
     xin.lo = bt.x_in_lo.as<bf16>();
@@ -293,6 +305,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.hagg.b = grow<bf16>(L.hagg_b, hb.rows() * L.hagg.ldb);
     L.hagg.lo = accurate ? grow<bf16>(L.hagg_lo, hb.rows() * L.hagg.ldb) : nullptr;
     const bool ar_h = !trivial(ctx, alay.col);
+    charge_all_reduce(ctx, alay.col, hb.rows() * hb.cols(), wire_bytes(wire));  // spmm (pmm.hpp:165)
     const int64_t* arp = A.row_ptr.as<int64_t>();
     if (l == 1 && st.preagg) {
       // hagg_1 = P . W_in with P = A_0 . x_in (built with the batch); X and Z
@@ -361,6 +374,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.xw_t.blk = xb;
     L.xw_t.ldf = ld8(xb.cols());
     L.xw_t.f = grow<float>(L.xw, xb.rows() * L.xw_t.ldf);
+    charge_all_reduce(ctx, hb.lay.col, xb.rows() * xb.cols(), wire_bytes(wire));  // contract (pmm.hpp:128)
     pipelined_all_reduce(ctx, hb.lay.col, xb.rows(), 128, L.xw_t.f, L.xw_t.ldf, wire, [&](int64_t r0, int64_t r1) {
       Tensor sub = L.hagg;
       sub.b = L.hagg.b + r0 * L.hagg.ldb;
@@ -375,6 +389,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     if (cfg.use_rmsnorm) {
       ss = grow<float>(L.ss, xb.rows());
       rms = grow<float>(L.rms, xb.rows());
+      charge_all_reduce(ctx, xb.lay.col, xb.rows(), 4);  // pmm.hpp:229
       if (!row_local) {  // partial sums of squares, all-reduced along the column axis
         ProfScope ps(ctx, kProfElementwise, 4.0 * xb.rows() * xb.cols());
         rowsumsq(ctx, L.xw_t.f, L.xw_t.ldf, xb.rows(), xb.cols(), ss);
@@ -392,6 +407,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
       Block rb = make_block(ctx, out, bt.b, H, bt.batch_off[out.row], hoff(ctx, H, out.col));
       contract(rb.r0 == xb.r0 && rb.r1 == xb.r1 && rb.c0 == xb.c0 && rb.c1 == xb.c1,
                "fused_elementwise: residual layout mismatch");
+      charge_reshard(ctx, F, out);
       if (pmm_trivial(ctx)) {
         res = prev->f;
         ldres = prev->ldf;
@@ -470,6 +486,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     st.logits_blk = lb;
     float* lg = grow<float>(st.logits, lb.rows() * lb.cols());
     fwd_gemm(st, lb.rows(), lb.cols(), F.cols(), *prev, w, lg, lb.cols(), nullptr, 0);
+    charge_all_reduce(ctx, F.lay.col, lb.rows() * lb.cols(), wire_bytes(wire));
     all_reduce_sum(ctx, F.lay.col, lg, lb.rows() * lb.cols(), wire);
   }
   st.have_forward = true;
@@ -494,6 +511,9 @@ void cross_entropy(State& st, const Batch& bt) {
   c.lddlogb = ld8(c.cols);
   c.loss_part = grow<float>(st.ce_part, ce_grad_blocks(c.rows) + 1);
   c.loss_acc = grow<float>(st.loss_acc, 1);
+  charge_all_reduce(ctx, lb.lay.col, c.rows, 4);      // row max (pmm.hpp:368)
+  charge_all_reduce(ctx, lb.lay.col, 2 * c.rows, 4);  // [sum exp, label logit] (pmm.hpp:381)
+  charge_all_reduce(ctx, lb.lay.row, 1, 4);           // loss (pmm.hpp:398)
   if (trivial(ctx, lb.lay.col)) {  // class block complete here: one pass per row
     ProfScope ps(ctx, kProfCe, static_cast<double>(c.rows) * c.cols * (4 + 2));
     ce_fused(ctx, c);
@@ -533,6 +553,7 @@ void backward(State& st, const Batch& bt, int precision) {
       gemm_wgrad_bf16(ctx, lb.rows(), XL.blk.cols(), lb.cols(), XL.b, XL.ldb, st.dlog_b.as<bf16>(), lddlog,
                       G + w.off, w.blk.cols(), st.ws_wgrad);
     }
+    charge_all_reduce(ctx, XL.blk.lay.row, w.n, wire_bytes(wire));
     all_reduce_sum(ctx, XL.blk.lay.row, G + w.off, w.n, wire);
   }
   // dxh = dlogits . W_out^T -> (X_L.row, X_L.col), all-reduce logits.col
@@ -545,6 +566,7 @@ void backward(State& st, const Batch& bt, int precision) {
                  2.0 * db.rows() * db.cols() * lb.cols());
     gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, dxh,
               ld8(db.cols()), nullptr, 0);
+    charge_all_reduce(ctx, lb.lay.col, db.rows() * db.cols(), wire_bytes(wire));
     all_reduce_sum(ctx, lb.lay.col, dxh, db.rows() * ld8(db.cols()), wire);
   }
   const bf16* pre_dhb = nullptr;  // layer 1 under pre-aggregation: dhagg_1 (bf16) and the residual gradient
@@ -559,6 +581,7 @@ void backward(State& st, const Batch& bt, int precision) {
     const Block& F = (l == 1) ? st.x0.blk : st.layers[l - 2].x.blk;
     float* dres = nullptr;
     if (cfg.use_residual) {
+      charge_reshard(ctx, db, F.lay);
       if (pmm_trivial(ctx)) {
         dres = dxh;  // identical block; the SpMM below accumulates into it
       } else {
@@ -592,6 +615,8 @@ void backward(State& st, const Batch& bt, int precision) {
       ba.gamma = W + gp.off;
       ba.rms = L.rms.as<float>();
       ba.s = grow<float>(st.s_row, rows);
+      charge_all_reduce(ctx, xb.lay.col, rows, 4);  // pmm.hpp:268
+      charge_all_reduce(ctx, xb.lay.row, cols, 4);  // dgamma (pmm.hpp:285)
       if (!row_local) {
         bwd_stats(ctx, ba);
         all_reduce_sum(ctx, xb.lay.col, ba.s, rows, false);
@@ -614,10 +639,12 @@ void backward(State& st, const Batch& bt, int precision) {
       gemm_wgrad_bf16(ctx, rows, hg.blk.cols(), cols, hg.b, hg.ldb, ba.dxb, lddxw, G + w.off, w.blk.cols(),
                       st.ws_wgrad);
     }
+    charge_all_reduce(ctx, hg.blk.lay.row, w.n, wire_bytes(wire));
     all_reduce_sum(ctx, hg.blk.lay.row, G + w.off, w.n, wire);
     // dhagg = dxw . W_l^T -> (xw.row, hagg.col), all-reduce xw.col
     const int64_t hc = hg.blk.cols();
     const bool ar_d = !trivial(ctx, xb.lay.col);
+    charge_all_reduce(ctx, xb.lay.col, rows * hc, wire_bytes(wire));
     const int64_t ldhb = ld8(hc);
     bf16* dhb = grow<bf16>(st.dhagg_b, rows * ldhb);
     {
@@ -637,6 +664,8 @@ void backward(State& st, const Batch& bt, int precision) {
       gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, nullptr, 0, dhb, ldhb);
     }
     }
+    // dxh = spmm(A_t, dhagg) (pmm.hpp:165), charged also when pre-aggregation folds it into dW_in
+    charge_all_reduce(ctx, adjacency_layout(l).row, bt.csrs[bt.csrt_of[(l - 1) % 3]].n_rows * hc, wire_bytes(wire));
     if (l == 1 && st.preagg) {
       // layer 1 was (A_0 . x_in) . W_in: dX_0 is not formed; dW_in takes
       // P^T . dhagg_1 plus the residual term x_in^T . dres (below)
@@ -703,6 +732,7 @@ void backward(State& st, const Batch& bt, int precision) {
     }
     gemm_wgrad_bf16(ctx, rows, kin, cols, bt.p_in.as<bf16>(), bt.x_ld, pre_dhb, pre_ldhb, G + w.off, w.blk.cols(),
                     st.ws_wgrad, pre_dres ? 1 : 0);
+    charge_all_reduce(ctx, kInputFeatureLayout.row, w.n, wire_bytes(wire));
     all_reduce_sum(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
     return;
   }
@@ -720,6 +750,7 @@ void backward(State& st, const Batch& bt, int precision) {
     ProfScope ps(ctx, kProfGemmWgrad, gemm_bytes(kin, cols, rows, 2, 2, 4), 2.0 * rows * kin * cols);
     gemm_wgrad_bf16(ctx, rows, kin, cols, bt.x_in.as<bf16>(), bt.x_ld, dxb, ldb, G + w.off, w.blk.cols(),
                     st.ws_wgrad);
+    charge_all_reduce(ctx, kInputFeatureLayout.row, w.n, wire_bytes(wire));
     all_reduce_sum(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
   }
 }
@@ -728,6 +759,8 @@ void backward(State& st, const Batch& bt, int precision) {
 void dp_sync(State& st) {
   Ctx& ctx = *st.ctx;
   const int gd = ctx.grid.dims[0];
+  PhaseScope ps(ctx, kPhaseDpSync);
+  for (const ParamSlot& p : st.params) charge_all_reduce(ctx, kD, p.n, 4);  // one all-reduce per view (model.hpp:428-429)
   all_reduce_sum(ctx, kD, st.G.as<float>(), st.total, false);
   if (gd > 1) scale(ctx, st.G.as<float>(), st.total, 1.0f / static_cast<float>(gd));
 }

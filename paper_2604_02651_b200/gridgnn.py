@@ -142,6 +142,22 @@ class Context:
         check(lib().ggb_ctx_counters(self.h, c))
         return {"launches": int(c[0]), "h2d_bytes": int(c[1]), "d2h_bytes": int(c[2])}
 
+    AXES = ("D", "X", "Y", "Z")
+    PHASES = ("sampling", "forward", "backward", "dp_sync", "other")
+
+    def comm_stats(self, grid_total: bool = False, reset: bool = False) -> dict:
+        """CommStats (comm.hpp:75-117): the reference's byte accounting of the
+        logical collectives, {"bytes": {axis: {phase: n}}, "allreduce_calls":
+        {axis: n}, "allgather_calls": {axis: n}}. grid_total sums over every
+        rank (Communicator::snapshot; every rank must call it)."""
+        c = (C.c_uint64 * 28)()
+        check(lib().ggb_ctx_comm_stats(self.h, int(grid_total), int(reset), c))
+        return {
+            "bytes": {a: {p: int(c[i * 5 + j]) for j, p in enumerate(self.PHASES)} for i, a in enumerate(self.AXES)},
+            "allreduce_calls": {a: int(c[20 + i]) for i, a in enumerate(self.AXES)},
+            "allgather_calls": {a: int(c[24 + i]) for i, a in enumerate(self.AXES)},
+        }
+
     def launches(self) -> int:
         return self.counters()["launches"]
 

@@ -67,6 +67,17 @@ def main():
     ev = gg.build_eval_batch(ctx, g, seed)
     counts = gg.evaluate_full_graph(ctx, st, ev, g, prec)
     result["eval"] = (counts.correct, counts.total)
+    # CommStats (comm.hpp:385-403): the byte accounting of 2 train_run steps +
+    # one evaluation, summed over the grid, vs the reference's snapshot
+    ctx.comm_stats(reset=True)
+    sb = None
+    for t in range(2):
+        sb = gg.build_step_batch(ctx, g, b, gs, t, reuse=sb)
+        gg.train_step(ctx, st, sb, prec, seed, t)
+        gg.dp_sync(ctx, st)
+        gg.optimizer_step(ctx, st, gg.ADAM, 1e-3)
+    gg.evaluate_full_graph(ctx, st, ev, g, prec)
+    stats = ctx.comm_stats(grid_total=True)
     gathered = [None] * world
     dist.all_gather_object(gathered, result)
     if rank == 0:
@@ -130,6 +141,13 @@ def main():
         ev_dev = max(abs(evs[0][0][s] - int(want[s])) for s in range(3))
         ok &= ev_dev <= slack
         report.update(eval_correct_dev=ev_dev, eval_slack=slack)
+        want_stats = R.comm_stats(h, dims, ocfg, b, seed, 2, prec=ref_prec, evaluate=True)
+        stats_ok = stats == want_stats
+        if not stats_ok:
+            print(json.dumps({"comm_stats": stats, "want": want_stats}), flush=True)
+        ok &= stats_ok
+        report.update(comm_stats_equal=stats_ok,
+                      comm_bytes_total=sum(v for ax in stats["bytes"].values() for v in ax.values()))
         R.free_dataset(h)
         report = {k: float(v) for k, v in report.items()}
         print(json.dumps({"grid": dims, "prec": prec, "ok": bool(ok), **report}), flush=True)
