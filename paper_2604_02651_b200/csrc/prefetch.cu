@@ -15,6 +15,7 @@
 #include <thread>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -58,6 +59,15 @@ Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t see
     GGB_CUDA(cudaEventCreateWithFlags(&ready[s], cudaEventDisableTiming));
     GGB_CUDA(cudaEventCreateWithFlags(&released[s], cudaEventDisableTiming));
   }
+  {
+    const char* e = std::getenv("GGB_PF_TIMING");
+    timing = e && e[0] == '1';
+    if (timing)
+      for (int s = 0; s < 2; ++s) {
+        GGB_CUDA(cudaEventCreate(&tb[s]));
+        GGB_CUDA(cudaEventCreate(&te[s]));
+      }
+  }
   th = std::thread([this] { run(); });
 }
 
@@ -73,7 +83,14 @@ Prefetcher::~Prefetcher() {
   for (int s = 0; s < 2; ++s) {
     cudaEventDestroy(ready[s]);
     cudaEventDestroy(released[s]);
+    if (timing) {
+      cudaEventDestroy(tb[s]);
+      cudaEventDestroy(te[s]);
+    }
   }
+  if (timing && builds > 0)
+    std::fprintf(stderr, "[prefetch] %lld batch builds, %.3f ms device time each\n", static_cast<long long>(builds),
+                 build_ms / static_cast<double>(builds));
 }
 
 void Prefetcher::run() {
@@ -88,10 +105,12 @@ void Prefetcher::run() {
         if (stop) return;
       }
       if (k >= 2) GGB_CUDA(cudaStreamWaitEvent(sctx.stream, released[slot], 0));
+      if (timing) GGB_CUDA(cudaEventRecord(tb[slot], sctx.stream));
       const bool pre = preagg_enabled() && preagg_in_prefetch();
       build_step_batch(sctx, *g, b, seed, step0 + static_cast<uint64_t>(k), slots[slot], pre);
       if (pre && preagg_eligible(sctx, slots[slot])) preaggregate(sctx, slots[slot]);
       if (drop_layers > 0) make_masks(slots[slot], step0 + static_cast<uint64_t>(k));
+      if (timing) GGB_CUDA(cudaEventRecord(te[slot], sctx.stream));
       GGB_CUDA(cudaEventRecord(ready[slot], sctx.stream));
       {
         std::lock_guard<std::mutex> lk(m);
@@ -142,6 +161,13 @@ Batch* Prefetcher::next() {
   if (failed && produced <= consumed) std::rethrow_exception(err);
   const int slot = static_cast<int>(consumed & 1);
   GGB_CUDA(cudaStreamWaitEvent(consumer->stream, ready[slot], 0));
+  if (timing) {
+    float ms = 0.f;
+    GGB_CUDA(cudaEventSynchronize(te[slot]));
+    GGB_CUDA(cudaEventElapsedTime(&ms, tb[slot], te[slot]));
+    build_ms += ms;
+    ++builds;
+  }
   consumer->h2d_bytes += slots[slot].h2d_bytes;  // the batch's PCIe feature reads count for the consumer
   ++consumed;
   return &slots[slot];

@@ -23,6 +23,12 @@ struct Prefetcher {
   int64_t produced = 0, consumed = 0, released_count = 0;
   bool stop = false, failed = false;
   std::exception_ptr err;
+  // GGB_PF_TIMING=1: device time of each batch build on the sampling stream,
+  // summed and printed at destruction (diagnostic; syncs on each batch)
+  bool timing = false;
+  cudaEvent_t tb[2] = {}, te[2] = {};
+  double build_ms = 0.0;
+  int64_t builds = 0;
 
   // dropout keep-bits generated ahead with each batch (drop_layers == 0: none)
   uint64_t run_seed = 0;

@@ -41,6 +41,21 @@ struct SamplerWork {
   DevBuf cnt;       // int32 per-row kept counts
   DevBuf dev_misc;  // small device scalars (offsets, totals, counters)
   PinnedBuf host_misc;
+  // second stream of the build: the PCIe gather of host-resident features
+  // runs on it beside the shard extraction (created on first use, same
+  // priority as the build's stream)
+  struct Aux {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    Aux() = default;
+    Aux(const Aux&) = delete;
+    Aux& operator=(const Aux&) = delete;
+    ~Aux() {
+      if (s) cudaStreamDestroy(s);
+      if (fork) cudaEventDestroy(fork);
+      if (join) cudaEventDestroy(join);
+    }
+  } aux;
 };
 
 struct Ctx {

@@ -399,6 +399,15 @@ void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t
 
 }  // namespace
 
+// GGB_AUX_GATHER=0 keeps the PCIe feature gather on the build's stream
+bool aux_gather_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GGB_AUX_GATHER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
                       Batch& bt, bool want_xf) {
   require(b >= 2 && b <= g.n, "build_local_minibatch: need 2 <= b <= N");
@@ -437,6 +446,51 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
       bt.batch_off[a].assign(hmisc + m + k, hmisc + m + k + ctx.grid.dims[a] + 1);
       k += ctx.grid.dims[a] + 1;
     }
+  }
+
+  bt.p_ready = false;
+  // x_in (X,Z) = features[S rows of this X block, Z column block] (model.hpp:293-303).
+  // Needs only the sample and the batch offsets: host-resident features are
+  // gathered over PCIe on the second stream while the shard blocks are
+  // extracted on this one (joined before the build returns).
+  const bool gather_aside = g.features_on_host() && aux_gather_enabled();
+  {
+    const auto& xo = bt.batch_off[kInputFeatureLayout.row];
+    const int cx = ctx.coord[kInputFeatureLayout.row];
+    bt.x_r0 = xo[cx];
+    bt.x_r1 = xo[cx + 1];
+    bt.x_c0 = g.feat_c0;
+    bt.x_c1 = g.feat_c1;
+    const int64_t cols = bt.x_c1 - bt.x_c0;
+    bt.x_ld = round_up(std::max<int64_t>(cols, 1), 8);
+    const int64_t rows = bt.x_r1 - bt.x_r0;
+    bf16* xb = bt.x_in.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
+    bf16* xl = bt.x_in_lo.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
+    // fp32 rows too when the first layer will be pre-aggregated (one gather)
+    // (host-resident features: always, so the rows cross PCIe once)
+    bt.x_f_ready = (want_xf || g.features_on_host()) && preagg_enabled() && preagg_eligible(ctx, bt);
+    float* xf = bt.x_f_ready ? bt.x_f.reserve_n<float>(std::max<int64_t>(rows, 1) * bt.x_ld) : nullptr;
+    cudaStream_t xs = s;
+    if (gather_aside) {
+      SamplerWork::Aux& ax = ctx.sw.aux;
+      if (!ax.s) {
+        int prio = 0;
+        GGB_CUDA(cudaStreamGetPriority(s, &prio));
+        GGB_CUDA(cudaStreamCreateWithPriority(&ax.s, cudaStreamNonBlocking, prio));
+        GGB_CUDA(cudaEventCreateWithFlags(&ax.fork, cudaEventDisableTiming));
+        GGB_CUDA(cudaEventCreateWithFlags(&ax.join, cudaEventDisableTiming));
+      }
+      GGB_CUDA(cudaEventRecord(ax.fork, s));
+      GGB_CUDA(cudaStreamWaitEvent(ax.s, ax.fork, 0));
+      xs = ax.s;
+    }
+    if (rows > 0) {
+      launch_gather_x(ctx, xs, g.features_on_host(), rows, cols, bt.x_ld, d_sample, bt.x_r0, g.feat_ptr, cols, xb,
+                      xl, xf, bt.x_ld);
+      ctx.launches += 1;
+    }
+    bt.h2d_bytes = g.features_on_host() ? static_cast<uint64_t>(rows) * cols * 4 : 0;
+    ctx.h2d_bytes += bt.h2d_bytes;
   }
 
   // Plane blocks. Identical static shards (e.g. every plane on 1x1x1 grids)
@@ -503,31 +557,9 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
   for (size_t k = 0; k < nk; ++k)
     fill_block(ctx, g.shards[keys[k].shard], d_sample, keys[k].rl, keys[k].cl, b, g.n, bt.csrs[k]);
 
-  bt.p_ready = false;
-  // x_in (X,Z) = features[S rows of this X block, Z column block] (model.hpp:293-303)
-  {
-    const auto& xo = bt.batch_off[kInputFeatureLayout.row];
-    const int cx = ctx.coord[kInputFeatureLayout.row];
-    bt.x_r0 = xo[cx];
-    bt.x_r1 = xo[cx + 1];
-    bt.x_c0 = g.feat_c0;
-    bt.x_c1 = g.feat_c1;
-    const int64_t cols = bt.x_c1 - bt.x_c0;
-    bt.x_ld = round_up(std::max<int64_t>(cols, 1), 8);
-    const int64_t rows = bt.x_r1 - bt.x_r0;
-    bf16* xb = bt.x_in.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
-    bf16* xl = bt.x_in_lo.reserve_n<bf16>(std::max<int64_t>(rows, 1) * bt.x_ld);
-    // fp32 rows too when the first layer will be pre-aggregated (one gather)
-    // (host-resident features: always, so the rows cross PCIe once)
-    bt.x_f_ready = (want_xf || g.features_on_host()) && preagg_enabled() && preagg_eligible(ctx, bt);
-    float* xf = bt.x_f_ready ? bt.x_f.reserve_n<float>(std::max<int64_t>(rows, 1) * bt.x_ld) : nullptr;
-    if (rows > 0) {
-      launch_gather_x(ctx, s, g.features_on_host(), rows, cols, bt.x_ld, d_sample, bt.x_r0, g.feat_ptr, cols, xb,
-                      xl, xf, bt.x_ld);
-      ctx.launches += 1;
-    }
-    bt.h2d_bytes = g.features_on_host() ? static_cast<uint64_t>(rows) * cols * 4 : 0;
-    ctx.h2d_bytes += bt.h2d_bytes;
+  if (gather_aside) {  // join the PCIe gather
+    GGB_CUDA(cudaEventRecord(ctx.sw.aux.join, ctx.sw.aux.s));
+    GGB_CUDA(cudaStreamWaitEvent(s, ctx.sw.aux.join, 0));
   }
   int32_t* lab = bt.labels.reserve_n<int32_t>(b);
   k_gather_labels<<<blocks(b), kThreads, 0, s>>>(b, d_sample, g.labels.as<int32_t>(), lab);
