@@ -166,3 +166,32 @@ def test_numpy_adam_matches_reference(orc, ref):
             assert np.max(np.abs(a - w)) < 1e-6
     finally:
         ref.free_dataset(h)
+
+
+def test_reference_comm_stats_accounting(orc, ref):
+    """The accounting the GPU path is checked against (tests/test_gpu_commstats.py,
+    tests/mgpu_worker.py): the reference's CommStats snapshot. Acceptance
+    criterion 6 (Fig. 9): with a fixed PMM grid, per-group X bytes
+    per step are exactly constant as G_d grows, D bytes follow the
+    ring-equivalent rule, sampling is communication-free, and singleton groups
+    charge nothing but still count their calls."""
+    n, d_in, ncls, b, seed = 1200, 10, 5, 300, 4
+    ds = orc.generate_synthetic(n, 8.0, d_in, ncls, 1)
+    h = ref.dataset_from(ds, orc.synthetic_edges(n, 8.0, 1))
+    try:
+        cfg = orc.ModelConfig(d_in=d_in, d_out=ncls, layers=2, d_h=32)
+        one = ref.comm_stats(h, (1, 1, 1, 1), cfg, b, seed, 1)
+        assert all(v == 0 for ax in one["bytes"].values() for v in ax.values())
+        assert one["allreduce_calls"]["D"] == len(cfg.param_shapes())  # dp_sync: one per parameter view
+        per_group = []
+        for gd in (1, 2, 4):
+            s = ref.comm_stats(h, (gd, 2, 1, 1), cfg, b // gd * gd, seed, 1)
+            assert s["bytes"]["Y"] == s["bytes"]["Z"] == {p: 0 for p in s["bytes"]["Y"]}
+            assert all(ax["sampling"] == 0 for ax in s["bytes"].values())
+            per_group.append((s["bytes"]["X"]["forward"] // gd, s["bytes"]["X"]["backward"] // gd))
+            dp = s["bytes"]["D"]["dp_sync"]
+            # every rank all-reduces its parameter block over D: count * 4 * (gd-1)/gd each
+            assert (dp == 0) if gd == 1 else (dp > 0)
+        assert per_group[0] == per_group[1] == per_group[2]
+    finally:
+        ref.free_dataset(h)
