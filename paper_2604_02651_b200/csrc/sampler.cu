@@ -232,16 +232,21 @@ __device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) 
 }
 __device__ __forceinline__ float lo_of(float v) { return v - __bfloat162float(__float2bfloat16_rn(v)); }
 
-template <int U>  // rows in flight per warp (U > 1 for the PCIe-latency-bound host gather)
+// U: rows in flight per warp (U > 1 for the PCIe-latency-bound host gather);
+// Q: 16-byte quads per lane (rows of <= 128 Q floats). Q is sized to the row
+// so the register footprint stays small: the host gather runs for
+// milliseconds beside the step's persistent SpMM / GEMM CTAs and must fit the
+// register file next to them (Q = 4 at U = 4 took 102 registers per thread,
+// which kept those CTAs off the SMs holding gather blocks)
+template <int U, int Q>
 __global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t* __restrict__ sample,
                            int64_t row_lo, const float* __restrict__ feats, int64_t fld,
                            bf16* __restrict__ xb, bf16* __restrict__ xl, float* __restrict__ xf, int64_t xfld) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const bool vec = (cols & 3) == 0 && (fld & 3) == 0 && (ld & 3) == 0 && (!xf || (xfld & 3) == 0) && ld <= 128 * 4;
+  const bool vec = (cols & 3) == 0 && (fld & 3) == 0 && (ld & 3) == 0 && (!xf || (xfld & 3) == 0) && ld <= 128 * Q;
   if (vec) {
-    constexpr int Q = 4;  // up to 4 quads per lane: rows of <= 512 floats
     for (int64_t rb = w0; rb < rows; rb += nw * U) {
       float4 x[U][Q];
 #pragma unroll
@@ -303,12 +308,21 @@ void launch_gather_x(const Ctx& ctx, cudaStream_t s, bool host, int64_t rows, in
                      float* xf, int64_t xfld) {
   if (rows <= 0) return;
   if (host) {
-    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 8 * 4), host_gather_blocks()));
-    k_gather_x<4><<<std::max(blocks, 1u), 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+    const unsigned blocks =
+        std::max(1u, static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 8 * 4), host_gather_blocks())));
+    if (ld <= 128)
+      k_gather_x<4, 1><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+    else if (ld <= 256)
+      k_gather_x<4, 2><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+    else
+      k_gather_x<4, 4><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
   } else {
     const unsigned blocks =
         static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8), ctx.num_sms * 64)));
-    k_gather_x<1><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+    if (ld <= 128)
+      k_gather_x<1, 1><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+    else
+      k_gather_x<1, 4><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
   }
   GGB_LAUNCH_CHECK();
 }
