@@ -25,6 +25,9 @@ struct FwdApply {
   bf16* outb;  // bf16 copy (nullable) = hi part of the split pair
   bf16* outlo; // bf16 lo part (nullable): out == hi + lo to ~2^-16
   int64_t ldob;
+  uint8_t* outp;  // 24-bit copy for the next SpMM's gather (nullable): per row [hi16 x C16][lo8 x C16]
+  int64_t ldp;    // its row stride in bytes
+  int64_t hoff;   // byte offset of the lo8 plane (2 * C16)
   const uint32_t* keep;  // precomputed dropout keep-bits (same layout) or null: hash in-kernel
   uint32_t* mask;  // [rows][ldm] keep bits, row-kernel layout (see kRowChunk)
   int64_t ldm;     // words per row = mask_words(cols)
@@ -117,6 +120,10 @@ void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, con
               const bf16* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb,
               int64_t ldob, int accumulate);
 // fp32 feature operand; optional split-bf16 (hi, lo) outputs
+/// Forward SpMM over 24-bit rows (spmm_pipe.cu P24): out = A . F to the split
+/// bf16 pair; false when the pipelined kernel does not apply (caller falls back).
+bool spmm_pipe_p24(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
+                   const uint8_t* f, int64_t ld_bytes, int64_t fcols, bf16* out_hi, bf16* out_lo, int64_t ldob);
 void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
                   const float* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* out_hi,
                   bf16* out_lo, int64_t ldob, int accumulate);

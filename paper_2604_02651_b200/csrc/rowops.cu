@@ -62,6 +62,26 @@ __device__ __forceinline__ void st4_bf16(bf16* row, int64_t c, int64_t n, const 
     for (int i = 0; i < 4 && c + i < n; ++i) row[c + i] = __float2bfloat16_rn(v[i]);
   }
 }
+// fp32 -> 24 bits (round to nearest even at bit 8): the P24 gather format
+__device__ __forceinline__ uint32_t round24(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b + 0x7fu + ((b >> 8) & 1u)) & 0xffffff00u;
+}
+__device__ __forceinline__ void st4_p24(uint8_t* row, int64_t hoff, int64_t c, int64_t n, const float* v) {
+  uint32_t r[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r[i] = round24(v[i]);
+  if (c + 4 <= n) {
+    *reinterpret_cast<uint2*>(row + 2 * c) = make_uint2(__byte_perm(r[0], r[1], 0x7632), __byte_perm(r[2], r[3], 0x7632));
+    *reinterpret_cast<uint32_t*>(row + hoff + c) =
+        __byte_perm(__byte_perm(r[0], r[1], 0x0051), __byte_perm(r[2], r[3], 0x0051), 0x5410);
+  } else {
+    for (int i = 0; i < 4 && c + i < n; ++i) {
+      reinterpret_cast<uint16_t*>(row)[c + i] = static_cast<uint16_t>(r[i] >> 16);
+      row[hoff + c + i] = static_cast<uint8_t>(r[i] >> 8);
+    }
+  }
+}
 __device__ __forceinline__ void f4(const float4& a, float* v) {
   v[0] = a.x;
   v[1] = a.y;
@@ -194,6 +214,7 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
         o[i] = y[j][i] * (on ? sc_on : 0.f) + res[j][i];
       }
       if (p.out) st4(p.out + r * p.ldo, c, ncols, o);
+      if (p.outp) st4_p24(p.outp + r * p.ldp, p.hoff, c, ncols, o);
       if (p.outb) {
         st4_bf16(p.outb + r * p.ldob, c, ncols, o);
         if (p.outlo) {

@@ -13,10 +13,18 @@
 // The consumer accumulates in fp32 registers (lane l owns 16-byte chunks l and
 // l+32 of the row) and flushes a row when the stream crosses its row_ptr
 // boundary; empty rows flush zeros.
+#include <type_traits>
+
 #include "runtime.hpp"
 
 namespace ggb {
 namespace {
+
+// 24-bit rows (the forward's layer activations, written by the fused row
+// kernel): each value's fp32 bits rounded to the nearest multiple of 2^8,
+// stored as a 16-bit high plane [C16 x u16] then an 8-bit low plane
+// [C16 x u8] (C16 = cols rounded up to 8); decoded as (hi << 16) | (lo << 8).
+struct P24 {};
 
 constexpr int kWarps = 16;
 constexpr int kStages = 3;
@@ -37,6 +45,8 @@ struct PipeArgs {
   bf16* outlo;
   int64_t ldob;
   int accumulate;
+  int ocpr;  // output chunks of EPC columns (the flush's unit)
+  int hoff;  // P24: byte offset of the low plane in a row
 };
 
 __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -58,10 +68,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // TIn: element type of F; RB: smem bytes per gathered row.
 template <class TIn, int RB>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) {
-  constexpr int EPC = 16 / static_cast<int>(sizeof(TIn));  // elements per 16-byte chunk
-  constexpr int CPR = RB / 16;                              // chunks per row slot
-  constexpr int S = kStageBytes / RB;                       // nonzeros per stage
-  constexpr int CPL = CPR > 32 ? 2 : 1;                     // chunks per lane (consumer)
+  constexpr bool kP24 = std::is_same_v<TIn, P24>;
+  constexpr int EPC = kP24 ? 8 : 16 / static_cast<int>(sizeof(TIn));  // elements per lane chunk
+  constexpr int CPR = RB / 16;                                         // 16-byte chunks per row slot
+  constexpr int S = kStageBytes / RB;                                  // nonzeros per stage
+  constexpr int CPL = kP24 ? 1 : (CPR > 32 ? 2 : 1);                   // chunks per lane (consumer)
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint8_t* ring = smem + static_cast<size_t>(wib) * kStages * kStageBytes;
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
     for (int q = 0; q < CPL; ++q) {
       const int ch = lane + 32 * q;
       const int64_t cc = static_cast<int64_t>(ch) * EPC;
-      if (ch < a.vcpr) {
+      if (ch < a.ocpr) {
         const bool whole = cc + EPC <= a.fcols;
         if (a.out) {
           float* dst = a.out + row * a.ldo + cc;
@@ -202,6 +213,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
           row_end_e = a.rp[row + 1];
         }
         const float v = meta_val[slot * 32 + k];
+        if constexpr (kP24) {
+          if (lane < a.ocpr) {  // lane owns columns 8 lane .. 8 lane + 7
+            const uint4 h = *reinterpret_cast<const uint4*>(base + k * RB + lane * 16);
+            const uint2 w = *reinterpret_cast<const uint2*>(base + k * RB + a.hoff + lane * 8);
+            const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[2] = {w.x, w.y};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t hi = (i & 1) ? (hw[i >> 1] & 0xffff0000u) : (hw[i >> 1] << 16);
+              const uint32_t lo = __byte_perm(lw[i >> 2], 0u, 0x4404u | ((i & 3) << 4));  // byte (i&3) -> byte 1
+              acc[0][i] = fmaf(v, __uint_as_float(hi | lo), acc[0][i]);
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
           const int ch = lane + 32 * q;
@@ -270,6 +295,7 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
   a.outlo = outlo;
   a.ldob = ldob;
   a.accumulate = accumulate;
+  a.ocpr = a.vcpr;
   if (esize == 2) {
     if (row_bytes <= 256)
       launch_pipe<bf16, 256>(ctx, a);
@@ -285,6 +311,39 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
     else
       launch_pipe<float, 1024>(ctx, a);
   }
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+  return true;
+}
+
+// Forward SpMM gathering 24-bit rows (see P24): fcols <= 256, row stride
+// ld_bytes (a multiple of 16, >= 3 * round_up(fcols, 8)).
+bool spmm_pipe_p24(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
+                   const uint8_t* f, int64_t ld_bytes, int64_t fcols, bf16* out_hi, bf16* out_lo, int64_t ldob) {
+  const int64_t c16 = round_up(fcols, 8);
+  const int64_t row_bytes = round_up(3 * c16, 16);
+  if (rows <= 0 || fcols <= 0 || fcols > 256 || ctx.side_stream) return false;
+  require(ld_bytes % 16 == 0 && ld_bytes >= row_bytes && (reinterpret_cast<uintptr_t>(f) & 15) == 0,
+          "spmm: 24-bit rows need 16-byte aligned rows");
+  if (ld_bytes >= (int64_t{1} << 32)) return false;
+  PipeArgs a{};
+  a.rows = rows;
+  a.rp = rp;
+  a.col = col;
+  a.val = val;
+  a.F = f;
+  a.ldf_bytes = static_cast<uint32_t>(ld_bytes);
+  a.vcpr = static_cast<int>(row_bytes / 16);
+  a.fcols = static_cast<int>(fcols);
+  a.outb = out_hi;
+  a.outlo = out_lo;
+  a.ldob = ldob;
+  a.ocpr = static_cast<int>(c16 / 8);
+  a.hoff = static_cast<int>(2 * c16);
+  if (row_bytes <= 384)
+    launch_pipe<P24, 384>(ctx, a);
+  else
+    launch_pipe<P24, 768>(ctx, a);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
   return true;

@@ -229,6 +229,17 @@ bool preagg_enabled() {
   return !(e && e[0] == '0');
 }
 
+// GGB_GATHER24=1: the fused row kernel also writes a 24-bit copy of each
+// layer's activations and the next forward SpMM gathers it (3 instead of 4
+// bytes per element, 2^-16 relative like the split-bf16 GEMMs). Measured at
+// C2: forward SpMM 2.75 -> 2.24 ms/step, but the step only 10.73 -> 10.60 ms
+// (the sampling stream's batch build is the critical chain) and e2e 11.43 ->
+// 11.66 ms (the extra write traffic lands on the build), so it is off.
+bool gather24_enabled() {
+  const char* e = std::getenv("GGB_GATHER24");
+  return e && e[0] == '1';
+}
+
 bool preagg_in_prefetch() {
   const char* e = std::getenv("GGB_PREAGG_PF");
   return !(e && e[0] == '0');
@@ -257,6 +268,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     st.x0.ldf = ld8(ob.cols());
     st.x0.ldb = ld8(ob.cols());
     st.x0.f = grow<float>(st.x0_f, ob.rows() * st.x0.ldf);
+    st.x0.p = nullptr;
     st.x0.b = grow<bf16>(st.x0_b, ob.rows() * st.x0.ldb);
     // accurate: X0 stays fp32 (the next SpMM gathers fp32); fast: + bf16 operand copy
     const bool want_b = st.compute != kAccurate;
@@ -349,11 +361,16 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
               cast_bf16(ctx, L.hagg.f + r0 * ldf, r1 - r0, hb.cols(), ldf, L.hagg.b + r0 * ldb, ldb);
           });
     } else {
-    ProfScope ps(ctx, kProfSpmmFwd, spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, accurate ? 4 : 2),
+    // accurate: the gathered rows are the previous layer's 24-bit copies when
+    // it wrote them (3 bytes per element instead of 4)
+    const bool p24 = accurate && prev->p != nullptr;
+    ProfScope ps(ctx, kProfSpmmFwd, spmm_bytes(A.n_rows, A.nnz, F.cols(), p24 ? 3 : (accurate ? 4 : 2), accurate ? 4 : 2),
                  2.0 * A.nnz * F.cols());
     if (accurate) {
-      spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), nullptr, 0, L.hagg.b, L.hagg.lo,
-                   L.hagg.ldb, 0);
+      if (!(p24 && spmm_pipe_p24(ctx, A.n_rows, arp, acol, aval, prev->p, prev->ldp, F.cols(), L.hagg.b, L.hagg.lo,
+                                 L.hagg.ldb)))
+        spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), nullptr, 0, L.hagg.b, L.hagg.lo,
+                     L.hagg.ldb, 0);
     } else {
       spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
     }
@@ -455,6 +472,19 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     fa.outlo = L.x.lo;
     fa.ldob = L.x.ldb;
     fa.mask = grow<uint32_t>(L.mask, xb.rows() * L.ldm);
+    // 24-bit copy of X_l for the next layer's forward SpMM (its gathers are
+    // the step's largest traffic) when that SpMM runs whole on this rank
+    L.x.p = nullptr;
+    if (accurate && !last && gather24_enabled() && xb.cols() <= 256 &&
+        trivial(ctx, adjacency_layout(l + 1).col)) {
+      const int64_t c16 = round_up(xb.cols(), 8);
+      L.x.hoff = 2 * c16;
+      L.x.ldp = round_up(3 * c16, 16);
+      L.x.p = grow<uint8_t>(L.x_p, xb.rows() * L.x.ldp);
+    }
+    fa.outp = L.x.p;
+    fa.ldp = L.x.ldp;
+    fa.hoff = L.x.hoff;
     fa.ldm = L.ldm;
     fa.keep = nullptr;  // keep-bits precomputed by the prefetcher for exactly this block?
     if (drop && bt.masks.size() >= static_cast<size_t>(l)) {
@@ -465,7 +495,8 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     }
     {
       const double e = static_cast<double>(xb.rows()) * xb.cols();
-      ProfScope ps(ctx, kProfFwdRow, e * (4 + (res ? 4 : 0) + 4 + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0)) + e / 8);
+      ProfScope ps(ctx, kProfFwdRow,
+                   e * (4 + (res ? 4 : 0) + 4 + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0) + (L.x.p ? 3 : 0)) + e / 8);
       fwd_apply(ctx, fa);
     }
     prev = &L.x;

@@ -33,6 +33,8 @@ struct Tensor {  // device activation block: fp32 and/or bf16 copy (+ lo of the 
   bf16* b = nullptr;
   bf16* lo = nullptr;
   int64_t ldb = 0;
+  uint8_t* p = nullptr;  // 24-bit gather copy (spmm_pipe.cu P24): row stride ldp bytes, lo plane at hoff
+  int64_t ldp = 0, hoff = 0;
 };
 
 /// Compute precision of the forward pass. kAccurate (default): fp32
@@ -42,7 +44,7 @@ struct Tensor {  // device activation block: fp32 and/or bf16 copy (+ lo of the 
 enum Compute : int { kAccurate = 0, kFast = 1 };
 
 struct LayerBufs {
-  DevBuf hagg_f, hagg_b, hagg_lo, xw, ss, rms, mask, x_f, x_b, x_lo;
+  DevBuf hagg_f, hagg_b, hagg_lo, xw, ss, rms, mask, x_f, x_b, x_lo, x_p;
   Tensor hagg, xw_t, x;  // x = layer output X_l
   int64_t ldm = 0;
 };

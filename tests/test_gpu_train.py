@@ -43,10 +43,14 @@ CFGS = [
 
 # preagg "1": the first layer as (A_0 . x_in) . W_in (default on this grid);
 # "0": the reference's association A_0 . (x_in . W_in)
+# gather24 "1": the forward SpMMs gather 24-bit copies of the layer activations
+# (opt-in, GGB_GATHER24=1; same tolerances)
+@pytest.mark.parametrize("gather24", ["0", "1"])
 @pytest.mark.parametrize("preagg", ["1", "0"])
 @pytest.mark.parametrize("cfg_kw", CFGS)
-def test_train_step_matches_reference(gg, orc, ref, cfg_kw, preagg, monkeypatch):
+def test_train_step_matches_reference(gg, orc, ref, cfg_kw, preagg, gather24, monkeypatch):
     monkeypatch.setenv("GGB_PREAGG", preagg)
+    monkeypatch.setenv("GGB_GATHER24", gather24)
     n, d_in, ncls, b, seed, step = 4000, 24, 7, 1000, 7, 4
     ds, h, ctx, g = _setup(gg, orc, ref, n, 10.0, d_in, ncls, 3, cfg_kw["layers"])
     try:
