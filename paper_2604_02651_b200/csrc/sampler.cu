@@ -435,16 +435,27 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
   int64_t* d_sample = bt.sample.reserve_n<int64_t>(b);
   sample_set(ctx, g.n, b, group_seed, step, d_sample);
 
-  // batch_off[a] = sample_partition(S, block_partition(N, g_a)) (model.hpp:257-259)
+  // batch_off[a] = sample_partition(S, block_partition(N, g_a)) (model.hpp:257-259);
+  // with X, Y and Z unsplit every partition is [0, N), so every offset list is
+  // {0, b} and the device rank query (a host round trip) is skipped
+  const bool flat = ctx.grid.dims[1] == 1 && ctx.grid.dims[2] == 1 && ctx.grid.dims[3] == 1;
+  int64_t* dmisc = nullptr;
+  int64_t* hmisc = nullptr;
+  int m = 0;
+  if (flat) {
+    for (int a = 1; a < 4; ++a) bt.batch_off[a] = {0, b};
+    dmisc = ctx.sw.dev_misc.reserve_n<int64_t>(64);
+    hmisc = static_cast<int64_t*>(ctx.sw.host_misc.reserve(64 * 8));
+  } else {
   std::vector<int64_t> q;
   for (int a = 1; a < 4; ++a) {
     auto off = block_partition(g.n, ctx.grid.dims[a]);
     q.insert(q.end(), off.begin(), off.end());
   }
-  const int m = static_cast<int>(q.size());
+  m = static_cast<int>(q.size());
   // device scratch: [0,m) queries, [m,2m) ranks, [2m, 2m+2) extracted counters
-  int64_t* dmisc = ctx.sw.dev_misc.reserve_n<int64_t>(2 * m + 64);
-  int64_t* hmisc = static_cast<int64_t*>(ctx.sw.host_misc.reserve((2 * m + 64) * 8));
+  dmisc = ctx.sw.dev_misc.reserve_n<int64_t>(2 * m + 64);
+  hmisc = static_cast<int64_t*>(ctx.sw.host_misc.reserve((2 * m + 64) * 8));
   std::copy(q.begin(), q.end(), hmisc);
   GGB_CUDA(cudaMemcpyAsync(dmisc, hmisc, m * 8, cudaMemcpyHostToDevice, s));
   k_ranks<<<1, 128, 0, s>>>(m, dmisc, ctx.sw.bitmap.as<uint32_t>(), ctx.sw.wpfx.as<int32_t>(),
@@ -460,6 +471,7 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
       bt.batch_off[a].assign(hmisc + m + k, hmisc + m + k + ctx.grid.dims[a] + 1);
       k += ctx.grid.dims[a] + 1;
     }
+  }
   }
 
   bt.p_ready = false;
