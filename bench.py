@@ -327,6 +327,38 @@ def main():
     barrier()
     prof = ctx.profile_read(reset=True)
     ctx.profile(False)
+    # ---- sampling only: build_step_batch alone on the main
+    # stream (prefetcher stopped), the reference's communication-free sampler +
+    # induced-subgraph CSR build (model.hpp:250-309); not part of `value`
+    if pf:
+        pf.close()
+        pf = None
+    samp_info = None
+    sbatch = None
+    sbatch = gg.build_step_batch(ctx, graph, b, group_seed, gstep, reuse=sbatch)  # warm (buffers sized)
+    s_reps = max(3, min(args.steps, 10))
+    barrier()
+    ctx.profile(True)
+    ctx.profile_read(reset=True)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for i in range(s_reps):
+        gg.build_step_batch(ctx, graph, b, group_seed, gstep + 1 + i, reuse=sbatch)
+    s1.record(stream)
+    barrier()
+    sprof = ctx.profile_read(reset=True)["sampling"]
+    ctx.profile(False)
+    ms_build = max_over_ranks(s0.elapsed_time(s1)) / s_reps
+    samp_info = {
+        "build_ms": ms_build, "sampled_vertices_per_s": b * gd / (ms_build / 1e3),
+        "nnz_kept_per_build": sbatch.nnz_kept, "nnz_extracted_per_build": sbatch.nnz_extracted,
+        "kept_nnz_per_s": sbatch.nnz_kept * gd / (ms_build / 1e3),
+        "device_ms": sprof["ms"] / s_reps,
+        "GB_per_s": sprof["bytes"] / (sprof["ms"] / 1e3) / 1e9 if sprof["ms"] > 0 else None,
+        "builds": s_reps,
+        "note": "events around build_step_batch on the main stream (host round trips included); device_ms and "
+                "GB_per_s from the sampler's own kernel-class events over its algorithmic bytes (SURVEY 8d)"}
+    del sbatch
     # ---- per-epoch full-graph evaluation (train_run's evaluate_full_graph), timed
     # separately: the reference's epoch time excludes it; it is the
     # paper's full-graph inference metric
@@ -470,6 +502,7 @@ def main():
         "loss_last": losses[-1] if losses else None,
         "graph_build_s": t_graph,
         "eval": ev_info,
+        "sampling_only": samp_info,
         "step_ms_rank0": step_ms,
         "e2e_step_ms_rank0": e2e_step_ms,
     }
