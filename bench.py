@@ -254,7 +254,10 @@ def main():
         graph.features_to_host()
     t_graph = time.time() - t0
     gd = dims[0]
-    b = cfg["batch"] // gd  # per data-parallel group: the global batch stays fixed
+    # per data-parallel group: the global batch stays fixed, rounded up so that
+    # b * Gd >= B and the epoch keeps ceil(n / B) steps (steps_per_epoch,
+    # model.hpp:539-542) at every Gd (612,500 / 8 is not an integer)
+    b = -(-cfg["batch"] // gd)
     S = math.ceil(cfg["n"] / (b * gd))
     mcfg = gg.ModelConfig(layers=cfg["layers"], d_in=cfg["d_in"], d_h=cfg["d_h"], d_out=cfg["n_classes"],
                           dropout_rate=DROPOUT)
@@ -475,7 +478,7 @@ def main():
         "dtype": "bf16",
         "data": "synthetic",
         "config": {
-            "workload": cfg["workload"], "config_id": args.config, "global_batch": cfg["batch"],
+            "workload": cfg["workload"], "config_id": args.config, "global_batch": b * gd,
             "batch_per_dp_group": b, "steps_per_epoch": S, "grid": "x".join(map(str, dims)),
             "layers": cfg["layers"], "hidden": cfg["d_h"], "d_in": cfg["d_in"], "classes": cfg["n_classes"],
             "n_vertices": cfg["n"], "nnz": graph.nnz, "compute": args.compute, "precision": args.precision,
