@@ -165,6 +165,14 @@ def reference_baseline(cfg: dict, steps: int, warmup: int, cores: int | None = N
     }
 
 
+def group_batch(batch: int, gd: int) -> int:
+    """Per data-parallel group batch: the global batch stays fixed, rounded up
+    so that b * Gd >= B and the epoch keeps ceil(n / B) steps
+    (steps_per_epoch, model.hpp:539-542) at every Gd (612,500 / 8 is not an
+    integer)."""
+    return -(-batch // gd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -254,10 +262,7 @@ def main():
         graph.features_to_host()
     t_graph = time.time() - t0
     gd = dims[0]
-    # per data-parallel group: the global batch stays fixed, rounded up so that
-    # b * Gd >= B and the epoch keeps ceil(n / B) steps (steps_per_epoch,
-    # model.hpp:539-542) at every Gd (612,500 / 8 is not an integer)
-    b = -(-cfg["batch"] // gd)
+    b = group_batch(cfg["batch"], gd)
     S = math.ceil(cfg["n"] / (b * gd))
     mcfg = gg.ModelConfig(layers=cfg["layers"], d_in=cfg["d_in"], d_h=cfg["d_h"], d_out=cfg["n_classes"],
                           dropout_rate=DROPOUT)
