@@ -262,6 +262,12 @@ int ggb_gemm_wgrad_bf16(ggb_ctx_t ctx, int64_t m, int64_t kw, int64_t nw, const 
 int ggb_spmm_csr(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const int32_t* col,
                  const float* val, const void* f, int64_t ldf, int64_t fcols, float* out,
                  int64_t ldo, void* out_bf16, int64_t ldob, int32_t accumulate);
+/* Same with fp32 F (the accurate forward's gathers; pmm.hpp:160 casts the fp64
+ * value to Real and accumulates in Real): out fp32 and/or the bf16 (hi, lo)
+ * split pair of the fp32 result (out_hi, out_lo may be NULL). */
+int ggb_spmm_csr_f32(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const int32_t* col,
+                     const float* val, const float* f, int64_t ldf, int64_t fcols, float* out,
+                     int64_t ldo, void* out_hi, void* out_lo, int64_t ldob, int32_t accumulate);
 
 #ifdef __cplusplus
 }

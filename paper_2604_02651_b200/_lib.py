@@ -86,6 +86,7 @@ _SIGS = [
     ("ggb_gemm_split_bf16", C.c_int, [P, I64, I64, I64, P, P, I64, P, P, I64, P, I64]),
     ("ggb_gemm_wgrad_bf16", C.c_int, [P, I64, I64, I64, P, I64, P, I64, P, I64]),
     ("ggb_spmm_csr", C.c_int, [P, I64, P, P, P, P, I64, I64, P, I64, P, I64, I32]),
+    ("ggb_spmm_csr_f32", C.c_int, [P, I64, P, P, P, P, I64, I64, P, I64, P, P, I64, I32]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGS]

@@ -960,4 +960,14 @@ int ggb_spmm_csr(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const int3
   });
 }
 
+int ggb_spmm_csr_f32(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const int32_t* col, const float* val,
+                     const float* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, void* out_hi,
+                     void* out_lo, int64_t ldob, int32_t accumulate) {
+  return guard([&] {
+    use_device(*ctx);
+    spmm_csr_f32(*ctx, rows, row_ptr, col, val, f, ldf, fcols, out, ldo, static_cast<bf16*>(out_hi),
+                 static_cast<bf16*>(out_lo), ldob, accumulate);
+  });
+}
+
 }  // extern "C"

@@ -125,3 +125,35 @@ def test_spmm(env, gg, rows, fcols, deg, accumulate):
     want = A @ f[:, :fcols].float() + (base if accumulate else 0)
     assert (out - want).abs().max().item() < 1e-4 * max(1.0, want.abs().max().item())
     assert torch.equal(outb[:, :fcols], out.to(torch.bfloat16))
+
+
+# The accurate forward's SpMM: fp32 feature rows (k_spmm_pipe<float, RB>;
+# H = 256 gives 1 KB rows, the production instance of the C2/C3 step), fp32
+# accumulation in CSR order as pmm.hpp:157-164, optional split-bf16 output.
+@pytest.mark.parametrize("rows,frows,fcols,deg", [(20000, 30000, 256, 14), (1000, 900, 256, 40),
+                                                  (3000, 5000, 128, 9), (777, 900, 100, 30),
+                                                  (500, 600, 64, 5), (64, 300, 256, 200), (5, 7, 256, 3)])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_spmm_f32_rows(env, gg, rows, frows, fcols, deg, accumulate):
+    ctx, torch = env
+    rp, col, val = _random_csr(rows, frows, deg, rows + fcols + 1)
+    g = torch.Generator(device="cuda").manual_seed(fcols)
+    ldf = _ld8(fcols)
+    f = torch.zeros(frows, ldf, device="cuda")
+    f[:, :fcols] = torch.randn(frows, fcols, generator=g, device="cuda")
+    trp, tcol, tval = (torch.from_numpy(x).cuda() for x in (rp, col, val))
+    base = torch.randn(rows, fcols, device="cuda")
+    out = base.clone() if accumulate else torch.full((rows, fcols), float("nan"), device="cuda")
+    ldob = _ld8(fcols)
+    hi = torch.zeros(rows, ldob, dtype=torch.bfloat16, device="cuda")
+    lo = torch.zeros_like(hi)
+    gg.check(gg.lib().ggb_spmm_csr_f32(ctx.h, rows, trp.data_ptr(), tcol.data_ptr(), tval.data_ptr(), f.data_ptr(),
+                                       ldf, fcols, out.data_ptr(), fcols, hi.data_ptr(), lo.data_ptr(), ldob,
+                                       accumulate))
+    ctx.synchronize()
+    A = torch.sparse_csr_tensor(trp, tcol.long(), tval.double(), size=(rows, frows))
+    want = A @ f[:, :fcols].double() + (base.double() if accumulate else 0)
+    scale = max(1.0, want.abs().max().item())
+    assert (out.double() - want).abs().max().item() <= 1e-5 * scale
+    assert torch.equal(hi[:, :fcols], out.to(torch.bfloat16))
+    assert torch.equal(lo[:, :fcols], (out - hi[:, :fcols].float()).to(torch.bfloat16))

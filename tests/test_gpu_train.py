@@ -303,3 +303,65 @@ def test_wide_odd_input_features(gg, orc, ref, d_in):
             assert _rel(mine, want) <= GRAD_RTOL, (name, _rel(mine, want))
     finally:
         ref.free_dataset(h)
+
+
+# The headline shapes at reduced n: hidden 256 with the C2
+# (ogbn-products: d_in 100, 47 classes, avg degree 50.5) and C3 (Reddit: d_in
+# 602, 41 classes) model dims. At H = 256 the step runs the production kernel
+# instances of the C2 bench: k_spmm_pipe<float, 1024> (fp32 1 KB row gathers),
+# k_fwd_row<2, true> and k_bwd_row<2>, the 256-wide tcgen05 tiles.
+H256 = {"C2dims": dict(n=24000, deg=50.53, d_in=100, ncls=47),
+        "C3dims": dict(n=9000, deg=120.0, d_in=602, ncls=41)}
+
+
+@pytest.mark.parametrize("gather24", ["0", "1"])
+@pytest.mark.parametrize("preagg", ["1", "0"])
+@pytest.mark.parametrize("shape", list(H256))
+def test_train_step_h256_matches_reference(gg, orc, ref, shape, preagg, gather24, monkeypatch):
+    monkeypatch.setenv("GGB_PREAGG", preagg)
+    monkeypatch.setenv("GGB_GATHER24", gather24)
+    s = H256[shape]
+    n, d_in, ncls, seed, step = s["n"], s["d_in"], s["ncls"], 1, 2
+    b = n // 4
+    cfg_kw = dict(layers=3, d_h=256, dropout_rate=0.1)
+    ds, h, ctx, g = _setup(gg, orc, ref, n, s["deg"], d_in, ncls, 7, 3)
+    try:
+        gcfg = gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw)
+        st = gg.init_state(ctx, gcfg, seed)
+        batch = gg.build_step_batch(ctx, g, b, gg.hash_combine(seed, 0), step)
+        loss = gg.train_step(ctx, st, batch, gg.FP32, seed, step)
+        losses, logits, grads, _ = ref.train(h, (1, 1, 1, 1), orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), b,
+                                             seed, step0=step)
+        assert abs(loss - losses[0]) <= LOSS_RTOL * abs(losses[0]), (loss, losses[0])
+        _, lg = st.logits()
+        assert np.max(np.abs(lg - logits)) <= 2e-2 * max(1.0, np.max(np.abs(logits)))
+        for name, mine, want in zip(gcfg.param_names(), st.grads(), grads):
+            assert _rel(mine, want) <= GRAD_RTOL, (name, _rel(mine, want))
+    finally:
+        ref.free_dataset(h)
+
+
+@pytest.mark.parametrize("shape", list(H256))
+def test_h256_adam_trajectory_matches_reference(gg, orc, ref, shape):
+    """Four steps of train_run's loop (batch -> train_step -> dp_sync -> Adam)
+    at hidden 256: per-step losses and the final weights track the reference."""
+    s = H256[shape]
+    n, d_in, ncls, seed = s["n"], s["d_in"], s["ncls"], 1
+    b = n // 4
+    cfg_kw = dict(layers=3, d_h=256, dropout_rate=0.1)
+    ds, h, ctx, g = _setup(gg, orc, ref, n, s["deg"], d_in, ncls, 7, 3)
+    try:
+        st = gg.init_state(ctx, gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), seed)
+        got, batch = [], None
+        for t in range(4):
+            batch = gg.build_step_batch(ctx, g, b, gg.hash_combine(seed, 0), t, reuse=batch)
+            got.append(gg.train_step(ctx, st, batch, gg.FP32, seed, t))
+            gg.dp_sync(ctx, st)
+            gg.optimizer_step(ctx, st, gg.ADAM, 1e-3)
+        losses, _, _, W = ref.train(h, (1, 1, 1, 1), orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), b, seed, 0, 4,
+                                    optimizer=1, want_logits=False, want_weights=True)
+        assert np.all(np.abs(np.array(got) - losses) <= LOSS_RTOL * np.abs(losses)), (got, losses)
+        for mine, want in zip(st.weights(), W):
+            assert _rel(mine, want) <= 1e-3
+    finally:
+        ref.free_dataset(h)
