@@ -119,26 +119,41 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _host_ram_gb() -> float:
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 2**30
+    except (ValueError, OSError):
+        return 0.0
+
+
+# Peak RSS of the reference's full C2 step (measured on the GPU box host, 196 GB,
+# scripts/ref_full_probe.py): 1x2x2x2 59 GB, 1x2x2x4 94 GB -> ~24 GB + ~4.4 GB/rank
+REF_GRIDS = [(2, 2, 4), (2, 2, 3), (2, 2, 2), (1, 2, 2), (1, 1, 2), (1, 1, 1)]
+
+
+def reference_grid(cores: int, ram_gb: float, cfg: dict) -> tuple[int, int, int]:
+    """The largest PMM grid (one std::thread per rank, as train_run,
+    model.hpp:724-733) that fits the host's cores and RAM."""
+    scale = cfg["batch"] / 612_500 * cfg["d_h"] / 256  # activation footprint relative to C2
+    for g in REF_GRIDS:
+        ranks = g[0] * g[1] * g[2]
+        need = (24.0 + 4.4 * ranks) * max(scale, 0.05)
+        if ranks <= cores and (ram_gb <= 0 or need <= 0.85 * ram_gb):
+            return g
+    return (1, 1, 1)
+
+
 def reference_baseline(cfg: dict, steps: int, warmup: int, cores: int | None = None) -> dict:
     """The reference CPU implementation (oracle/_ref: /root/reference compiled
-    in place) timed on this host's cores on a bounded sample of the workload:
-    same graph, model and grid rule, batch reduced by a factor f, step time
-    scaled by f (linear in the batch; this UNDERSTATES the reference's cost,
-    since its SpMM/extraction work grows with batch^2 / n)."""
+    in place, unmodified) timed on this host's cores on the SAME workload: the
+    full global batch, the train_run step body (model.hpp:646-685: sample ->
+    forward + cross-entropy -> backward -> dp_sync -> Adam) with one thread
+    per rank of the largest PMM grid that fits the host. No scaling factor."""
     from oracle import oracle as O
 
     ncores = cores or os.cpu_count() or 1
-    # one std::thread per rank (train_run); the largest PMM grid <= cores, up to 3x3x3
-    best = (1, 1, 1)
-    for gx in (1, 2, 3):
-        for gy in (1, 2, 3):
-            for gz in (1, 2, 3):
-                if gx * gy * gz <= ncores and gx * gy * gz > best[0] * best[1] * best[2]:
-                    best = (gx, gy, gz)
-    dims = (1, *best)
-    target = 20_000  # rows per sampled step: a few seconds of reference work on ~8 cores
-    f = max(1, cfg["batch"] // target)
-    b_s = max(2, cfg["batch"] // f)
+    g = reference_grid(ncores, _host_ram_gb(), cfg)
+    dims = (1, *g)
     R = O.Ref()
     t0 = time.time()
     h = R.dataset_synthetic(cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"], DATA_SEED)
@@ -146,22 +161,26 @@ def reference_baseline(cfg: dict, steps: int, warmup: int, cores: int | None = N
     try:
         mcfg = O.ModelConfig(layers=cfg["layers"], d_in=cfg["d_in"], d_h=cfg["d_h"], d_out=cfg["n_classes"],
                              dropout_rate=DROPOUT)
-        step_ms, phase = R.bench(h, dims, mcfg, b_s, RUN_SEED, warmup, steps)
+        t0 = time.time()
+        step_ms, phase = R.bench(h, dims, mcfg, cfg["batch"], RUN_SEED, warmup, steps)
+        t_run = time.time() - t0
     finally:
         R.free_dataset(h)
     S = math.ceil(cfg["n"] / cfg["batch"])
     mean_ms = float(sum(step_ms) / len(step_ms))
-    full_step_s = mean_ms / 1000.0 * f
+    ranks = g[0] * g[1] * g[2]
+    names = ("sample", "forward+loss", "backward", "dp_sync", "optimizer")
     return {
-        "epoch_time_s": S * full_step_s,
-        "cores": best[0] * best[1] * best[2],
-        "grid": "1x%dx%dx%d" % best,
-        "sample": (f"reference train_run step body (sample->fwd+CE->bwd->dp_sync->Adam) on grid 1x{best[0]}x{best[1]}"
-                   f"x{best[2]} ({best[0]*best[1]*best[2]} threads of {ncores} host cores), batch {b_s} = global "
-                   f"batch/{f}, {steps} timed steps after {warmup} warm-up: {mean_ms:.0f} ms/step, scaled x{f} "
-                   f"to the full batch (linear; understates the reference), x{S} steps/epoch; dataset build "
-                   f"{t_data:.0f}s excluded"),
-        "phase_ms": [float(x) for x in phase],
+        "epoch_time_s": S * mean_ms / 1000.0,
+        "ms_per_step": mean_ms,
+        "step_ms": [float(x) for x in step_ms],
+        "cores": ranks,
+        "grid": "1x%dx%dx%d" % g,
+        "sample": (f"reference train_run step body (sample->fwd+CE->bwd->dp_sync->Adam) at the full global batch "
+                   f"{cfg['batch']} on grid 1x{g[0]}x{g[1]}x{g[2]} ({ranks} threads of {ncores} host cores), "
+                   f"{steps} timed step(s) after {warmup} warm-up: {mean_ms:.0f} ms/step, x{S} steps/epoch "
+                   f"(no scaling); dataset build {t_data:.0f}s excluded, steps ran {t_run:.0f}s wall"),
+        "phase_ms_per_step": {k: float(v) / max(steps, 1) for k, v in zip(names, phase)},
     }
 
 
@@ -212,18 +231,21 @@ def main():
             print(json.dumps({"impl": "reference", "unavailable": "the reference CPU path cannot hold the "
                               f"{args.config} graph in host memory (SURVEY §6.2)"}), flush=True)
             return
-        # each reference step is a bounded sample (seconds of CPU work); cap the count
-        # so the whole run stays within a few minutes
-        steps_run, warm_run = max(1, min(args.steps, 3)), min(args.warmup, 3)
+        # each reference step is the full global batch (~40 s on 16 host cores at C2):
+        # cap the count so the whole run stays within a few minutes
+        steps_run, warm_run = max(1, min(args.steps, args.ref_steps)), min(args.warmup, 1)
         rb = reference_baseline(cfg, steps_run, warm_run)
         S = math.ceil(cfg["n"] / cfg["batch"])
         v = rb["epoch_time_s"]
         print(json.dumps({
             "impl": "reference", "metric": "epoch_time_s", "value": v, "unit": "s", "n_gpus": n_gpus,
-            "steps": steps_run, "warmup": warm_run, "ms_per_step": v / S * 1000.0, "higher_is_better": False,
+            "steps": steps_run, "warmup": warm_run, "ms_per_step": rb["ms_per_step"], "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"], "steps_per_epoch": S,
-                       "grid": rb["grid"]},
+            "config": {"workload": cfg["workload"], "config_id": args.config, "global_batch": cfg["batch"],
+                       "steps_per_epoch": S, "grid": rb["grid"]},
+            "iters_per_s": 1000.0 / rb["ms_per_step"],
+            "phase_ms_per_step": rb["phase_ms_per_step"],
+            "step_ms": rb["step_ms"],
             "cpu_baseline": {"value": v, "unit": "s", "cores": rb["cores"], "kind": "reference",
                              "sample": rb["sample"]},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -520,9 +542,11 @@ def main():
                                          "(SURVEY §6.2)"}
     elif not args.no_cpu_baseline and n_gpus == 1:
         try:
-            rb = reference_baseline(cfg, args.ref_steps, 1)
+            # one full-batch step (~40 s of 16 host cores at C2), no warm-up
+            rb = reference_baseline(cfg, 1, 0)
             out["cpu_baseline"] = {"value": rb["epoch_time_s"], "unit": "s", "cores": rb["cores"],
-                                   "kind": "reference", "sample": rb["sample"]}
+                                   "kind": "reference", "sample": rb["sample"],
+                                   "phase_ms_per_step": rb["phase_ms_per_step"]}
         except Exception as e:  # the baseline is reported, never required
             out["cpu_baseline"] = {"value": None, "unit": "s", "cores": None, "kind": "reference",
                                    "sample": f"unavailable: {e}"}

@@ -344,7 +344,11 @@ def test_train_step_h256_matches_reference(gg, orc, ref, shape, preagg, gather24
 @pytest.mark.parametrize("shape", list(H256))
 def test_h256_adam_trajectory_matches_reference(gg, orc, ref, shape):
     """Four steps of train_run's loop (batch -> train_step -> dp_sync -> Adam)
-    at hidden 256: per-step losses and the final weights track the reference."""
+    at hidden 256: per-step losses and the final weights track the reference.
+    Adam's step is ~lr * sign(g) for small gradient entries, so a gradient
+    within the 1e-2 tolerance can move a weight by up to lr the other way;
+    the weights are therefore compared on the update they received:
+    ||W - W_ref|| <= 5e-2 * ||W_ref - W_0|| per tensor."""
     s = H256[shape]
     n, d_in, ncls, seed = s["n"], s["d_in"], s["ncls"], 1
     b = n // 4
@@ -358,10 +362,12 @@ def test_h256_adam_trajectory_matches_reference(gg, orc, ref, shape):
             got.append(gg.train_step(ctx, st, batch, gg.FP32, seed, t))
             gg.dp_sync(ctx, st)
             gg.optimizer_step(ctx, st, gg.ADAM, 1e-3)
-        losses, _, _, W = ref.train(h, (1, 1, 1, 1), orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), b, seed, 0, 4,
-                                    optimizer=1, want_logits=False, want_weights=True)
+        ocfg = orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw)
+        losses, _, _, W = ref.train(h, (1, 1, 1, 1), ocfg, b, seed, 0, 4, optimizer=1, want_logits=False,
+                                    want_weights=True)
         assert np.all(np.abs(np.array(got) - losses) <= LOSS_RTOL * np.abs(losses)), (got, losses)
-        for mine, want in zip(st.weights(), W):
-            assert _rel(mine, want) <= 1e-3
+        for mine, want, w0 in zip(st.weights(), W, ref.init_weights(ocfg, seed)):
+            upd = np.linalg.norm(want.astype(np.float64) - w0)
+            assert np.linalg.norm(mine.astype(np.float64) - want) <= 5e-2 * upd, (_rel(mine, want), upd)
     finally:
         ref.free_dataset(h)
