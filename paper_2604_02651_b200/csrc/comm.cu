@@ -27,6 +27,25 @@ __global__ void k_from_bf16(const bf16* __restrict__ in, int64_t n, float* __res
   if (i < n) out[i] = __bfloat162float(in[i]);
 }
 
+// bf16_round (comm.hpp:29-39) as integer arithmetic: RNE to 8 exponent + 7
+// fraction bits; Inf/NaN truncated, NaN keeps a payload bit
+__device__ __forceinline__ float bf16_round_ref(float x) {
+  const uint32_t u = __float_as_uint(x);
+  if ((u & 0x7f800000u) == 0x7f800000u) {
+    uint32_t r = u & 0xffff0000u;
+    if ((u & 0x007fffffu) != 0 && (r & 0x007f0000u) == 0) r |= 0x00400000u;
+    return __uint_as_float(r);
+  }
+  return __uint_as_float((u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u);
+}
+
+// a one-member group's kBf16Roundtrip all-reduce: out = 0 + bf16_round(x)
+// (Channel::rendezvous runs the same compute for size 1, comm.hpp:135-145)
+__global__ void k_round_bf16_inplace(float* __restrict__ buf, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) buf[i] = 0.0f + bf16_round_ref(buf[i]);
+}
+
 // out[i] = 0 + c_0[i] + c_1[i] + ... in ascending member order (comm.hpp:282-295)
 __global__ void k_ordered_sum_bf16(const bf16* __restrict__ parts, int g, int64_t n, float* __restrict__ out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -159,7 +178,15 @@ void all_reduce_sum_on(Ctx& ctx, int axis, float* buf, int64_t count, int mode, 
 }  // namespace
 
 void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, int wire) {
-  if (trivial(ctx, axis) || count <= 0) return;
+  if (count <= 0) return;
+  if (trivial(ctx, axis)) {  // one member: the bf16 wires still round its contribution
+    if (wire != GGB_FP32) {
+      k_round_bf16_inplace<<<static_cast<unsigned>(ceil_div(count, 256)), 256, 0, ctx.stream>>>(buf, count);
+      GGB_LAUNCH_CHECK();
+      ctx.launches += 1;
+    }
+    return;
+  }
   need(ctx, axis);
   all_reduce_sum_on(ctx, axis, buf, count, wire, ctx.stream, ctx.comm->wire, ctx.comm->gather);
 }

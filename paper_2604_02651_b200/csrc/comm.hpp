@@ -63,5 +63,8 @@ struct BlockXfer {
 void exchange_blocks(Ctx& ctx, const std::vector<BlockXfer>& sends, const std::vector<BlockXfer>& recvs);
 void barrier(Ctx& ctx);
 inline bool trivial(const Ctx& ctx, int axis) { return ctx.grid.dims[axis] == 1; }
+/// A contraction's all-reduce changes values here: a multi-member group, or a
+/// bf16 wire (which rounds even a single member's contribution, comm.hpp:135-145).
+inline bool reduces(const Ctx& ctx, int axis, int wire) { return !trivial(ctx, axis) || wire != GGB_FP32; }
 
 }  // namespace ggb

@@ -272,7 +272,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     st.x0.b = grow<bf16>(st.x0_b, ob.rows() * st.x0.ldb);
     // accurate: X0 stays fp32 (the next SpMM gathers fp32); fast: + bf16 operand copy
     const bool want_b = st.compute != kAccurate;
-    const bool ar = !trivial(ctx, kInputFeatureLayout.col);
+    const bool ar = reduces(ctx, kInputFeatureLayout.col, wire);
     charge_all_reduce(ctx, kInputFeatureLayout.col, ob.rows() * ob.cols(), wire_bytes(wire));
     Tensor xin;
     xin.b = bt.x_in.as<bf16>();
@@ -294,7 +294,8 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
   const uint64_t thresh = drop ? static_cast<uint64_t>(std::ceil(rate * 0x1.0p53)) : 0;
 
   // layer 1 as (A_0 . x_in) . W_in: same product, d_in-wide instead of H-wide gathers
-  st.preagg = preagg_enabled() && preagg_eligible(ctx, bt);
+  // (not under a bf16 wire: it would skip the rounded X0 and hagg_1 intermediates)
+  st.preagg = preagg_enabled() && preagg_eligible(ctx, bt) && wire == GGB_FP32;
   const Tensor* prev = &st.x0;
   for (int l = 1; l <= cfg.layers; ++l) {
     LayerBufs& L = st.layers[l - 1];
@@ -316,7 +317,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.hagg.ldb = ld8(hb.cols());
     L.hagg.b = grow<bf16>(L.hagg_b, hb.rows() * L.hagg.ldb);
     L.hagg.lo = accurate ? grow<bf16>(L.hagg_lo, hb.rows() * L.hagg.ldb) : nullptr;
-    const bool ar_h = !trivial(ctx, alay.col);
+    const bool ar_h = reduces(ctx, alay.col, wire);
     charge_all_reduce(ctx, alay.col, hb.rows() * hb.cols(), wire_bytes(wire));  // spmm (pmm.hpp:165)
     const int64_t* arp = A.row_ptr.as<int64_t>();
     if (l == 1 && st.preagg) {
@@ -674,7 +675,7 @@ void backward(State& st, const Batch& bt, int precision) {
     all_reduce_sum(ctx, hg.blk.lay.row, G + w.off, w.n, wire);
     // dhagg = dxw . W_l^T -> (xw.row, hagg.col), all-reduce xw.col
     const int64_t hc = hg.blk.cols();
-    const bool ar_d = !trivial(ctx, xb.lay.col);
+    const bool ar_d = reduces(ctx, xb.lay.col, wire);
     charge_all_reduce(ctx, xb.lay.col, rows * hc, wire_bytes(wire));
     const int64_t ldhb = ld8(hc);
     bf16* dhb = grow<bf16>(st.dhagg_b, rows * ldhb);
@@ -711,8 +712,7 @@ void backward(State& st, const Batch& bt, int precision) {
     const BatchCsr& At = bt.csrs[bt.csrt_of[p]];
     const Layout alay = adjacency_layout(l);
     contract(At.c0 == hg.blk.r0 && At.c1 == hg.blk.r1, "spmm: inner partitions differ");
-    const bool ar_s = !trivial(ctx, alay.row);
-    const bool inplace = pmm_trivial(ctx) && cfg.use_residual;
+    const bool inplace = pmm_trivial(ctx) && cfg.use_residual && wire == GGB_FP32;
     ProfScope ps(ctx, kProfSpmmBwd, spmm_bytes(At.n_rows, At.nnz, hc, 2, inplace ? 8 : 4), 2.0 * At.nnz * hc);
     if (inplace) {
       // dxh (== dres) += A_t . dhagg; the first layer also emits the bf16

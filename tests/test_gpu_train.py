@@ -371,3 +371,35 @@ def test_h256_adam_trajectory_matches_reference(gg, orc, ref, shape):
             assert np.linalg.norm(mine.astype(np.float64) - want) <= 5e-2 * upd, (_rel(mine, want), upd)
     finally:
         ref.free_dataset(h)
+
+
+@pytest.mark.parametrize("wire", ["BF16_WIRE", "BF16_SUM"])
+@pytest.mark.parametrize("d_h", [64, 256])
+def test_bf16_wire_on_one_gpu_matches_reference(gg, orc, ref, wire, d_h):
+    """Precision::kBf16Roundtrip on the 1x1x1x1 grid: every contract/spmm
+    all-reduce is a one-member group, and the reference still rounds that
+    member's contribution to bf16 (Channel::rendezvous computes for size 1,
+    comm.hpp:135-145, 271-303). The GPU step rounds the same intermediates
+    (pre-aggregation is off under a bf16 wire) and matches the reference's
+    bf16 run with the fp32 tolerances: loss 1e-3, gradients 1e-2."""
+    n, d_in, ncls, b, seed, step = 6000, 32, 9, 1500, 3, 1
+    cfg_kw = dict(layers=3, d_h=d_h, dropout_rate=0.1)
+    ds, h, ctx, g = _setup(gg, orc, ref, n, 12.0, d_in, ncls, 5, 3)
+    try:
+        st = gg.init_state(ctx, gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), seed)
+        batch = gg.build_step_batch(ctx, g, b, gg.hash_combine(seed, 0), step)
+        loss = gg.train_step(ctx, st, batch, getattr(gg, wire), seed, step)
+        ocfg = orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw)
+        losses, logits, grads, _ = ref.train(h, (1, 1, 1, 1), ocfg, b, seed, step0=step, prec=1)
+        losses32, _, grads32, _ = ref.train(h, (1, 1, 1, 1), ocfg, b, seed, step0=step, prec=0)
+        assert abs(loss - losses[0]) <= LOSS_RTOL * abs(losses[0])
+        _, lg = st.logits()
+        assert np.max(np.abs(lg - logits)) <= 2e-2 * max(1.0, np.max(np.abs(logits)))
+        worst, worst32 = 0.0, 0.0
+        for name, mine, want, w32 in zip(st.cfg.param_names(), st.grads(), grads, grads32):
+            assert _rel(mine, want) <= GRAD_RTOL, (name, _rel(mine, want))
+            worst, worst32 = max(worst, _rel(mine, want)), max(worst32, _rel(mine, w32))
+        # the GPU run is closer to the reference's bf16 run than to its fp32 run
+        assert worst < worst32, (worst, worst32)
+    finally:
+        ref.free_dataset(h)
