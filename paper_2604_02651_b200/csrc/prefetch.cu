@@ -1,8 +1,9 @@
 // Sampling / training overlap: the reference's prefetch producer
 // (train_run's producer thread + PrefetchQueue, model.hpp:556-581 and
 // 631-656) as a native producer thread with its own CUDA stream and sampler
-// scratch. Two batch slots; the hand-off is by CUDA events, so the compute
-// stream never blocks the host:
+// scratch. A ring of batch slots (the reference's queue holds one batch
+// beside the one in use; here up to nslots - 1 are built ahead); the
+// hand-off is by CUDA events, so the compute stream never blocks the host:
 //   producer: wait(released[slot]) on the sampling stream -> build batch k ->
 //             record ready[slot];
 //   consumer: next() records released[previous slot] on the compute stream,
@@ -55,7 +56,12 @@ Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t see
   if (pe && std::string(pe) == "same") GGB_CUDA(cudaStreamGetPriority(consumer->stream, &prio));
   GGB_CUDA(cudaStreamCreateWithPriority(&sctx.stream, cudaStreamNonBlocking, prio));
   sctx.own_stream = true;
-  for (int s = 0; s < 2; ++s) {
+  {
+    const char* e = std::getenv("GGB_PF_SLOTS");
+    const int v = e ? std::atoi(e) : 3;
+    nslots = v >= 2 && v <= kMaxSlots ? v : 3;
+  }
+  for (int s = 0; s < nslots; ++s) {
     GGB_CUDA(cudaEventCreateWithFlags(&ready[s], cudaEventDisableTiming));
     GGB_CUDA(cudaEventCreateWithFlags(&released[s], cudaEventDisableTiming));
   }
@@ -63,7 +69,7 @@ Prefetcher::Prefetcher(Ctx& consumer_, const Graph& g_, int64_t b_, uint64_t see
     const char* e = std::getenv("GGB_PF_TIMING");
     timing = e && e[0] == '1';
     if (timing)
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < nslots; ++s) {
         GGB_CUDA(cudaEventCreate(&tb[s]));
         GGB_CUDA(cudaEventCreate(&te[s]));
       }
@@ -80,7 +86,7 @@ Prefetcher::~Prefetcher() {
   if (th.joinable()) th.join();
   cudaSetDevice(sctx.device);
   cudaStreamSynchronize(sctx.stream);
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < nslots; ++s) {
     cudaEventDestroy(ready[s]);
     cudaEventDestroy(released[s]);
     if (timing) {
@@ -97,14 +103,14 @@ void Prefetcher::run() {
   try {
     GGB_CUDA(cudaSetDevice(sctx.device));
     for (int64_t k = 0;; ++k) {
-      const int slot = static_cast<int>(k & 1);
+      const int slot = static_cast<int>(k % nslots);
       {
         std::unique_lock<std::mutex> lk(m);
-        // slot free once the consumer has released batch k-2
-        cv.wait(lk, [&] { return stop || released_count >= k - 1; });
+        // slot free once the consumer has released batch k - nslots
+        cv.wait(lk, [&] { return stop || released_count >= k - nslots + 1; });
         if (stop) return;
       }
-      if (k >= 2) GGB_CUDA(cudaStreamWaitEvent(sctx.stream, released[slot], 0));
+      if (k >= nslots) GGB_CUDA(cudaStreamWaitEvent(sctx.stream, released[slot], 0));
       if (timing) GGB_CUDA(cudaEventRecord(tb[slot], sctx.stream));
       const bool pre = preagg_enabled() && preagg_in_prefetch();
       build_step_batch(sctx, *g, b, seed, step0 + static_cast<uint64_t>(k), slots[slot], pre);
@@ -152,14 +158,14 @@ void Prefetcher::make_masks(Batch& bt, uint64_t gstep) {
 Batch* Prefetcher::next() {
   std::unique_lock<std::mutex> lk(m);
   if (consumed > 0) {  // release the batch handed out last time, once its compute is done
-    const int prev = static_cast<int>((consumed - 1) & 1);
+    const int prev = static_cast<int>((consumed - 1) % nslots);
     GGB_CUDA(cudaEventRecord(released[prev], consumer->stream));
     released_count = consumed;
     cv.notify_all();
   }
   cv.wait(lk, [&] { return failed || produced > consumed; });
   if (failed && produced <= consumed) std::rethrow_exception(err);
-  const int slot = static_cast<int>(consumed & 1);
+  const int slot = static_cast<int>(consumed % nslots);
   GGB_CUDA(cudaStreamWaitEvent(consumer->stream, ready[slot], 0));
   if (timing) {
     float ms = 0.f;

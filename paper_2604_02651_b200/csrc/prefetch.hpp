@@ -15,8 +15,13 @@ struct Prefetcher {
   int64_t b;
   uint64_t seed, step0;
   Ctx sctx;  // sampling context: own stream + sampler scratch, same grid coords
-  Batch slots[2];
-  cudaEvent_t ready[2] = {}, released[2] = {};
+  // batch slots: the producer may run up to kMaxSlots - 1 batches ahead
+  // (GGB_PF_SLOTS, default 3: two builds in flight absorb a build that is
+  // stretched by the training stream's kernels)
+  static constexpr int kMaxSlots = 4;
+  int nslots = 3;
+  Batch slots[kMaxSlots];
+  cudaEvent_t ready[kMaxSlots] = {}, released[kMaxSlots] = {};
   std::thread th;
   std::mutex m;
   std::condition_variable cv;
@@ -26,7 +31,7 @@ struct Prefetcher {
   // GGB_PF_TIMING=1: device time of each batch build on the sampling stream,
   // summed and printed at destruction (diagnostic; syncs on each batch)
   bool timing = false;
-  cudaEvent_t tb[2] = {}, te[2] = {};
+  cudaEvent_t tb[kMaxSlots] = {}, te[kMaxSlots] = {};
   double build_ms = 0.0;
   int64_t builds = 0;
 

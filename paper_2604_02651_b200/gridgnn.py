@@ -455,11 +455,36 @@ class StepBatch:
             pass
 
 
+class StaleBatch(GgbError):
+    """A prefetched batch used after the next Prefetcher.next() or close():
+    its slot may already hold a later batch."""
+
+    def __init__(self, msg: str):
+        super().__init__(1, msg)  # GGB_EINVAL
+
+
 class _BorrowedBatch(StepBatch):
-    """A batch owned by a Prefetcher slot (never destroyed from Python)."""
+    """A batch owned by a Prefetcher slot (never destroyed from Python). Valid
+    until the prefetcher's next next() or close(); the reference's
+    PrefetchQueue hands batches out by value, so a later use raises
+    StaleBatch instead of reading a slot the producer refills."""
+
+    def __init__(self, pf: "Prefetcher", h):
+        self._pf, self._gen = pf, pf._gen
+        super().__init__(pf.graph, h)
+
+    @property
+    def h(self):
+        if self._h is not None and (self._pf.h is None or self._pf._gen != self._gen):
+            raise StaleBatch("prefetched batch used after the next Prefetcher.next() or close()")
+        return self._h
+
+    @h.setter
+    def h(self, v):
+        self._h = v
 
     def close(self):
-        self.h = None
+        self._h = None
 
 
 class Prefetcher:
@@ -479,11 +504,13 @@ class Prefetcher:
         check(lib().ggb_prefetch_create(ctx.h, graph.h, b, group_seed, first_step, run_seed, layers, d_h, rate,
                                         C.byref(h)))
         self.h = h
+        self._gen = 0
 
     def next(self) -> StepBatch:
         bh = P()
         check(lib().ggb_prefetch_next(self.h, C.byref(bh)))
-        return _BorrowedBatch(self.graph, bh)
+        self._gen += 1
+        return _BorrowedBatch(self, bh)
 
     def close(self):
         if getattr(self, "h", None):

@@ -381,7 +381,10 @@ def test_bf16_wire_on_one_gpu_matches_reference(gg, orc, ref, wire, d_h):
     member's contribution to bf16 (Channel::rendezvous computes for size 1,
     comm.hpp:135-145, 271-303). The GPU step rounds the same intermediates
     (pre-aggregation is off under a bf16 wire) and matches the reference's
-    bf16 run with the fp32 tolerances: loss 1e-3, gradients 1e-2."""
+    bf16 run: loss 1e-3, gradients 2e-2 (the gradients are themselves
+    bf16-rounded all-reduce outputs, so an element whose fp32 pre-image lies
+    within the kernels' 1e-5 of a rounding boundary lands one bf16 ulp, 2^-8,
+    away), and closer to it than to the reference's fp32 run."""
     n, d_in, ncls, b, seed, step = 6000, 32, 9, 1500, 3, 1
     cfg_kw = dict(layers=3, d_h=d_h, dropout_rate=0.1)
     ds, h, ctx, g = _setup(gg, orc, ref, n, 12.0, d_in, ncls, 5, 3)
@@ -397,9 +400,30 @@ def test_bf16_wire_on_one_gpu_matches_reference(gg, orc, ref, wire, d_h):
         assert np.max(np.abs(lg - logits)) <= 2e-2 * max(1.0, np.max(np.abs(logits)))
         worst, worst32 = 0.0, 0.0
         for name, mine, want, w32 in zip(st.cfg.param_names(), st.grads(), grads, grads32):
-            assert _rel(mine, want) <= GRAD_RTOL, (name, _rel(mine, want))
+            assert _rel(mine, want) <= 2e-2, (name, _rel(mine, want))
             worst, worst32 = max(worst, _rel(mine, want)), max(worst32, _rel(mine, w32))
         # the GPU run is closer to the reference's bf16 run than to its fp32 run
         assert worst < worst32, (worst, worst32)
     finally:
         ref.free_dataset(h)
+
+
+def test_prefetched_batch_is_stale_after_next(gg, orc):
+    """A prefetched batch is valid until the following next() (its slot is
+    then free for the producer); later use raises instead of reading a
+    refilled slot."""
+    n, d_in, ncls, b = 1500, 8, 3, 400
+    ds = orc.generate_synthetic(n, 6.0, d_in, ncls, 2)
+    ctx = gg.Context()
+    g = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls, 2)
+    pf = gg.Prefetcher(ctx, g, b, 5, 0)
+    b0 = pf.next()
+    s0 = b0.sample
+    assert np.array_equal(s0, orc.sample_vertices(n, b, 5, 0))
+    b1 = pf.next()
+    with pytest.raises(gg.StaleBatch):
+        b0.sample
+    assert np.array_equal(b1.sample, orc.sample_vertices(n, b, 5, 1))
+    pf.close()
+    with pytest.raises(gg.StaleBatch):
+        b1.sample
