@@ -231,6 +231,7 @@ void graph_build(Ctx& ctx, Graph& g, int64_t n, const int64_t* rp, const int64_t
   g.feat_ptr = g.features.as<float>();
   g.device_bytes = g.features.bytes + g.labels.bytes;
   for (auto& s : g.shards) g.device_bytes += s.row_ptr.bytes + s.col.bytes + s.val.bytes;
+  for (auto& s : g.shards) shard_degree_profile(ctx, s);
 }
 
 // graph_build from a device-generated dataset (gendata.cu): the plane
@@ -305,6 +306,7 @@ void graph_build_device(Ctx& ctx, Graph& g, DevDataset& ds, int layers) {
   g.feat_ptr = g.features.as<float>();
   g.device_bytes = g.features.bytes + g.labels.bytes + g.split.bytes;
   for (auto& s : g.shards) g.device_bytes += s.row_ptr.bytes + s.col.bytes + s.val.bytes;
+  for (auto& s : g.shards) shard_degree_profile(ctx, s);
 }
 
 template <class T>
@@ -710,6 +712,8 @@ int ggb_batch_destroy(ggb_batch_t batch) {
 
 int ggb_batch_info(ggb_batch_t bt, int64_t* info) {
   return guard([&] {
+    if (bt->ctx) use_device(*bt->ctx);
+    settle_totals(*bt);
     info[0] = bt->b;
     info[1] = bt->n;
     info[2] = bt->planes;
@@ -741,6 +745,7 @@ int ggb_batch_plane(ggb_batch_t bt, int32_t plane, int32_t transposed, int64_t* 
   return guard([&] {
     require(plane >= 0 && plane < bt->planes, "batch_plane: plane out of range");
     use_device(*bt->ctx);
+    settle_totals(*bt);
     const BatchCsr& c = bt->csrs[transposed ? bt->csrt_of[plane] : bt->csr_of[plane]];
     dims[0] = c.n_rows;
     dims[1] = c.n_cols;

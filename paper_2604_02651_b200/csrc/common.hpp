@@ -116,6 +116,21 @@ struct PinnedBuf {
   }
 };
 
+/// A lazily created CUDA event owned by a host object.
+struct EventHandle {
+  cudaEvent_t e = nullptr;
+  EventHandle() = default;
+  EventHandle(const EventHandle&) = delete;
+  EventHandle& operator=(const EventHandle&) = delete;
+  ~EventHandle() {
+    if (e) cudaEventDestroy(e);
+  }
+  cudaEvent_t get() {
+    if (!e) GGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+  }
+};
+
 /// Reference block_partition (shardsample.cpp:8-17).
 inline std::vector<int64_t> block_partition(int64_t n, int g) {
   require(g >= 1, "block_partition: g must be >= 1");

@@ -110,6 +110,18 @@ struct PlaneShard {
   DevBuf row_ptr;  // int64 [r1-r0+1]
   DevBuf col;      // int32 [nnz]
   DevBuf val;      // double [nnz]
+  // rows per degree (host, built with the graph): the n largest row degrees
+  // bound the entries a batch block of n sampled rows can extract
+  std::vector<int64_t> rows_of_degree;
+  int64_t top_rows_nnz(int64_t rows) const {
+    int64_t sum = 0;
+    for (int64_t d = static_cast<int64_t>(rows_of_degree.size()) - 1; d > 0 && rows > 0; --d) {
+      const int64_t k = std::min(rows, rows_of_degree[static_cast<size_t>(d)]);
+      sum += k * d;
+      rows -= k;
+    }
+    return sum;
+  }
 };
 
 struct Graph {
@@ -133,7 +145,8 @@ struct Graph {
 /// One rank's CSR block of a rescaled batch adjacency (ShardedSparse,
 /// tensor.hpp:88-96) with device arrays for the kernels.
 struct BatchCsr {
-  int64_t n_rows = 0, n_cols = 0, nnz = 0;
+  int64_t n_rows = 0, n_cols = 0;
+  mutable int64_t nnz = 0;  // host copy, valid once the batch's totals are settled
   int64_t r0 = 0, r1 = 0, c0 = 0, c1 = 0;  // global batch coordinates
   DevBuf row_ptr;  // int64 [n_rows+1]
   DevBuf col;      // int32
@@ -159,6 +172,7 @@ struct Batch {
   std::vector<int> csr_of;   // plane -> index in csrs (forward block)
   std::vector<int> csrt_of;  // plane -> index in csrs (transposed block)
   std::vector<BatchCsr> csrs;
+  int nblocks = 0;  // csrs in use (csrs only grows)
   int64_t x_r0 = 0, x_r1 = 0, x_c0 = 0, x_c1 = 0, x_ld = 0;
   DevBuf x_in;    // bf16 [x_r1-x_r0][x_ld], zero padded (hi of the split pair)
   DevBuf x_in_lo; // bf16 lo residual: x == hi + lo to ~2^-16
@@ -167,7 +181,13 @@ struct Batch {
   // x_in rows, P as split bf16 [A_0 rows][x_ld]; a cache of the batch, hence mutable
   mutable DevBuf x_f, p_in, p_in_lo;
   mutable bool p_ready = false, x_f_ready = false;
-  uint64_t nnz_extracted = 0, nnz_kept = 0;
+  // host view of the build's device totals (per block nnz, per block
+  // extracted count): copied to pinned memory as the build is enqueued and
+  // settled (settle_totals) on first host use, so the build never waits
+  mutable uint64_t nnz_extracted = 0, nnz_kept = 0;
+  PinnedBuf totals;
+  EventHandle totals_ready;
+  mutable bool totals_pending = false;
   uint64_t h2d_bytes = 0;  // feature bytes this build read over PCIe (host-resident features)
   const Graph* graph = nullptr;
 };
@@ -178,6 +198,10 @@ void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, in
 void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
                       Batch& out, bool want_xf = false);
 void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out);
+/// Fill the host nnz / extraction counters of a batch (waits for its build).
+void settle_totals(const Batch& bt);
+/// Degree histogram of a static shard (one download of its row pointers).
+void shard_degree_profile(Ctx& ctx, PlaneShard& sh);
 bool preagg_eligible(const Ctx& ctx, const Batch& bt);
 void preaggregate(Ctx& ctx, const Batch& bt);
 

@@ -395,13 +395,11 @@ void extract_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int6
 }
 
 void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t row_lo,
-                int64_t col_lo, int64_t b, int64_t n, BatchCsr& out) {
-  // nonzero counts fluctuate step to step: size with headroom once
-  const int64_t cap = out.nnz + out.nnz / 16 + 1024;
+                int64_t col_lo, int64_t b, int64_t n, BatchCsr& out, int64_t cap) {
   out.col.reserve_n<int32_t>(cap);
   out.val.reserve_n<float>(cap);
   out.val64.reserve_n<double>(cap);
-  if (out.n_rows == 0 || out.nnz == 0) return;
+  if (out.n_rows == 0) return;
   const double p = static_cast<double>(b - 1) / static_cast<double>(n - 1);  // shardsample.cpp:116
   k_extract_fill<<<blocks(out.n_rows, kThreads / 32), kThreads, 0, ctx.stream>>>(
       out.n_rows, d_sample, row_lo, sh.r0, sh.row_ptr.as<int64_t>(), sh.col.as<int32_t>(),
@@ -563,25 +561,38 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     extract_block(ctx, g.shards[kk.shard], d_sample, kk.rl, kk.rh, kk.cl, kk.ch, b, g.n, out,
                   d_cnt + k * (max_rows + 1), d_ext + k);
   }
-  // totals: row_ptr[n_rows] of every block, plus the extracted counters
+  // totals: row_ptr[n_rows] of every block, plus the extracted counters, to
+  // the batch's pinned buffer; the host reads them only when it needs them
   const size_t nk = keys.size();
+  bt.nblocks = static_cast<int>(nk);
+  int64_t* tot = static_cast<int64_t*>(bt.totals.reserve(16 * nk + 16));
   for (size_t k = 0; k < nk; ++k)
-    GGB_CUDA(cudaMemcpyAsync(hmisc + k, bt.csrs[k].row_ptr.as<int64_t>() + bt.csrs[k].n_rows, 8,
+    GGB_CUDA(cudaMemcpyAsync(tot + k, bt.csrs[k].row_ptr.as<int64_t>() + bt.csrs[k].n_rows, 8,
                              cudaMemcpyDeviceToHost, s));
-  GGB_CUDA(cudaMemcpyAsync(hmisc + nk, d_ext, 8 * nk, cudaMemcpyDeviceToHost, s));
+  GGB_CUDA(cudaMemcpyAsync(tot + nk, d_ext, 8 * nk, cudaMemcpyDeviceToHost, s));
+  GGB_CUDA(cudaEventRecord(bt.totals_ready.get(), s));
+  bt.totals_pending = true;
   ctx.d2h_bytes += 16 * nk;
-  GGB_CUDA(cudaStreamSynchronize(s));
-  for (size_t k = 0; k < nk; ++k) bt.csrs[k].nnz = hmisc[k];
-  // counters as build_step_batch accumulates them (model.hpp:265-268): one
-  // build_local_minibatch per plane, counting its forward block
-  bt.nnz_extracted = 0;
-  bt.nnz_kept = 0;
-  for (int p = 0; p < g.planes; ++p) {
-    bt.nnz_extracted += static_cast<uint64_t>(hmisc[nk + bt.csr_of[p]]);
-    bt.nnz_kept += static_cast<uint64_t>(bt.csrs[bt.csr_of[p]].nnz);
+  // Output capacity of every block without a host round trip: its kept
+  // entries are at most its extracted ones, at most the n_rows largest row
+  // degrees of its static shard. Past a memory budget (papers100M-scale
+  // blocks), or when profiling needs the byte counts, wait for the exact
+  // totals instead.
+  std::vector<int64_t> cap(nk);
+  size_t need = 0;
+  bool bounded = true;
+  for (size_t k = 0; k < nk; ++k) {
+    const PlaneShard& sh = g.shards[keys[k].shard];
+    bounded = bounded && !sh.rows_of_degree.empty();
+    cap[k] = sh.top_rows_nnz(bt.csrs[k].n_rows) + 1;
+    need += static_cast<size_t>(cap[k]) * (4 + 4 + 8);
+  }
+  if (!bounded || need > (size_t{2} << 30) || prof_of(ctx).on) {
+    settle_totals(bt);
+    for (size_t k = 0; k < nk; ++k) cap[k] = bt.csrs[k].nnz + bt.csrs[k].nnz / 16 + 1024;  // headroom for later steps
   }
   for (size_t k = 0; k < nk; ++k)
-    fill_block(ctx, g.shards[keys[k].shard], d_sample, keys[k].rl, keys[k].cl, b, g.n, bt.csrs[k]);
+    fill_block(ctx, g.shards[keys[k].shard], d_sample, keys[k].rl, keys[k].cl, b, g.n, bt.csrs[k], cap[k]);
 
   if (gather_aside) {  // join the PCIe gather
     GGB_CUDA(cudaEventRecord(ctx.sw.aux.join, ctx.sw.aux.s));
@@ -595,13 +606,45 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
   // its prefix over n/32 words, per block the sampled row pointers, the
   // extracted column ids, the kept entries (fp64 value read; int32 col, fp32
   // and fp64 value writes), the feature gather and the labels.
-  double bytes = 8.0 * b * 4 + (g.n / 32.0) * 12;
-  for (size_t k = 0; k < nk; ++k) {
-    const BatchCsr& c = bt.csrs[k];
-    bytes += c.n_rows * 16.0 * 2 + static_cast<double>(hmisc[nk + k]) * 4.0 * 2 + c.nnz * (8.0 + 4 + 4 + 8);
+  if (!bt.totals_pending) {  // settled above (profiling)
+    double bytes = 8.0 * b * 4 + (g.n / 32.0) * 12;
+    for (size_t k = 0; k < nk; ++k) {
+      const BatchCsr& c = bt.csrs[k];
+      bytes += c.n_rows * 16.0 * 2 + static_cast<double>(tot[nk + k]) * 4.0 * 2 + c.nnz * (8.0 + 4 + 4 + 8);
+    }
+    bytes += static_cast<double>(bt.x_r1 - bt.x_r0) * (bt.x_c1 - bt.x_c0) * (4 + 2 + 2) + b * 12.0;
+    prof.bytes = bytes;
   }
-  bytes += static_cast<double>(bt.x_r1 - bt.x_r0) * (bt.x_c1 - bt.x_c0) * (4 + 2 + 2) + b * 12.0;
-  prof.bytes = bytes;
+}
+
+void settle_totals(const Batch& bt) {
+  if (!bt.totals_pending) return;
+  GGB_CUDA(cudaEventSynchronize(bt.totals_ready.e));
+  const int64_t* tot = static_cast<const int64_t*>(bt.totals.p);
+  const size_t nk = static_cast<size_t>(bt.nblocks);
+  for (size_t k = 0; k < nk; ++k) bt.csrs[k].nnz = tot[k];
+  // counters as build_step_batch accumulates them (model.hpp:265-268): one
+  // build_local_minibatch per plane, counting its forward block
+  bt.nnz_extracted = 0;
+  bt.nnz_kept = 0;
+  for (int p = 0; p < bt.planes; ++p) {
+    bt.nnz_extracted += static_cast<uint64_t>(tot[nk + bt.csr_of[p]]);
+    bt.nnz_kept += static_cast<uint64_t>(bt.csrs[bt.csr_of[p]].nnz);
+  }
+  bt.totals_pending = false;
+}
+
+void shard_degree_profile(Ctx& ctx, PlaneShard& sh) {
+  const int64_t rows = sh.r1 - sh.r0;
+  sh.rows_of_degree.clear();
+  if (rows <= 0) return;
+  std::vector<int64_t> rp(static_cast<size_t>(rows) + 1);
+  GGB_CUDA(cudaMemcpyAsync(rp.data(), sh.row_ptr.p, rp.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+  GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+  int64_t dmax = 0;
+  for (int64_t r = 0; r < rows; ++r) dmax = std::max(dmax, rp[r + 1] - rp[r]);
+  sh.rows_of_degree.assign(static_cast<size_t>(dmax) + 1, 0);
+  for (int64_t r = 0; r < rows; ++r) ++sh.rows_of_degree[static_cast<size_t>(rp[r + 1] - rp[r])];
 }
 
 void gather_x_in_fp32(Ctx& ctx, const Batch& bt, float* d_out) {

@@ -254,6 +254,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
   const int wire = precision;  // ggb_precision: the all-reduce wire mode
   const int64_t H = cfg.d_h;
   const int dp = ctx.coord[0];
+  if (prof_of(ctx).on) settle_totals(bt);  // the kernel-class byte counts need the block sizes
   contract(bt.planes == std::min(cfg.layers, 3), "forward: batch planes do not match the model layers");
   float* W = st.W.as<float>();
 
