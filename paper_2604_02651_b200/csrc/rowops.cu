@@ -82,6 +82,22 @@ __device__ __forceinline__ void st4_p24(uint8_t* row, int64_t hoff, int64_t c, i
     }
   }
 }
+// 4 consecutive values at column c of a 24-bit row (st4_p24's layout)
+__device__ __forceinline__ float4 ld4_p24(const uint8_t* row, int64_t hoff, int64_t c, int64_t n) {
+  if (c + 4 <= n) {
+    const uint2 h = *reinterpret_cast<const uint2*>(row + 2 * c);
+    const uint32_t l = *reinterpret_cast<const uint32_t*>(row + hoff + c);
+    return make_float4(__uint_as_float((h.x << 16) | ((l & 0xffu) << 8)),
+                       __uint_as_float((h.x & 0xffff0000u) | (l & 0xff00u)),
+                       __uint_as_float((h.y << 16) | ((l >> 8) & 0xff00u)),
+                       __uint_as_float((h.y & 0xffff0000u) | ((l >> 16) & 0xff00u)));
+  }
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < 4 && c + i < n; ++i)
+    v[i] = __uint_as_float((static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(row)[c + i]) << 16) |
+                           (static_cast<uint32_t>(row[hoff + c + i]) << 8));
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
 __device__ __forceinline__ void f4(const float4& a, float* v) {
   v[0] = a.x;
   v[1] = a.y;
@@ -126,6 +142,8 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
       f4(ld4(xr, c, ncols), x[j]);
       if (p.res)
         f4(ld4(p.res + r * p.ldres, c, ncols), res[j]);
+      else if (p.resp)
+        f4(ld4_p24(p.resp + r * p.ldresp, p.reshoff, c, ncols), res[j]);
       else
         res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
     }

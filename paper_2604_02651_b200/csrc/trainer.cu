@@ -235,6 +235,16 @@ bool preagg_enabled() {
 // C2: forward SpMM 2.75 -> 2.24 ms/step, but the step only 10.73 -> 10.60 ms
 // (the sampling stream's batch build is the critical chain) and e2e 11.43 ->
 // 11.66 ms (the extra write traffic lands on the build), so it is off.
+// GGB_KEEP_IN_SPMM=0: the fused row kernel hashes its own dropout keep-bits
+// instead of taking them from the forward SpMM's side warps
+bool keep_in_spmm_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GGB_KEEP_IN_SPMM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool gather24_enabled() {
   const char* e = std::getenv("GGB_GATHER24");
   return e && e[0] == '1';
@@ -300,6 +310,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
   const Tensor* prev = &st.x0;
   for (int l = 1; l <= cfg.layers; ++l) {
     LayerBufs& L = st.layers[l - 1];
+    L.keep_ready = false;
     const int p = (l - 1) % 3;
     const BatchCsr& A = bt.csrs[bt.csr_of[p]];
     const Layout alay = adjacency_layout(l);
@@ -366,13 +377,32 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     // accurate: the gathered rows are the previous layer's 24-bit copies when
     // it wrote them (3 bytes per element instead of 4)
     const bool p24 = accurate && prev->p != nullptr;
+    // this layer's dropout keep-bits, hashed by the SpMM's side warps while
+    // its gathers are in flight (the row kernel then skips the hash)
+    KeepJob job;
+    const KeepJob* jobp = nullptr;
+    if (accurate && drop && keep_in_spmm_enabled() && st.wl.size() >= static_cast<size_t>(l)) {
+      const ParamSlot& wn = st.params[st.wl[l - 1]];  // xw's column block = W_l's
+      job.key = dropout_key(run_seed, dp, global_step, l);
+      job.thresh = thresh;
+      job.rows = A.n_rows;
+      job.cols = wn.blk.cols();
+      job.row_g0 = A.r0;
+      job.col_g0 = wn.blk.c0;
+      job.ldm = mask_words(std::max<int64_t>(job.cols, 1));
+      job.out = grow<uint32_t>(L.keep, std::max<int64_t>(job.rows, 1) * job.ldm);
+      jobp = &job;
+    }
+    bool job_done = false;
     ProfScope ps(ctx, kProfSpmmFwd, spmm_bytes(A.n_rows, A.nnz, F.cols(), p24 ? 3 : (accurate ? 4 : 2), accurate ? 4 : 2),
                  2.0 * A.nnz * F.cols());
     if (accurate) {
       if (!(p24 && spmm_pipe_p24(ctx, A.n_rows, arp, acol, aval, prev->p, prev->ldp, F.cols(), L.hagg.b, L.hagg.lo,
-                                 L.hagg.ldb)))
+                                 L.hagg.ldb, jobp, &job_done)))
         spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), nullptr, 0, L.hagg.b, L.hagg.lo,
-                     L.hagg.ldb, 0);
+                     L.hagg.ldb, 0, jobp, &job_done);
+      L.keep_ready = job_done;
+      L.keep_key = job.key;
     } else {
       spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
     }
@@ -421,6 +451,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     // residual: X_{l-1} resharded to feature_layout(l+1)
     const Layout out = feature_layout(l + 1);
     const float* res = nullptr;
+    const uint8_t* resp = nullptr;  // X_{l-1} kept only as 24-bit rows
     int64_t ldres = 0;
     if (cfg.use_residual) {
       Block rb = make_block(ctx, out, bt.b, H, bt.batch_off[out.row], hoff(ctx, H, out.col));
@@ -430,6 +461,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
       if (pmm_trivial(ctx)) {
         res = prev->f;
         ldres = prev->ldf;
+        if (!res) resp = prev->p;
       } else {
         float* r = grow<float>(st.dres, rb.rows() * ld8(rb.cols()));
         reshard(ctx, F, bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), prev->f, prev->ldf, rb,
@@ -462,13 +494,16 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     fa.rms = rms;
     fa.res = res;
     fa.ldres = ldres;
+    fa.resp = resp;
+    fa.ldresp = resp ? prev->ldp : 0;
+    fa.reshoff = resp ? prev->hoff : 0;
     fa.mask_key = dropout_key(run_seed, dp, global_step, l);
     fa.row_g0 = xb.r0;
     fa.col_g0 = xb.c0;
     fa.drop = drop;
     fa.thresh = thresh;
     fa.keep_scale = st.fwd_keep_scale;
-    fa.out = L.x.f;
+    fa.out = L.x.f;  // null when only the 24-bit rows are kept (set below, before the launch)
     fa.ldo = L.x.ldf;
     fa.outb = L.x.b;
     fa.outlo = L.x.lo;
@@ -477,19 +512,25 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     // 24-bit copy of X_l for the next layer's forward SpMM (its gathers are
     // the step's largest traffic) when that SpMM runs whole on this rank
     L.x.p = nullptr;
-    if (accurate && !last && gather24_enabled() && xb.cols() <= 256 &&
-        trivial(ctx, adjacency_layout(l + 1).col)) {
+    if (accurate && !last && gather24_enabled() && xb.cols() <= 256 && !reduces(ctx, adjacency_layout(l + 1).col, wire) &&
+        !ctx.side_stream) {
       const int64_t c16 = round_up(xb.cols(), 8);
       L.x.hoff = 2 * c16;
       L.x.ldp = round_up(3 * c16, 16);
       L.x.p = grow<uint8_t>(L.x_p, xb.rows() * L.x.ldp);
+      // the 24-bit rows also serve as the next layer's residual when it is
+      // not resharded: the fp32 copy of X_l then has no reader
+      if (pmm_trivial(ctx) || !cfg.use_residual) L.x.f = nullptr;
     }
+    fa.out = L.x.f;
     fa.outp = L.x.p;
     fa.ldp = L.x.ldp;
     fa.hoff = L.x.hoff;
     fa.ldm = L.ldm;
-    fa.keep = nullptr;  // keep-bits precomputed by the prefetcher for exactly this block?
-    if (drop && bt.masks.size() >= static_cast<size_t>(l)) {
+    fa.keep = nullptr;  // keep-bits precomputed for exactly this block?
+    if (drop && L.keep_ready && L.keep_key == fa.mask_key) {  // by this layer's forward SpMM
+      fa.keep = L.keep.as<uint32_t>();
+    } else if (drop && bt.masks.size() >= static_cast<size_t>(l)) {  // by the prefetcher
       const DropMask& dm = bt.masks[l - 1];
       if (dm.key == fa.mask_key && dm.thresh == thresh && dm.r0 == xb.r0 && dm.c0 == xb.c0 &&
           dm.rows == xb.rows() && dm.cols == xb.cols() && dm.ldm == L.ldm)
@@ -498,7 +539,8 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     {
       const double e = static_cast<double>(xb.rows()) * xb.cols();
       ProfScope ps(ctx, kProfFwdRow,
-                   e * (4 + (res ? 4 : 0) + 4 + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0) + (L.x.p ? 3 : 0)) + e / 8);
+                   e * (4 + (res ? 4 : resp ? 3 : 0) + (L.x.f ? 4 : 0) + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0) +
+                        (L.x.p ? 3 : 0)) + e / 8);
       fwd_apply(ctx, fa);
     }
     prev = &L.x;
