@@ -357,6 +357,11 @@ int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const ui
     int sms = 0;
     GGB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     c->num_sms = sms;
+    {  // GGB_SM_RESERVE=R: persistent kernels leave R SMs to the sampling stream
+      const char* e = std::getenv("GGB_SM_RESERVE");
+      const int r = e ? std::atoi(e) : 0;
+      c->sm_reserve = r >= 0 && r < sms / 2 ? r : 0;
+    }
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
     } else {

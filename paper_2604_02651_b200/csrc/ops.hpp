@@ -117,14 +117,6 @@ void gemm_split(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a_hi, con
                 bf16* cl = nullptr);
 void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x, int64_t ldx,
                      const bf16* dy, int64_t lddy, float* dw, int64_t lddw, DevBuf& ws, int accumulate = 0);
-// Dropout keep-bits of the layer whose forward SpMM this is, computed by
-// extra warps of the pipelined SpMM in the issue slots its memory-bound
-// warps leave idle (spmm_pipe.cu); same bits as dropout_keep.
-struct KeepJob {
-  uint64_t key = 0, thresh = 0;
-  int64_t rows = 0, cols = 0, row_g0 = 0, col_g0 = 0, ldm = 0;
-  uint32_t* out = nullptr;
-};
 // spmm.cu
 void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
               const bf16* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb,
@@ -132,13 +124,10 @@ void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, con
 // fp32 feature operand; optional split-bf16 (hi, lo) outputs
 /// Forward SpMM over 24-bit rows (spmm_pipe.cu P24): out = A . F to the split
 /// bf16 pair; false when the pipelined kernel does not apply (caller falls back).
-/// A KeepJob (nullable) runs inside the kernel; *job_done tells whether it did.
 bool spmm_pipe_p24(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
-                   const uint8_t* f, int64_t ld_bytes, int64_t fcols, bf16* out_hi, bf16* out_lo, int64_t ldob,
-                   const KeepJob* job = nullptr, bool* job_done = nullptr);
+                   const uint8_t* f, int64_t ld_bytes, int64_t fcols, bf16* out_hi, bf16* out_lo, int64_t ldob);
 void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
                   const float* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* out_hi,
-                  bf16* out_lo, int64_t ldob, int accumulate, const KeepJob* job = nullptr,
-                  bool* job_done = nullptr);
+                  bf16* out_lo, int64_t ldob, int accumulate);
 
 }  // namespace ggb

@@ -8,7 +8,6 @@
 // lane. fp32 accumulation in CSR order.
 #include <cstdlib>
 
-#include "ops.hpp"
 #include "runtime.hpp"
 
 namespace ggb {
@@ -213,7 +212,7 @@ void dispatch(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, con
 
 bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val, const void* f,
                int esize, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb, bf16* outlo, int64_t ldob,
-               int accumulate, const KeepJob* job = nullptr);
+               int accumulate);
 
 int spmm_kernel_choice() {  // GGB_SPMM=rowsplit forces the register-pipelined kernel
   static int v = -1;
@@ -239,17 +238,14 @@ void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, con
 
 void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
                   const float* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* out_hi,
-                  bf16* out_lo, int64_t ldob, int accumulate, const KeepJob* job, bool* job_done) {
-  if (job_done) *job_done = false;
+                  bf16* out_lo, int64_t ldob, int accumulate) {
   if (rows <= 0 || fcols <= 0) return;
   require(!(accumulate && !out), "spmm: accumulate needs an fp32 output");
   require(ldf % 8 == 0 && (reinterpret_cast<uintptr_t>(f) & 15) == 0,
           "spmm: feature operand needs 16-byte aligned rows of 8-element multiples");
   if (spmm_kernel_choice() == 0 && !ctx.side_stream &&
-      spmm_pipe(ctx, rows, rp, col, val, f, 4, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate, job)) {
-    if (job_done) *job_done = job != nullptr;
+      spmm_pipe(ctx, rows, rp, col, val, f, 4, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate))
     return;
-  }
   dispatch<float>(ctx, rows, rp, col, val, f, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate);
 }
 

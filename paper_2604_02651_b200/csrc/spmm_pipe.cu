@@ -15,8 +15,6 @@
 // boundary; empty rows flush zeros.
 #include <type_traits>
 
-#include "ops.hpp"
-#include "rng.cuh"
 #include "runtime.hpp"
 
 namespace ggb {
@@ -49,29 +47,7 @@ struct PipeArgs {
   int accumulate;
   int ocpr;  // output chunks of EPC columns (the flush's unit)
   int hoff;  // P24: byte offset of the low plane in a row
-  KeepJob job;  // keep-bits side job of the extra warps (job.out null: none)
 };
-
-constexpr int kHashWarps = 4;  // one per SM sub-partition
-
-// The side job: keep-bit words of the job's block, grid-stride over (row,
-// word) with one word (32 columns) per thread, exactly k_dropout_keep's bits
-// (rowops.cu) — element_unit(key, row, col) >= rate (pmm.hpp:317-322).
-__device__ __forceinline__ void keep_bits_job(const KeepJob& jb, int64_t t0, int64_t stride) {
-  const int64_t total = jb.rows * jb.ldm;
-  for (int64_t t = t0; t < total; t += stride) {
-    const int64_t r = t / jb.ldm, w = t % jb.ldm;
-    const int64_t j = w / 4, i = w % 4;
-    const uint64_t row_key = hash_combine(jb.key, static_cast<uint64_t>(jb.row_g0 + r));
-    uint32_t bits = 0;
-#pragma unroll 4
-    for (int l = 0; l < 32; ++l) {
-      const int64_t c = j * 128 + 4 * l + i;
-      if (c < jb.cols && element_keep(row_key, static_cast<uint64_t>(jb.col_g0 + c), jb.thresh)) bits |= 1u << l;
-    }
-    jb.out[t] = bits;
-  }
-}
 
 __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -89,10 +65,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// TIn: element type of F; RB: smem bytes per gathered row; HW: extra warps
-// running the keep-bit side job (0 or kHashWarps).
-template <class TIn, int RB, int HW>
-__global__ void __launch_bounds__((kWarps + HW) * 32, 1) k_spmm_pipe(const PipeArgs a) {
+// TIn: element type of F; RB: smem bytes per gathered row.
+template <class TIn, int RB>
+__global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) {
   constexpr bool kP24 = std::is_same_v<TIn, P24>;
   constexpr int EPC = kP24 ? 8 : 16 / static_cast<int>(sizeof(TIn));  // elements per lane chunk
   constexpr int CPR = RB / 16;                                         // 16-byte chunks per row slot
@@ -100,13 +75,6 @@ __global__ void __launch_bounds__((kWarps + HW) * 32, 1) k_spmm_pipe(const PipeA
   constexpr int CPL = kP24 ? 1 : (CPR > 32 ? 2 : 1);                   // chunks per lane (consumer)
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  if constexpr (HW > 0) {
-    if (wib >= kWarps) {
-      keep_bits_job(a.job, static_cast<int64_t>(blockIdx.x) * HW * 32 + (threadIdx.x - kWarps * 32),
-                    static_cast<int64_t>(gridDim.x) * HW * 32);
-      return;
-    }
-  }
   uint8_t* ring = smem + static_cast<size_t>(wib) * kStages * kStageBytes;
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
   float* meta_val = reinterpret_cast<float*>(smem + kWarps * kStages * kStageBytes) + wib * kStages * 32;
@@ -291,27 +259,15 @@ __global__ void __launch_bounds__((kWarps + HW) * 32, 1) k_spmm_pipe(const PipeA
   }
 }
 
-template <class TIn, int RB, int HW>
-void launch_pipe_hw(Ctx& ctx, const PipeArgs& a) {
+template <class TIn, int RB>
+void launch_pipe(Ctx& ctx, const PipeArgs& a) {
   const int smem = kWarps * kStages * kStageBytes + kWarps * kStages * 32 * 4;
   static bool attr = false;
   if (!attr) {
-    GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB, HW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  k_spmm_pipe<TIn, RB, HW><<<ctx.persistent_sms(), (kWarps + HW) * 32, smem, ctx.stream>>>(a);
-}
-
-// keep-bit side jobs ride on the forward instances (fp32 and 24-bit rows)
-template <class TIn, int RB>
-void launch_pipe(Ctx& ctx, const PipeArgs& a) {
-  if constexpr (!std::is_same_v<TIn, bf16>) {
-    if (a.job.out && a.job.rows > 0) {
-      launch_pipe_hw<TIn, RB, kHashWarps>(ctx, a);
-      return;
-    }
-  }
-  launch_pipe_hw<TIn, RB, 0>(ctx, a);
+  k_spmm_pipe<TIn, RB><<<ctx.persistent_sms(), kWarps * 32, smem, ctx.stream>>>(a);
 }
 
 }  // namespace
@@ -320,7 +276,7 @@ void launch_pipe(Ctx& ctx, const PipeArgs& a) {
 // 1 KB slot; returns false otherwise (the caller falls back).
 bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val, const void* f,
                int esize, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb, bf16* outlo, int64_t ldob,
-               int accumulate, const KeepJob* job) {
+               int accumulate) {
   const int64_t row_bytes = round_up(fcols * esize, 16);
   if (row_bytes > 1024 || rows <= 0 || fcols <= 0) return false;
   if (ldf * esize >= (int64_t{1} << 32)) return false;
@@ -340,7 +296,6 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
   a.ldob = ldob;
   a.accumulate = accumulate;
   a.ocpr = a.vcpr;
-  if (job && esize == 4) a.job = *job;
   if (esize == 2) {
     if (row_bytes <= 256)
       launch_pipe<bf16, 256>(ctx, a);
@@ -364,9 +319,7 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
 // Forward SpMM gathering 24-bit rows (see P24): fcols <= 256, row stride
 // ld_bytes (a multiple of 16, >= 3 * round_up(fcols, 8)).
 bool spmm_pipe_p24(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
-                   const uint8_t* f, int64_t ld_bytes, int64_t fcols, bf16* out_hi, bf16* out_lo, int64_t ldob,
-                   const KeepJob* job, bool* job_done) {
-  if (job_done) *job_done = false;
+                   const uint8_t* f, int64_t ld_bytes, int64_t fcols, bf16* out_hi, bf16* out_lo, int64_t ldob) {
   const int64_t c16 = round_up(fcols, 8);
   const int64_t row_bytes = round_up(3 * c16, 16);
   if (rows <= 0 || fcols <= 0 || fcols > 256 || ctx.side_stream) return false;
@@ -387,8 +340,6 @@ bool spmm_pipe_p24(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col
   a.ldob = ldob;
   a.ocpr = static_cast<int>(c16 / 8);
   a.hoff = static_cast<int>(2 * c16);
-  if (job) a.job = *job;
-  if (job_done) *job_done = job != nullptr;
   if (row_bytes <= 384)
     launch_pipe<P24, 384>(ctx, a);
   else

@@ -235,16 +235,6 @@ bool preagg_enabled() {
 // C2: forward SpMM 2.75 -> 2.24 ms/step, but the step only 10.73 -> 10.60 ms
 // (the sampling stream's batch build is the critical chain) and e2e 11.43 ->
 // 11.66 ms (the extra write traffic lands on the build), so it is off.
-// GGB_KEEP_IN_SPMM=0: the fused row kernel hashes its own dropout keep-bits
-// instead of taking them from the forward SpMM's side warps
-bool keep_in_spmm_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("GGB_KEEP_IN_SPMM");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 bool gather24_enabled() {
   const char* e = std::getenv("GGB_GATHER24");
   return e && e[0] == '1';
@@ -310,7 +300,6 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
   const Tensor* prev = &st.x0;
   for (int l = 1; l <= cfg.layers; ++l) {
     LayerBufs& L = st.layers[l - 1];
-    L.keep_ready = false;
     const int p = (l - 1) % 3;
     const BatchCsr& A = bt.csrs[bt.csr_of[p]];
     const Layout alay = adjacency_layout(l);
@@ -377,32 +366,13 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     // accurate: the gathered rows are the previous layer's 24-bit copies when
     // it wrote them (3 bytes per element instead of 4)
     const bool p24 = accurate && prev->p != nullptr;
-    // this layer's dropout keep-bits, hashed by the SpMM's side warps while
-    // its gathers are in flight (the row kernel then skips the hash)
-    KeepJob job;
-    const KeepJob* jobp = nullptr;
-    if (accurate && drop && keep_in_spmm_enabled() && st.wl.size() >= static_cast<size_t>(l)) {
-      const ParamSlot& wn = st.params[st.wl[l - 1]];  // xw's column block = W_l's
-      job.key = dropout_key(run_seed, dp, global_step, l);
-      job.thresh = thresh;
-      job.rows = A.n_rows;
-      job.cols = wn.blk.cols();
-      job.row_g0 = A.r0;
-      job.col_g0 = wn.blk.c0;
-      job.ldm = mask_words(std::max<int64_t>(job.cols, 1));
-      job.out = grow<uint32_t>(L.keep, std::max<int64_t>(job.rows, 1) * job.ldm);
-      jobp = &job;
-    }
-    bool job_done = false;
     ProfScope ps(ctx, kProfSpmmFwd, spmm_bytes(A.n_rows, A.nnz, F.cols(), p24 ? 3 : (accurate ? 4 : 2), accurate ? 4 : 2),
                  2.0 * A.nnz * F.cols());
     if (accurate) {
       if (!(p24 && spmm_pipe_p24(ctx, A.n_rows, arp, acol, aval, prev->p, prev->ldp, F.cols(), L.hagg.b, L.hagg.lo,
-                                 L.hagg.ldb, jobp, &job_done)))
+                                 L.hagg.ldb)))
         spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), nullptr, 0, L.hagg.b, L.hagg.lo,
-                     L.hagg.ldb, 0, jobp, &job_done);
-      L.keep_ready = job_done;
-      L.keep_key = job.key;
+                     L.hagg.ldb, 0);
     } else {
       spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), nullptr, 0, L.hagg.b, L.hagg.ldb, 0);
     }
@@ -527,10 +497,8 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     fa.ldp = L.x.ldp;
     fa.hoff = L.x.hoff;
     fa.ldm = L.ldm;
-    fa.keep = nullptr;  // keep-bits precomputed for exactly this block?
-    if (drop && L.keep_ready && L.keep_key == fa.mask_key) {  // by this layer's forward SpMM
-      fa.keep = L.keep.as<uint32_t>();
-    } else if (drop && bt.masks.size() >= static_cast<size_t>(l)) {  // by the prefetcher
+    fa.keep = nullptr;  // keep-bits precomputed by the prefetcher for exactly this block?
+    if (drop && bt.masks.size() >= static_cast<size_t>(l)) {
       const DropMask& dm = bt.masks[l - 1];
       if (dm.key == fa.mask_key && dm.thresh == thresh && dm.r0 == xb.r0 && dm.c0 == xb.c0 &&
           dm.rows == xb.rows() && dm.cols == xb.cols() && dm.ldm == L.ldm)

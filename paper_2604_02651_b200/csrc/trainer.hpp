@@ -45,11 +45,8 @@ enum Compute : int { kAccurate = 0, kFast = 1 };
 
 struct LayerBufs {
   DevBuf hagg_f, hagg_b, hagg_lo, xw, ss, rms, mask, x_f, x_b, x_lo, x_p;
-  DevBuf keep;  // dropout keep-bits made by the forward SpMM's side warps
   Tensor hagg, xw_t, x;  // x = layer output X_l
   int64_t ldm = 0;
-  bool keep_ready = false;  // keep holds this step's bits (key keep_key)
-  uint64_t keep_key = 0;
 };
 
 struct State {
