@@ -31,6 +31,29 @@ __host__ __device__ __forceinline__ bool element_keep(uint64_t row_key, uint64_t
   return (h >> 11) >= thresh;
 }
 
+/// The column term of hash_combine(row_key, j): hash_combine(a, j) =
+/// splitmix64(a ^ column_term(j)), so a row kernel computes it once per column.
+__host__ __device__ __forceinline__ uint64_t column_term(uint64_t j) { return kGolden + (j << 6) + (j >> 2); }
+
+#ifdef __CUDACC__
+/// element_keep(row_key, j, thresh) with cj = column_term(j) and
+/// T = thresh << 11 ((h >> 11) >= thresh <=> h >= T for thresh < 2^53): the
+/// last multiply of the second splitmix64 is formed for its high word only,
+/// and the full hash is finished only when the high words tie (p = 2^-32).
+__device__ __forceinline__ bool element_keep_cj(uint64_t row_key, uint64_t cj, uint64_t T) {
+  const uint64_t h1 = splitmix64(row_key ^ cj);
+  uint64_t x = h1 + kGolden;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  const uint32_t xl = static_cast<uint32_t>(x), xh = static_cast<uint32_t>(x >> 32);
+  const uint32_t hi = __umulhi(xl, 0x133111ebu) + xl * 0x94d049bbu + xh * 0x133111ebu;  // (x * C2) >> 32
+  const uint32_t hh = hi ^ (hi >> 31);
+  const uint32_t th = static_cast<uint32_t>(T >> 32);
+  if (hh != th) return hh > th;
+  return splitmix64(h1) >= T;
+}
+#endif
+
 /// detail::dropout_key (model.hpp:164-171).
 __host__ __device__ __forceinline__ uint64_t dropout_key(uint64_t seed, int dp, uint64_t gstep, int layer) {
   return hash_combine(hash_combine(hash_combine(hash_combine(seed, 0xd509), static_cast<uint64_t>(dp)), gstep),

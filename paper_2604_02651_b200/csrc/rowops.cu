@@ -129,6 +129,12 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
   // row's ReLU-active columns (compacted), and one keep byte per column
   __shared__ uint16_t s_list[kRowsPerBlock][32 * 4 * J];
   __shared__ __align__(16) uint8_t s_kb[kRowsPerBlock][kRowChunk * J];
+  __shared__ uint64_t s_cj[kRowChunk * J];  // column_term of every local column
+  if (hash) {
+    for (int c = threadIdx.x; c < kRowChunk * J; c += kT) s_cj[c] = column_term(static_cast<uint64_t>(p.col_g0 + c));
+    __syncthreads();
+  }
+  const uint64_t T = p.thresh << 11;
 
 #pragma unroll 1
   for (int64_t r = w0; r < p.rows; r += nw) {
@@ -203,7 +209,7 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
       const uint64_t row_key = hash_combine(p.mask_key, static_cast<uint64_t>(p.row_g0 + r));
       for (int k = lane; k < total; k += 32) {
         const int col = s_list[wib][k];
-        s_kb[wib][col] = element_keep(row_key, static_cast<uint64_t>(p.col_g0 + col), p.thresh) ? 1 : 0;
+        s_kb[wib][col] = element_keep_cj(row_key, s_cj[col], T) ? 1 : 0;
       }
       __syncwarp();
       // the lane's 4 keep bytes per chunk in one load (bytes of inactive
@@ -265,7 +271,8 @@ __global__ void __launch_bounds__(128) k_dropout_keep(uint64_t key, int64_t rows
 #pragma unroll 4
   for (int l = 0; l < 32; ++l) {
     const int64_t c = j * kRowChunk + 4 * l + i;
-    if (c < cols && element_keep(row_key, static_cast<uint64_t>(col_g0 + c), thresh)) bits |= 1u << l;
+    if (c < cols && element_keep_cj(row_key, column_term(static_cast<uint64_t>(col_g0 + c)), thresh << 11))
+      bits |= 1u << l;
   }
   out[t] = bits;
   }
