@@ -12,6 +12,7 @@
 // When the row is split over the grid's column axis the same kernels run in
 // two phases around the fp32 all-reduce of the row statistic.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.hpp"
 #include "rng.cuh"
@@ -515,10 +516,17 @@ inline unsigned row_blocks(int64_t rows) { return static_cast<unsigned>(ceil_div
 
 template <int J, bool Full>
 void launch_fwd_row(Ctx& ctx, const FwdApply& p) {
-  // a warp per row (the kernel also strides, for capped grids): the dropout
-  // hashing needs every resident warp it can get to hide its latency
-  const unsigned g = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(p.rows, kRowsPerBlock)));
-  k_fwd_row<J, Full><<<g, kT, 0, ctx.stream>>>(p);
+  // a warp per row: the row's load latency is hidden by the other resident
+  // warps rather than by a software pipeline. GGB_FWD_ROW_BPS=b caps the grid
+  // at b blocks per SM striding over the rows (measured slower: 4 -> 1.76
+  // ms/step, 8 -> 1.66, one warp per row 1.58)
+  static const int bps = [] {
+    const char* e = std::getenv("GGB_FWD_ROW_BPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  int64_t g = ceil_div(p.rows, kRowsPerBlock);
+  if (bps > 0) g = std::min<int64_t>(g, static_cast<int64_t>(bps) * ctx.num_sms);
+  k_fwd_row<J, Full><<<static_cast<unsigned>(std::max<int64_t>(1, g)), kT, 0, ctx.stream>>>(p);
 }
 
 void fwd_apply(Ctx& ctx, const FwdApply& p) {
