@@ -38,6 +38,12 @@ CONFIGS = {
     # BASELINE configs[0]: the reference's own CPU-runnable case (ER stand-in for RMAT)
     "C1": dict(workload="synthetic ER 2^16 vertices / 1M edges, 64 feat, 3-layer GCN hidden 128",
                n=65_536, avg_degree=30.52, d_in=64, n_classes=16, layers=3, d_h=128, batch=16_384),
+    # BASELINE configs[0] as named: R-MAT 2^16 vertices / 2^20 edge draws (Graph500 a,b,c,d =
+    # .57,.19,.19,.05; drawn on the GPU), 64 feat, 3-layer GCN hidden 128, batch N/4
+    "C1R": dict(workload="synthetic R-MAT scale 16 (65,536 vertices, 2^20 edge draws), 64 feat, "
+                         "3-layer GCN hidden 128",
+                n=65_536, rmat_scale=16, rmat_edges=1 << 20, avg_degree=None, d_in=64, n_classes=16, layers=3,
+                d_h=128, batch=16_384),
     # BASELINE configs[1]: the metric's configuration
     "C2": dict(workload="ogbn-products-shaped synthetic (2.45M vertices, 61.9M edges, 100 feat, 47 classes), "
                         "3-layer GCN hidden 256",
@@ -156,7 +162,11 @@ def reference_baseline(cfg: dict, steps: int, warmup: int, cores: int | None = N
     dims = (1, *g)
     R = O.Ref()
     t0 = time.time()
-    h = R.dataset_synthetic(cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"], DATA_SEED)
+    if cfg.get("rmat_scale"):  # the same R-MAT edge list (oracle restatement of the device generator)
+        uv = O.rmat_edges(cfg["rmat_scale"], cfg["rmat_edges"], DATA_SEED)
+        h = R.dataset_from(O.dataset_from_edges(cfg["n"], uv, cfg["d_in"], cfg["n_classes"], DATA_SEED), uv)
+    else:
+        h = R.dataset_synthetic(cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"], DATA_SEED)
     t_data = time.time() - t0
     try:
         mcfg = O.ModelConfig(layers=cfg["layers"], d_in=cfg["d_in"], d_h=cfg["d_h"], d_out=cfg["n_classes"],
@@ -278,8 +288,14 @@ def main():
     t0 = time.time()
     # generate_synthetic on the device (CSR, labels, split bit-identical to the
     # reference generator, features to within one fp32 ulp in rare elements)
-    graph = gg.Graph.generate_synthetic_device(ctx, cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"],
-                                               DATA_SEED, cfg["layers"])
+    if cfg.get("rmat_scale"):
+        rds = gg.Dataset.generate_rmat(ctx, cfg["rmat_scale"], cfg["rmat_edges"], cfg["d_in"], cfg["n_classes"],
+                                       DATA_SEED)
+        graph = rds.to_graph(ctx, cfg["layers"])
+        rds.close()
+    else:
+        graph = gg.Graph.generate_synthetic_device(ctx, cfg["n"], cfg["avg_degree"], cfg["d_in"], cfg["n_classes"],
+                                                   DATA_SEED, cfg["layers"])
     if args.host_features:
         graph.features_to_host()
     t_graph = time.time() - t0

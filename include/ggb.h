@@ -141,6 +141,18 @@ int ggb_dataset_load(const char* edges, const char* features, const char* labels
 /* generate_synthetic + synthetic_edges (dataset.cpp:85-150), host native. */
 int ggb_dataset_generate_synthetic(int64_t n, double avg_degree, int64_t d_in, int64_t n_classes,
                                    uint64_t seed, ggb_dataset_t* out);
+/* R-MAT input (BASELINE configs[0]; new code — the reference has only its ER
+ * generator, dataset.cpp:133-150): m edge draws over 2^scale vertices with
+ * Graph500 quadrant probabilities (a, b, c, 1-a-b-c), generated on the GPU
+ * (counter-based, one thread per edge). ggb_rmat_edges returns the raw list
+ * (host_uv = 2 x m); ggb_dataset_generate_rmat builds the dataset from it as
+ * generate_synthetic does from its ER list (normalize_adjacency,
+ * dataset.cpp:47-83; features, degree-quantile labels and split from seed),
+ * so ggb_dataset_save + the reference's load_dataset reproduce it. */
+int ggb_rmat_edges(ggb_ctx_t ctx, int32_t scale, int64_t m, double a, double b, double c, uint64_t seed,
+                   int64_t* host_uv);
+int ggb_dataset_generate_rmat(ggb_ctx_t ctx, int32_t scale, int64_t m, double a, double b, double c,
+                              int64_t d_in, int64_t n_classes, uint64_t seed, ggb_dataset_t* out);
 /* info = {n, nnz, d_in, n_classes, raw_edges} (5 entries) */
 int ggb_dataset_info(ggb_dataset_t d, int64_t* info);
 /* any pointer may be NULL; col_idx int64 (CsrMatrix), edges_uv = 2 x raw_edges */

@@ -354,3 +354,29 @@ void orc_dropout_keep(uint64_t key, int64_t r0, int64_t c0, int64_t rows, int64_
       out[i * cols + j] =
           orc_element_unit(key, (uint64_t)(r0 + i), (uint64_t)(c0 + j)) >= rate ? 1 : 0;
 }
+
+/* R-MAT edge list of gendata.cu k_rmat (new code, not in the reference: the
+ * BASELINE configs[0] input). Edge e descends `scale` levels; level k draws
+ * u = unit(splitmix64(hash_combine(hash_combine(key, e), k))) with
+ * key = hash_combine(seed, 0x7a3a7) and takes quadrant a | b | c | d. */
+void orc_rmat_edges(int scale, int64_t m, double a, double b, double c, uint64_t seed, int64_t* uv) {
+  const uint64_t key = orc_hash_combine(seed, 0x7a3a7);
+  for (int64_t e = 0; e < m; ++e) {
+    const uint64_t ke = orc_hash_combine(key, (uint64_t)e);
+    int64_t u = 0, v = 0;
+    for (int k = 0; k < scale; ++k) {
+      const double x = (double)(orc_splitmix64(orc_hash_combine(ke, (uint64_t)k)) >> 11) * 0x1.0p-53;
+      const int64_t bit = (int64_t)1 << (scale - 1 - k);
+      if (x >= a + b + c) {
+        u |= bit;
+        v |= bit;
+      } else if (x >= a + b) {
+        u |= bit;
+      } else if (x >= a) {
+        v |= bit;
+      }
+    }
+    uv[2 * e] = u;
+    uv[2 * e + 1] = v;
+  }
+}

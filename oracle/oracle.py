@@ -75,6 +75,7 @@ def orc() -> C.CDLL:
                                           P, P, P, P, P, P]
         L.orc_synthetic_edges.restype = I64
         L.orc_synthetic_edges.argtypes = [I64, C.c_double, U64, P]
+        L.orc_rmat_edges.argtypes = [C.c_int, I64, C.c_double, C.c_double, C.c_double, U64, P]
         L.orc_normalize_adjacency.restype = I64
         L.orc_normalize_adjacency.argtypes = [P, I64, I64, P, P, P]
         L.orc_features.argtypes = [I64, I64, U64, P]
@@ -196,6 +197,13 @@ def synthetic_edges(n: int, avg_degree: float, seed: int) -> np.ndarray:
     m = L.orc_synthetic_edges(n, avg_degree, seed, None)
     uv = np.empty((m, 2), np.int64)
     L.orc_synthetic_edges(n, avg_degree, seed, _ptr(uv))
+    return uv
+
+
+def rmat_edges(scale: int, m: int, seed: int, a: float = 0.57, b: float = 0.19, c: float = 0.19) -> np.ndarray:
+    """R-MAT edge list (oracle.c orc_rmat_edges; restates gendata.cu k_rmat)."""
+    uv = np.empty((m, 2), np.int64)
+    orc().orc_rmat_edges(scale, m, a, b, c, seed, _ptr(uv))
     return uv
 
 

@@ -48,6 +48,8 @@ _SIGS = [
     ("ggb_graph_export", C.c_int, [P, P, P, P, P, P, P]),
     ("ggb_dataset_load", C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, P]),
     ("ggb_dataset_generate_synthetic", C.c_int, [I64, F64, I64, I64, U64, P]),
+    ("ggb_rmat_edges", C.c_int, [P, I32, I64, F64, F64, F64, U64, P]),
+    ("ggb_dataset_generate_rmat", C.c_int, [P, I32, I64, F64, F64, F64, I64, I64, U64, P]),
     ("ggb_dataset_info", C.c_int, [P, P]),
     ("ggb_dataset_export", C.c_int, [P, P, P, P, P, P, P, P]),
     ("ggb_dataset_save", C.c_int, [P, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p]),

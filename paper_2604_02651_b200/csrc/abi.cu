@@ -569,6 +569,34 @@ int ggb_dataset_generate_synthetic(int64_t n, double avg_degree, int64_t d_in, i
   });
 }
 
+int ggb_rmat_edges(ggb_ctx_t ctx, int32_t scale, int64_t m, double a, double b, double c, uint64_t seed,
+                   int64_t* host_uv) {
+  return guard([&] {
+    require(host_uv || m == 0, "rmat: null output");
+    use_device(*ctx);
+    DevBuf uv;
+    int64_t* d = uv.reserve_n<int64_t>(static_cast<size_t>(std::max<int64_t>(2 * m, 1)));
+    rmat_edges_device(*ctx, scale, m, a, b, c, seed, d);
+    download(host_uv, d, static_cast<size_t>(2 * m), ctx->stream);
+  });
+}
+
+int ggb_dataset_generate_rmat(ggb_ctx_t ctx, int32_t scale, int64_t m, double a, double b, double c, int64_t d_in,
+                              int64_t n_classes, uint64_t seed, ggb_dataset_t* out) {
+  return guard([&] {
+    require(out != nullptr, "dataset: null handle slot");
+    use_device(*ctx);
+    auto d = std::make_unique<ggb_dataset_s>();
+    d->uv.resize(static_cast<size_t>(2 * m));
+    DevBuf uv;
+    int64_t* dev = uv.reserve_n<int64_t>(static_cast<size_t>(std::max<int64_t>(2 * m, 1)));
+    rmat_edges_device(*ctx, scale, m, a, b, c, seed, dev);
+    download(d->uv.data(), dev, d->uv.size(), ctx->stream);
+    static_cast<HostDataset&>(*d) = dataset_from_edges(int64_t{1} << scale, d->uv.data(), m, d_in, n_classes, seed);
+    *out = d.release();
+  });
+}
+
 int ggb_dataset_info(ggb_dataset_t d, int64_t* info) {
   return guard([&] {
     require(d && info, "dataset_info: null argument");

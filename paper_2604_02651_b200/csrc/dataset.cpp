@@ -216,11 +216,17 @@ HostDataset generate_synthetic(int64_t n, double avg_degree, int64_t d_in, int64
                                uint64_t seed) {
   require(n >= 1, "generate_synthetic: n must be >= 1");
   require(avg_degree >= 0, "generate_synthetic: avg_degree must be >= 0");
+  const auto uv = synthetic_edges(n, avg_degree, seed);
+  return dataset_from_edges(n, uv.data(), static_cast<int64_t>(uv.size() / 2), d_in, n_classes, seed);
+}
+
+HostDataset dataset_from_edges(int64_t n, const int64_t* uv, int64_t m, int64_t d_in, int64_t n_classes,
+                               uint64_t seed) {
+  require(n >= 1, "generate_synthetic: n must be >= 1");
   require(n_classes >= 2, "generate_synthetic: n_classes must be >= 2");
   require(n_classes <= n, "generate_synthetic: n_classes > n");
   HostDataset ds;
-  const auto uv = synthetic_edges(n, avg_degree, seed);
-  ds.adj = normalize_adjacency(uv.data(), static_cast<int64_t>(uv.size() / 2), n);
+  ds.adj = normalize_adjacency(uv, m, n);
   ds.n = n;
   ds.d_in = d_in;
   ds.n_classes = n_classes;

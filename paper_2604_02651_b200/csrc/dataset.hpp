@@ -29,5 +29,9 @@ void degree_labels(int64_t n, const int64_t* row_ptr, int64_t n_classes, int32_t
 void split_tags(int64_t n, uint64_t seed, uint8_t* split);
 HostDataset generate_synthetic(int64_t n, double avg_degree, int64_t d_in, int64_t n_classes,
                                uint64_t seed);
+/// generate_synthetic with the ER edge stream replaced by the given edge list
+/// (normalized adjacency, N(0,1) features, degree-quantile labels, 60/20/20 split)
+HostDataset dataset_from_edges(int64_t n, const int64_t* uv, int64_t m, int64_t d_in, int64_t n_classes,
+                               uint64_t seed);
 
 }  // namespace ggb

@@ -215,6 +215,50 @@ __global__ void k_shard_fill(const int32_t* __restrict__ col, const double* __re
   }
 }
 
+// R-MAT edge draws (Chakrabarti et al.; Graph500 parameters a, b, c, d = 1-a-b-c):
+// edge e descends `scale` levels of the adjacency quadtree, level k taking
+// quadrant q(u) for u = unit(splitmix64(hash_combine(hash_combine(key, e), k)))
+// (u < a: top-left, < a+b: top-right, < a+b+c: bottom-left, else
+// bottom-right); the row/col bits of level k have weight 2^(scale-1-k).
+// Counter-based, so every edge is independent and the list is a pure function
+// of (scale, m, a, b, c, seed); oracle.c restates it for the parity tests.
+__global__ void k_rmat(int scale, int64_t m, double a, double ab, double abc, uint64_t key,
+                       int64_t* __restrict__ uv) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const uint64_t ke = hash_combine(key, static_cast<uint64_t>(e));
+  int64_t u = 0, v = 0;
+  for (int k = 0; k < scale; ++k) {
+    const double x = static_cast<double>(splitmix64(hash_combine(ke, static_cast<uint64_t>(k))) >> 11) * 0x1.0p-53;
+    const int64_t bit = int64_t{1} << (scale - 1 - k);
+    if (x >= abc) {
+      u |= bit;
+      v |= bit;
+    } else if (x >= ab) {
+      u |= bit;
+    } else if (x >= a) {
+      v |= bit;
+    }
+  }
+  uv[2 * e] = u;
+  uv[2 * e + 1] = v;
+}
+
+}  // namespace
+
+void rmat_edges_device(Ctx& ctx, int scale, int64_t m, double a, double b, double c, uint64_t seed, int64_t* uv_dev) {
+  require(scale >= 1 && scale <= 40, "rmat: scale must be in [1, 40]");
+  require(m >= 0, "rmat: edge count must be >= 0");
+  require(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0, "rmat: need a, b, c >= 0 and a + b + c <= 1");
+  if (m == 0) return;
+  k_rmat<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, ctx.stream>>>(scale, m, a, a + b, a + b + c,
+                                                                          hash_combine(seed, 0x7a3a7), uv_dev);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
+namespace {
+
 int bits_for(uint64_t x) {  // smallest b with 2^b > x
   int b = 0;
   while (b < 64 && (x >> b) != 0) ++b;

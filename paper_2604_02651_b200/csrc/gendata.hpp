@@ -16,6 +16,9 @@ struct DevDataset {
 
 void generate_synthetic_device(Ctx& ctx, int64_t n, double avg_degree, int64_t d_in, int64_t n_classes,
                                uint64_t seed, DevDataset& ds);
+/// R-MAT edge list (Graph500 quadrant probabilities a, b, c; 2^scale
+/// vertices, m draws) into uv_dev [2m] int64 (gendata.cu k_rmat).
+void rmat_edges_device(Ctx& ctx, int scale, int64_t m, double a, double b, double c, uint64_t seed, int64_t* uv_dev);
 /// make_csr_shard (shardsample.cpp:19-45) of the device CSR.
 void build_shard_device(Ctx& ctx, int64_t n, const DevDataset& ds, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
                         PlaneShard& sh);

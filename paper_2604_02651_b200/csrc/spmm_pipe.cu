@@ -13,6 +13,8 @@
 // The consumer accumulates in fp32 registers (lane l owns 16-byte chunks l and
 // l+32 of the row) and flushes a row when the stream crosses its row_ptr
 // boundary; empty rows flush zeros.
+#include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "runtime.hpp"
@@ -47,9 +49,48 @@ struct PipeArgs {
   int accumulate;
   int ocpr;  // output chunks of EPC columns (the flush's unit)
   int hoff;  // P24: byte offset of the low plane in a row
+  int balanced;  // work-balanced row ranges (else an even row split)
 };
 
+// GGB_SPMM_SPLIT=rows: even row split across warps (the round-1 scheme)
+int balanced_split() {
+  static const int v = [] {
+    const char* e = std::getenv("GGB_SPMM_SPLIT");
+    return (e && std::string(e) == "rows") ? 0 : 1;
+  }();
+  return v;
+}
+
 __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// Work-balanced row ranges: warp w of W owns rows [first(w), first(w+1)),
+// first(w) = the smallest row r with cost(r) >= w * cost(rows) / W, where
+// cost(r) = (rp[r] - rp[0]) + r counts nonzeros (one gathered feature row
+// each) plus one flush per row. Power-law graphs (R-MAT) put thousands of
+// nonzeros in a few rows: an even row split leaves their warps running long
+// after the rest. Warp-cooperative 32-ary search: ~4 dependent loads.
+__device__ __forceinline__ int64_t balanced_first_row(const int64_t* rp, int64_t rows, int64_t w, int64_t W,
+                                                      int lane) {
+  if (w <= 0) return 0;
+  if (w >= W) return rows;
+  const int64_t base = rp[0];
+  const int64_t total = (rp[rows] - base) + rows;
+  // target = ceil(w * total / W) without overflowing 64 bits
+  const int64_t target = (total / W) * w + ((total % W) * w + W - 1) / W;
+  int64_t lo = 0, hi = rows;  // cost(hi) >= target; answer in (lo, hi] unless cost(lo) >= target
+  if (target <= 0) return 0;
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t probe = imin(hi, lo + (lane + 1) * step);
+    const bool ge = (__ldg(rp + probe) - base) + probe >= target;
+    const uint32_t m = __ballot_sync(0xffffffffu, ge);
+    const int first = m ? __ffs(m) - 1 : 31;
+    const int64_t nhi = imin(hi, lo + (first + 1) * step);
+    lo = lo + first * step;
+    hi = nhi;
+  }
+  return hi;
+}
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
@@ -81,8 +122,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
 
   const int64_t total_warps = static_cast<int64_t>(gridDim.x) * kWarps;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + wib;
-  const int64_t per = (a.rows + total_warps - 1) / total_warps;
-  const int64_t r_begin = imin(a.rows, gw * per), r_end = imin(a.rows, r_begin + per);
+  int64_t r_begin, r_end;
+  if (a.balanced) {
+    r_begin = balanced_first_row(a.rp, a.rows, gw, total_warps, lane);
+    r_end = balanced_first_row(a.rp, a.rows, gw + 1, total_warps, lane);
+  } else {
+    const int64_t per = (a.rows + total_warps - 1) / total_warps;
+    r_begin = imin(a.rows, gw * per);
+    r_end = imin(a.rows, r_begin + per);
+  }
   if (r_begin >= r_end) return;
   const int64_t e_begin = a.rp[r_begin], e_end = a.rp[r_end];
   const int64_t n_stages = (e_end - e_begin + S - 1) / S;
@@ -296,6 +344,7 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
   a.ldob = ldob;
   a.accumulate = accumulate;
   a.ocpr = a.vcpr;
+  a.balanced = balanced_split();
   if (esize == 2) {
     if (row_bytes <= 256)
       launch_pipe<bf16, 256>(ctx, a);
@@ -340,6 +389,7 @@ bool spmm_pipe_p24(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col
   a.ldob = ldob;
   a.ocpr = static_cast<int>(c16 / 8);
   a.hoff = static_cast<int>(2 * c16);
+  a.balanced = balanced_split();
   if (row_bytes <= 384)
     launch_pipe<P24, 384>(ctx, a);
   else

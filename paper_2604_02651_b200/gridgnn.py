@@ -35,6 +35,18 @@ def _ptr(a: np.ndarray | None):
 
 # ---- host-side layout algebra (grid.hpp, shardsample.cpp:8-17, pmm.hpp:31-63) -------
 
+# Graph500 R-MAT quadrant probabilities (d = 1 - a - b - c = 0.05)
+RMAT_A, RMAT_B, RMAT_C = 0.57, 0.19, 0.19
+
+
+def rmat_edges(ctx: "Context", scale: int, edges: int, seed: int, a: float = RMAT_A, b: float = RMAT_B,
+               c: float = RMAT_C) -> np.ndarray:
+    """The raw R-MAT edge list (edges x 2, int64) drawn on the GPU."""
+    out = np.empty((edges, 2), np.int64)
+    check(lib().ggb_rmat_edges(ctx.h, scale, edges, a, b, c, seed, _ptr(out)))
+    return out
+
+
 def block_partition(n: int, g: int) -> np.ndarray:
     if g < 1:
         raise InvalidArgument(1, "block_partition: g must be >= 1")
@@ -327,6 +339,15 @@ class Dataset:
     def generate_synthetic(n: int, avg_degree: float, d_in: int, n_classes: int, seed: int) -> "Dataset":
         h = P()
         check(lib().ggb_dataset_generate_synthetic(n, avg_degree, d_in, n_classes, seed, C.byref(h)))
+        return Dataset(h)
+
+    @staticmethod
+    def generate_rmat(ctx: "Context", scale: int, edges: int, d_in: int, n_classes: int, seed: int,
+                      a: float = RMAT_A, b: float = RMAT_B, c: float = RMAT_C) -> "Dataset":
+        """R-MAT graph (Graph500 parameters by default; edges drawn on the GPU)
+        with generate_synthetic's features, labels and split."""
+        h = P()
+        check(lib().ggb_dataset_generate_rmat(ctx.h, scale, edges, a, b, c, d_in, n_classes, seed, C.byref(h)))
         return Dataset(h)
 
     def save(self, edges=None, features=None, labels=None, split=None) -> None:

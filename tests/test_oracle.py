@@ -195,3 +195,26 @@ def test_reference_comm_stats_accounting(orc, ref):
         assert per_group[0] == per_group[1] == per_group[2]
     finally:
         ref.free_dataset(h)
+
+
+def test_rmat_restatement_matches_python(orc):
+    """orc_rmat_edges (restating gendata.cu k_rmat) against a pure-Python
+    evaluation of the same quadrant descent on a small case."""
+    scale, m, seed, a, b, c = 6, 200, 11, 0.57, 0.19, 0.19
+    key = orc.hash_combine(seed, 0x7a3a7)
+    want = []
+    for e in range(m):
+        ke = orc.hash_combine(key, e)
+        u = v = 0
+        for k in range(scale):
+            x = (orc.splitmix64(orc.hash_combine(ke, k)) >> 11) * 2.0 ** -53
+            bit = 1 << (scale - 1 - k)
+            if x >= a + b + c:
+                u |= bit
+                v |= bit
+            elif x >= a + b:
+                u |= bit
+            elif x >= a:
+                v |= bit
+        want.append((u, v))
+    assert np.array_equal(orc.rmat_edges(scale, m, seed, a, b, c), np.array(want, np.int64))
