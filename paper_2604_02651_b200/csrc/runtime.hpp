@@ -78,6 +78,7 @@ struct Ctx {
   int sm_reserve = 0;
   int persistent_sms() const { return num_sms - sm_reserve > 0 ? num_sms - sm_reserve : 1; }
   std::unique_ptr<Prof> prof;
+  DevBuf spmm_carry;  // per-warp partial rows of the pipelined SpMM's shared rows
   CommStats stats;
   int phase = kPhaseOther;
   ~Ctx();

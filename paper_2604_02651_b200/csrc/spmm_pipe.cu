@@ -50,13 +50,26 @@ struct PipeArgs {
   int ocpr;  // output chunks of EPC columns (the flush's unit)
   int hoff;  // P24: byte offset of the low plane in a row
   int balanced;  // work-balanced row ranges (else an even row split)
+  // rows longer than split_len nonzeros are split across warps along the
+  // merge path (rows, nonzeros); partial sums go to per-warp carry rows and
+  // k_spmm_carry_fixup adds them in warp order (deterministic)
+  int64_t split_mult;  // rows of more than max(64, split_mult * work per warp) nonzeros are split
+  float* lead;        // [warps][carry_ld]: partial of the warp's first row (owned by it, begun earlier)
+  float* tail;        // [warps][carry_ld]: partial of the row the warp leaves unfinished
+  int64_t* lead_row;  // [warps] row id or -1
+  int64_t* tail_row;  // [warps] row id or -1
+  int carry_ld;
 };
 
-// GGB_SPMM_SPLIT=rows: even row split across warps (the round-1 scheme)
-int balanced_split() {
+// Warp work split: 2 = merge path with long rows shared (default), 1 =
+// work-balanced whole rows (GGB_SPMM_SPLIT=balanced), 0 = even row split, the
+// round-1 scheme (GGB_SPMM_SPLIT=rows)
+int split_mode() {
   static const int v = [] {
     const char* e = std::getenv("GGB_SPMM_SPLIT");
-    return (e && std::string(e) == "rows") ? 0 : 1;
+    if (e && std::string(e) == "rows") return 0;
+    if (e && std::string(e) == "balanced") return 1;
+    return 2;
   }();
   return v;
 }
@@ -92,6 +105,38 @@ __device__ __forceinline__ int64_t balanced_first_row(const int64_t* rp, int64_t
   return hi;
 }
 
+// Point (row, nonzero) of warp w's start on the merge path of (row flushes,
+// nonzeros): diagonal d = ceil(w * total / W), total = nonzeros + rows. A
+// point inside a row of at most split_len nonzeros snaps back to that row's
+// start (the row stays whole); one at a row's end moves to the next row's
+// start. So only long rows are shared between warps.
+__device__ __forceinline__ void path_point(const int64_t* rp, int64_t rows, int64_t w, int64_t W, int64_t split_mult,
+                                           int lane, int64_t& r, int64_t& e) {
+  const int64_t base = rp[0];
+  const int64_t total = (rp[rows] - base) + rows;
+  const int64_t split_len = split_mult * (total / W) > 64 ? split_mult * (total / W) : 64;
+  if (w <= 0) {
+    r = 0;
+    e = base;
+    return;
+  }
+  const int64_t d = w >= W ? total : (total / W) * w + ((total % W) * w + W - 1) / W;
+  if (d >= total) {
+    r = rows;
+    e = rp[rows];
+    return;
+  }
+  // smallest r' with cost(r') >= d + 1, minus one (cost(r') = rp[r'] - base + r')
+  r = balanced_first_row(rp, rows, d + 1, total, lane) - 1;
+  e = base + (d - r);
+  const int64_t s = rp[r], t = rp[r + 1];
+  if (e > s && t - s <= split_len) {
+    e = s;
+  } else if (e == t && e > s) {
+    r += 1;
+  }
+}
+
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
@@ -122,17 +167,29 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
 
   const int64_t total_warps = static_cast<int64_t>(gridDim.x) * kWarps;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + wib;
-  int64_t r_begin, r_end;
-  if (a.balanced) {
+  int64_t r_begin, r_end, e_begin, e_end;
+  bool lead = false;  // the first row began in earlier warps: its flush goes to the carry
+  if (a.lead) {
+    path_point(a.rp, a.rows, gw, total_warps, a.split_mult, lane, r_begin, e_begin);
+    path_point(a.rp, a.rows, gw + 1, total_warps, a.split_mult, lane, r_end, e_end);
+    lead = r_begin < a.rows && e_begin > a.rp[r_begin];
+    if (lane == 0) {
+      a.lead_row[gw] = -1;
+      a.tail_row[gw] = -1;
+    }
+  } else if (a.balanced) {
     r_begin = balanced_first_row(a.rp, a.rows, gw, total_warps, lane);
     r_end = balanced_first_row(a.rp, a.rows, gw + 1, total_warps, lane);
+    e_begin = a.rp[r_begin];
+    e_end = a.rp[r_end];
   } else {
     const int64_t per = (a.rows + total_warps - 1) / total_warps;
     r_begin = imin(a.rows, gw * per);
     r_end = imin(a.rows, r_begin + per);
+    e_begin = a.rp[r_begin];
+    e_end = a.rp[r_end];
   }
-  if (r_begin >= r_end) return;
-  const int64_t e_begin = a.rp[r_begin], e_end = a.rp[r_end];
+  if (r_begin >= r_end && e_begin >= e_end) return;
   const int64_t n_stages = (e_end - e_begin + S - 1) / S;
 
   int32_t nx_col = 0;  // lane k < S: column id / value of entry k of the next stage to issue
@@ -177,7 +234,26 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
   int64_t row = r_begin;
   int64_t row_end_e = a.rp[row + 1];
 
+  // the partial sums of a shared row, in column order, to a carry row
+  auto to_carry = [&](float* dst) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int ch = lane + 32 * q;
+      if (ch < a.ocpr) {
+#pragma unroll
+        for (int i = 0; i < EPC; ++i) dst[ch * EPC + i] = acc[q][i];
+      }
+#pragma unroll
+      for (int i = 0; i < EPC; ++i) acc[q][i] = 0.f;
+    }
+  };
+
   auto flush = [&]() {
+    if (lead && row == r_begin) {
+      to_carry(a.lead + gw * a.carry_ld);
+      if (lane == 0) a.lead_row[gw] = row;
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int ch = lane + 32 * q;
@@ -305,17 +381,66 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
     flush();
     ++row;
   }
+  if (a.lead && r_end < a.rows && e_end > a.rp[r_end]) {  // row r_end continues in later warps
+    to_carry(a.tail + gw * a.carry_ld);
+    if (lane == 0) a.tail_row[gw] = r_end;
+  }
+}
+
+// Rows shared by several warps: (tails of the earlier warps in warp order) +
+// the owner's lead partial, then the flush epilogue (accumulate into the fp32
+// output; bf16 hi / lo split). One warp per owner.
+__global__ void k_spmm_carry_fixup(const PipeArgs a, int64_t warps) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= warps) return;
+  const int64_t row = a.lead_row[w];
+  if (row < 0) return;
+  int64_t w0 = w;
+  while (w0 > 0 && a.tail_row[w0 - 1] == row) --w0;
+  for (int64_t c = lane; c < a.fcols; c += 32) {
+    float s = 0.f;
+    for (int64_t k = w0; k < w; ++k) s += a.tail[k * a.carry_ld + c];
+    s += a.lead[w * a.carry_ld + c];
+    if (a.out) {
+      float* dst = a.out + row * a.ldo + c;
+      if (a.accumulate) s += *dst;
+      *dst = s;
+    }
+    if (a.outb) {
+      const bf16 h = __float2bfloat16_rn(s);
+      a.outb[row * a.ldob + c] = h;
+      if (a.outlo) a.outlo[row * a.ldob + c] = __float2bfloat16_rn(s - __bfloat162float(h));
+    }
+  }
 }
 
 template <class TIn, int RB>
-void launch_pipe(Ctx& ctx, const PipeArgs& a) {
+void launch_pipe(Ctx& ctx, PipeArgs a) {
   const int smem = kWarps * kStages * kStageBytes + kWarps * kStages * 32 * 4;
   static bool attr = false;
   if (!attr) {
     GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  k_spmm_pipe<TIn, RB><<<ctx.persistent_sms(), kWarps * 32, smem, ctx.stream>>>(a);
+  const int grid = ctx.persistent_sms();
+  const int64_t warps = static_cast<int64_t>(grid) * kWarps;
+  const int mode = split_mode();
+  a.balanced = mode >= 1;
+  if (mode == 2) {
+    a.carry_ld = static_cast<int>(round_up(a.fcols, 8));
+    a.split_mult = 4;
+    float* base = ctx.spmm_carry.reserve_n<float>(static_cast<size_t>(warps) * (2 * a.carry_ld + 4));
+    a.lead = base;
+    a.tail = base + warps * a.carry_ld;
+    a.lead_row = reinterpret_cast<int64_t*>(base + 2 * warps * a.carry_ld);
+    a.tail_row = a.lead_row + warps;
+  }
+  k_spmm_pipe<TIn, RB><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+  if (mode == 2) {
+    k_spmm_carry_fixup<<<static_cast<unsigned>(ceil_div(warps, 8)), 256, 0, ctx.stream>>>(a, warps);
+    ctx.launches += 1;
+  }
 }
 
 }  // namespace
@@ -344,7 +469,6 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
   a.ldob = ldob;
   a.accumulate = accumulate;
   a.ocpr = a.vcpr;
-  a.balanced = balanced_split();
   if (esize == 2) {
     if (row_bytes <= 256)
       launch_pipe<bf16, 256>(ctx, a);
@@ -389,7 +513,6 @@ bool spmm_pipe_p24(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col
   a.ldob = ldob;
   a.ocpr = static_cast<int>(c16 / 8);
   a.hoff = static_cast<int>(2 * c16);
-  a.balanced = balanced_split();
   if (row_bytes <= 384)
     launch_pipe<P24, 384>(ctx, a);
   else

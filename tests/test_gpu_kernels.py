@@ -157,3 +157,52 @@ def test_spmm_f32_rows(env, gg, rows, frows, fcols, deg, accumulate):
     assert (out.double() - want).abs().max().item() <= 1e-5 * scale
     assert torch.equal(hi[:, :fcols], out.to(torch.bfloat16))
     assert torch.equal(lo[:, :fcols], (out - hi[:, :fcols].float()).to(torch.bfloat16))
+
+
+def _skewed_csr(rows, cols, seed):
+    """Power-law rows (R-MAT-like): a few hub rows with thousands of nonzeros
+    among short ones and empty ones."""
+    rng = np.random.default_rng(seed)
+    deg = np.minimum(rng.zipf(1.6, rows), cols)
+    deg[rng.integers(0, rows, 3)] = cols  # full hub rows
+    deg[rng.integers(0, rows, rows // 20)] = 0
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    col = np.concatenate([np.sort(rng.choice(cols, d, replace=False)) for d in deg]).astype(np.int32)
+    return rp, col, rng.random(len(col)).astype(np.float32)
+
+
+# rows shared by several warps (merge-path split of the pipelined SpMM) must
+# give the same sums as the dense product; the fp32 and bf16 gathers, with
+# and without accumulation into the output
+@pytest.mark.parametrize("fcols", [256, 128, 100])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_spmm_skewed_rows(env, gg, fcols, accumulate):
+    ctx, torch = env
+    rows, frows = 6000, 20000
+    rp, col, val = _skewed_csr(rows, frows, fcols)
+    assert np.diff(rp).max() > 100 * np.diff(rp).mean()
+    g = torch.Generator(device="cuda").manual_seed(fcols)
+    ldf = _ld8(fcols)
+    f = torch.zeros(frows, ldf, device="cuda")
+    f[:, :fcols] = torch.randn(frows, fcols, generator=g, device="cuda")
+    fb = f.to(torch.bfloat16)
+    trp, tcol, tval = (torch.from_numpy(x).cuda() for x in (rp, col, val))
+    A = torch.sparse_csr_tensor(trp, tcol.long(), tval.double(), size=(rows, frows))
+    base = torch.randn(rows, fcols, device="cuda")
+    for name, src in (("f32", f), ("bf16", fb)):
+        out = base.clone() if accumulate else torch.full((rows, fcols), float("nan"), device="cuda")
+        hi = torch.zeros(rows, ldf, dtype=torch.bfloat16, device="cuda")
+        lo = torch.zeros_like(hi)
+        if name == "f32":
+            gg.check(gg.lib().ggb_spmm_csr_f32(ctx.h, rows, trp.data_ptr(), tcol.data_ptr(), tval.data_ptr(),
+                                               src.data_ptr(), ldf, fcols, out.data_ptr(), fcols, hi.data_ptr(),
+                                               lo.data_ptr(), ldf, accumulate))
+        else:
+            gg.check(gg.lib().ggb_spmm_csr(ctx.h, rows, trp.data_ptr(), tcol.data_ptr(), tval.data_ptr(),
+                                           src.data_ptr(), ldf, fcols, out.data_ptr(), fcols, hi.data_ptr(), ldf,
+                                           accumulate))
+        ctx.synchronize()
+        want = A @ src[:, :fcols].double() + (base.double() if accumulate else 0)
+        scale = max(1.0, want.abs().max().item())
+        assert (out.double() - want).abs().max().item() <= 1e-5 * scale, name
+        assert torch.equal(hi[:, :fcols], out.to(torch.bfloat16)), name
