@@ -993,6 +993,7 @@ int ggb_spmm_csr(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const int3
                  int32_t accumulate) {
   return guard([&] {
     use_device(*ctx);
+    LongRowsScope lrs(*ctx, true);  // test entry: the merge-path kernel (any row-length profile)
     spmm_csr(*ctx, rows, row_ptr, col, val, static_cast<const bf16*>(f), ldf, fcols, out, ldo,
              static_cast<bf16*>(out_bf16), ldob, accumulate);
   });
@@ -1003,6 +1004,7 @@ int ggb_spmm_csr_f32(ggb_ctx_t ctx, int64_t rows, const int64_t* row_ptr, const 
                      void* out_lo, int64_t ldob, int32_t accumulate) {
   return guard([&] {
     use_device(*ctx);
+    LongRowsScope lrs(*ctx, true);
     spmm_csr_f32(*ctx, rows, row_ptr, col, val, f, ldf, fcols, out, ldo, static_cast<bf16*>(out_hi),
                  static_cast<bf16*>(out_lo), ldob, accumulate);
   });

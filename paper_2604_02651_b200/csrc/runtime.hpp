@@ -79,9 +79,22 @@ struct Ctx {
   int persistent_sms() const { return num_sms - sm_reserve > 0 ? num_sms - sm_reserve : 1; }
   std::unique_ptr<Prof> prof;
   DevBuf spmm_carry;  // per-warp partial rows of the pipelined SpMM's shared rows
+  // the next SpMMs' CSR has power-law rows (the pipelined kernel then shares
+  // long rows across warps); set per call site from BatchCsr::long_rows
+  bool spmm_long_rows = false;
   CommStats stats;
   int phase = kPhaseOther;
   ~Ctx();
+};
+
+/// Marks the SpMMs of a scope as running over a power-law CSR block.
+struct LongRowsScope {
+  Ctx& ctx;
+  bool prev;
+  LongRowsScope(Ctx& c, bool v) : ctx(c), prev(c.spmm_long_rows) { ctx.spmm_long_rows = v; }
+  ~LongRowsScope() { ctx.spmm_long_rows = prev; }
+  LongRowsScope(const LongRowsScope&) = delete;
+  LongRowsScope& operator=(const LongRowsScope&) = delete;
 };
 
 /// PhaseScope (comm.hpp:411-421).
@@ -114,6 +127,10 @@ struct PlaneShard {
   // rows per degree (host, built with the graph): the n largest row degrees
   // bound the entries a batch block of n sampled rows can extract
   std::vector<int64_t> rows_of_degree;
+  bool power_law() const {
+    const int64_t rows = r1 - r0, dmax = static_cast<int64_t>(rows_of_degree.size()) - 1;
+    return rows > 0 && dmax > 8 * (nnz / rows + 1);
+  }
   int64_t top_rows_nnz(int64_t rows) const {
     int64_t sum = 0;
     for (int64_t d = static_cast<int64_t>(rows_of_degree.size()) - 1; d > 0 && rows > 0; --d) {
@@ -147,6 +164,7 @@ struct Graph {
 /// tensor.hpp:88-96) with device arrays for the kernels.
 struct BatchCsr {
   int64_t n_rows = 0, n_cols = 0;
+  bool long_rows = false;  // cut from a power-law shard (max degree > 8x mean)
   mutable int64_t nnz = 0;  // host copy, valid once the batch's totals are settled
   int64_t r0 = 0, r1 = 0, c0 = 0, c1 = 0;  // global batch coordinates
   DevBuf row_ptr;  // int64 [n_rows+1]

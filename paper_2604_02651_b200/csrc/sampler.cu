@@ -554,6 +554,7 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
   for (size_t k = 0; k < keys.size(); ++k) {
     const Key& kk = keys[k];
     BatchCsr& out = bt.csrs[k];
+    out.long_rows = g.shards[kk.shard].power_law();
     out.r0 = kk.rl;
     out.r1 = kk.rh;
     out.c0 = kk.cl;
@@ -684,6 +685,7 @@ void preaggregate(Ctx& ctx, const Batch& bt) {
     // padding columns of P stay zero (the GEMM reads K up to x_ld)
     GGB_CUDA(cudaMemsetAsync(ph, 0, static_cast<size_t>(A.n_rows) * bt.x_ld * 2, ctx.stream));
     GGB_CUDA(cudaMemsetAsync(pl, 0, static_cast<size_t>(A.n_rows) * bt.x_ld * 2, ctx.stream));
+    LongRowsScope lrs(ctx, A.long_rows);
     spmm_csr_f32(ctx, A.n_rows, A.row_ptr.as<int64_t>(), A.col.as<int32_t>(), A.val.as<float>(), xf, bt.x_ld, cols,
                  nullptr, 0, ph, pl, bt.x_ld, 0);
   }

@@ -151,8 +151,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// TIn: element type of F; RB: smem bytes per gathered row.
-template <class TIn, int RB>
+// TIn: element type of F; RB: smem bytes per gathered row; kMerge: merge-path
+// ranges with long rows shared across warps (power-law inputs) — a separate
+// instance, so the whole-row kernel keeps its code generation.
+template <class TIn, int RB, bool kMerge>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) {
   constexpr bool kP24 = std::is_same_v<TIn, P24>;
   constexpr int EPC = kP24 ? 8 : 16 / static_cast<int>(sizeof(TIn));  // elements per lane chunk
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + wib;
   int64_t r_begin, r_end, e_begin, e_end;
   bool lead = false;  // the first row began in earlier warps: its flush goes to the carry
-  if (a.lead) {
+  if constexpr (kMerge) {
     path_point(a.rp, a.rows, gw, total_warps, a.split_mult, lane, r_begin, e_begin);
     path_point(a.rp, a.rows, gw + 1, total_warps, a.split_mult, lane, r_end, e_end);
     lead = r_begin < a.rows && e_begin > a.rp[r_begin];
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
     e_begin = a.rp[r_begin];
     e_end = a.rp[r_end];
   }
-  if (r_begin >= r_end && e_begin >= e_end) return;
+  if (kMerge ? (r_begin >= r_end && e_begin >= e_end) : r_begin >= r_end) return;
   const int64_t n_stages = (e_end - e_begin + S - 1) / S;
 
   int32_t nx_col = 0;  // lane k < S: column id / value of entry k of the next stage to issue
@@ -249,10 +251,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
   };
 
   auto flush = [&]() {
-    if (lead && row == r_begin) {
-      to_carry(a.lead + gw * a.carry_ld);
-      if (lane == 0) a.lead_row[gw] = row;
-      return;
+    if constexpr (kMerge) {
+      if (lead && row == r_begin) {
+        to_carry(a.lead + gw * a.carry_ld);
+        if (lane == 0) a.lead_row[gw] = row;
+        return;
+      }
     }
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
@@ -381,9 +385,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
     flush();
     ++row;
   }
-  if (a.lead && r_end < a.rows && e_end > a.rp[r_end]) {  // row r_end continues in later warps
-    to_carry(a.tail + gw * a.carry_ld);
-    if (lane == 0) a.tail_row[gw] = r_end;
+  if constexpr (kMerge) {
+    if (r_end < a.rows && e_end > a.rp[r_end]) {  // row r_end continues in later warps
+      to_carry(a.tail + gw * a.carry_ld);
+      if (lane == 0) a.tail_row[gw] = r_end;
+    }
   }
 }
 
@@ -415,17 +421,24 @@ __global__ void k_spmm_carry_fixup(const PipeArgs a, int64_t warps) {
   }
 }
 
+template <class TIn, int RB, bool kMerge>
+void set_smem_attr() {
+  static bool attr = false;
+  if (!attr) {
+    GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB, kMerge>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kWarps * kStages * kStageBytes + kWarps * kStages * 32 * 4));
+    attr = true;
+  }
+}
+
 template <class TIn, int RB>
 void launch_pipe(Ctx& ctx, PipeArgs a) {
   const int smem = kWarps * kStages * kStageBytes + kWarps * kStages * 32 * 4;
-  static bool attr = false;
-  if (!attr) {
-    GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
   const int grid = ctx.persistent_sms();
   const int64_t warps = static_cast<int64_t>(grid) * kWarps;
-  const int mode = split_mode();
+  // merge path when the caller flags long rows (ctx.spmm_long_rows: a power-law
+  // shard) unless GGB_SPMM_SPLIT forces a whole-row split
+  const int mode = split_mode() == 2 ? (ctx.spmm_long_rows ? 2 : 1) : split_mode();
   a.balanced = mode >= 1;
   if (mode == 2) {
     a.carry_ld = static_cast<int>(round_up(a.fcols, 8));
@@ -436,7 +449,13 @@ void launch_pipe(Ctx& ctx, PipeArgs a) {
     a.lead_row = reinterpret_cast<int64_t*>(base + 2 * warps * a.carry_ld);
     a.tail_row = a.lead_row + warps;
   }
-  k_spmm_pipe<TIn, RB><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+  if (mode == 2) {
+    set_smem_attr<TIn, RB, true>();
+    k_spmm_pipe<TIn, RB, true><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+  } else {
+    set_smem_attr<TIn, RB, false>();
+    k_spmm_pipe<TIn, RB, false><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+  }
   if (mode == 2) {
     k_spmm_carry_fixup<<<static_cast<unsigned>(ceil_div(warps, 8)), 256, 0, ctx.stream>>>(a, warps);
     ctx.launches += 1;

@@ -321,6 +321,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     const bool ar_h = reduces(ctx, alay.col, wire);
     charge_all_reduce(ctx, alay.col, hb.rows() * hb.cols(), wire_bytes(wire));  // spmm (pmm.hpp:165)
     const int64_t* arp = A.row_ptr.as<int64_t>();
+    LongRowsScope lrs(ctx, A.long_rows);
     if (l == 1 && st.preagg) {
       // hagg_1 = P . W_in with P = A_0 . x_in (built with the batch); X and Z
       // unsplit, so neither product needs an all-reduce
@@ -723,6 +724,7 @@ void backward(State& st, const Batch& bt, int precision) {
     const BatchCsr& At = bt.csrs[bt.csrt_of[p]];
     const Layout alay = adjacency_layout(l);
     contract(At.c0 == hg.blk.r0 && At.c1 == hg.blk.r1, "spmm: inner partitions differ");
+    LongRowsScope lrs(ctx, At.long_rows);
     const bool inplace = pmm_trivial(ctx) && cfg.use_residual && wire == GGB_FP32;
     ProfScope ps(ctx, kProfSpmmBwd, spmm_bytes(At.n_rows, At.nnz, hc, 2, inplace ? 8 : 4), 2.0 * At.nnz * hc);
     if (inplace) {
