@@ -257,6 +257,85 @@ int ggb_evaluate_full_graph(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t eval_batc
 int ggb_dp_sync(ggb_ctx_t ctx, ggb_state_t st);
 int ggb_optimizer_step(ggb_ctx_t ctx, ggb_state_t st, int32_t optimizer, double lr);
 
+/* ---- layer operators (include/gridgnn/pmm.hpp:76-401) --------------------------
+ * A ggb_block is one rank's block of a 2D-sharded fp32 matrix: the metadata of
+ * the reference's ShardedTensor (tensor.hpp:75-86) with the block in HBM.
+ * Layout = (row_axis, col_axis), distinct PMM axes (1 = X, 2 = Y, 3 = Z);
+ * row_off / col_off are HOST arrays of dims[row_axis] + 1 / dims[col_axis] + 1
+ * partition offsets into [0, g_rows] / [0, g_cols] (explicit, as the batch
+ * rows are split where the sorted sample meets the vertex partition); this
+ * rank's block is rows [row_off[x_r], row_off[x_r + 1]) x cols
+ * [col_off[x_c], col_off[x_c + 1]) with x_r, x_c its grid coordinates, stored
+ * row-major at `data` with leading dimension `ld` (elements). Outputs are
+ * caller-allocated blocks whose metadata must equal the result's (CommContract
+ * otherwise). Collectives run on the context's NCCL axis communicators; every
+ * member of a group calls with matching shapes, as in the reference. */
+typedef struct {
+  int32_t row_axis, col_axis;
+  int64_t g_rows, g_cols;
+  const int64_t* row_off;
+  const int64_t* col_off;
+  float* data;
+  int64_t ld;
+} ggb_block;
+/* A ShardedSparse (tensor.hpp:88-96): the block as CSR in HBM with LOCAL
+ * column ids (int64 row_ptr, int32 col, fp32 values = (float) of the fp64
+ * reference values, pmm.hpp:160). */
+typedef struct {
+  int32_t row_axis, col_axis;
+  int64_t g_rows, g_cols;
+  const int64_t* row_off;
+  const int64_t* col_off;
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const float* val;
+} ggb_csr_block;
+/* contract (pmm.hpp:97-130): c = a . b, all-reduce along a.col_axis with the
+ * precision's wire; a (r, k), b (k, t) -> c (r, t). Split-bf16 tcgen05 GEMM
+ * (fp32-accurate to ~2^-16). */
+int ggb_contract(ggb_ctx_t ctx, const ggb_block* a, const ggb_block* b, const ggb_block* c, int32_t precision);
+/* spmm (pmm.hpp:134-167): h = a . f, all-reduce along a.col_axis. */
+int ggb_spmm(ggb_ctx_t ctx, const ggb_csr_block* a, const ggb_block* f, const ggb_block* h, int32_t precision);
+/* transposed (pmm.hpp:76-92): out is the transposed shard's block (layout and offsets swapped). */
+int ggb_transposed(ggb_ctx_t ctx, const ggb_block* t, const ggb_block* out);
+/* gather_full (pmm.hpp:171-195): the whole g_rows x g_cols matrix (row-major,
+ * leading dimension ld_full) on every rank of the DP group. */
+int ggb_gather_full(ggb_ctx_t ctx, const ggb_block* t, float* full, int64_t ld_full);
+/* reshard (pmm.hpp:197-204) to dst's layout / offsets, as a point-to-point
+ * block permutation (the reference all-gathers the whole matrix). */
+int ggb_reshard(ggb_ctx_t ctx, const ggb_block* src, const ggb_block* dst);
+/* parallel_rmsnorm_fwd (pmm.hpp:214-243): y = gamma . x / rms, rms over the
+ * full g_cols (fp32 all-reduce of the row sums of squares along x.col_axis);
+ * gamma = this rank's column slice (device), rms = one per local row (device). */
+int ggb_rmsnorm_fwd(ggb_ctx_t ctx, const ggb_block* x, const float* gamma, double eps, const ggb_block* y,
+                    float* rms);
+/* parallel_rmsnorm_bwd (pmm.hpp:251-287): dx and the column slice of dgamma
+ * (all-reduced along x.row_axis), device pointers. */
+int ggb_rmsnorm_bwd(ggb_ctx_t ctx, const ggb_block* x, const float* gamma, const float* rms, const ggb_block* dy,
+                    const ggb_block* dx, float* dgamma);
+/* fused_elementwise_fwd (pmm.hpp:299-328): out = x . scale + h_prev (nullable),
+ * scale = (x > 0) . (training && rate > 0 ? [element_unit(key, row, col) >= rate] / (1 - rate) : 1);
+ * keep_bits (device, nullable) receives scale != 0 as ggb_mask_words(cols)
+ * words per row (the row kernels' layout) instead of the fp32 scale matrix. */
+int ggb_fused_elementwise_fwd(ggb_ctx_t ctx, const ggb_block* x, const ggb_block* h_prev, double rate,
+                              uint64_t mask_key, int32_t training, const ggb_block* out, uint32_t* keep_bits);
+/* fused_elementwise_bwd (pmm.hpp:331-341): dx = dy . scale from those bits. */
+int ggb_fused_elementwise_bwd(ggb_ctx_t ctx, const ggb_block* dy, const uint32_t* keep_bits, double rate,
+                              int32_t training, const ggb_block* dx);
+/* keep-bit words per row of a block with `cols` local columns */
+int64_t ggb_mask_words(int64_t cols);
+/* parallel_cross_entropy (pmm.hpp:352-401): loss (device float, replicated),
+ * grad = (softmax - onehot) / g_rows; labels = the global batch's labels (device int32). */
+int ggb_cross_entropy(ggb_ctx_t ctx, const ggb_block* logits, const int32_t* labels, float* loss,
+                      const ggb_block* grad);
+/* A batch plane's CSR block as a ggb_csr_block (pointers stay valid while the batch lives). */
+int ggb_batch_csr_block(ggb_batch_t batch, int32_t plane, int32_t transposed, ggb_csr_block* out);
+/* train_step split at the reference's seams (model.hpp:459-478): ggb_forward
+ * (above), then ggb_loss = parallel_cross_entropy on its logits (the gradient
+ * stays in the state), then ggb_backward (model.hpp:378-420). */
+int ggb_loss(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, float* loss_out);
+int ggb_backward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, int32_t precision);
+
 /* ---- kernels exposed for unit tests (device pointers, row-major) ------------- */
 /* C[m x n] = A[m x k] . Bt[n x k]^T in bf16 x bf16 -> fp32 on tcgen05.
  * c (fp32) and/or c_bf16 may be NULL. Leading dimensions in elements. */

@@ -470,6 +470,11 @@ class Ref:
                                      C.c_double, P, P]
         L.ref_bench.argtypes = [P, P, P, P, I64, U64, C.c_int, C.c_int, C.c_int, P, P]
         L.ref_comm_stats.argtypes = [P, P, P, P, I64, U64, C.c_int, C.c_int, C.c_int, P]
+        L.ref_contract.argtypes = [I64, I64, I64, P, P, C.c_int, P]
+        L.ref_spmm.argtypes = [I64, I64, P, P, P, P, I64, C.c_int, P]
+        L.ref_rmsnorm.argtypes = [I64, I64, P, P, C.c_float, P, P, P, P, P]
+        L.ref_fused.argtypes = [I64, I64, P, P, C.c_double, U64, C.c_int, P, P, P, P]
+        L.ref_cross_entropy.argtypes = [I64, I64, P, P, P, P]
         self.L = L
 
     def _check(self, rc: int):
@@ -642,6 +647,51 @@ class Ref:
             "allreduce_calls": {a: int(out[20 + i]) for i, a in enumerate(axes)},
             "allgather_calls": {a: int(out[24 + i]) for i, a in enumerate(axes)},
         }
+
+    # layer operators on the one-rank grid (ref_shim.cpp, pmm.hpp:76-401)
+    def contract(self, a: np.ndarray, b: np.ndarray, prec: int = 0) -> np.ndarray:
+        a, b = np.ascontiguousarray(a, np.float32), np.ascontiguousarray(b, np.float32)
+        c = np.empty((a.shape[0], b.shape[1]), np.float32)
+        self._check(self.L.ref_contract(a.shape[0], a.shape[1], b.shape[1], _ptr(a), _ptr(b), prec, _ptr(c)))
+        return c
+
+    def spmm(self, a: Csr, f: np.ndarray, prec: int = 0) -> np.ndarray:
+        f = np.ascontiguousarray(f, np.float32)
+        h = np.empty((a.n_rows, f.shape[1]), np.float32)
+        rp, ci = np.ascontiguousarray(a.row_ptr, np.int64), np.ascontiguousarray(a.col_idx, np.int64)
+        va = np.ascontiguousarray(a.values, np.float64)
+        self._check(self.L.ref_spmm(a.n_rows, a.n_cols, _ptr(rp), _ptr(ci), _ptr(va), _ptr(f), f.shape[1], prec,
+                                    _ptr(h)))
+        return h
+
+    def rmsnorm(self, x, gamma, eps, dy=None):
+        x, gamma = np.ascontiguousarray(x, np.float32), np.ascontiguousarray(gamma, np.float32)
+        m, n = x.shape
+        y, rms = np.empty_like(x), np.empty(m, np.float32)
+        dx, dg = (np.empty_like(x), np.empty(n, np.float32)) if dy is not None else (None, None)
+        dy = np.ascontiguousarray(dy, np.float32) if dy is not None else None
+        self._check(self.L.ref_rmsnorm(m, n, _ptr(x), _ptr(gamma), eps, _ptr(dy), _ptr(y), _ptr(rms), _ptr(dx),
+                                       _ptr(dg)))
+        return y, rms, dx, dg
+
+    def fused(self, x, h_prev, rate, key, training, dy=None):
+        x = np.ascontiguousarray(x, np.float32)
+        h = np.ascontiguousarray(h_prev, np.float32) if h_prev is not None else None
+        out, scale = np.empty_like(x), np.empty_like(x)
+        dx = np.empty_like(x) if dy is not None else None
+        dy = np.ascontiguousarray(dy, np.float32) if dy is not None else None
+        self._check(self.L.ref_fused(x.shape[0], x.shape[1], _ptr(x), _ptr(h), rate, key, int(training), _ptr(dy),
+                                     _ptr(out), _ptr(scale), _ptr(dx)))
+        return out, scale, dx
+
+    def cross_entropy(self, logits, labels):
+        logits = np.ascontiguousarray(logits, np.float32)
+        labels = np.ascontiguousarray(labels, np.int32)
+        loss = np.zeros(1, np.float32)
+        grad = np.empty_like(logits)
+        self._check(self.L.ref_cross_entropy(logits.shape[0], logits.shape[1], _ptr(logits), _ptr(labels),
+                                             _ptr(loss), _ptr(grad)))
+        return float(loss[0]), grad
 
     def init_weights(self, cfg: ModelConfig, seed: int):
         mc, md = cfg.arrays()

@@ -566,4 +566,109 @@ int ref_bench(void* dsp, const int* dims, const std::int64_t* mc, const double* 
   });
 }
 
+
+// ---- layer operators (pmm.hpp:76-401) on the one-rank grid ------------------
+// Each runs the reference operator on full-matrix shards (offsets {0, n}) of a
+// 1x1x1x1 grid, layout (X, Y) for dense operands.
+}  // extern "C"
+
+namespace {
+ShardedTensor<float> full_shard(Layout lay, std::int64_t rows, std::int64_t cols, const float* v) {
+  DeviceGrid g(1, 1, 1, 1);
+  auto t = make_sharded<float>(g, g.coord_of(0), lay, rows, cols, {0, rows}, {0, cols});
+  if (v) std::copy(v, v + rows * cols, t.local.v.begin());
+  return t;
+}
+template <class Body>
+void one_rank(Body&& body) {
+  Communicator comm(DeviceGrid(1, 1, 1, 1));
+  RankComm rc(comm, 0);
+  body(rc);
+}
+}  // namespace
+
+extern "C" {
+
+int ref_contract(std::int64_t m, std::int64_t k, std::int64_t n, const float* a, const float* b, int prec, float* c) {
+  return guard([&] {
+    one_rank([&](RankComm& rc) {
+      auto A = full_shard({Axis::X, Axis::Y}, m, k, a);
+      auto B = full_shard({Axis::Y, Axis::Z}, k, n, b);
+      auto C = contract(rc, A, B, prec ? Precision::kBf16Roundtrip : Precision::kFp32);
+      std::copy(C.local.v.begin(), C.local.v.end(), c);
+    });
+  });
+}
+
+int ref_spmm(std::int64_t rows, std::int64_t cols, const std::int64_t* rp, const std::int64_t* col, const double* val,
+             const float* f, std::int64_t n, int prec, float* h) {
+  return guard([&] {
+    one_rank([&](RankComm& rc) {
+      ShardedSparse A;
+      A.layout = {Axis::Z, Axis::X};
+      A.g_rows = rows;
+      A.g_cols = cols;
+      A.row_off = {0, rows};
+      A.col_off = {0, cols};
+      A.r1 = rows;
+      A.c1 = cols;
+      A.local.n_rows = rows;
+      A.local.n_cols = cols;
+      A.local.row_ptr.assign(rp, rp + rows + 1);
+      A.local.col_idx.assign(col, col + rp[rows]);
+      A.local.values.assign(val, val + rp[rows]);
+      auto F = full_shard({Axis::X, Axis::Y}, cols, n, f);
+      auto H = spmm(rc, A, F, prec ? Precision::kBf16Roundtrip : Precision::kFp32);
+      std::copy(H.local.v.begin(), H.local.v.end(), h);
+    });
+  });
+}
+
+int ref_rmsnorm(std::int64_t m, std::int64_t n, const float* x, const float* gamma, float eps, const float* dy,
+                float* y, float* rms, float* dx, float* dgamma) {
+  return guard([&] {
+    one_rank([&](RankComm& rc) {
+      auto X = full_shard({Axis::X, Axis::Y}, m, n, x);
+      auto r = parallel_rmsnorm_fwd(rc, X, std::span<const float>(gamma, static_cast<std::size_t>(n)), eps);
+      std::copy(r.y.local.v.begin(), r.y.local.v.end(), y);
+      std::copy(r.rms.begin(), r.rms.end(), rms);
+      if (dy) {
+        auto DY = full_shard({Axis::X, Axis::Y}, m, n, dy);
+        auto g = parallel_rmsnorm_bwd(rc, X, std::span<const float>(gamma, static_cast<std::size_t>(n)), r.rms, DY);
+        std::copy(g.dx.local.v.begin(), g.dx.local.v.end(), dx);
+        std::copy(g.dgamma.begin(), g.dgamma.end(), dgamma);
+      }
+    });
+  });
+}
+
+int ref_fused(std::int64_t m, std::int64_t n, const float* x, const float* h_prev, double rate, std::uint64_t key,
+              int training, const float* dy, float* out, float* scale, float* dx) {
+  return guard([&] {
+    auto X = full_shard({Axis::X, Axis::Y}, m, n, x);
+    ShardedTensor<float> H;
+    if (h_prev) H = full_shard({Axis::X, Axis::Y}, m, n, h_prev);
+    auto r = fused_elementwise_fwd<float>(X, h_prev ? &H : nullptr, rate, key, training != 0);
+    std::copy(r.out.local.v.begin(), r.out.local.v.end(), out);
+    std::copy(r.scale.v.begin(), r.scale.v.end(), scale);
+    if (dy) {
+      auto DY = full_shard({Axis::X, Axis::Y}, m, n, dy);
+      auto d = fused_elementwise_bwd(DY, r.scale);
+      std::copy(d.local.v.begin(), d.local.v.end(), dx);
+    }
+  });
+}
+
+int ref_cross_entropy(std::int64_t m, std::int64_t n, const float* logits, const std::int32_t* labels, float* loss,
+                      float* grad) {
+  return guard([&] {
+    one_rank([&](RankComm& rc) {
+      auto L = full_shard({Axis::X, Axis::Z}, m, n, logits);
+      auto r = parallel_cross_entropy(rc, L, std::vector<std::int32_t>(labels, labels + m));
+      *loss = r.loss;
+      std::copy(r.grad_logits.local.v.begin(), r.grad_logits.local.v.end(), grad);
+    });
+  });
+}
+
 }  // extern "C"

@@ -28,6 +28,20 @@ class ModelConfigC(C.Structure):
                 ("use_residual", I32)]
 
 
+class BlockC(C.Structure):
+    """ggb_block == one rank's block of a ShardedTensor (tensor.hpp:75-86)."""
+
+    _fields_ = [("row_axis", I32), ("col_axis", I32), ("g_rows", I64), ("g_cols", I64), ("row_off", P),
+                ("col_off", P), ("data", P), ("ld", I64)]
+
+
+class CsrBlockC(C.Structure):
+    """ggb_csr_block == one rank's block of a ShardedSparse (tensor.hpp:88-96)."""
+
+    _fields_ = [("row_axis", I32), ("col_axis", I32), ("g_rows", I64), ("g_cols", I64), ("row_off", P),
+                ("col_off", P), ("row_ptr", P), ("col", P), ("val", P)]
+
+
 # (name, restype, argtypes)
 _SIGS = [
     ("ggb_last_error", C.c_char_p, []),
@@ -89,6 +103,20 @@ _SIGS = [
     ("ggb_gemm_wgrad_bf16", C.c_int, [P, I64, I64, I64, P, I64, P, I64, P, I64]),
     ("ggb_spmm_csr", C.c_int, [P, I64, P, P, P, P, I64, I64, P, I64, P, I64, I32]),
     ("ggb_spmm_csr_f32", C.c_int, [P, I64, P, P, P, P, I64, I64, P, I64, P, P, I64, I32]),
+    ("ggb_contract", C.c_int, [P, P, P, P, I32]),
+    ("ggb_spmm", C.c_int, [P, P, P, P, I32]),
+    ("ggb_transposed", C.c_int, [P, P, P]),
+    ("ggb_gather_full", C.c_int, [P, P, P, I64]),
+    ("ggb_reshard", C.c_int, [P, P, P]),
+    ("ggb_rmsnorm_fwd", C.c_int, [P, P, P, F64, P, P]),
+    ("ggb_rmsnorm_bwd", C.c_int, [P, P, P, P, P, P, P]),
+    ("ggb_fused_elementwise_fwd", C.c_int, [P, P, P, F64, U64, I32, P, P]),
+    ("ggb_fused_elementwise_bwd", C.c_int, [P, P, P, F64, I32, P]),
+    ("ggb_mask_words", I64, [I64]),
+    ("ggb_cross_entropy", C.c_int, [P, P, P, P, P]),
+    ("ggb_batch_csr_block", C.c_int, [P, I32, I32, P]),
+    ("ggb_loss", C.c_int, [P, P, P, P]),
+    ("ggb_backward", C.c_int, [P, P, P, I32]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGS]

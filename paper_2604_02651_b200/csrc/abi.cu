@@ -8,6 +8,7 @@
 
 #include "comm.hpp"
 #include "gendata.hpp"
+#include "layers.hpp"
 #include "dataset.hpp"
 #include "dsio.hpp"
 #include "prefetch.hpp"
@@ -907,6 +908,136 @@ int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precis
       download(loss_out, st->loss.p, 1, ctx->stream);
       ctx->d2h_bytes += sizeof(float);
     }
+  });
+}
+
+int ggb_loss(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, float* loss_out) {
+  return guard([&] {
+    use_device(*ctx);
+    contract(st->ctx == ctx && st->have_forward, "loss: no forward of this state on this rank");
+    {
+      PhaseScope ps(*ctx, kPhaseForward);
+      cross_entropy(*st, *bt);
+    }
+    if (loss_out) {
+      download(loss_out, st->loss.p, 1, ctx->stream);
+      ctx->d2h_bytes += sizeof(float);
+    }
+  });
+}
+
+int ggb_backward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precision) {
+  return guard([&] {
+    use_device(*ctx);
+    contract(st->ctx == ctx, "backward: state belongs to another rank");
+    PhaseScope ps(*ctx, kPhaseBackward);
+    backward(*st, *bt, precision);
+  });
+}
+
+int ggb_contract(ggb_ctx_t ctx, const ggb_block* a, const ggb_block* b, const ggb_block* c, int32_t precision) {
+  return guard([&] {
+    require(a && b && c, "contract: null block");
+    use_device(*ctx);
+    layer_contract(*ctx, *a, *b, *c, precision);
+  });
+}
+
+int ggb_spmm(ggb_ctx_t ctx, const ggb_csr_block* a, const ggb_block* f, const ggb_block* h, int32_t precision) {
+  return guard([&] {
+    require(a && f && h, "spmm: null block");
+    use_device(*ctx);
+    layer_spmm(*ctx, *a, *f, *h, precision);
+  });
+}
+
+int ggb_transposed(ggb_ctx_t ctx, const ggb_block* t, const ggb_block* out) {
+  return guard([&] {
+    require(t && out, "transposed: null block");
+    use_device(*ctx);
+    layer_transposed(*ctx, *t, *out);
+  });
+}
+
+int ggb_gather_full(ggb_ctx_t ctx, const ggb_block* t, float* full, int64_t ld_full) {
+  return guard([&] {
+    require(t && full && ld_full >= t->g_cols, "gather_full: bad output");
+    use_device(*ctx);
+    layer_gather_full(*ctx, *t, full, ld_full);
+  });
+}
+
+int ggb_reshard(ggb_ctx_t ctx, const ggb_block* src, const ggb_block* dst) {
+  return guard([&] {
+    require(src && dst, "reshard: null block");
+    use_device(*ctx);
+    layer_reshard(*ctx, *src, *dst);
+  });
+}
+
+int ggb_rmsnorm_fwd(ggb_ctx_t ctx, const ggb_block* x, const float* gamma, double eps, const ggb_block* y,
+                    float* rms) {
+  return guard([&] {
+    require(x && y && gamma, "rmsnorm: null argument");
+    use_device(*ctx);
+    layer_rmsnorm_fwd(*ctx, *x, gamma, eps, *y, rms);
+  });
+}
+
+int ggb_rmsnorm_bwd(ggb_ctx_t ctx, const ggb_block* x, const float* gamma, const float* rms, const ggb_block* dy,
+                    const ggb_block* dx, float* dgamma) {
+  return guard([&] {
+    require(x && gamma && rms && dy && dx && dgamma, "rmsnorm_bwd: missing cache");
+    use_device(*ctx);
+    layer_rmsnorm_bwd(*ctx, *x, gamma, rms, *dy, *dx, dgamma);
+  });
+}
+
+int ggb_fused_elementwise_fwd(ggb_ctx_t ctx, const ggb_block* x, const ggb_block* h_prev, double rate,
+                              uint64_t mask_key, int32_t training, const ggb_block* out, uint32_t* keep_bits) {
+  return guard([&] {
+    require(x && out, "fused_elementwise: null block");
+    use_device(*ctx);
+    layer_fused_fwd(*ctx, *x, h_prev, rate, mask_key, training, *out, keep_bits);
+  });
+}
+
+int ggb_fused_elementwise_bwd(ggb_ctx_t ctx, const ggb_block* dy, const uint32_t* keep_bits, double rate,
+                              int32_t training, const ggb_block* dx) {
+  return guard([&] {
+    require(dy && dx, "fused_elementwise_bwd: null block");
+    contract(keep_bits != nullptr, "fused_elementwise_bwd: missing cache");
+    use_device(*ctx);
+    layer_fused_bwd(*ctx, *dy, keep_bits, rate, training, *dx);
+  });
+}
+
+int64_t ggb_mask_words(int64_t cols) { return mask_words(std::max<int64_t>(cols, 1)); }
+
+int ggb_cross_entropy(ggb_ctx_t ctx, const ggb_block* logits, const int32_t* labels, float* loss,
+                      const ggb_block* grad) {
+  return guard([&] {
+    require(logits && labels && loss && grad, "cross_entropy: null argument");
+    use_device(*ctx);
+    layer_cross_entropy(*ctx, *logits, labels, loss, *grad);
+  });
+}
+
+int ggb_batch_csr_block(ggb_batch_t bt, int32_t plane, int32_t transposed, ggb_csr_block* out) {
+  return guard([&] {
+    require(bt && out && plane >= 0 && plane < bt->planes, "batch_csr_block: plane out of range");
+    const Layout lay = adjacency_layout(plane + 1);
+    const BatchCsr& c = bt->csrs[transposed ? bt->csrt_of[plane] : bt->csr_of[plane]];
+    const int ra = transposed ? lay.col : lay.row, ca = transposed ? lay.row : lay.col;
+    out->row_axis = ra;
+    out->col_axis = ca;
+    out->g_rows = bt->b;
+    out->g_cols = bt->b;
+    out->row_off = bt->batch_off[ra].data();
+    out->col_off = bt->batch_off[ca].data();
+    out->row_ptr = c.row_ptr.as<int64_t>();
+    out->col = c.col.as<int32_t>();
+    out->val = c.val.as<float>();
   });
 }
 

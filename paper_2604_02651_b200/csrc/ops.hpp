@@ -34,6 +34,7 @@ struct FwdApply {
   uint32_t* mask;  // [rows][ldm] keep bits, row-kernel layout (see kRowChunk)
   int64_t ldm;     // words per row = mask_words(cols)
   int fuse_ss;     // 1: the row is complete here, compute ss in-kernel (ss ignored)
+  int no_relu;     // 1: no ReLU (y passes; the layer API's RMSNorm alone)
 };
 
 // Row kernels: lane l of a warp owns columns c = 128*j + 4*l + i (i < 4) of
@@ -46,7 +47,7 @@ struct BwdApply {
   int64_t rows, cols;
   const float* dy;  // upstream gradient fp32
   int64_t lddy;
-  const uint32_t* mask;
+  const uint32_t* mask;  // keep bits; null: every element kept (RMSNorm backward alone)
   int64_t ldm;
   int fuse_s;  // 1: the row is complete here, compute s in-kernel
   float keep_scale;  // scale value of a kept element (1 without dropout)
@@ -56,8 +57,10 @@ struct BwdApply {
   const float* rms;  // null: no rmsnorm
   float* s;          // row dot products (stats out / apply in)
   float d;
-  bf16* dxb;  // out: dxw bf16
+  bf16* dxb;  // out: dxw bf16 (nullable)
   int64_t lddxb;
+  float* dxf;  // out: dxw fp32 (nullable; the layer API's parallel_rmsnorm_bwd)
+  int64_t lddxf;
   float* dgamma_part;  // [blocks][cols] or null
 };
 

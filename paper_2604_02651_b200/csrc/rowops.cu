@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         y[j][i] = p.gamma ? g[j][i] * x[j][i] * inv : x[j][i];
-        if (y[j][i] > 0.f && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
+        if ((p.no_relu || y[j][i] > 0.f) && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
       }
     }
     uint32_t keepm = posm;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
         }
       }
     }
-    if (lane < 4 * nj) p.mask[r * p.ldm + lane] = myword;
+    if (p.mask && lane < 4 * nj) p.mask[r * p.ldm + lane] = myword;
   }
 }
 
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kT) k_bwd_row_stats(BwdApply p) {
     f4(ld4(p.gamma, c, p.cols), g);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const bool keep = (p.mask[r * p.ldm + 4 * j + i] >> lane) & 1u;
+      const bool keep = !p.mask || ((p.mask[r * p.ldm + 4 * j + i] >> lane) & 1u);
       const float dxn = keep ? dy[i] * p.keep_scale : 0.f;
       s += dxn * g[i] * x[i];
     }
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
     for (int h = 0; h < R; ++h) {
       const int64_t r = r0 + h * stride;
       if (r >= p.rows) break;
-      const uint32_t* mrow = p.mask + r * p.ldm;
+      const uint32_t* mrow = p.mask ? p.mask + r * p.ldm : nullptr;
 #pragma unroll
       for (int j = 0; j < kMaxJ; ++j) {
         if (j >= nj) break;
@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
         f4(ld4(p.dy + r * p.lddy, c, p.cols), dy);
         f4(ld4(p.x + r * p.ldx, c, p.cols), xr[h][j]);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dxr[h][j][i] = ((mrow[4 * j + i] >> lane) & 1u) ? dy[i] * p.keep_scale : 0.f;
+        for (int i = 0; i < 4; ++i)
+          dxr[h][j][i] = (!p.mask || ((mrow[4 * j + i] >> lane) & 1u)) ? dy[i] * p.keep_scale : 0.f;
       }
     }
 #pragma unroll
@@ -386,7 +387,8 @@ __global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) dx[i] = dxn[j][i];
       }
-      st4_bf16(p.dxb + r * p.lddxb, c, p.cols, dx);
+      if (p.dxb) st4_bf16(p.dxb + r * p.lddxb, c, p.cols, dx);
+      if (p.dxf) st4(p.dxf + r * p.lddxf, c, p.cols, dx);
     }
     }
   }

@@ -109,6 +109,12 @@ bool pmm_trivial(const Ctx& ctx) { return ctx.grid.dims[1] == 1 && ctx.grid.dims
 
 }  // namespace
 
+void reshard_block(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff, const std::vector<int64_t>& s_coff,
+                   const float* src, int64_t lds, const Block& db, const std::vector<int64_t>& d_roff,
+                   const std::vector<int64_t>& d_coff, float* dst, int64_t ldd) {
+  reshard(ctx, sb, s_roff, s_coff, src, lds, db, d_roff, d_coff, dst, ldd);
+}
+
 // ---- init_state (model.hpp:175-208) -------------------------------------------------
 void state_init(Ctx& ctx, State& st, const ggb_model_config& cfg, uint64_t seed) {
   require(cfg.layers >= 1, "ModelConfig: layers must be >= 1");

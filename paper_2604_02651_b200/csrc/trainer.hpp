@@ -78,6 +78,11 @@ bool preagg_enabled();
 /// ... computed by the prefetcher with the batch (GGB_PREAGG_PF=0: lazily by forward)
 bool preagg_in_prefetch();
 
+/// reshard (pmm.hpp:197-204) as a block permutation: this rank's block of src
+/// (layout sb, offsets s_roff / s_coff) to its block of the new layout db.
+void reshard_block(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff, const std::vector<int64_t>& s_coff,
+                   const float* src, int64_t lds, const Block& db, const std::vector<int64_t>& d_roff,
+                   const std::vector<int64_t>& d_coff, float* dst, int64_t ldd);
 void state_init(Ctx& ctx, State& st, const ggb_model_config& cfg, uint64_t seed);
 void refresh_bf16(State& st);
 void forward(State& st, const Batch& bt, int precision, bool training, uint64_t run_seed,

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import (ADAM, BF16_SUM, BF16_WIRE, COMPUTE_ACCURATE, COMPUTE_FAST, FP32, SGD, CommContract, CommTimeout, GgbError,  # noqa: F401
+from ._lib import (ADAM, BF16_SUM, BF16_WIRE, BlockC, CsrBlockC, COMPUTE_ACCURATE, COMPUTE_FAST, FP32, SGD, CommContract, CommTimeout, GgbError,  # noqa: F401
                    InvalidArgument, ModelConfigC, check, lib)
 
 P = C.c_void_p
@@ -723,3 +723,106 @@ def hash_combine(a: int, b: int) -> int:
         return x ^ (x >> 31)
 
     return sm((a ^ ((0x9E3779B97F4A7C15 + ((b << 6) & m) + (b >> 2)) & m)) & m)
+
+
+# ---- layer operators (pmm.hpp:76-401) over device blocks -----------------------
+
+@dataclass
+class DeviceBlock:
+    """One rank's block of a ShardedTensor (tensor.hpp:75-86) in HBM: ordered
+    layout (grid axes X=1, Y=2, Z=3), global shape, explicit partition
+    offsets, the block at device pointer `ptr` with leading dimension `ld`."""
+    layout: tuple[int, int]
+    g_rows: int
+    g_cols: int
+    row_off: np.ndarray
+    col_off: np.ndarray
+    ptr: int
+    ld: int
+
+    def c(self) -> BlockC:
+        self._ro = np.ascontiguousarray(self.row_off, np.int64)
+        self._co = np.ascontiguousarray(self.col_off, np.int64)
+        return BlockC(self.layout[0], self.layout[1], self.g_rows, self.g_cols, self._ro.ctypes.data,
+                      self._co.ctypes.data, self.ptr, self.ld)
+
+
+def _pb(x):
+    return C.byref(x) if x is not None else None
+
+
+def contract(ctx: Context, a: DeviceBlock, b: DeviceBlock, out: DeviceBlock, prec: int = FP32) -> None:
+    ca, cb, cc = a.c(), b.c(), out.c()
+    check(lib().ggb_contract(ctx.h, C.byref(ca), C.byref(cb), C.byref(cc), prec))
+
+
+def spmm(ctx: Context, a: CsrBlockC, f: DeviceBlock, out: DeviceBlock, prec: int = FP32) -> None:
+    cf, co = f.c(), out.c()
+    check(lib().ggb_spmm(ctx.h, C.byref(a), C.byref(cf), C.byref(co), prec))
+
+
+def transposed(ctx: Context, t: DeviceBlock, out: DeviceBlock) -> None:
+    ct, co = t.c(), out.c()
+    check(lib().ggb_transposed(ctx.h, C.byref(ct), C.byref(co)))
+
+
+def gather_full(ctx: Context, t: DeviceBlock, full_ptr: int, ld_full: int) -> None:
+    ct = t.c()
+    check(lib().ggb_gather_full(ctx.h, C.byref(ct), full_ptr, ld_full))
+
+
+def reshard(ctx: Context, src: DeviceBlock, dst: DeviceBlock) -> None:
+    cs, cd = src.c(), dst.c()
+    check(lib().ggb_reshard(ctx.h, C.byref(cs), C.byref(cd)))
+
+
+def rmsnorm_fwd(ctx: Context, x: DeviceBlock, gamma_ptr: int, eps: float, y: DeviceBlock, rms_ptr: int) -> None:
+    cx, cy = x.c(), y.c()
+    check(lib().ggb_rmsnorm_fwd(ctx.h, C.byref(cx), gamma_ptr, eps, C.byref(cy), rms_ptr))
+
+
+def rmsnorm_bwd(ctx: Context, x: DeviceBlock, gamma_ptr: int, rms_ptr: int, dy: DeviceBlock, dx: DeviceBlock,
+                dgamma_ptr: int) -> None:
+    cx, cdy, cdx = x.c(), dy.c(), dx.c()
+    check(lib().ggb_rmsnorm_bwd(ctx.h, C.byref(cx), gamma_ptr, rms_ptr, C.byref(cdy), C.byref(cdx), dgamma_ptr))
+
+
+def fused_elementwise_fwd(ctx: Context, x: DeviceBlock, h_prev: DeviceBlock | None, rate: float, mask_key: int,
+                          training: bool, out: DeviceBlock, keep_bits_ptr: int | None) -> None:
+    cx, co = x.c(), out.c()
+    ch = h_prev.c() if h_prev is not None else None
+    check(lib().ggb_fused_elementwise_fwd(ctx.h, C.byref(cx), _pb(ch), rate, mask_key, int(training), C.byref(co),
+                                          keep_bits_ptr))
+
+
+def fused_elementwise_bwd(ctx: Context, dy: DeviceBlock, keep_bits_ptr: int, rate: float, training: bool,
+                          dx: DeviceBlock) -> None:
+    cdy, cdx = dy.c(), dx.c()
+    check(lib().ggb_fused_elementwise_bwd(ctx.h, C.byref(cdy), keep_bits_ptr, rate, int(training), C.byref(cdx)))
+
+
+def mask_words(cols: int) -> int:
+    return int(lib().ggb_mask_words(cols))
+
+
+def cross_entropy(ctx: Context, logits: DeviceBlock, labels_ptr: int, loss_ptr: int, grad: DeviceBlock) -> None:
+    cl, cg = logits.c(), grad.c()
+    check(lib().ggb_cross_entropy(ctx.h, C.byref(cl), labels_ptr, loss_ptr, C.byref(cg)))
+
+
+def batch_csr_block(batch: StepBatch, plane: int, transposed: bool = False) -> CsrBlockC:
+    out = CsrBlockC()
+    check(lib().ggb_batch_csr_block(batch.h, plane, int(transposed), C.byref(out)))
+    out._batch = batch  # the pointers live as long as the batch
+    return out
+
+
+def loss(ctx: Context, st: "ModelState", batch: StepBatch) -> float:
+    """parallel_cross_entropy on the last forward's logits (train_step's seam)."""
+    out = C.c_float()
+    check(lib().ggb_loss(ctx.h, st.h, batch.h, C.byref(out)))
+    return out.value
+
+
+def backward(ctx: Context, st: "ModelState", batch: StepBatch, prec: int = FP32) -> None:
+    check(lib().ggb_backward(ctx.h, st.h, batch.h, prec))
