@@ -6,8 +6,9 @@ oracle/_ref on the one-rank grid).
 
 Tolerances: contract (split-bf16 tcgen05, ~2^-16 per operand) and spmm
 (fp32 FMA vs the reference's separate multiply-add) 1e-5 of the output scale;
-RMSNorm / cross-entropy 1e-5 relative; dropout masks and the fused
-element-wise outputs bit-exact (same counter hash, same fp32 arithmetic).
+RMSNorm / cross-entropy 1e-5 relative; dropout masks and the element-wise
+backward bit-exact (same counter hash), the fused forward within one rounding
+(FMA).
 """
 import numpy as np
 import pytest
@@ -122,7 +123,10 @@ def test_fused_elementwise(env, gg, ref, rate, training, res):
     gg.fused_elementwise_bwd(ctx, _blk(gg, tdy, (X, Y)), tbits.data_ptr(), rate, training, _blk(gg, tdx, (X, Y)))
     ctx.synchronize()
     out, scale, dx = ref.fused(x, h, rate, key, training, dy)
-    assert np.array_equal(tout.cpu().numpy(), out)
+    # out = x * scale + h: one fused multiply-add here, a multiply then an add
+    # in the reference -> within one rounding (the masks themselves are exact)
+    got = tout.cpu().numpy()
+    assert np.all(np.abs(got - out) <= 2 ** -23 * np.maximum(np.abs(out), np.abs(x * scale)) + 1e-30)
     assert np.array_equal(tdx.cpu().numpy(), dx)
     # the keep bits are scale != 0 (word 4j+i, bit l <-> column 128j + 4l + i)
     bits = tbits.cpu().numpy().view(np.uint32)
