@@ -319,9 +319,11 @@ int ggb_rmsnorm_bwd(ggb_ctx_t ctx, const ggb_block* x, const float* gamma, const
  * words per row (the row kernels' layout) instead of the fp32 scale matrix. */
 int ggb_fused_elementwise_fwd(ggb_ctx_t ctx, const ggb_block* x, const ggb_block* h_prev, double rate,
                               uint64_t mask_key, int32_t training, const ggb_block* out, uint32_t* keep_bits);
-/* fused_elementwise_bwd (pmm.hpp:331-341): dx = dy . scale from those bits. */
-int ggb_fused_elementwise_bwd(ggb_ctx_t ctx, const ggb_block* dy, const uint32_t* keep_bits, double rate,
-                              int32_t training, const ggb_block* dx);
+/* fused_elementwise_bwd (pmm.hpp:331-341): dx = dy . scale from those bits,
+ * scale = keep_scale where a bit is set (keep_scale = (float)(1 / (1 - rate))
+ * when the forward dropped, else 1), 0 elsewhere. */
+int ggb_fused_elementwise_bwd(ggb_ctx_t ctx, const ggb_block* dy, const uint32_t* keep_bits, float keep_scale,
+                              const ggb_block* dx);
 /* keep-bit words per row of a block with `cols` local columns */
 int64_t ggb_mask_words(int64_t cols);
 /* parallel_cross_entropy (pmm.hpp:352-401): loss (device float, replicated),
@@ -335,6 +337,14 @@ int ggb_batch_csr_block(ggb_batch_t batch, int32_t plane, int32_t transposed, gg
  * stays in the state), then ggb_backward (model.hpp:378-420). */
 int ggb_loss(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, float* loss_out);
 int ggb_backward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, int32_t precision);
+
+/* device memory for host-side callers of the layer operators (the C++
+ * drop-in headers cpp/gridgnn/tensor.hpp / pmm.hpp stage ShardedTensor blocks
+ * through these; copies run on the context's stream and complete on return) */
+int ggb_device_alloc(ggb_ctx_t ctx, size_t bytes, void** out);
+int ggb_device_free(ggb_ctx_t ctx, void* p);
+int ggb_memcpy_h2d(ggb_ctx_t ctx, void* dst, const void* src, size_t bytes);
+int ggb_memcpy_d2h(ggb_ctx_t ctx, void* dst, const void* src, size_t bytes);
 
 /* ---- kernels exposed for unit tests (device pointers, row-major) ------------- */
 /* C[m x n] = A[m x k] . Bt[n x k]^T in bf16 x bf16 -> fp32 on tcgen05.

@@ -111,12 +111,16 @@ _SIGS = [
     ("ggb_rmsnorm_fwd", C.c_int, [P, P, P, F64, P, P]),
     ("ggb_rmsnorm_bwd", C.c_int, [P, P, P, P, P, P, P]),
     ("ggb_fused_elementwise_fwd", C.c_int, [P, P, P, F64, U64, I32, P, P]),
-    ("ggb_fused_elementwise_bwd", C.c_int, [P, P, P, F64, I32, P]),
+    ("ggb_fused_elementwise_bwd", C.c_int, [P, P, P, C.c_float, P]),
     ("ggb_mask_words", I64, [I64]),
     ("ggb_cross_entropy", C.c_int, [P, P, P, P, P]),
     ("ggb_batch_csr_block", C.c_int, [P, I32, I32, P]),
     ("ggb_loss", C.c_int, [P, P, P, P]),
     ("ggb_backward", C.c_int, [P, P, P, I32]),
+    ("ggb_device_alloc", C.c_int, [P, C.c_size_t, P]),
+    ("ggb_device_free", C.c_int, [P, P]),
+    ("ggb_memcpy_h2d", C.c_int, [P, P, P, C.c_size_t]),
+    ("ggb_memcpy_d2h", C.c_int, [P, P, P, C.c_size_t]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGS]

@@ -164,6 +164,16 @@ class RankComm {
   }
   int rank() const { return rank_; }
   const DeviceGrid& grid() const { return grid_; }
+  /// grid.hpp Coord4 of this rank: rank = ((d*gx + x)*gy + y)*gz + z
+  std::array<int, 4> coord() const {
+    std::array<int, 4> c{};
+    int r = rank_;
+    for (int a = 3; a >= 0; --a) {
+      c[static_cast<size_t>(a)] = r % grid_.dims[a];
+      r /= grid_.dims[a];
+    }
+    return c;
+  }
   void synchronize() { detail::check(ggb_ctx_synchronize(h_)); }
   ggb_ctx_t handle() const { return h_; }
   /// This rank's counters (RankStats), or with grid_total the sum over the

@@ -935,6 +935,43 @@ int ggb_backward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precisio
   });
 }
 
+int ggb_device_alloc(ggb_ctx_t ctx, size_t bytes, void** out) {
+  return guard([&] {
+    require(out != nullptr, "device_alloc: null slot");
+    use_device(*ctx);
+    *out = nullptr;
+    GGB_CUDA(cudaMalloc(out, std::max<size_t>(bytes, 16)));
+  });
+}
+
+int ggb_device_free(ggb_ctx_t ctx, void* p) {
+  return guard([&] {
+    use_device(*ctx);
+    GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (p) GGB_CUDA(cudaFree(p));
+  });
+}
+
+int ggb_memcpy_h2d(ggb_ctx_t ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    use_device(*ctx);
+    if (bytes == 0) return;
+    GGB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->h2d_bytes += bytes;
+  });
+}
+
+int ggb_memcpy_d2h(ggb_ctx_t ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    use_device(*ctx);
+    if (bytes == 0) return;
+    GGB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->d2h_bytes += bytes;
+  });
+}
+
 int ggb_contract(ggb_ctx_t ctx, const ggb_block* a, const ggb_block* b, const ggb_block* c, int32_t precision) {
   return guard([&] {
     require(a && b && c, "contract: null block");
@@ -1002,13 +1039,13 @@ int ggb_fused_elementwise_fwd(ggb_ctx_t ctx, const ggb_block* x, const ggb_block
   });
 }
 
-int ggb_fused_elementwise_bwd(ggb_ctx_t ctx, const ggb_block* dy, const uint32_t* keep_bits, double rate,
-                              int32_t training, const ggb_block* dx) {
+int ggb_fused_elementwise_bwd(ggb_ctx_t ctx, const ggb_block* dy, const uint32_t* keep_bits, float keep_scale,
+                              const ggb_block* dx) {
   return guard([&] {
     require(dy && dx, "fused_elementwise_bwd: null block");
     contract(keep_bits != nullptr, "fused_elementwise_bwd: missing cache");
     use_device(*ctx);
-    layer_fused_bwd(*ctx, *dy, keep_bits, rate, training, *dx);
+    layer_fused_bwd(*ctx, *dy, keep_bits, keep_scale, *dx);
   });
 }
 

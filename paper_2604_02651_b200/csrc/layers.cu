@@ -393,14 +393,13 @@ void layer_fused_fwd(Ctx& ctx, const ggb_block& x, const ggb_block* h_prev, doub
 }
 
 // fused_elementwise_bwd (pmm.hpp:331-341): dx = dy * scale from the keep bits
-void layer_fused_bwd(Ctx& ctx, const ggb_block& dy, const uint32_t* keep_bits, double rate, int training,
+void layer_fused_bwd(Ctx& ctx, const ggb_block& dy, const uint32_t* keep_bits, float keep_scale,
                      const ggb_block& dx) {
   const View DY = view(ctx, dy, "fused_elementwise_bwd"), DX = view(ctx, dx, "fused_elementwise_bwd");
   contract(same_meta(DY, DX), "fused_elementwise_bwd: missing cache");
   const int64_t m = DY.blk.rows(), n = DY.blk.cols();
   if (m <= 0 || n <= 0) return;
-  const bool drop = training && rate > 0.0;
-  const float ks = drop ? static_cast<float>(1.0 / (1.0 - rate)) : 1.0f;
+  const float ks = keep_scale;
   k_masked_scale<<<static_cast<unsigned>(ceil_div(m * n, 256)), 256, 0, ctx.stream>>>(
       dy.data, dy.ld, keep_bits, mask_words(n), m, n, ks, dx.data, dx.ld);
   GGB_LAUNCH_CHECK();

@@ -15,7 +15,7 @@ void layer_rmsnorm_bwd(Ctx& ctx, const ggb_block& x, const float* gamma, const f
                        const ggb_block& dx, float* dgamma);
 void layer_fused_fwd(Ctx& ctx, const ggb_block& x, const ggb_block* h_prev, double rate, uint64_t key, int training,
                      const ggb_block& out, uint32_t* keep_bits);
-void layer_fused_bwd(Ctx& ctx, const ggb_block& dy, const uint32_t* keep_bits, double rate, int training,
+void layer_fused_bwd(Ctx& ctx, const ggb_block& dy, const uint32_t* keep_bits, float keep_scale,
                      const ggb_block& dx);
 void layer_cross_entropy(Ctx& ctx, const ggb_block& logits, const int32_t* labels, float* loss, const ggb_block& grad);
 

@@ -795,10 +795,14 @@ def fused_elementwise_fwd(ctx: Context, x: DeviceBlock, h_prev: DeviceBlock | No
                                           keep_bits_ptr))
 
 
-def fused_elementwise_bwd(ctx: Context, dy: DeviceBlock, keep_bits_ptr: int, rate: float, training: bool,
-                          dx: DeviceBlock) -> None:
+def keep_scale(rate: float, training: bool) -> float:
+    """The fp32 scale of a kept element (pmm.hpp:311)."""
+    return float(np.float32(1.0 / (1.0 - rate))) if training and rate > 0 else 1.0
+
+
+def fused_elementwise_bwd(ctx: Context, dy: DeviceBlock, keep_bits_ptr: int, scale: float, dx: DeviceBlock) -> None:
     cdy, cdx = dy.c(), dx.c()
-    check(lib().ggb_fused_elementwise_bwd(ctx.h, C.byref(cdy), keep_bits_ptr, rate, int(training), C.byref(cdx)))
+    check(lib().ggb_fused_elementwise_bwd(ctx.h, C.byref(cdy), keep_bits_ptr, scale, C.byref(cdx)))
 
 
 def mask_words(cols: int) -> int:

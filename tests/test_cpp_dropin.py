@@ -1,5 +1,7 @@
-"""The C++ drop-in surface (cpp/gridgnn/ggb.hpp): compiles against the C ABI on
-CPU; its acceptance-style program (tests/cpp/test_dropin.cpp) runs on a B200."""
+"""The C++ drop-in surface (cpp/gridgnn/ggb.hpp; the layer headers pmm.hpp,
+tensor.hpp, shardsample.hpp under the reference's names): compiles against the
+C ABI on CPU; its acceptance-style programs (tests/cpp/test_dropin.cpp,
+tests/cpp/test_layers.cpp) run on a B200 against oracle/_ref."""
 import os
 import subprocess
 
@@ -7,6 +9,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+LAYERS = os.path.join(ROOT, "tests", "cpp", "test_layers")
 
 
 def _build():
@@ -17,7 +20,7 @@ def test_dropin_header_compiles_and_links():
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libgridgnn_ref.so")):
         pytest.skip("oracle/_ref not built")
     _build()
-    assert os.path.exists(BIN)
+    assert os.path.exists(BIN) and os.path.exists(LAYERS)
 
 
 @pytest.mark.gpu
@@ -28,3 +31,16 @@ def test_dropin_acceptance_on_gpu():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") == 5
+
+
+@pytest.mark.gpu
+def test_layer_dropin_on_gpu():
+    """contract / spmm / RMSNorm / fused element-wise / cross-entropy /
+    transposed / gather_full / reshard through pmm.hpp with the reference's
+    argument lists, against the reference's operators and its unit-test KATs."""
+    if not os.path.exists(LAYERS):
+        _build()
+    r = subprocess.run([LAYERS], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 14 and "FAIL" not in r.stdout

@@ -120,7 +120,8 @@ def test_fused_elementwise(env, gg, ref, rate, training, res):
     tbits = torch.zeros(m, ldm, dtype=torch.int32, device="cuda")
     gg.fused_elementwise_fwd(ctx, _blk(gg, tx, (X, Y)), _blk(gg, th, (X, Y)) if res else None, rate, key, training,
                              _blk(gg, tout, (X, Y)), tbits.data_ptr())
-    gg.fused_elementwise_bwd(ctx, _blk(gg, tdy, (X, Y)), tbits.data_ptr(), rate, training, _blk(gg, tdx, (X, Y)))
+    gg.fused_elementwise_bwd(ctx, _blk(gg, tdy, (X, Y)), tbits.data_ptr(), gg.keep_scale(rate, training),
+                             _blk(gg, tdx, (X, Y)))
     ctx.synchronize()
     out, scale, dx = ref.fused(x, h, rate, key, training, dy)
     # out = x * scale + h: one fused multiply-add here, a multiply then an add
