@@ -43,4 +43,4 @@ def test_layer_dropin_on_gpu():
     r = subprocess.run([LAYERS], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 14 and "FAIL" not in r.stdout
+    assert r.stdout.count("PASS") == 15 and "FAIL" not in r.stdout
