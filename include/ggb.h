@@ -72,6 +72,14 @@ int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const ui
 int ggb_ctx_destroy(ggb_ctx_t ctx);
 int ggb_ctx_set_stream(ggb_ctx_t ctx, void* stream);
 int ggb_ctx_synchronize(ggb_ctx_t ctx);
+/* CommConfig::timeout (comm.hpp:195-198, default 60 s; also GGB_COMM_TIMEOUT_MS):
+ * a host wait on the context's stream (ggb_ctx_synchronize, the loss read of
+ * ggb_train_step, barriers) polls the NCCL communicators' asynchronous errors
+ * and this deadline; on either it aborts the communicators (their in-flight
+ * kernels return) and fails with GGB_ENCCL / GGB_ETIMEOUT (CommTimeout:
+ * "collective timed out: not all group members arrived", comm.hpp:157-158).
+ * Later collectives on the context fail with GGB_ETIMEOUT. */
+int ggb_ctx_set_comm_timeout(ggb_ctx_t ctx, int64_t timeout_ms);
 /* counters = {kernels launched on ctx since creation, host->device bytes,
  * device->host bytes} */
 int ggb_ctx_counters(ggb_ctx_t ctx, uint64_t* counters);

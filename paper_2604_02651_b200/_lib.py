@@ -51,6 +51,7 @@ _SIGS = [
     ("ggb_ctx_destroy", C.c_int, [P]),
     ("ggb_ctx_set_stream", C.c_int, [P, P]),
     ("ggb_ctx_synchronize", C.c_int, [P]),
+    ("ggb_ctx_set_comm_timeout", C.c_int, [P, I64]),
     ("ggb_ctx_counters", C.c_int, [P, P]),
     ("ggb_ctx_comm_stats", C.c_int, [P, I32, I32, P]),
     ("ggb_ctx_profile", C.c_int, [P, I32]),

@@ -403,7 +403,14 @@ int ggb_ctx_set_stream(ggb_ctx_t ctx, void* stream) {
 int ggb_ctx_synchronize(ggb_ctx_t ctx) {
   return guard([&] {
     use_device(*ctx);
-    GGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    sync_stream(*ctx, ctx->stream);  // with the collective watchdog (CommTimeout)
+  });
+}
+
+int ggb_ctx_set_comm_timeout(ggb_ctx_t ctx, int64_t timeout_ms) {
+  return guard([&] {
+    require(timeout_ms > 0, "comm timeout must be positive");
+    if (ctx->comm) ctx->comm->timeout_ms = timeout_ms;
   });
 }
 
@@ -905,7 +912,8 @@ int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precis
       backward(*st, *bt, precision);
     }
     if (loss_out) {
-      download(loss_out, st->loss.p, 1, ctx->stream);
+      GGB_CUDA(cudaMemcpyAsync(loss_out, st->loss.p, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+      sync_stream(*ctx, ctx->stream);  // with the collective watchdog
       ctx->d2h_bytes += sizeof(float);
     }
   });
@@ -920,7 +928,8 @@ int ggb_loss(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, float* loss_out) {
       cross_entropy(*st, *bt);
     }
     if (loss_out) {
-      download(loss_out, st->loss.p, 1, ctx->stream);
+      GGB_CUDA(cudaMemcpyAsync(loss_out, st->loss.p, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+      sync_stream(*ctx, ctx->stream);  // with the collective watchdog
       ctx->d2h_bytes += sizeof(float);
     }
   });

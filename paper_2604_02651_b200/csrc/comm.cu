@@ -4,8 +4,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 namespace ggb {
 namespace {
@@ -77,6 +79,8 @@ int comm_chunks() {
 }
 
 void need(const Ctx& ctx, int axis) {
+  if (ctx.comm && ctx.comm->aborted)
+    fail(GGB_ETIMEOUT, "communicators were aborted after a collective timed out or failed");
   if (!ctx.comm || !ctx.comm->axis[axis])
     fail(GGB_ECONTRACT, "collective over a multi-rank group on a context without communicators");
 }
@@ -91,6 +95,51 @@ Comm::~Comm() {
   if (world) ncclCommDestroy(as_nccl(world));
 }
 
+namespace {
+void abort_all(Comm& c) {
+  for (auto& a : c.axis)
+    if (a) {
+      ncclCommAbort(as_nccl(a));
+      a = nullptr;
+    }
+  if (c.world) {
+    ncclCommAbort(as_nccl(c.world));
+    c.world = nullptr;
+  }
+  c.aborted = true;
+}
+}  // namespace
+
+void sync_stream(Ctx& ctx, cudaStream_t s) {
+  if (!ctx.comm || ctx.comm->aborted) {
+    GGB_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
+  Comm& c = *ctx.comm;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return;
+    if (q != cudaErrorNotReady) GGB_CUDA(q);
+    void* comms[5] = {c.world, c.axis[0], c.axis[1], c.axis[2], c.axis[3]};
+    for (void* k : comms) {
+      if (!k) continue;
+      ncclResult_t st = ncclSuccess;
+      if (ncclCommGetAsyncError(as_nccl(k), &st) == ncclSuccess && st != ncclSuccess && st != ncclInProgress) {
+        const std::string why = ncclGetErrorString(st);
+        abort_all(c);
+        fail(GGB_ENCCL, "collective failed on a peer (" + why + "); communicators aborted");
+      }
+    }
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > c.timeout_ms) {
+      abort_all(c);
+      fail(GGB_ETIMEOUT, "collective timed out: not all group members arrived");
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(spin > 4096 ? 500 : 20));
+  }
+}
+
 int comm_get_unique_id(uint8_t out[128]) {
   ncclUniqueId id;
   GGB_NCCL(ncclGetUniqueId(&id));
@@ -101,6 +150,10 @@ int comm_get_unique_id(uint8_t out[128]) {
 
 std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid) {
   auto c = std::make_unique<Comm>();
+  if (const char* e = std::getenv("GGB_COMM_TIMEOUT_MS")) {
+    const long long v = std::atoll(e);
+    if (v > 0) c->timeout_ms = v;
+  }
   ncclUniqueId id;
   std::memcpy(&id, uid, 128);
   ncclComm_t world;
@@ -263,6 +316,7 @@ void all_gather(Ctx& ctx, int axis, const float* in, int64_t count, float* out) 
 void exchange_blocks(Ctx& ctx, const std::vector<BlockXfer>& sends, const std::vector<BlockXfer>& recvs) {
   if (sends.empty() && recvs.empty()) return;
   if (!ctx.comm) fail(GGB_ECONTRACT, "block exchange on a context without communicators");
+  if (ctx.comm->aborted) fail(GGB_ETIMEOUT, "communicators were aborted after a collective timed out or failed");
   Comm& c = *ctx.comm;
   int64_t ns = 0, nr = 0;
   for (const auto& x : sends) ns += x.rows * x.cols;
@@ -305,9 +359,10 @@ void exchange_blocks(Ctx& ctx, const std::vector<BlockXfer>& sends, const std::v
 void barrier(Ctx& ctx) {
   if (ctx.grid.total() == 1) return;
   if (!ctx.comm) fail(GGB_ECONTRACT, "barrier on a context without communicators");
+  if (ctx.comm->aborted) fail(GGB_ETIMEOUT, "communicators were aborted after a collective timed out or failed");
   float* one = ctx.comm->gather.reserve_n<float>(1);
   GGB_NCCL(ncclAllReduce(one, one, 1, ncclFloat32, ncclSum, as_nccl(ctx.comm->world), ctx.stream));
-  GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+  sync_stream(ctx, ctx.stream);
 }
 
 }  // namespace ggb

@@ -21,8 +21,21 @@ struct Comm {
   cudaStream_t cstream = nullptr;
   DevBuf gather2, wire2;
   std::vector<cudaEvent_t> ev;
+  // CommConfig::timeout (comm.hpp:195-198; default 60 s, GGB_COMM_TIMEOUT_MS
+  // or ggb_ctx_set_comm_timeout): how long a host wait on a stream holding
+  // collectives may last before the communicators are aborted
+  int64_t timeout_ms = 60000;
+  bool aborted = false;
   ~Comm();
 };
+
+/// Host wait for stream s with the collective watchdog: polls the stream,
+/// the communicators' asynchronous errors (a failed / aborted peer) and the
+/// deadline. On an NCCL error or the deadline, aborts every communicator of
+/// the context (their in-flight kernels return) and fails with GGB_ENCCL /
+/// GGB_ETIMEOUT (CommTimeout: "collective timed out: not all group members
+/// arrived", comm.hpp:157-158). Without communicators: cudaStreamSynchronize.
+void sync_stream(Ctx& ctx, cudaStream_t s);
 
 int comm_get_unique_id(uint8_t out[128]);
 std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid);

@@ -146,6 +146,10 @@ class Context:
     def set_stream(self, stream: int | None):
         check(lib().ggb_ctx_set_stream(self.h, stream))
 
+    def set_comm_timeout(self, ms: int):
+        """CommConfig::timeout (comm.hpp:195-198): collective watchdog deadline."""
+        check(lib().ggb_ctx_set_comm_timeout(self.h, ms))
+
     def synchronize(self):
         check(lib().ggb_ctx_synchronize(self.h))
 
