@@ -190,6 +190,12 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
       GGB_NCCL(ncclRecv(buf + n + p, 1, ncclFloat32, p, world, nullptr));
     }
     GGB_NCCL(ncclGroupEnd());
+    // collectives connect their rings / trees on first use too, with a host
+    // handshake between the members: one tiny all-reduce per communicator
+    // here, so no step (and no collective watchdog wait) pays for it
+    GGB_NCCL(ncclAllReduce(buf, buf, 1, ncclFloat32, ncclSum, world, nullptr));
+    for (int a = 0; a < 4; ++a)
+      if (c->axis[a]) GGB_NCCL(ncclAllReduce(buf, buf, 1, ncclFloat32, ncclSum, as_nccl(c->axis[a]), nullptr));
     GGB_CUDA(cudaDeviceSynchronize());
     GGB_CUDA(cudaFree(buf));
   }

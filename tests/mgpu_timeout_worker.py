@@ -27,10 +27,13 @@ def main():
     cfg = gg.ModelConfig(layers=2, d_in=8, d_h=16, d_out=3)
     st = gg.init_state(ctx, cfg, 1)
     res = {}
+    log = lambda m: print(f"[rank {rank}] {m}", file=sys.stderr, flush=True)
+    log("contexts up")
     if rank == 0:
         ctx.set_comm_timeout(3000)
         t0 = time.time()
         gg.dp_sync(ctx, st)  # rank 1 never arrives
+        log("dp_sync enqueued")
         try:
             ctx.synchronize()
             res["raised"] = None
@@ -38,6 +41,7 @@ def main():
             res["raised"] = "CommTimeout"
             res["msg"] = str(e)
         res["seconds"] = time.time() - t0
+        log(f"synchronize returned: {res}")
         try:  # the aborted communicators fail fast afterwards
             gg.dp_sync(ctx, st)
             res["after"] = None
