@@ -355,6 +355,12 @@ int ggb_memcpy_h2d(ggb_ctx_t ctx, void* dst, const void* src, size_t bytes);
 int ggb_memcpy_d2h(ggb_ctx_t ctx, void* dst, const void* src, size_t bytes);
 
 /* ---- kernels exposed for unit tests (device pointers, row-major) ------------- */
+/* sample_vertices with an extra, test-only rejection rule (a draw x is also
+ * rejected when x % reject_mod == 0): rejections of next_below (rng.hpp:38-45)
+ * otherwise occur with probability < n / 2^64 per draw, too rarely to test the
+ * parallel re-draw passes; the oracle applies the same rule. */
+int ggb_sample_vertices_test_reject(ggb_ctx_t ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step,
+                                    uint64_t reject_mod, int64_t* host_out);
 /* C[m x n] = A[m x k] . Bt[n x k]^T in bf16 x bf16 -> fp32 on tcgen05.
  * c (fp32) and/or c_bf16 may be NULL. Leading dimensions in elements. */
 int ggb_gemm_bf16(ggb_ctx_t ctx, int64_t m, int64_t n, int64_t k, const void* a, int64_t lda,

@@ -58,6 +58,16 @@ static uint64_t st_next_below(orc_stream* s, uint64_t bound) {
   } while (x >= limit);
   return x % bound;
 }
+/* next_below with the test-only extra rejection rule of
+ * ggb_sample_vertices_test_reject (x % reject_mod == 0 also rejected) */
+static uint64_t st_next_below_rej(orc_stream* s, uint64_t bound, uint64_t reject_mod) {
+  const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+  uint64_t x;
+  do {
+    x = st_next_u64(s);
+  } while (x >= limit || (reject_mod && x % reject_mod == 0));
+  return x % bound;
+}
 static double st_next_normal(orc_stream* s) {
   if (s->have_spare) {
     s->have_spare = 0;
@@ -379,4 +389,24 @@ void orc_rmat_edges(int scale, int64_t m, double a, double b, double c, uint64_t
     uv[2 * e] = u;
     uv[2 * e + 1] = v;
   }
+}
+
+/* sample_vertices (src/sampling.cpp:11-33) with the extra rejection rule */
+int orc_sample_vertices_reject(int64_t n, int64_t b, uint64_t seed, uint64_t step, uint64_t reject_mod,
+                               int64_t* out) {
+  if (b <= 0 || b > n) return 1;
+  orc_stream s = {orc_splitmix64(seed + step), 0.0, 0};
+  int64_t* perm = (int64_t*)malloc((size_t)n * sizeof(int64_t));
+  if (!perm) return 2;
+  for (int64_t i = 0; i < n; ++i) perm[i] = i;
+  for (int64_t i = 0; i < b; ++i) {
+    const int64_t j = i + (int64_t)st_next_below_rej(&s, (uint64_t)(n - i), reject_mod);
+    const int64_t t = perm[i];
+    perm[i] = perm[j];
+    perm[j] = t;
+  }
+  memcpy(out, perm, (size_t)b * sizeof(int64_t));
+  free(perm);
+  qsort(out, (size_t)b, sizeof(int64_t), cmp_i64);
+  return 0;
 }

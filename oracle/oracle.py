@@ -75,6 +75,7 @@ def orc() -> C.CDLL:
                                           P, P, P, P, P, P]
         L.orc_synthetic_edges.restype = I64
         L.orc_synthetic_edges.argtypes = [I64, C.c_double, U64, P]
+        L.orc_sample_vertices_reject.argtypes = [I64, I64, U64, U64, U64, P]
         L.orc_rmat_edges.argtypes = [C.c_int, I64, C.c_double, C.c_double, C.c_double, U64, P]
         L.orc_normalize_adjacency.restype = I64
         L.orc_normalize_adjacency.argtypes = [P, I64, I64, P, P, P]
@@ -113,6 +114,13 @@ def sample_vertices(n: int, b: int, seed: int, step: int) -> np.ndarray:
     out = np.empty(b, np.int64)
     if orc().orc_sample_vertices(n, b, seed, step, _ptr(out)) != 0:
         raise ValueError("sample_vertices: need 1 <= b <= n")
+    return out
+
+
+def sample_vertices_reject(n: int, b: int, seed: int, step: int, reject_mod: int) -> np.ndarray:
+    """sample_vertices with the test-only extra rejection rule (x % reject_mod == 0)."""
+    out = np.empty(b, np.int64)
+    orc().orc_sample_vertices_reject(n, b, seed, step, reject_mod, _ptr(out))
     return out
 
 

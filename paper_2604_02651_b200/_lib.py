@@ -103,6 +103,7 @@ _SIGS = [
     ("ggb_gemm_split_bf16", C.c_int, [P, I64, I64, I64, P, P, I64, P, P, I64, P, I64]),
     ("ggb_gemm_wgrad_bf16", C.c_int, [P, I64, I64, I64, P, I64, P, I64, P, I64]),
     ("ggb_spmm_csr", C.c_int, [P, I64, P, P, P, P, I64, I64, P, I64, P, I64, I32]),
+    ("ggb_sample_vertices_test_reject", C.c_int, [P, I64, I64, U64, U64, U64, P]),
     ("ggb_spmm_csr_f32", C.c_int, [P, I64, P, P, P, P, I64, I64, P, I64, P, P, I64, I32]),
     ("ggb_contract", C.c_int, [P, P, P, P, I32]),
     ("ggb_spmm", C.c_int, [P, P, P, P, I32]),

@@ -483,6 +483,18 @@ int ggb_sample_vertices(ggb_ctx_t ctx, int64_t n, int64_t b, uint64_t seed, uint
   });
 }
 
+int ggb_sample_vertices_test_reject(ggb_ctx_t ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step,
+                                    uint64_t reject_mod, int64_t* host_out) {
+  return guard([&] {
+    use_device(*ctx);
+    require(b >= 1 && b <= n, "sample_vertices: need 1 <= b <= n");
+    DevBuf out;
+    int64_t* d = out.reserve_n<int64_t>(b);
+    sample_set(*ctx, n, b, seed, step, d, reject_mod);
+    download(host_out, d, static_cast<size_t>(b), ctx->stream);
+  });
+}
+
 int ggb_graph_create(ggb_ctx_t ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const double* values,
                      int32_t symmetric, int64_t d_in, const float* features, int64_t n_classes,
                      const int32_t* labels, int32_t layers, ggb_graph_t* out) {

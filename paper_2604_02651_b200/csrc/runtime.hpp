@@ -212,7 +212,9 @@ struct Batch {
 };
 
 // sampler.cu
-void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* d_sample);
+// reject_mod: test-only extra rejection rule (0 = the reference's sampler)
+void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* d_sample,
+                uint64_t reject_mod = 0);
 // want_xf: also keep the fp32 x_in rows for preaggregate() (same gather)
 void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, uint64_t step,
                       Batch& out, bool want_xf = false);

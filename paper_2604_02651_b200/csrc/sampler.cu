@@ -42,21 +42,37 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__global__ void k_draw(int64_t n, int64_t b, uint64_t s0, int32_t* __restrict__ j,
-                       int* __restrict__ reject) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// Rejection sampling of next_below (rng.hpp:38-45): a draw x >= limit is
+// discarded and the stream advances, so every later step reads its counter
+// one further. reject_mod > 0 adds "x % reject_mod == 0" as a rejection
+// (a test-only rule that makes rejections frequent, mirrored by the oracle).
+__device__ __forceinline__ bool rejected(uint64_t x, uint64_t limit, uint64_t reject_mod) {
+  return x >= limit || (reject_mod && x % reject_mod == 0);
+}
+
+// Draws of steps i >= from, assuming `shift` rejections before them: step i
+// reads counter i + shift. The first rejected step goes to *next_first
+// (atomicMin); steps before `from` keep their draws. Pass 0 covers all steps
+// with no rejections assumed; pass p > 0 re-draws only the suffix from the
+// first rejection the previous pass found (a no-op when there was none).
+__global__ void k_draw(int64_t n, int64_t b, uint64_t s0, const int64_t* __restrict__ first_in, int shift,
+                       int64_t* __restrict__ next_first, uint64_t reject_mod, int32_t* __restrict__ j) {
+  const int64_t from = first_in ? *first_in : 0;
+  if (from >= b) return;
+  const int64_t i = from + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= b) return;
   const uint64_t bound = static_cast<uint64_t>(n - i);
   const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
-  const uint64_t x = stream_draw(s0, static_cast<uint64_t>(i));
-  if (x >= limit) atomicOr(reject, 1);
+  const uint64_t x = stream_draw(s0, static_cast<uint64_t>(i + shift));
+  if (rejected(x, limit, reject_mod)) atomicMin(reinterpret_cast<unsigned long long*>(next_first), i);
   j[i] = static_cast<int32_t>(i + static_cast<int64_t>(x % bound));
 }
 
-// Exact sequential replay when any draw was rejected (probability < n/2^64
-// per draw); a no-op otherwise.
-__global__ void k_draw_fixup(int64_t n, int64_t b, uint64_t s0, int32_t* j, const int* reject) {
-  if (*reject == 0) return;
+// More rejections than the passes cover (probability ~ (b n / 2^64)^3 per
+// batch): exact sequential replay from the start.
+__global__ void k_draw_replay(int64_t n, int64_t b, uint64_t s0, const int64_t* last_first, uint64_t reject_mod,
+                              int32_t* j) {
+  if (*last_first >= b) return;
   uint64_t k = 0;
   for (int64_t i = 0; i < b; ++i) {
     const uint64_t bound = static_cast<uint64_t>(n - i);
@@ -64,9 +80,13 @@ __global__ void k_draw_fixup(int64_t n, int64_t b, uint64_t s0, int32_t* j, cons
     uint64_t x;
     do {
       x = stream_draw(s0, k++);
-    } while (x >= limit);
+    } while (rejected(x, limit, reject_mod));
     j[i] = static_cast<int32_t>(i + static_cast<int64_t>(x % bound));
   }
+}
+
+__global__ void k_fill_i64(int64_t* p, int n, int64_t v) {
+  if (threadIdx.x < n) p[threadIdx.x] = v;
 }
 
 __global__ void k_link(int64_t b, const int32_t* __restrict__ j, unsigned long long* head,
@@ -337,7 +357,10 @@ inline unsigned blocks(int64_t n, int t = kThreads) { return static_cast<unsigne
 
 }  // namespace
 
-void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* d_sample) {
+constexpr int kDrawPasses = 3;  // re-draw passes after the first (rejections they absorb: kDrawPasses - 1)
+
+void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, int64_t* d_sample,
+                uint64_t reject_mod) {
   require(b >= 1 && b <= n, "sample_vertices: need 1 <= b <= n");
   require(n < (int64_t{1} << 31) - 64, "sample_vertices: n must be < 2^31");
   SamplerWork& sw = ctx.sw;
@@ -355,15 +378,17 @@ void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, in
   const int64_t words = n / 32 + 2;
   int32_t* j = sw.j.reserve_n<int32_t>(b);
   int32_t* next = sw.next.reserve_n<int32_t>(b);
-  int* flag = sw.flag.reserve_n<int>(1);
+  int64_t* first = sw.flag.reserve_n<int64_t>(kDrawPasses + 1);  // first rejected step found by each pass
   uint32_t* bitmap = sw.bitmap.reserve_n<uint32_t>(words);
   int32_t* wcount = sw.wcount.reserve_n<int32_t>(words);
   int32_t* wpfx = sw.wpfx.reserve_n<int32_t>(words + 1);
-  GGB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
   GGB_CUDA(cudaMemsetAsync(bitmap, 0, static_cast<size_t>(words) * 4, s));
   const uint64_t s0 = splitmix64(seed + step);  // sampling.cpp:16
-  k_draw<<<blocks(b), kThreads, 0, s>>>(n, b, s0, j, flag);
-  k_draw_fixup<<<1, 1, 0, s>>>(n, b, s0, j, flag);
+  k_fill_i64<<<1, 32, 0, s>>>(first, kDrawPasses + 1, b);
+  k_draw<<<blocks(b), kThreads, 0, s>>>(n, b, s0, nullptr, 0, first, reject_mod, j);
+  for (int p = 1; p < kDrawPasses; ++p)
+    k_draw<<<blocks(b), kThreads, 0, s>>>(n, b, s0, first + p - 1, p, first + p, reject_mod, j);
+  k_draw_replay<<<1, 1, 0, s>>>(n, b, s0, first + kDrawPasses - 1, reject_mod, j);
   k_link<<<blocks(b), kThreads, 0, s>>>(b, j, sw.head.as<unsigned long long>(), sw.tag, next);
   k_resolve<<<blocks(b), kThreads, 0, s>>>(b, j, sw.head.as<unsigned long long>(), next, sw.tag,
                                            bitmap);
@@ -371,7 +396,7 @@ void sample_set(Ctx& ctx, int64_t n, int64_t b, uint64_t seed, uint64_t step, in
   exclusive_scan_i32(wcount, wpfx, words, sw.scan_tmp, s);
   k_compact<<<blocks(words), kThreads, 0, s>>>(words, bitmap, wpfx, d_sample);
   GGB_LAUNCH_CHECK();
-  ctx.launches += 9;
+  ctx.launches += 8 + kDrawPasses;
 }
 
 namespace {

@@ -220,8 +220,9 @@ double gemm_bytes(int64_t m, int64_t n, int64_t k, int ea, int eb, int ec) {
 void fwd_gemm(State& st, int64_t m, int64_t n, int64_t k, const Tensor& a, const ParamSlot& w, float* c,
               int64_t ldc, bf16* cb, int64_t ldcb, bf16* cl = nullptr) {
   const int e = st.compute == kAccurate ? 4 : 2;
+  // algorithmic flops 2mnk: the split form's 3 MMAs reproduce ONE fp32 product
   ProfScope ps(*st.ctx, kProfGemmFwd, gemm_bytes(m, n, k, e, e, (c ? 4 : 0) + (cb ? 2 : 0) + (cl ? 2 : 0)),
-               2.0 * m * n * k * (st.compute == kAccurate ? 3 : 1));
+               2.0 * m * n * k);
   if (st.compute == kAccurate)
     gemm_split(*st.ctx, m, n, k, a.b, a.lo, a.ldb, w.wt.as<bf16>(), w.wtl.as<bf16>(), w.ldt, c, ldc, cb, ldcb, cl);
   else
@@ -658,8 +659,10 @@ void backward(State& st, const Batch& bt, int precision) {
     ba.dxb = grow<bf16>(st.dxw_b, rows * lddxw);
     ba.lddxb = lddxw;
     {
-    // reads dy + xw twice (stats, apply) + mask, writes dxw bf16
-    ProfScope ps(ctx, kProfBwdRow, static_cast<double>(rows) * cols * (2 * 8 + 2) + rows * cols / 4.0);
+    // reads dy + xw (once more for the row statistics when the row is split),
+    // the keep bits, writes dxw bf16
+    ProfScope ps(ctx, kProfBwdRow,
+                 static_cast<double>(rows) * cols * ((row_local ? 8 : 16) + 2) + static_cast<double>(rows) * cols / 8.0);
     if (cfg.use_rmsnorm) {
       const ParamSlot& gp = st.params[st.gamma[l - 1]];
       ba.gamma = W + gp.off;

@@ -291,3 +291,21 @@ def test_c2_batch_properties_at_full_size(gg):
         assert ci[pos] == v
         want = va[pos] if u == v else va[pos] / p
         assert np.float64(want).view(np.uint64) == np.float64(a.values[k]).view(np.uint64)
+
+
+@pytest.mark.parametrize("n,b,reject_mod,seed", [(5000, 1000, 0, 1), (5000, 1000, 1 << 62, 3),
+                                                 (100000, 20000, 25000, 7), (100000, 20000, 12000, 8),
+                                                 (100000, 20000, 7000, 9), (20000, 20000, 900, 2),
+                                                 (3000, 700, 3, 5)])
+def test_rejected_draws_redrawn_exactly(gg, orc, n, b, reject_mod, seed):
+    """next_below rejections (rng.hpp:38-45) shift every later draw's counter:
+    the parallel re-draw passes (and the sequential replay beyond them) give
+    the exact partial Fisher-Yates sample. A test-only rule (x % reject_mod
+    == 0) makes rejections frequent: ~b / reject_mod per batch (0: none, up
+    to hundreds, which takes the replay)."""
+    ctx = gg.Context()
+    out = np.empty(b, np.int64)
+    gg.check(gg.lib().ggb_sample_vertices_test_reject(ctx.h, n, b, seed, 4, reject_mod, gg._ptr(out)))
+    assert np.array_equal(out, orc.sample_vertices_reject(n, b, seed, 4, reject_mod))
+    if reject_mod == 0:
+        assert np.array_equal(out, orc.sample_vertices(n, b, seed, 4))
