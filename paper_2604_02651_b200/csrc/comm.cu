@@ -88,6 +88,9 @@ void need(const Ctx& ctx, int axis) {
 }  // namespace
 
 Comm::~Comm() {
+  if (gstream) cudaStreamDestroy(gstream);
+  if (gfork) cudaEventDestroy(gfork);
+  if (gjoin) cudaEventDestroy(gjoin);
   for (auto& e : ev) cudaEventDestroy(e);
   if (cstream) cudaStreamDestroy(cstream);
   for (auto& a : axis)
@@ -248,6 +251,45 @@ void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, int wire) {
   }
   need(ctx, axis);
   all_reduce_sum_on(ctx, axis, buf, count, wire, ctx.stream, ctx.comm->wire, ctx.comm->gather);
+}
+
+namespace {
+bool async_grad() {
+  static const bool on = [] {
+    const char* e = std::getenv("GGB_ASYNC_GRAD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace
+
+void all_reduce_sum_async(Ctx& ctx, int axis, float* buf, int64_t count, int wire) {
+  if (count <= 0) return;
+  if (trivial(ctx, axis) || !async_grad()) {
+    all_reduce_sum(ctx, axis, buf, count, wire);
+    return;
+  }
+  need(ctx, axis);
+  Comm& c = *ctx.comm;
+  if (!c.gstream) {
+    int lo = 0, hi = 0;
+    GGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GGB_CUDA(cudaStreamCreateWithPriority(&c.gstream, cudaStreamNonBlocking, hi));
+    GGB_CUDA(cudaEventCreateWithFlags(&c.gfork, cudaEventDisableTiming));
+    GGB_CUDA(cudaEventCreateWithFlags(&c.gjoin, cudaEventDisableTiming));
+  }
+  GGB_CUDA(cudaEventRecord(c.gfork, ctx.stream));
+  GGB_CUDA(cudaStreamWaitEvent(c.gstream, c.gfork, 0));
+  all_reduce_sum_on(ctx, axis, buf, count, wire, c.gstream, c.gwire, c.ggather);
+  c.gpending = true;
+}
+
+void join_async(Ctx& ctx) {
+  if (!ctx.comm || !ctx.comm->gpending) return;
+  Comm& c = *ctx.comm;
+  GGB_CUDA(cudaEventRecord(c.gjoin, c.gstream));
+  GGB_CUDA(cudaStreamWaitEvent(ctx.stream, c.gjoin, 0));
+  c.gpending = false;
 }
 
 void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, float* buf, int64_t ld, int bf16_wire,

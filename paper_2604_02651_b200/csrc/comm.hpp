@@ -26,6 +26,11 @@ struct Comm {
   // collectives may last before the communicators are aborted
   int64_t timeout_ms = 60000;
   bool aborted = false;
+  // gradient all-reduces issued beside the backward (all_reduce_sum_async)
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gfork = nullptr, gjoin = nullptr;
+  DevBuf gwire, ggather;
+  bool gpending = false;
   ~Comm();
 };
 
@@ -46,6 +51,12 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
 // (comm.hpp:271-303) reproduced exactly by an all-gather of bf16
 // contributions; 2 bf16 payloads summed by one NCCL all-reduce.
 void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, int wire);
+// all_reduce_sum on the gradient stream: the compute stream goes on (the
+// backward's dX products need no dW), join_async makes it wait for every
+// such reduction issued since the last join. Same sums as all_reduce_sum.
+// GGB_ASYNC_GRAD=0 runs them inline.
+void all_reduce_sum_async(Ctx& ctx, int axis, float* buf, int64_t count, int wire);
+void join_async(Ctx& ctx);
 void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count);
 // Row-chunked overlap of a producer and its all-reduce: chunk k
 // of `rows` rows (row stride ld floats of buf) is produced on the compute

@@ -605,7 +605,7 @@ void backward(State& st, const Batch& bt, int precision) {
                       G + w.off, w.blk.cols(), st.ws_wgrad);
     }
     charge_all_reduce(ctx, XL.blk.lay.row, w.n, wire_bytes(wire));
-    all_reduce_sum(ctx, XL.blk.lay.row, G + w.off, w.n, wire);
+    all_reduce_sum_async(ctx, XL.blk.lay.row, G + w.off, w.n, wire);
   }
   // dxh = dlogits . W_out^T -> (X_L.row, X_L.col), all-reduce logits.col
   Block db = XL.blk;
@@ -678,7 +678,7 @@ void backward(State& st, const Batch& bt, int precision) {
       ba.dgamma_part = grow<float>(st.dg_part, static_cast<int64_t>(blocks) * cols);
       bwd_apply(ctx, ba, blocks);
       reduce_rows(ctx, ba.dgamma_part, blocks, cols, G + gp.off);
-      all_reduce_sum(ctx, xb.lay.row, G + gp.off, cols, false);
+      all_reduce_sum_async(ctx, xb.lay.row, G + gp.off, cols, false);
     } else {
       bwd_apply(ctx, ba, bwd_apply_blocks(ctx, rows, cols));
     }
@@ -693,7 +693,7 @@ void backward(State& st, const Batch& bt, int precision) {
                       st.ws_wgrad);
     }
     charge_all_reduce(ctx, hg.blk.lay.row, w.n, wire_bytes(wire));
-    all_reduce_sum(ctx, hg.blk.lay.row, G + w.off, w.n, wire);
+    all_reduce_sum_async(ctx, hg.blk.lay.row, G + w.off, w.n, wire);
     // dhagg = dxw . W_l^T -> (xw.row, hagg.col), all-reduce xw.col
     const int64_t hc = hg.blk.cols();
     const bool ar_d = reduces(ctx, xb.lay.col, wire);
@@ -786,7 +786,8 @@ void backward(State& st, const Batch& bt, int precision) {
     gemm_wgrad_bf16(ctx, rows, kin, cols, bt.p_in.as<bf16>(), bt.x_ld, pre_dhb, pre_ldhb, G + w.off, w.blk.cols(),
                     st.ws_wgrad, pre_dres ? 1 : 0);
     charge_all_reduce(ctx, kInputFeatureLayout.row, w.n, wire_bytes(wire));
-    all_reduce_sum(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
+    all_reduce_sum_async(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
+    join_async(ctx);  // every gradient reduced before dp_sync / the optimizer read G
     return;
   }
   // dW_in = x_in^T . dxh, all-reduce x_in.row (X)
@@ -804,8 +805,9 @@ void backward(State& st, const Batch& bt, int precision) {
     gemm_wgrad_bf16(ctx, rows, kin, cols, bt.x_in.as<bf16>(), bt.x_ld, dxb, ldb, G + w.off, w.blk.cols(),
                     st.ws_wgrad);
     charge_all_reduce(ctx, kInputFeatureLayout.row, w.n, wire_bytes(wire));
-    all_reduce_sum(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
+    all_reduce_sum_async(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
   }
+  join_async(ctx);  // every gradient reduced before dp_sync / the optimizer read G
 }
 
 // ---- dp_sync (model.hpp:423-433) ------------------------------------------------------
