@@ -103,8 +103,10 @@ __global__ void k_csr_fill(const uint64_t* __restrict__ keys, const int64_t* __r
     for (int64_t k = b + lane; k < e; k += 32) {
       const int64_t c = static_cast<int64_t>(keys[k] - base);
       col[k] = static_cast<int32_t>(c);
-      const double dc = static_cast<double>(rp[c + 1] - rp[c]);
-      val[k] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dr, dc)));
+      if (val) {
+        const double dc = static_cast<double>(rp[c + 1] - rp[c]);
+        val[k] = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dr, dc)));
+      }
     }
   }
 }
@@ -164,6 +166,14 @@ __global__ void k_degrees(const int64_t* __restrict__ rp, int64_t n, uint32_t* _
   }
 }
 
+// full-graph row degrees (self-loop included): the normalized values are
+// 1 / sqrt(deg_u deg_v) (dataset.cpp:78-79), recomputed wherever needed
+__global__ void k_row_degrees(const int64_t* __restrict__ rp, int64_t n, int32_t* __restrict__ deg) {
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    deg[v] = static_cast<int32_t>(rp[v + 1] - rp[v]);
+}
+
 __global__ void k_labels(const int32_t* __restrict__ order, int64_t n, int64_t n_classes, int32_t* __restrict__ labels) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -210,7 +220,7 @@ __global__ void k_shard_fill(const int32_t* __restrict__ col, const double* __re
     const int64_t o = orp[r], len = orp[r + 1] - o, l = lo[r];
     for (int64_t k = lane; k < len; k += 32) {
       ocol[o + k] = col[l + k];
-      oval[o + k] = val[l + k];
+      if (oval) oval[o + k] = val[l + k];
     }
   }
 }
@@ -329,9 +339,11 @@ void generate_synthetic_device(Ctx& ctx, int64_t n, double avg_degree, int64_t d
   ds.nnz = nnz;
   int64_t* rp = ds.row_ptr.reserve_n<int64_t>(static_cast<size_t>(n) + 1);
   int32_t* col = ds.col.reserve_n<int32_t>(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
-  double* val = ds.val.reserve_n<double>(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+  double* val = ds.value_free ? nullptr : ds.val.reserve_n<double>(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
   k_row_ptr<<<grid_for(n + 1), kT, 0, s>>>(ka, nnz, n, rp);
   k_csr_fill<<<grid_for(n * 32), kT, 0, s>>>(ka, rp, n, col, val);
+  if (ds.value_free)
+    k_row_degrees<<<grid_for(n), kT, 0, s>>>(rp, n, ds.degree.reserve_n<int32_t>(static_cast<size_t>(n)));
   GGB_LAUNCH_CHECK();
   GGB_CUDA(cudaStreamSynchronize(s));
   keys_a.release();
@@ -410,10 +422,10 @@ void build_shard_device(Ctx& ctx, int64_t n, const DevDataset& ds, int64_t r0, i
   GGB_CUDA(cudaStreamSynchronize(s));
   sh.nnz = nnz;
   int32_t* ocol = sh.col.reserve_n<int32_t>(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
-  double* oval = sh.val.reserve_n<double>(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+  double* oval = ds.value_free ? nullptr : sh.val.reserve_n<double>(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
   if (rows > 0)
-    k_shard_fill<<<grid_for(rows * 32), kT, 0, s>>>(ds.col.as<int32_t>(), ds.val.as<double>(), rows, lo, orp, ocol,
-                                                     oval);
+    k_shard_fill<<<grid_for(rows * 32), kT, 0, s>>>(ds.col.as<int32_t>(), oval ? ds.val.as<double>() : nullptr, rows,
+                                                     lo, orp, ocol, oval);
   GGB_LAUNCH_CHECK();
   GGB_CUDA(cudaStreamSynchronize(s));
   ctx.launches += 3;

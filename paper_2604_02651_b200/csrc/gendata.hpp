@@ -12,6 +12,10 @@ namespace ggb {
 struct DevDataset {
   int64_t n = 0, d_in = 0, n_classes = 0, nnz = 0;
   DevBuf row_ptr, col, val, features, labels, split;
+  // value-free CSR: no fp64 value array; the row degrees (self-loop included)
+  // give every value as 1 / sqrt(deg_u deg_v) (dataset.cpp:78-79), exactly
+  bool value_free = false;
+  DevBuf degree;  // int32 [n]
 };
 
 void generate_synthetic_device(Ctx& ctx, int64_t n, double avg_degree, int64_t d_in, int64_t n_classes,

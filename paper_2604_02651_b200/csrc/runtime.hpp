@@ -157,6 +157,10 @@ struct Graph {
   bool features_on_host() const { return features_host.p != nullptr; }
   DevBuf labels;                     // int32 [n]
   DevBuf split;                      // uint8 [n] SplitTag (dataset.hpp:12), for evaluation
+  // value-free shards (no fp64 value arrays): values recomputed from the
+  // full-graph row degrees, 1 / sqrt(deg_u deg_v) in IEEE fp64 (dataset.cpp:78-79)
+  bool value_free = false;
+  DevBuf degree;                     // int32 [n] when value_free
   size_t device_bytes = 0;
 };
 

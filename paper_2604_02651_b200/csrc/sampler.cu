@@ -208,7 +208,7 @@ __global__ void k_extract_count(int64_t nr, const int64_t* __restrict__ sample, 
 __global__ void k_extract_fill(int64_t nr, const int64_t* __restrict__ sample, int64_t row_lo,
                                int64_t shard_r0, const int64_t* __restrict__ srp,
                                const int32_t* __restrict__ scol, const double* __restrict__ sval,
-                               const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ wpfx,
+                               const int32_t* __restrict__ deg, const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ wpfx,
                                int64_t col_lo, double p, const int64_t* __restrict__ row_ptr,
                                int32_t* __restrict__ col_out, float* __restrict__ val_out,
                                double* __restrict__ val64_out) {
@@ -234,7 +234,10 @@ __global__ void k_extract_fill(int64_t nr, const int64_t* __restrict__ sample, i
       const int64_t dst = pos + __popc(mask & lt);
       const int64_t rk = wpfx[col >> 5] + __popc(word & ((1u << (col & 31)) - 1u));
       col_out[dst] = static_cast<int32_t>(rk - col_lo);
-      double x = sval[k];
+      // value-free shards: the normalized value from the two row degrees
+      // (dataset.cpp:78-79; IEEE fp64 multiply, sqrt and divide, so exact)
+      double x = deg ? __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(static_cast<double>(deg[v]), static_cast<double>(deg[col]))))
+                     : sval[k];
       if (v != static_cast<int64_t>(col)) x = x / p;
       val_out[dst] = static_cast<float>(x);
       val64_out[dst] = x;
@@ -419,7 +422,7 @@ void extract_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int6
   (void)n;
 }
 
-void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t row_lo,
+void fill_block(Ctx& ctx, const PlaneShard& sh, const int32_t* deg, const int64_t* d_sample, int64_t row_lo,
                 int64_t col_lo, int64_t b, int64_t n, BatchCsr& out, int64_t cap) {
   out.col.reserve_n<int32_t>(cap);
   out.val.reserve_n<float>(cap);
@@ -428,7 +431,7 @@ void fill_block(Ctx& ctx, const PlaneShard& sh, const int64_t* d_sample, int64_t
   const double p = static_cast<double>(b - 1) / static_cast<double>(n - 1);  // shardsample.cpp:116
   k_extract_fill<<<blocks(out.n_rows, kThreads / 32), kThreads, 0, ctx.stream>>>(
       out.n_rows, d_sample, row_lo, sh.r0, sh.row_ptr.as<int64_t>(), sh.col.as<int32_t>(),
-      sh.val.as<double>(), ctx.sw.bitmap.as<uint32_t>(), ctx.sw.wpfx.as<int32_t>(), col_lo, p,
+      sh.val.as<double>(), deg, ctx.sw.bitmap.as<uint32_t>(), ctx.sw.wpfx.as<int32_t>(), col_lo, p,
       out.row_ptr.as<int64_t>(), out.col.as<int32_t>(), out.val.as<float>(), out.val64.as<double>());
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
@@ -618,7 +621,8 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     for (size_t k = 0; k < nk; ++k) cap[k] = bt.csrs[k].nnz + bt.csrs[k].nnz / 16 + 1024;  // headroom for later steps
   }
   for (size_t k = 0; k < nk; ++k)
-    fill_block(ctx, g.shards[keys[k].shard], d_sample, keys[k].rl, keys[k].cl, b, g.n, bt.csrs[k], cap[k]);
+    fill_block(ctx, g.shards[keys[k].shard], g.value_free ? g.degree.as<int32_t>() : nullptr, d_sample, keys[k].rl,
+               keys[k].cl, b, g.n, bt.csrs[k], cap[k]);
 
   if (gather_aside) {  // join the PCIe gather
     GGB_CUDA(cudaEventRecord(ctx.sw.aux.join, ctx.sw.aux.s));
