@@ -106,7 +106,9 @@ __device__ __forceinline__ void f4(const float4& a, float* v) {
   v[3] = a.w;
 }
 
-template <int J, bool Full>  // chunks of 128 columns held per row; Full: cols == 128 J
+// chunks of 128 columns held per row; Full: cols == 128 J; kLayer: the layer
+// API's instance (RMSNorm without ReLU, optional mask output)
+template <int J, bool Full, bool kLayer>
 __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
   // Warp per row (grid-stride, so a capped grid also works), gamma and the
   // per-lane constants held across rows.
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         y[j][i] = p.gamma ? g[j][i] * x[j][i] * inv : x[j][i];
-        if ((p.no_relu || y[j][i] > 0.f) && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
+        if (((kLayer && p.no_relu) || y[j][i] > 0.f) && (Full || c + i < ncols)) posm |= 1u << (4 * j + i);
       }
     }
     uint32_t keepm = posm;
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
         }
       }
     }
-    if (p.mask && lane < 4 * nj) p.mask[r * p.ldm + lane] = myword;
+    if ((!kLayer || p.mask) && lane < 4 * nj) p.mask[r * p.ldm + lane] = myword;
   }
 }
 
@@ -307,7 +309,10 @@ __global__ void __launch_bounds__(kT) k_bwd_row_stats(BwdApply p) {
 // dx = gamma*dxn/r - x*s/(d r^3) (bf16 out); dgamma_j += dxn*x/r accumulated
 // per lane over the block's rows (grid-stride), then reduced across the
 // block's warps into dgamma_part[block][cols].
-template <int J>
+// kLayer: the layer API's parallel_rmsnorm_bwd / element-wise backward
+// (fp32 dx, optional mask); the training step's instance (bf16 dx, mask
+// always present) keeps its own code generation.
+template <int J, bool kLayer>
 __global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
   constexpr int kMaxJ = J;
   __shared__ float sh[kRowsPerBlock][kMaxJ * kRowChunk];
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
     for (int h = 0; h < R; ++h) {
       const int64_t r = r0 + h * stride;
       if (r >= p.rows) break;
-      const uint32_t* mrow = p.mask ? p.mask + r * p.ldm : nullptr;
+      const uint32_t* mrow = (!kLayer || p.mask) ? p.mask + r * p.ldm : nullptr;
 #pragma unroll
       for (int j = 0; j < kMaxJ; ++j) {
         if (j >= nj) break;
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
         f4(ld4(p.x + r * p.ldx, c, p.cols), xr[h][j]);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          dxr[h][j][i] = (!p.mask || ((mrow[4 * j + i] >> lane) & 1u)) ? dy[i] * p.keep_scale : 0.f;
+          dxr[h][j][i] = ((kLayer && !mrow) || ((mrow[4 * j + i] >> lane) & 1u)) ? dy[i] * p.keep_scale : 0.f;
       }
     }
 #pragma unroll
@@ -387,8 +392,10 @@ __global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) dx[i] = dxn[j][i];
       }
-      if (p.dxb) st4_bf16(p.dxb + r * p.lddxb, c, p.cols, dx);
-      if (p.dxf) st4(p.dxf + r * p.lddxf, c, p.cols, dx);
+      if constexpr (kLayer)
+        st4(p.dxf + r * p.lddxf, c, p.cols, dx);
+      else
+        st4_bf16(p.dxb + r * p.lddxb, c, p.cols, dx);
     }
     }
   }
@@ -516,8 +523,8 @@ inline unsigned row_blocks(int64_t rows) { return static_cast<unsigned>(ceil_div
 
 }  // namespace
 
-template <int J, bool Full>
-void launch_fwd_row(Ctx& ctx, const FwdApply& p) {
+template <int J, bool Full, bool kLayer>
+void launch_fwd_row_k(Ctx& ctx, const FwdApply& p) {
   // a warp per row: the row's load latency is hidden by the other resident
   // warps rather than by a software pipeline. GGB_FWD_ROW_BPS=b caps the grid
   // at b blocks per SM striding over the rows (measured slower: 4 -> 1.76
@@ -528,7 +535,16 @@ void launch_fwd_row(Ctx& ctx, const FwdApply& p) {
   }();
   int64_t g = ceil_div(p.rows, kRowsPerBlock);
   if (bps > 0) g = std::min<int64_t>(g, static_cast<int64_t>(bps) * ctx.num_sms);
-  k_fwd_row<J, Full><<<static_cast<unsigned>(std::max<int64_t>(1, g)), kT, 0, ctx.stream>>>(p);
+  k_fwd_row<J, Full, kLayer><<<static_cast<unsigned>(std::max<int64_t>(1, g)), kT, 0, ctx.stream>>>(p);
+}
+
+template <int J, bool Full>
+void launch_fwd_row(Ctx& ctx, const FwdApply& p) {
+  if (p.no_relu || !p.mask) {
+    launch_fwd_row_k<J, Full, true>(ctx, p);
+    return;
+  }
+  launch_fwd_row_k<J, Full, false>(ctx, p);
 }
 
 void fwd_apply(Ctx& ctx, const FwdApply& p) {
@@ -575,12 +591,20 @@ void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks) {
   if (p.rows <= 0) return;
   require(p.cols <= kMaxJ * kRowChunk, "row kernels: at most 512 local feature columns");
   require(p.lddy % 4 == 0 && p.ldx % 4 == 0, "row kernels: fp32 rows must be 16-byte aligned");
-  if (p.cols <= kRowChunk)
-    k_bwd_row<1><<<blocks, kT, 0, ctx.stream>>>(p);
+  if (p.dxf) {
+    require(!p.dxb, "row kernels: one dx format per call");
+    if (p.cols <= kRowChunk)
+      k_bwd_row<1, true><<<blocks, kT, 0, ctx.stream>>>(p);
+    else if (p.cols <= 2 * kRowChunk)
+      k_bwd_row<2, true><<<blocks, kT, 0, ctx.stream>>>(p);
+    else
+      k_bwd_row<kMaxJ, true><<<blocks, kT, 0, ctx.stream>>>(p);
+  } else if (p.cols <= kRowChunk)
+    k_bwd_row<1, false><<<blocks, kT, 0, ctx.stream>>>(p);
   else if (p.cols <= 2 * kRowChunk)
-    k_bwd_row<2><<<blocks, kT, 0, ctx.stream>>>(p);
+    k_bwd_row<2, false><<<blocks, kT, 0, ctx.stream>>>(p);
   else
-    k_bwd_row<kMaxJ><<<blocks, kT, 0, ctx.stream>>>(p);
+    k_bwd_row<kMaxJ, false><<<blocks, kT, 0, ctx.stream>>>(p);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
 }
