@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(kT) k_bwd_row_stats(BwdApply p) {
 // kLayer: the layer API's parallel_rmsnorm_bwd / element-wise backward
 // (fp32 dx, optional mask); the training step's instance (bf16 dx, mask
 // always present) keeps its own code generation.
-template <int J, bool kLayer, int RR = (J == 1 ? 2 : 1)>
-__global__ void __launch_bounds__(kT, J <= 2 ? (J == 2 && RR == 2 ? 3 : 4) : 2) k_bwd_row(BwdApply p) {
+template <int J, bool kLayer>
+__global__ void __launch_bounds__(kT, J <= 2 ? 4 : 2) k_bwd_row(BwdApply p) {
   constexpr int kMaxJ = J;
   __shared__ float sh[kRowsPerBlock][kMaxJ * kRowChunk];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kT, J <= 2 ? (J == 2 && RR == 2 ? 3 : 4) : 2) 
   // row's reductions) to double the warp's memory-level parallelism; wider
   // rows already hold enough loads in flight and need the registers for
   // occupancy
-  constexpr int R = RR;
+  constexpr int R = J == 1 ? 2 : 1;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kRowsPerBlock;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRowsPerBlock + wib; r0 < p.rows; r0 += R * stride) {
     float dxr[R][kMaxJ][4], xr[R][kMaxJ][4];
@@ -601,16 +601,8 @@ void bwd_apply(Ctx& ctx, const BwdApply& p, int blocks) {
       k_bwd_row<kMaxJ, true><<<blocks, kT, 0, ctx.stream>>>(p);
   } else if (p.cols <= kRowChunk)
     k_bwd_row<1, false><<<blocks, kT, 0, ctx.stream>>>(p);
-  else if (p.cols <= 2 * kRowChunk) {
-    static const bool r2 = [] {  // GGB_BWD_R2=1: two rows per warp iteration at 256 columns
-      const char* e = std::getenv("GGB_BWD_R2");
-      return e && e[0] == '1';
-    }();
-    if (r2)
-      k_bwd_row<2, false, 2><<<blocks, kT, 0, ctx.stream>>>(p);
-    else
-      k_bwd_row<2, false><<<blocks, kT, 0, ctx.stream>>>(p);
-  }
+  else if (p.cols <= 2 * kRowChunk)  // (two rows per iteration here measured 2.1x slower: spills at 3 blocks/SM)
+    k_bwd_row<2, false><<<blocks, kT, 0, ctx.stream>>>(p);
   else
     k_bwd_row<kMaxJ, false><<<blocks, kT, 0, ctx.stream>>>(p);
   GGB_LAUNCH_CHECK();
