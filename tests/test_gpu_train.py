@@ -427,3 +427,42 @@ def test_prefetched_batch_is_stale_after_next(gg, orc):
     pf.close()
     with pytest.raises(gg.StaleBatch):
         b1.sample
+
+
+# Edge cases the reference handles (sampling.cpp:12-13, shardsample.cpp:114-115,
+# 127-128): the smallest batch (b = 2: p = 1/(n-1)), the whole graph (b = n:
+# p = 1, the evaluation batch's shape), a graph with no edges (self-loops
+# only: every block is diagonal), and hubs with isolated vertices (R-MAT-like).
+@pytest.mark.parametrize("n,deg,b", [(50, 4.0, 2), (300, 6.0, 300), (400, 0.0, 100), (64, 30.0, 17)])
+def test_edge_case_batches_match_reference(gg, orc, ref, n, deg, b):
+    d_in, ncls, seed, step = 6, 3, 2, 1
+    cfg_kw = dict(layers=3, d_h=32, dropout_rate=0.1)
+    ds, h, ctx, g = _setup(gg, orc, ref, n, deg, d_in, ncls, 5, 3)
+    try:
+        gs = gg.hash_combine(seed, 0)
+        batch = gg.build_step_batch(ctx, g, b, gs, step)
+        want = ref.step_batch(h, (1, 1, 1, 1), 0, 3, b, gs, step)
+        assert np.array_equal(batch.sample, want["sample"])
+        for p in range(3):
+            mine, w = batch.a(p), want["planes"][p][0]["csr"]
+            assert np.array_equal(mine.row_ptr, w.row_ptr) and np.array_equal(mine.col_idx, w.col_idx)
+            assert np.array_equal(mine.values.view(np.uint64), w.values.view(np.uint64))
+        st = gg.init_state(ctx, gg.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), seed)
+        loss = gg.train_step(ctx, st, batch, gg.FP32, seed, step)
+        losses, _, grads, _ = ref.train(h, (1, 1, 1, 1), orc.ModelConfig(d_in=d_in, d_out=ncls, **cfg_kw), b, seed,
+                                        step0=step)
+        assert abs(loss - losses[0]) <= LOSS_RTOL * abs(losses[0])
+        for name, mine, want_g in zip(st.cfg.param_names(), st.grads(), grads):
+            assert _rel(mine, want_g) <= GRAD_RTOL, (name, _rel(mine, want_g))
+    finally:
+        ref.free_dataset(h)
+
+
+def test_batch_size_errors(gg, orc):
+    """std::invalid_argument for b outside [2, n] (shardsample.cpp:127-128)."""
+    ds = orc.generate_synthetic(100, 4.0, 4, 2, 1)
+    ctx = gg.Context()
+    g = gg.Graph.from_csr(ctx, 100, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, 2, 2)
+    for b in (1, 0, 101):
+        with pytest.raises(gg.InvalidArgument):
+            gg.build_step_batch(ctx, g, b, 1, 0)
