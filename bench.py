@@ -519,6 +519,10 @@ def main():
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "bf16",
+        "dtype_detail": ("forward: split-bf16 tcgen05 GEMMs (hi+lo operands, 3 MMAs, fp32 accumulate: ~2^-16 relative) "
+                         "and fp32 SpMM gathers, fp32 activations; backward: bf16 operands, fp32 accumulate; "
+                         "sampling / CSR integer-exact with fp64 values; Adam in fp64"
+                         if args.compute == "accurate" else "bf16 operands throughout, fp32 accumulate"),
         "data": "synthetic",
         "config": {
             "workload": cfg["workload"], "config_id": args.config, "global_batch": b * gd,
