@@ -182,14 +182,14 @@ __global__ void k_extract_count(int64_t nr, const int64_t* __restrict__ sample, 
     const int64_t v = sample[row_lo + w];
     const int64_t e0 = srp[v - shard_r0], e1 = srp[v - shard_r0 + 1];
     int32_t c = 0;
-    for (int64_t e = e0; e < e1; e += 32) {
-      const int64_t k = e + lane;
-      bool keep = false;
-      if (k < e1) {
-        const int32_t col = scol[k];
-        keep = (__ldg(bitmap + (col >> 5)) >> (col & 31)) & 1u;
-      }
-      c += __popc(__ballot_sync(0xffffffffu, keep));
+    // 64 entries per iteration (two per lane), all loads issued before the
+    // ballots: the col -> bitmap chain is paid once per 64 entries
+    for (int64_t e = e0; e < e1; e += 64) {
+      const int64_t k0 = e + lane, k1 = k0 + 32;
+      const int32_t c0 = k0 < e1 ? scol[k0] : -1, c1 = k1 < e1 ? scol[k1] : -1;
+      const uint32_t w0 = c0 >= 0 ? __ldg(bitmap + (c0 >> 5)) : 0u, w1 = c1 >= 0 ? __ldg(bitmap + (c1 >> 5)) : 0u;
+      const bool keep0 = c0 >= 0 && ((w0 >> (c0 & 31)) & 1u), keep1 = c1 >= 0 && ((w1 >> (c1 & 31)) & 1u);
+      c += __popc(__ballot_sync(0xffffffffu, keep0)) + __popc(__ballot_sync(0xffffffffu, keep1));
     }
     if (lane == 0) cnt[w] = c;
     ext = static_cast<unsigned long long>(e1 - e0);
@@ -219,30 +219,28 @@ __global__ void k_extract_fill(int64_t nr, const int64_t* __restrict__ sample, i
   const int64_t e0 = srp[v - shard_r0], e1 = srp[v - shard_r0 + 1];
   int64_t pos = row_ptr[w];
   const uint32_t lt = (1u << lane) - 1u;
-  for (int64_t e = e0; e < e1; e += 32) {
-    const int64_t k = e + lane;
-    bool keep = false;
-    int32_t col = 0;
-    uint32_t word = 0;
-    if (k < e1) {
-      col = scol[k];
-      word = __ldg(bitmap + (col >> 5));
-      keep = (word >> (col & 31)) & 1u;
-    }
-    const uint32_t mask = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      const int64_t dst = pos + __popc(mask & lt);
-      const int64_t rk = wpfx[col >> 5] + __popc(word & ((1u << (col & 31)) - 1u));
-      col_out[dst] = static_cast<int32_t>(rk - col_lo);
-      // value-free shards: the normalized value from the two row degrees
-      // (dataset.cpp:78-79; IEEE fp64 multiply, sqrt and divide, so exact)
-      double x = deg ? __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(static_cast<double>(deg[v]), static_cast<double>(deg[col]))))
-                     : sval[k];
-      if (v != static_cast<int64_t>(col)) x = x / p;
-      val_out[dst] = static_cast<float>(x);
-      val64_out[dst] = x;
-    }
-    pos += __popc(mask);
+  const double dv = deg ? static_cast<double>(deg[v]) : 0.0;
+  // 64 entries per iteration (two per lane, loads hoisted), in CSR order:
+  // entries k0 = e + lane first, then k1 = e + 32 + lane
+  auto emit = [&](int64_t k, int32_t col, uint32_t word, int64_t dst) {
+    const int64_t rk = wpfx[col >> 5] + __popc(word & ((1u << (col & 31)) - 1u));
+    col_out[dst] = static_cast<int32_t>(rk - col_lo);
+    // value-free shards: the normalized value from the two row degrees
+    // (dataset.cpp:78-79; IEEE fp64 multiply, sqrt and divide, so exact)
+    double x = deg ? __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(dv, static_cast<double>(deg[col])))) : sval[k];
+    if (v != static_cast<int64_t>(col)) x = x / p;
+    val_out[dst] = static_cast<float>(x);
+    val64_out[dst] = x;
+  };
+  for (int64_t e = e0; e < e1; e += 64) {
+    const int64_t k0 = e + lane, k1 = k0 + 32;
+    const int32_t c0 = k0 < e1 ? scol[k0] : -1, c1 = k1 < e1 ? scol[k1] : -1;
+    const uint32_t w0 = c0 >= 0 ? __ldg(bitmap + (c0 >> 5)) : 0u, w1 = c1 >= 0 ? __ldg(bitmap + (c1 >> 5)) : 0u;
+    const bool keep0 = c0 >= 0 && ((w0 >> (c0 & 31)) & 1u), keep1 = c1 >= 0 && ((w1 >> (c1 & 31)) & 1u);
+    const uint32_t m0 = __ballot_sync(0xffffffffu, keep0), m1 = __ballot_sync(0xffffffffu, keep1);
+    if (keep0) emit(k0, c0, w0, pos + __popc(m0 & lt));
+    if (keep1) emit(k1, c1, w1, pos + __popc(m0) + __popc(m1 & lt));
+    pos += __popc(m0) + __popc(m1);
   }
 }
 
