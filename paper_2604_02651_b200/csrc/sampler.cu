@@ -638,7 +638,9 @@ void build_step_batch(Ctx& ctx, const Graph& g, int64_t b, uint64_t group_seed, 
     double bytes = 8.0 * b * 4 + (g.n / 32.0) * 12;
     for (size_t k = 0; k < nk; ++k) {
       const BatchCsr& c = bt.csrs[k];
-      bytes += c.n_rows * 16.0 * 2 + static_cast<double>(tot[nk + k]) * 4.0 * 2 + c.nnz * (8.0 + 4 + 4 + 8);
+      // per kept entry: the value read (fp64, or a 4-byte degree when value-free), int32 col + fp32 + fp64 writes
+      bytes += c.n_rows * 16.0 * 2 + static_cast<double>(tot[nk + k]) * 4.0 * 2 +
+               c.nnz * ((g.value_free ? 4.0 : 8.0) + 4 + 4 + 8);
     }
     bytes += static_cast<double>(bt.x_r1 - bt.x_r0) * (bt.x_c1 - bt.x_c0) * (4 + 2 + 2) + b * 12.0;
     prof.bytes = bytes;
