@@ -251,6 +251,11 @@ int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, int32_t pre
                    uint64_t run_seed, uint64_t global_step, double rmsnorm_eps, float* loss_out);
 /* device-side loss of the last train_step (one float) */
 int ggb_last_loss_device(ggb_state_t st, const float** dev_ptr);
+/* Enqueues the device->host copy of the last train_step's loss into host_dst
+ * (pinned host memory for a truly asynchronous copy) on the ctx stream and
+ * returns without waiting: the caller reads it after a later wait (a training
+ * loop that logs step t's loss while step t+1 runs). */
+int ggb_loss_to_host_async(ggb_ctx_t ctx, ggb_state_t st, float* host_dst);
 /* logits block of the last forward: dims = {r0, r1, c0, c1}; out may be NULL */
 int ggb_state_logits(ggb_state_t st, int64_t* dims, float* host_out);
 int ggb_forward(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t batch, int32_t precision,

@@ -118,6 +118,7 @@ _SIGS = [
     ("ggb_cross_entropy", C.c_int, [P, P, P, P, P]),
     ("ggb_batch_csr_block", C.c_int, [P, I32, I32, P]),
     ("ggb_loss", C.c_int, [P, P, P, P]),
+    ("ggb_loss_to_host_async", C.c_int, [P, P, P]),
     ("ggb_backward", C.c_int, [P, P, P, I32]),
     ("ggb_device_alloc", C.c_int, [P, C.c_size_t, P]),
     ("ggb_device_free", C.c_int, [P, P]),

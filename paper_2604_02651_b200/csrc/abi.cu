@@ -3,6 +3,9 @@
 // code; nothing throws across the ABI.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -44,9 +47,23 @@ void prof_collect(Ctx& ctx) {
   Prof& p = prof_of(ctx);
   if (p.marks.empty()) return;
   GGB_CUDA(cudaStreamSynchronize(ctx.stream));
+  // GGB_PROF_TRACE=<dir>: every timed range of this collect as a timeline row
+  // (class, start relative to the first range, duration, bytes) per rank
+  static const char* trace_dir = std::getenv("GGB_PROF_TRACE");
+  FILE* tf = nullptr;
+  if (trace_dir) {
+    GGB_CUDA(cudaDeviceSynchronize());
+    tf = std::fopen((std::string(trace_dir) + "/trace_rank" + std::to_string(ctx.rank) + ".txt").c_str(), "a");
+    if (tf) std::fprintf(tf, "# collect\n");
+  }
   for (auto& m : p.marks) {
     float ms = 0.f;
     GGB_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+    if (tf) {
+      float t0 = 0.f;
+      cudaEventElapsedTime(&t0, p.marks.front().a, m.a);
+      std::fprintf(tf, "%d %.4f %.4f %.0f\n", m.cat, t0, ms, m.bytes);
+    }
     p.ms[m.cat] += ms;
     p.bytes[m.cat] += m.bytes;
     p.flops[m.cat] += m.flops;
@@ -54,6 +71,7 @@ void prof_collect(Ctx& ctx) {
     p.pool.push_back(m.a);
     p.pool.push_back(m.b);
   }
+  if (tf) std::fclose(tf);
   p.marks.clear();
 }
 
@@ -947,6 +965,16 @@ int ggb_train_step(ggb_ctx_t ctx, ggb_state_t st, ggb_batch_t bt, int32_t precis
       sync_stream(*ctx, ctx->stream);  // with the collective watchdog
       ctx->d2h_bytes += sizeof(float);
     }
+  });
+}
+
+int ggb_loss_to_host_async(ggb_ctx_t ctx, ggb_state_t st, float* host_dst) {
+  return guard([&] {
+    use_device(*ctx);
+    contract(st->ctx == ctx && st->have_forward, "loss_to_host_async: no train_step of this state on this rank");
+    require(host_dst != nullptr, "loss_to_host_async: null destination");
+    GGB_CUDA(cudaMemcpyAsync(host_dst, st->loss.p, sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->d2h_bytes += sizeof(float);
   });
 }
 

@@ -95,6 +95,7 @@ Comm::~Comm() {
   if (cstream) cudaStreamDestroy(cstream);
   for (auto& a : axis)
     if (a) ncclCommDestroy(as_nccl(a));
+  if (pmm) ncclCommDestroy(as_nccl(pmm));
   if (world) ncclCommDestroy(as_nccl(world));
 }
 
@@ -105,6 +106,10 @@ void abort_all(Comm& c) {
       ncclCommAbort(as_nccl(a));
       a = nullptr;
     }
+  if (c.pmm) {
+    ncclCommAbort(as_nccl(c.pmm));
+    c.pmm = nullptr;
+  }
   if (c.world) {
     ncclCommAbort(as_nccl(c.world));
     c.world = nullptr;
@@ -122,9 +127,13 @@ void sync_stream(Ctx& ctx, cudaStream_t s) {
   const auto t0 = std::chrono::steady_clock::now();
   for (int spin = 0;; ++spin) {
     const cudaError_t q = cudaStreamQuery(s);
+    if (peer_timed_out(c)) {  // a peer-memory reduction gave up waiting for a member
+      abort_all(c);
+      fail(GGB_ETIMEOUT, "collective timed out: not all group members arrived");
+    }
     if (q == cudaSuccess) return;
     if (q != cudaErrorNotReady) GGB_CUDA(q);
-    void* comms[5] = {c.world, c.axis[0], c.axis[1], c.axis[2], c.axis[3]};
+    void* comms[6] = {c.world, c.axis[0], c.axis[1], c.axis[2], c.axis[3], c.pmm};
     for (void* k : comms) {
       if (!k) continue;
       ncclResult_t st = ncclSuccess;
@@ -177,6 +186,12 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
     GGB_NCCL(ncclCommSplit(world, colour, co[a], &sub, &cfg));
     if (grid.dims[a] > 1) c->axis[a] = sub;
   }
+  {  // the DP group's PMM grid (peer-memory reshards)
+    const int p = grid.dims[1] * grid.dims[2] * grid.dims[3];
+    ncclComm_t sub = nullptr;
+    GGB_NCCL(ncclCommSplit(world, p > 1 ? co[0] : NCCL_SPLIT_NOCOLOR, rank % p, &sub, nullptr));
+    if (p > 1) c->pmm = sub;
+  }
   // NCCL connects point-to-point peers lazily, on their first send/recv; the
   // reshard's block permutation meets new peer pairs in later steps, so one
   // tiny exchange with every peer here keeps that setup (tens of ms) out of
@@ -199,6 +214,7 @@ std::unique_ptr<Comm> comm_create(const Grid& grid, int rank, const uint8_t* uid
     GGB_NCCL(ncclAllReduce(buf, buf, 1, ncclFloat32, ncclSum, world, nullptr));
     for (int a = 0; a < 4; ++a)
       if (c->axis[a]) GGB_NCCL(ncclAllReduce(buf, buf, 1, ncclFloat32, ncclSum, as_nccl(c->axis[a]), nullptr));
+    if (c->pmm) GGB_NCCL(ncclAllReduce(buf, buf, 1, ncclFloat32, ncclSum, as_nccl(c->pmm), nullptr));
     GGB_CUDA(cudaDeviceSynchronize());
     GGB_CUDA(cudaFree(buf));
   }

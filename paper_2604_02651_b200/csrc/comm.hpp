@@ -10,9 +10,23 @@
 
 namespace ggb {
 
+// One axis group's peer-memory state (peer.cu): this member's IPC-exported
+// [flag words | slot 0 | slot 1] buffer and every member's mapping of it.
+struct PeerAxis {
+  int g = 0, me = 0;
+  size_t cap = 0;                // bytes per slot
+  char* base = nullptr;          // this member's buffer
+  char* rbase[8] = {};           // member q's buffer as mapped here (rbase[me] = base)
+  uint64_t epoch = 0;            // reductions issued on this axis
+  int* err = nullptr;            // mapped host word: a peer never arrived
+  int* err_dev = nullptr;
+  ~PeerAxis();
+};
+
 struct Comm {
   void* world = nullptr;     // ncclComm_t
   void* axis[4] = {};        // ncclComm_t per axis (null for singleton groups)
+  void* pmm = nullptr;       // ncclComm_t of this rank's DP group (X*Y*Z ranks; null when 1)
   int size[4] = {1, 1, 1, 1};
   int pos[4] = {0, 0, 0, 0};  // coordinate on the axis
   DevBuf gather;             // all-gather staging
@@ -31,6 +45,10 @@ struct Comm {
   cudaEvent_t gfork = nullptr, gjoin = nullptr;
   DevBuf gwire, ggather;
   bool gpending = false;
+  // peer-memory reductions per axis: 0 not probed, 1 on, -1 unavailable
+  // (index 4: the DP group's PMM grid, for the reshard's block permutation)
+  int peer_state[5] = {0, 0, 0, 0, 0};
+  std::unique_ptr<PeerAxis> peer[5];
   ~Comm();
 };
 
@@ -86,6 +104,42 @@ struct BlockXfer {
 };
 void exchange_blocks(Ctx& ctx, const std::vector<BlockXfer>& sends, const std::vector<BlockXfer>& recvs);
 void barrier(Ctx& ctx);
+
+// ---- peer-memory all-reduce over NVLink (peer.cu) ----------------------------
+// peer_ok: the axis group can sum through mapped peer memory (every member
+// on this node, IPC-mappable; GGB_PEER=0 disables; not for the NCCL-bf16
+// wire). The first call per axis is collective (a probe agreed by all).
+bool peer_ok(Ctx& ctx, int axis, int wire);
+// The slot the producer of the next peer_all_reduce on `axis` writes its
+// partial block into (collective when it has to grow).
+void* peer_slot(Ctx& ctx, int axis, size_t bytes);
+// The ordered sum 0 + p_0 + ... + p_{g-1} (axis order) of the members' slot
+// blocks (rows x cols, stride ld elements), written as fp32 (out, optionally
+// + add) and/or bf16 hi (+ lo = x - hi) operand copies. Partials are fp32, or
+// bf16 already rounded by their producer (src_bf16: the bf16 wire's
+// contributions, half the NVLink bytes); fp32 partials are rounded here under
+// GGB_BF16_WIRE — either way exactly kBf16Roundtrip (comm.hpp:271-303).
+void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld, bool src_bf16, int wire, float* out,
+                     int64_t ldo, bf16* outb, bf16* outlo, int64_t ldb, const float* add = nullptr,
+                     int64_t ldadd = 0);
+bool peer_timed_out(const Comm& c);
+// The reshard's block permutation through peer memory (group kPeerPmm, the
+// ranks of this DP group): every rank stages its source block (rows x cols,
+// packed with ld_stage) in its group slot, then pulls the pieces of its
+// destination block from the members' slots (one kernel, after every member
+// arrived). Pure copies, so bit-exact like exchange_blocks. reserve_bytes:
+// the largest staged block of the group (equal on every member).
+constexpr int kPeerPmm = 4;
+float* peer_stage(Ctx& ctx, const float* src, int64_t lds, int64_t rows, int64_t cols, int64_t ld_stage,
+                  size_t reserve_bytes);
+struct PeerPiece {
+  int member;       // position in the DP group (world rank mod X*Y*Z) of the provider
+  int64_t src_off;  // element offset of the piece in that member's staged block
+  int64_t lds;      // that block's ld_stage
+  float* dst;
+  int64_t ldd, rows, cols;
+};
+void peer_pull(Ctx& ctx, const std::vector<PeerPiece>& pieces);
 inline bool trivial(const Ctx& ctx, int axis) { return ctx.grid.dims[axis] == 1; }
 /// A contraction's all-reduce changes values here: a multi-member group, or a
 /// bf16 wire (which rounds even a single member's contribution, comm.hpp:135-145).

@@ -59,6 +59,30 @@ void reshard(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff, cons
   G.coord_of(me, mc);
   const Layout sl = sb.lay, dl = db.lay;
   const int s_rep = third_axis(sl);
+  if (peer_ok(ctx, kPeerPmm, GGB_FP32)) {
+    // through peer memory: stage the source block, pull the destination's pieces
+    size_t reserve = 0;  // the group's largest source block (same offsets on every member)
+    for (int i = 0; i + 1 < static_cast<int>(s_roff.size()); ++i)
+      for (int j = 0; j + 1 < static_cast<int>(s_coff.size()); ++j)
+        reserve = std::max(reserve, static_cast<size_t>((s_roff[i + 1] - s_roff[i]) * ld8(s_coff[j + 1] - s_coff[j])) * 4);
+    peer_stage(ctx, src, lds, sb.rows(), sb.cols(), ld8(sb.cols()), reserve);
+    const int psize = G.dims[1] * G.dims[2] * G.dims[3];
+    std::vector<PeerPiece> pieces;
+    for (int i = 0; i + 1 < static_cast<int>(s_roff.size()); ++i)
+      for (int j = 0; j + 1 < static_cast<int>(s_coff.size()); ++j) {
+        const Span r = meet(s_roff[i], s_roff[i + 1], db.r0, db.r1), c = meet(s_coff[j], s_coff[j + 1], db.c0, db.c1);
+        if (r.lo >= r.hi || c.lo >= c.hi) continue;
+        int pc[4] = {mc[0], mc[1], mc[2], mc[3]};
+        pc[sl.row] = i;
+        pc[sl.col] = j;
+        pc[s_rep] = mc[s_rep];
+        const int64_t ldp = ld8(s_coff[j + 1] - s_coff[j]);
+        pieces.push_back({G.rank_of(pc) % psize, (r.lo - s_roff[i]) * ldp + (c.lo - s_coff[j]), ldp,
+                          dst + (r.lo - db.r0) * ldd + (c.lo - db.c0), ldd, r.hi - r.lo, c.hi - c.lo});
+      }
+    peer_pull(ctx, pieces);
+    return;
+  }
   std::vector<BlockXfer> sends, recvs;
   // receives: pieces of my destination block
   for (int i = 0; i + 1 < static_cast<int>(s_roff.size()); ++i)
@@ -216,6 +240,25 @@ double gemm_bytes(int64_t m, int64_t n, int64_t k, int ea, int eb, int ec) {
   return static_cast<double>(m) * k * ea + static_cast<double>(n) * k * eb + static_cast<double>(m) * n * ec;
 }
 
+// A producer's partial block for peer_all_reduce (comm.hpp): fp32, or bf16
+// under the bf16 wire (the reference rounds every contribution to bf16 before
+// summing, so the producer's RNE output is exactly that contribution and half
+// the bytes cross NVLink).
+struct PeerPart {
+  void* p = nullptr;
+  bool b16 = false;
+  int64_t ld = 0;
+  float* f() const { return b16 ? nullptr : static_cast<float*>(p); }
+  bf16* h() const { return b16 ? static_cast<bf16*>(p) : nullptr; }
+};
+PeerPart peer_part(Ctx& ctx, int axis, int wire, int64_t rows, int64_t cols) {
+  PeerPart pp;
+  pp.b16 = wire == GGB_BF16_WIRE;
+  pp.ld = ld8(cols);
+  pp.p = peer_slot(ctx, axis, static_cast<size_t>(rows * pp.ld) * (pp.b16 ? 2 : 4));
+  return pp;
+}
+
 // C = A . W (forward contract): split-bf16 in the accurate mode, bf16 otherwise.
 void fwd_gemm(State& st, int64_t m, int64_t n, int64_t k, const Tensor& a, const ParamSlot& w, float* c,
               int64_t ldc, bf16* cb, int64_t ldcb, bf16* cl = nullptr) {
@@ -286,11 +329,19 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     xin.b = bt.x_in.as<bf16>();
     xin.lo = bt.x_in_lo.as<bf16>();
     xin.ldb = bt.x_ld;
+    if (ar && peer_ok(ctx, kInputFeatureLayout.col, wire)) {
+      // partial into the peer slot; the ordered sum lands in X0 (+ its bf16 copy)
+      const PeerPart pp = peer_part(ctx, kInputFeatureLayout.col, wire, ob.rows(), ob.cols());
+      fwd_gemm(st, ob.rows(), ob.cols(), w.blk.rows(), xin, w, pp.f(), pp.ld, pp.h(), pp.ld);
+      peer_all_reduce(ctx, kInputFeatureLayout.col, ob.rows(), ob.cols(), pp.ld, pp.b16, wire, st.x0.f, st.x0.ldf,
+                      want_b ? st.x0.b : nullptr, nullptr, st.x0.ldb);
+    } else {
     fwd_gemm(st, ob.rows(), ob.cols(), w.blk.rows(), xin, w, st.x0.f, st.x0.ldf, (ar || !want_b) ? nullptr : st.x0.b,
              st.x0.ldb);
     if (ar) {
       all_reduce_sum(ctx, kInputFeatureLayout.col, st.x0.f, ob.rows() * st.x0.ldf, wire);
       if (want_b) cast_bf16(ctx, st.x0.f, ob.rows(), ob.cols(), st.x0.ldf, st.x0.b, st.x0.ldb);
+    }
     }
   }
   const bool accurate = st.compute == kAccurate;
@@ -344,7 +395,22 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     } else {
     const int32_t* acol = A.col.as<int32_t>();
     const float* aval = A.val.as<float>();
-    if (ar_h) {
+    if (ar_h && peer_ok(ctx, alay.col, wire)) {
+      // partial sums over A's column blocks into the peer slot; the ordered
+      // sum is written as hagg's bf16 operand copies (no fp32 hagg, no cast pass)
+      const PeerPart pp = peer_part(ctx, alay.col, wire, A.n_rows, hb.cols());
+      {
+        ProfScope ps(ctx, kProfSpmmFwd, spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, pp.b16 ? 2 : 4),
+                     2.0 * A.nnz * F.cols());
+        if (accurate)
+          spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), pp.f(), pp.ld, pp.h(), nullptr,
+                       pp.ld, 0);
+        else
+          spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), pp.f(), pp.ld, pp.h(), pp.ld, 0);
+      }
+      peer_all_reduce(ctx, alay.col, A.n_rows, hb.cols(), pp.ld, pp.b16, wire, nullptr, 0, L.hagg.b, L.hagg.lo,
+                      L.hagg.ldb);
+    } else if (ar_h) {
       // partial sums over A's column blocks: row chunks of the SpMM pipelined
       // with their all-reduce (and the bf16 split of the reduced rows)
       L.hagg.ldf = ld8(hb.cols());
@@ -402,12 +468,19 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.xw_t.ldf = ld8(xb.cols());
     L.xw_t.f = grow<float>(L.xw, xb.rows() * L.xw_t.ldf);
     charge_all_reduce(ctx, hb.lay.col, xb.rows() * xb.cols(), wire_bytes(wire));  // contract (pmm.hpp:128)
+    if (reduces(ctx, hb.lay.col, wire) && peer_ok(ctx, hb.lay.col, wire)) {
+      const PeerPart pp = peer_part(ctx, hb.lay.col, wire, xb.rows(), xb.cols());
+      fwd_gemm(st, xb.rows(), xb.cols(), hb.cols(), L.hagg, w, pp.f(), pp.ld, pp.h(), pp.ld);
+      peer_all_reduce(ctx, hb.lay.col, xb.rows(), xb.cols(), pp.ld, pp.b16, wire, L.xw_t.f, L.xw_t.ldf, nullptr,
+                      nullptr, 0);
+    } else {
     pipelined_all_reduce(ctx, hb.lay.col, xb.rows(), 128, L.xw_t.f, L.xw_t.ldf, wire, [&](int64_t r0, int64_t r1) {
       Tensor sub = L.hagg;
       sub.b = L.hagg.b + r0 * L.hagg.ldb;
       sub.lo = L.hagg.lo ? L.hagg.lo + r0 * L.hagg.ldb : nullptr;
       fwd_gemm(st, r1 - r0, xb.cols(), hb.cols(), sub, w, L.xw_t.f + r0 * L.xw_t.ldf, L.xw_t.ldf, nullptr, 0);
     });
+    }
     // RMSNorm statistics: row sum of squares, all-reduce along the column axis (fp32)
     float* ss = nullptr;
     float* rms = nullptr;
@@ -615,10 +688,20 @@ void backward(State& st, const Batch& bt, int precision) {
     const ParamSlot& w = st.params[st.wout];
     ProfScope ps(ctx, kProfGemmDx, gemm_bytes(db.rows(), db.cols(), lb.cols(), 2, 2, 4),
                  2.0 * db.rows() * db.cols() * lb.cols());
+    charge_all_reduce(ctx, lb.lay.col, db.rows() * db.cols(), wire_bytes(wire));
+    if (reduces(ctx, lb.lay.col, wire) && peer_ok(ctx, lb.lay.col, wire)) {
+      const PeerPart pp = peer_part(ctx, lb.lay.col, wire, db.rows(), db.cols());
+      gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, pp.f(),
+                pp.ld, pp.h(), pp.ld);
+      ps.end();
+      peer_all_reduce(ctx, lb.lay.col, db.rows(), db.cols(), pp.ld, pp.b16, wire, dxh, ld8(db.cols()), nullptr,
+                      nullptr, 0);
+    } else {
     gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, dxh,
               ld8(db.cols()), nullptr, 0);
-    charge_all_reduce(ctx, lb.lay.col, db.rows() * db.cols(), wire_bytes(wire));
+    ps.end();
     all_reduce_sum(ctx, lb.lay.col, dxh, db.rows() * ld8(db.cols()), wire);
+    }
   }
   const bf16* pre_dhb = nullptr;  // layer 1 under pre-aggregation: dhagg_1 (bf16) and the residual gradient
   int64_t pre_ldhb = 0;
@@ -702,7 +785,12 @@ void backward(State& st, const Batch& bt, int precision) {
     bf16* dhb = grow<bf16>(st.dhagg_b, rows * ldhb);
     {
     ProfScope ps(ctx, kProfGemmDx, gemm_bytes(rows, hc, cols, 2, 2, ar_d ? 4 : 2), 2.0 * rows * hc * cols);
-    if (ar_d) {
+    if (ar_d && peer_ok(ctx, xb.lay.col, wire)) {
+      const PeerPart pp = peer_part(ctx, xb.lay.col, wire, rows, hc);
+      gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, pp.f(), pp.ld, pp.h(), pp.ld);
+      ps.end();
+      peer_all_reduce(ctx, xb.lay.col, rows, hc, pp.ld, pp.b16, wire, nullptr, 0, dhb, nullptr, ldhb);
+    } else if (ar_d) {
       ps.end();
       float* dhf = grow<float>(st.dhagg_f, rows * hc);
       pipelined_all_reduce(
@@ -745,6 +833,17 @@ void backward(State& st, const Batch& bt, int precision) {
       spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
                dxh, ld8(F.cols()), outb, ld8(F.cols()), 1);
       dxh_b_ready = emit_b;
+    } else if (peer_ok(ctx, alay.row, wire) && reduces(ctx, alay.row, wire)) {
+      // partial into the peer slot; ordered sum + residual gradient in one pass
+      float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
+      const int64_t ldn = ld8(F.cols());
+      const PeerPart pp = peer_part(ctx, alay.row, wire, At.n_rows, F.cols());
+      spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
+               pp.f(), pp.ld, pp.h(), pp.ld, 0);
+      ps.end();
+      peer_all_reduce(ctx, alay.row, At.n_rows, F.cols(), pp.ld, pp.b16, wire, nd, ldn, nullptr, nullptr, 0, dres, ldn);
+      std::swap(st.dxh, st.dxh2);
+      dxh = nd;
     } else {
       ps.end();
       float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));

@@ -684,6 +684,12 @@ def train_step(ctx: Context, st: ModelState, batch: StepBatch, prec: int, run_se
     return float(loss.value) if sync_loss else None
 
 
+def loss_to_host_async(ctx: Context, st: ModelState, host_dst_ptr: int) -> None:
+    """Enqueue the D2H copy of the last train_step's loss into pinned host
+    memory at host_dst_ptr without waiting (read it after a later wait)."""
+    check(lib().ggb_loss_to_host_async(ctx.h, st.h, C.c_void_p(host_dst_ptr)))
+
+
 @dataclass
 class EvalCounts:
     """EvalCounts (model.hpp:480-490): index 0 train, 1 val, 2 test."""

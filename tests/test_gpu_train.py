@@ -201,6 +201,30 @@ def test_prefetch_is_transparent(gg, orc):
     pf.close()
 
 
+def test_async_loss_readback_matches_sync(gg, orc):
+    """ggb_loss_to_host_async: the lagged loss copies of a step loop (the
+    bench's e2e pattern) equal the synchronous train_step losses."""
+    import torch
+    n, d_in, ncls, b, seed = 3000, 16, 5, 700, 4
+    ds = orc.generate_synthetic(n, 9.0, d_in, ncls, 8)
+    ctx = gg.Context()
+    g = gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features, ds.labels, ncls, 3)
+    cfg = gg.ModelConfig(layers=3, d_in=d_in, d_h=32, d_out=ncls, dropout_rate=0.2)
+    gs = gg.hash_combine(seed, 0)
+    st_a, st_b = gg.init_state(ctx, cfg, seed), gg.init_state(ctx, cfg, seed)
+    host = torch.zeros(5, dtype=torch.float32, pin_memory=True)
+    want, bt = [], None
+    for t in range(5):
+        bt = gg.build_step_batch(ctx, g, b, gs, t, reuse=bt)
+        gg.train_step(ctx, st_a, bt, gg.FP32, seed, t, sync_loss=False)
+        gg.loss_to_host_async(ctx, st_a, host.data_ptr() + 4 * t)
+        gg.optimizer_step(ctx, st_a, gg.ADAM, 1e-3)
+        want.append(gg.train_step(ctx, st_b, bt, gg.FP32, seed, t))
+        gg.optimizer_step(ctx, st_b, gg.ADAM, 1e-3)
+    ctx.synchronize()
+    assert host.tolist() == want
+
+
 def test_host_resident_features(gg, orc):
     """Features kept in host memory (the reference's Dataset) and gathered over
     PCIe per batch: bit-identical x_in and losses to the HBM-resident graph,
