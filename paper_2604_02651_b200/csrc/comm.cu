@@ -88,6 +88,9 @@ void need(const Ctx& ctx, int axis) {
 }  // namespace
 
 Comm::~Comm() {
+  if (rstream) cudaStreamDestroy(rstream);
+  if (rfork) cudaEventDestroy(rfork);
+  if (rjoin) cudaEventDestroy(rjoin);
   if (gstream) cudaStreamDestroy(gstream);
   if (gfork) cudaEventDestroy(gfork);
   if (gjoin) cudaEventDestroy(gjoin);
@@ -298,6 +301,45 @@ void all_reduce_sum_async(Ctx& ctx, int axis, float* buf, int64_t count, int wir
   GGB_CUDA(cudaStreamWaitEvent(c.gstream, c.gfork, 0));
   all_reduce_sum_on(ctx, axis, buf, count, wire, c.gstream, c.gwire, c.ggather);
   c.gpending = true;
+}
+
+void reshard_async(Ctx& ctx, const std::function<void()>& f) {
+  static const bool on = [] {
+    const char* e = std::getenv("GGB_ASYNC_RESHARD");
+    return !(e && e[0] == '0');
+  }();
+  Comm& c = *ctx.comm;
+  if (!on) {
+    f();
+    return;
+  }
+  if (!c.rstream) {
+    int lo = 0, hi = 0;
+    GGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GGB_CUDA(cudaStreamCreateWithPriority(&c.rstream, cudaStreamNonBlocking, hi));
+    GGB_CUDA(cudaEventCreateWithFlags(&c.rfork, cudaEventDisableTiming));
+    GGB_CUDA(cudaEventCreateWithFlags(&c.rjoin, cudaEventDisableTiming));
+  }
+  reshard_join(ctx);  // one reshard in flight at a time
+  GGB_CUDA(cudaEventRecord(c.rfork, ctx.stream));
+  GGB_CUDA(cudaStreamWaitEvent(c.rstream, c.rfork, 0));
+  cudaStream_t saved = ctx.stream;
+  ctx.stream = c.rstream;
+  try {
+    f();
+  } catch (...) {
+    ctx.stream = saved;
+    throw;
+  }
+  ctx.stream = saved;
+  GGB_CUDA(cudaEventRecord(c.rjoin, c.rstream));
+  c.rpending = true;
+}
+
+void reshard_join(Ctx& ctx) {
+  if (!ctx.comm || !ctx.comm->rpending) return;
+  GGB_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.comm->rjoin, 0));
+  ctx.comm->rpending = false;
 }
 
 void join_async(Ctx& ctx) {

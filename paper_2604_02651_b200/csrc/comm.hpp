@@ -46,6 +46,10 @@ struct Comm {
   DevBuf gwire, ggather;
   bool gpending = false;
   // peer-memory reductions per axis: 0 not probed, 1 on, -1 unavailable
+  // peer-memory reshards on their own stream beside the compute (reshard_join)
+  cudaStream_t rstream = nullptr;
+  cudaEvent_t rfork = nullptr, rjoin = nullptr;
+  bool rpending = false;
   // (index 4: the DP group's PMM grid, for the reshard's block permutation)
   int peer_state[5] = {0, 0, 0, 0, 0};
   std::unique_ptr<PeerAxis> peer[5];
@@ -140,6 +144,11 @@ struct PeerPiece {
   int64_t ldd, rows, cols;
 };
 void peer_pull(Ctx& ctx, const std::vector<PeerPiece>& pieces);
+// Runs f (peer_stage + peer_pull) on the reshard stream once the compute
+// stream's work so far is done; the compute stream goes on until
+// reshard_join. GGB_ASYNC_RESHARD=0 runs it inline.
+void reshard_async(Ctx& ctx, const std::function<void()>& f);
+void reshard_join(Ctx& ctx);
 inline bool trivial(const Ctx& ctx, int axis) { return ctx.grid.dims[axis] == 1; }
 /// A contraction's all-reduce changes values here: a multi-member group, or a
 /// bf16 wire (which rounds even a single member's contribution, comm.hpp:135-145).

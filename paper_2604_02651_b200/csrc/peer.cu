@@ -7,10 +7,12 @@
 // kernel, not a message exchange:
 //   * each member's producer (the SpMM / GEMM of pmm.hpp:128,165) writes its
 //     partial block straight into a slot of an IPC-exported buffer;
-//   * k_peer_reduce signals arrival into every peer's flag word, waits for
-//     theirs, and reads all g partials (its own from HBM, the others over
-//     NVLink) in axis order: out = 0 + p_0 + p_1 + ... — the reference's exact
-//     summation order for any g (NCCL's ring order is not);
+//   * k_peer_wait (one CTA) signals arrival into every peer's flag word and
+//     waits for theirs; k_peer_reduce then reads all g partials (its own from
+//     HBM, the others over NVLink) in axis order: out = 0 + p_0 + p_1 + ... —
+//     the reference's exact summation order for any g (NCCL's ring order is
+//     not). Only the one-CTA wait kernel ever spins, so a waiting rank never
+//     holds the SMs another stream's arrival kernel needs;
 //   * the consumer's format is written directly: fp32, bf16 hi (+ lo) operand
 //     copies for the next tcgen05 GEMM, or fp32 plus the residual gradient —
 //     the cast / add passes that follow an NCCL all-reduce are fused away.
@@ -37,11 +39,8 @@ constexpr int kMaxPeers = 8;
 constexpr size_t kFlagBytes = 4096;  // flag words at the head of each member's buffer
 
 struct ReduceArgs {
-  const void* src[kMaxPeers];          // partial block of member q (axis order)
-  unsigned long long* arrive[kMaxPeers];  // member q's flag word for this member
-  const unsigned long long* mine;      // this member's flag words [g]
-  int g, me, wire;
-  unsigned long long epoch, timeout_ns;
+  const void* src[kMaxPeers];  // partial block of member q (axis order)
+  int g, wire;
   int64_t rows, cols, ld;
   float* out;
   int64_t ldo;
@@ -50,7 +49,6 @@ struct ReduceArgs {
   int64_t ldb;
   const float* add;  // optional: out = sum + add (fp32 out only)
   int64_t ldadd;
-  int* err;  // mapped host word: a peer never arrived
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -110,6 +108,35 @@ __device__ __forceinline__ void put_bf16x4(bf16* p, const float* v) {
   *reinterpret_cast<uint2*>(p) = u;
 }
 
+// Arrival barrier of one peer collective: thread q < g posts this member's
+// arrival into member q's flag word, then waits for every member's arrival
+// in its own flag words (system-scope release / acquire; the partials
+// written by earlier kernels are published by the fence before the flag).
+// A wait beyond the deadline raises the mapped host error word and returns.
+struct WaitArgs {
+  unsigned long long* arrive[kMaxPeers];  // member q's flag word for this member
+  const unsigned long long* mine;         // this member's flag words [g]
+  int g, me;
+  unsigned long long epoch, timeout_ns;
+  int* err;
+};
+__global__ void __launch_bounds__(32) k_peer_wait(WaitArgs a) {
+  const int q = threadIdx.x;
+  if (q < a.g && q != a.me) {
+    __threadfence_system();
+    st_release_sys(a.arrive[q], a.epoch);
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(a.mine + q) < a.epoch) {
+      if (globaltimer() - t0 > a.timeout_ns) {
+        *reinterpret_cast<volatile int*>(a.err) = 1;
+        break;
+      }
+      __nanosleep(128);
+    }
+  }
+  __syncwarp();
+}
+
 // Grid-stride over the block's 16-byte units (row-major, so a warp reads
 // 512 contiguous bytes of every member); each thread issues the loads of U
 // units of every member before summing any, so enough NVLink reads are in
@@ -119,28 +146,6 @@ __global__ void __launch_bounds__(256) k_peer_reduce(ReduceArgs a) {
   constexpr int V = Vec<T>::V;
   constexpr int NG = G > 0 ? G : kMaxPeers;
   constexpr int U = G == 2 ? 4 : (G == 4 ? 2 : 1);
-  __shared__ int s_timeout;
-  if (blockIdx.x == 0 && threadIdx.x < a.g && static_cast<int>(threadIdx.x) != a.me) {
-    __threadfence_system();  // this member's partial (written by the previous kernel) before its flag
-    st_release_sys(a.arrive[threadIdx.x], a.epoch);
-  }
-  if (threadIdx.x == 0) {
-    s_timeout = 0;
-    const unsigned long long t0 = globaltimer();
-    for (int q = 0; q < a.g && !s_timeout; ++q) {
-      if (q == a.me) continue;
-      while (ld_acquire_sys(a.mine + q) < a.epoch) {
-        if (globaltimer() - t0 > a.timeout_ns) {
-          s_timeout = 1;
-          *reinterpret_cast<volatile int*>(a.err) = 1;
-          break;
-        }
-        __nanosleep(64);
-      }
-    }
-  }
-  __syncthreads();
-  if (s_timeout) return;
   const int n = G > 0 ? G : a.g;
   const uint32_t cv = static_cast<uint32_t>((a.cols + V - 1) / V);
   const uint32_t total = static_cast<uint32_t>(a.rows) * cv;
@@ -341,6 +346,23 @@ void* peer_slot(Ctx& ctx, int axis, size_t bytes) {
   return P.base + kFlagBytes + (e & 1) * P.cap;
 }
 
+namespace {
+// arrival barrier of collective e on the group (one CTA, ctx.stream)
+void launch_wait(Ctx& ctx, PeerAxis& P, uint64_t e) {
+  WaitArgs w{};
+  for (int q = 0; q < P.g; ++q) w.arrive[q] = reinterpret_cast<unsigned long long*>(P.rbase[q]) + P.me;
+  w.mine = reinterpret_cast<const unsigned long long*>(P.base);
+  w.g = P.g;
+  w.me = P.me;
+  w.epoch = e;
+  w.timeout_ns = static_cast<unsigned long long>(ctx.comm->timeout_ms) * 1000000ull;
+  w.err = P.err_dev;
+  k_peer_wait<<<1, 32, 0, ctx.stream>>>(w);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+}  // namespace
+
 void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld, bool src_bf16, int wire, float* out,
                      int64_t ldo, bf16* outb, bf16* outlo, int64_t ldb, const float* add, int64_t ldadd) {
   Comm& c = *ctx.comm;
@@ -352,16 +374,9 @@ void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld,
   require(rows * ld < (int64_t(1) << 32), "peer_all_reduce: block too large for 32-bit unit indices");
   const uint64_t e = ++P.epoch;
   ReduceArgs a{};
-  for (int q = 0; q < P.g; ++q) {
-    a.src[q] = P.rbase[q] + kFlagBytes + (e & 1) * P.cap;
-    a.arrive[q] = reinterpret_cast<unsigned long long*>(P.rbase[q]) + P.me;
-  }
-  a.mine = reinterpret_cast<const unsigned long long*>(P.base);
+  for (int q = 0; q < P.g; ++q) a.src[q] = P.rbase[q] + kFlagBytes + (e & 1) * P.cap;
   a.g = P.g;
-  a.me = P.me;
   a.wire = wire == GGB_BF16_WIRE ? 1 : 0;
-  a.epoch = e;
-  a.timeout_ns = static_cast<unsigned long long>(c.timeout_ms) * 1000000ull;
   a.rows = rows;
   a.cols = cols;
   a.ld = ld;
@@ -372,10 +387,10 @@ void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld,
   a.ldb = ldb;
   a.add = add;
   a.ldadd = ldadd;
-  a.err = P.err_dev;
   // bytes this member pulls over NVLink
   const double pulled = static_cast<double>(rows) * cols * (src_bf16 ? 2 : 4) * (P.g - 1);
   ProfScope ps(ctx, kProfComm, pulled, 0);
+  launch_wait(ctx, P, e);
   const int blocks = ctx.num_sms * 3;
   if (src_bf16) {
     if (P.g == 2)
@@ -412,50 +427,47 @@ struct PullArgs {
   PullPiece pc[kMaxPieces];
   int npieces;
   uint32_t total;
-  unsigned long long* arrive[kMaxPeers];
-  const unsigned long long* mine;
-  int g, me;
-  unsigned long long epoch, timeout_ns;
-  int* err;
 };
 
+// Grid-stride over the pieces' units; every thread issues U units' loads
+// (NVLink reads for remote pieces) before storing any.
 __global__ void __launch_bounds__(256) k_peer_pull(PullArgs a) {
-  __shared__ int s_timeout;
-  if (blockIdx.x == 0 && threadIdx.x < a.g && static_cast<int>(threadIdx.x) != a.me) {
-    __threadfence_system();
-    st_release_sys(a.arrive[threadIdx.x], a.epoch);
-  }
-  if (threadIdx.x == 0) {
-    s_timeout = 0;
-    const unsigned long long t0 = globaltimer();
-    for (int q = 0; q < a.g && !s_timeout; ++q) {
-      if (q == a.me) continue;
-      while (ld_acquire_sys(a.mine + q) < a.epoch) {
-        if (globaltimer() - t0 > a.timeout_ns) {
-          s_timeout = 1;
-          *reinterpret_cast<volatile int*>(a.err) = 1;
-          break;
-        }
-        __nanosleep(64);
+  constexpr int U = 4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < a.total; base += U * stride) {
+    float4 v[U];
+    float* dst[U];
+    int vec[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t t = base + u * stride;
+      dst[u] = nullptr;
+      vec[u] = 0;
+      if (t >= a.total) continue;
+      int k = 0;
+      while (k + 1 < a.npieces && a.pc[k + 1].unit0 <= t) ++k;
+      const PullPiece& p = a.pc[k];
+      const uint32_t i = t - p.unit0;
+      vec[u] = p.vec;
+      if (p.vec) {
+        const uint32_t cv = static_cast<uint32_t>(p.cols / 4);
+        const uint32_t r = i / cv, c = (i - r * cv) * 4;
+        v[u] = *reinterpret_cast<const float4*>(p.src + r * p.lds + c);
+        dst[u] = p.dst + r * p.ldd + c;
+      } else {
+        const uint32_t cc = static_cast<uint32_t>(p.cols);
+        const uint32_t r = i / cc, c = i - r * cc;
+        v[u].x = p.src[r * p.lds + c];
+        dst[u] = p.dst + r * p.ldd + c;
       }
     }
-  }
-  __syncthreads();
-  if (s_timeout) return;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.total; t += stride) {
-    int k = 0;
-    while (k + 1 < a.npieces && a.pc[k + 1].unit0 <= t) ++k;
-    const PullPiece& p = a.pc[k];
-    const uint32_t u = t - p.unit0;
-    if (p.vec) {
-      const uint32_t cv = static_cast<uint32_t>(p.cols / 4);
-      const uint32_t r = u / cv, c = (u - r * cv) * 4;
-      *reinterpret_cast<float4*>(p.dst + r * p.ldd + c) = *reinterpret_cast<const float4*>(p.src + r * p.lds + c);
-    } else {
-      const uint32_t cc = static_cast<uint32_t>(p.cols);
-      const uint32_t r = u / cc, c = u - r * cc;
-      p.dst[r * p.ldd + c] = p.src[r * p.lds + c];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!dst[u]) continue;
+      if (vec[u])
+        *reinterpret_cast<float4*>(dst[u]) = v[u];
+      else
+        *dst[u] = v[u].x;
     }
   }
 }
@@ -477,13 +489,6 @@ void peer_pull(Ctx& ctx, const std::vector<PeerPiece>& pieces) {
   PeerAxis& P = *c.peer[kPeerPmm];
   const uint64_t e = ++P.epoch;
   PullArgs a{};
-  for (int q = 0; q < P.g; ++q) a.arrive[q] = reinterpret_cast<unsigned long long*>(P.rbase[q]) + P.me;
-  a.mine = reinterpret_cast<const unsigned long long*>(P.base);
-  a.g = P.g;
-  a.me = P.me;
-  a.epoch = e;
-  a.timeout_ns = static_cast<unsigned long long>(c.timeout_ms) * 1000000ull;
-  a.err = P.err_dev;
   double bytes = 0;
   uint64_t units = 0;
   int np = 0;
@@ -511,8 +516,10 @@ void peer_pull(Ctx& ctx, const std::vector<PeerPiece>& pieces) {
   a.npieces = np;
   a.total = static_cast<uint32_t>(units);
   ProfScope ps(ctx, kProfComm, bytes, 0);
-  // every member launches (its arrival is what releases the others), even with nothing to pull
-  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms * 3, ceil_div(static_cast<int64_t>(units), 256))));
+  launch_wait(ctx, P, e);  // every member arrives, even with nothing to pull
+  if (units == 0) return;
+  const unsigned blocks = static_cast<unsigned>(
+      std::min<int64_t>(ctx.num_sms * 4, ceil_div(static_cast<int64_t>(units), 256 * 4)));
   k_peer_pull<<<blocks, 256, 0, ctx.stream>>>(a);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;

@@ -60,12 +60,12 @@ void reshard(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff, cons
   const Layout sl = sb.lay, dl = db.lay;
   const int s_rep = third_axis(sl);
   if (peer_ok(ctx, kPeerPmm, GGB_FP32)) {
-    // through peer memory: stage the source block, pull the destination's pieces
+    // through peer memory: stage the source block, pull the destination's
+    // pieces — on the reshard stream, joined by the consumer (reshard_join)
     size_t reserve = 0;  // the group's largest source block (same offsets on every member)
     for (int i = 0; i + 1 < static_cast<int>(s_roff.size()); ++i)
       for (int j = 0; j + 1 < static_cast<int>(s_coff.size()); ++j)
         reserve = std::max(reserve, static_cast<size_t>((s_roff[i + 1] - s_roff[i]) * ld8(s_coff[j + 1] - s_coff[j])) * 4);
-    peer_stage(ctx, src, lds, sb.rows(), sb.cols(), ld8(sb.cols()), reserve);
     const int psize = G.dims[1] * G.dims[2] * G.dims[3];
     std::vector<PeerPiece> pieces;
     for (int i = 0; i + 1 < static_cast<int>(s_roff.size()); ++i)
@@ -80,7 +80,10 @@ void reshard(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff, cons
         pieces.push_back({G.rank_of(pc) % psize, (r.lo - s_roff[i]) * ldp + (c.lo - s_coff[j]), ldp,
                           dst + (r.lo - db.r0) * ldd + (c.lo - db.c0), ldd, r.hi - r.lo, c.hi - c.lo});
       }
-    peer_pull(ctx, pieces);
+    reshard_async(ctx, [&] {
+      peer_stage(ctx, src, lds, sb.rows(), sb.cols(), ld8(sb.cols()), reserve);
+      peer_pull(ctx, pieces);
+    });
     return;
   }
   std::vector<BlockXfer> sends, recvs;
@@ -137,6 +140,7 @@ void reshard_block(Ctx& ctx, const Block& sb, const std::vector<int64_t>& s_roff
                    const float* src, int64_t lds, const Block& db, const std::vector<int64_t>& d_roff,
                    const std::vector<int64_t>& d_coff, float* dst, int64_t ldd) {
   reshard(ctx, sb, s_roff, s_coff, src, lds, db, d_roff, d_coff, dst, ldd);
+  reshard_join(ctx);
 }
 
 // ---- init_state (model.hpp:175-208) -------------------------------------------------
@@ -363,6 +367,29 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     const Layout alay = adjacency_layout(l);
     const Block& F = prev->blk;
     contract(alay.col == F.lay.row && A.c0 == F.r0 && A.c1 == F.r1, "spmm: inner partitions differ");
+    // residual: X_{l-1} resharded to feature_layout(l+1); issued first so a
+    // peer-memory reshard runs beside this layer's SpMM and GEMM (joined
+    // before the fused row kernel reads it)
+    const Layout out = feature_layout(l + 1);
+    const float* res = nullptr;
+    const uint8_t* resp = nullptr;  // X_{l-1} kept only as 24-bit rows
+    int64_t ldres = 0;
+    Block rb;
+    if (cfg.use_residual) {
+      rb = make_block(ctx, out, bt.b, H, bt.batch_off[out.row], hoff(ctx, H, out.col));
+      charge_reshard(ctx, F, out);
+      if (pmm_trivial(ctx)) {
+        res = prev->f;
+        ldres = prev->ldf;
+        if (!res) resp = prev->p;
+      } else {
+        float* r = grow<float>(st.dres, rb.rows() * ld8(rb.cols()));
+        reshard(ctx, F, bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), prev->f, prev->ldf, rb,
+                bt.batch_off[out.row], hoff(ctx, H, out.col), r, ld8(rb.cols()));
+        res = r;
+        ldres = ld8(rb.cols());
+      }
+    }
     // hagg = A . F -> (A.row, F.col), all-reduce A.col
     Block hb;
     hb.lay = {alay.row, F.lay.col};
@@ -499,28 +526,10 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
       contract(gp.blk.c0 == xb.c0 && gp.blk.c1 == xb.c1, "rmsnorm: gamma slice does not match the column block");
       gam = W + gp.off;
     }
-    // residual: X_{l-1} resharded to feature_layout(l+1)
-    const Layout out = feature_layout(l + 1);
-    const float* res = nullptr;
-    const uint8_t* resp = nullptr;  // X_{l-1} kept only as 24-bit rows
-    int64_t ldres = 0;
-    if (cfg.use_residual) {
-      Block rb = make_block(ctx, out, bt.b, H, bt.batch_off[out.row], hoff(ctx, H, out.col));
+    // residual X_{l-1} (resharded to feature_layout(l+1) at the top of the layer)
+    if (cfg.use_residual)
       contract(rb.r0 == xb.r0 && rb.r1 == xb.r1 && rb.c0 == xb.c0 && rb.c1 == xb.c1,
                "fused_elementwise: residual layout mismatch");
-      charge_reshard(ctx, F, out);
-      if (pmm_trivial(ctx)) {
-        res = prev->f;
-        ldres = prev->ldf;
-        if (!res) resp = prev->p;
-      } else {
-        float* r = grow<float>(st.dres, rb.rows() * ld8(rb.cols()));
-        reshard(ctx, F, bt.batch_off[F.lay.row], hoff(ctx, H, F.lay.col), prev->f, prev->ldf, rb,
-                bt.batch_off[out.row], hoff(ctx, H, out.col), r, ld8(rb.cols()));
-        res = r;
-        ldres = ld8(rb.cols());
-      }
-    }
     // fused RMSNorm apply + ReLU + dropout + residual -> X_l
     L.x.blk = xb;
     L.x.ldf = ld8(xb.cols());
@@ -590,6 +599,7 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
       ProfScope ps(ctx, kProfFwdRow,
                    e * (4 + (res ? 4 : resp ? 3 : 0) + (L.x.f ? 4 : 0) + (L.x.b ? 2 : 0) + (L.x.lo ? 2 : 0) +
                         (L.x.p ? 3 : 0)) + e / 8);
+      reshard_join(ctx);
       fwd_apply(ctx, fa);
     }
     prev = &L.x;
@@ -805,6 +815,7 @@ void backward(State& st, const Batch& bt, int precision) {
       gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, nullptr, 0, dhb, ldhb);
     }
     }
+    reshard_join(ctx);  // dres (its peer-memory reshard ran beside the element-wise backward and the GEMMs)
     // dxh = spmm(A_t, dhagg) (pmm.hpp:165), charged also when pre-aggregation folds it into dW_in
     charge_all_reduce(ctx, adjacency_layout(l).row, bt.csrs[bt.csrt_of[(l - 1) % 3]].n_rows * hc, wire_bytes(wire));
     if (l == 1 && st.preagg) {
@@ -886,6 +897,7 @@ void backward(State& st, const Batch& bt, int precision) {
                     st.ws_wgrad, pre_dres ? 1 : 0);
     charge_all_reduce(ctx, kInputFeatureLayout.row, w.n, wire_bytes(wire));
     all_reduce_sum_async(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
+    reshard_join(ctx);
     join_async(ctx);  // every gradient reduced before dp_sync / the optimizer read G
     return;
   }
@@ -906,6 +918,7 @@ void backward(State& st, const Batch& bt, int precision) {
     charge_all_reduce(ctx, kInputFeatureLayout.row, w.n, wire_bytes(wire));
     all_reduce_sum_async(ctx, kInputFeatureLayout.row, G + w.off, w.n, wire);
   }
+  reshard_join(ctx);
   join_async(ctx);  // every gradient reduced before dp_sync / the optimizer read G
 }
 
