@@ -88,6 +88,8 @@ void need(const Ctx& ctx, int axis) {
 }  // namespace
 
 Comm::~Comm() {
+  if (pstream) cudaStreamDestroy(pstream);
+  for (auto& e : pev) cudaEventDestroy(e);
   if (rstream) cudaStreamDestroy(rstream);
   if (rfork) cudaEventDestroy(rfork);
   if (rjoin) cudaEventDestroy(rjoin);

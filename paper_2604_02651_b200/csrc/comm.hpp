@@ -17,7 +17,9 @@ struct PeerAxis {
   size_t cap = 0;                // bytes per slot
   char* base = nullptr;          // this member's buffer
   char* rbase[8] = {};           // member q's buffer as mapped here (rbase[me] = base)
-  uint64_t epoch = 0;            // reductions issued on this axis
+  uint64_t epoch = 0;            // arrival barriers issued on this group
+  uint64_t calls = 0;            // slots handed out (their parity picks the slot)
+  int parity = 0;                // slot of the current call
   int* err = nullptr;            // mapped host word: a peer never arrived
   int* err_dev = nullptr;
   ~PeerAxis();
@@ -50,6 +52,9 @@ struct Comm {
   cudaStream_t rstream = nullptr;
   cudaEvent_t rfork = nullptr, rjoin = nullptr;
   bool rpending = false;
+  // chunked peer reductions (peer_pipelined): their stream and events
+  cudaStream_t pstream = nullptr;
+  std::vector<cudaEvent_t> pev;
   // (index 4: the DP group's PMM grid, for the reshard's block permutation)
   int peer_state[5] = {0, 0, 0, 0, 0};
   std::unique_ptr<PeerAxis> peer[5];
@@ -123,9 +128,18 @@ void* peer_slot(Ctx& ctx, int axis, size_t bytes);
 // bf16 already rounded by their producer (src_bf16: the bf16 wire's
 // contributions, half the NVLink bytes); fp32 partials are rounded here under
 // GGB_BF16_WIRE — either way exactly kBf16Roundtrip (comm.hpp:271-303).
+// row0: first row of the slot block this call sums (a chunk of the block;
+// out / outb / add point at that chunk's first row).
 void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld, bool src_bf16, int wire, float* out,
                      int64_t ldo, bf16* outb, bf16* outlo, int64_t ldb, const float* add = nullptr,
-                     int64_t ldadd = 0);
+                     int64_t ldadd = 0, int64_t row0 = 0);
+// Producer / peer reduction overlap: rows in GGB_PEER_CHUNKS chunks (multiples
+// of quantum); chunk k is produced on the compute stream (leaving
+// GGB_PEER_RESERVE SMs free once a reduction may run) and reduced on the peer
+// stream while chunk k+1 is produced; the compute stream waits for the last
+// reduction. One chunk (default): produce, then reduce, inline.
+void peer_pipelined(Ctx& ctx, int64_t rows, int64_t quantum, const std::function<void(int64_t, int64_t)>& produce,
+                    const std::function<void(int64_t, int64_t)>& reduce);
 bool peer_timed_out(const Comm& c);
 // The reshard's block permutation through peer memory (group kPeerPmm, the
 // ranks of this DP group): every rank stages its source block (rows x cols,

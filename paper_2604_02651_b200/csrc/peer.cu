@@ -258,6 +258,7 @@ void grow(Ctx& ctx, int axis, PeerAxis& P, size_t bytes) {
   GGB_CUDA(cudaMemsetAsync(P.base, 0, kFlagBytes, ctx.stream));
   P.cap = want;
   P.epoch = 0;
+  P.calls = 0;
   cudaIpcMemHandle_t h;
   GGB_CUDA(cudaIpcGetMemHandle(&h, P.base));
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
@@ -342,8 +343,8 @@ bool peer_ok(Ctx& ctx, int axis, int wire) {
 void* peer_slot(Ctx& ctx, int axis, size_t bytes) {
   PeerAxis& P = *ctx.comm->peer[axis];
   if (bytes > P.cap) grow(ctx, axis, P, bytes);
-  const uint64_t e = P.epoch + 1;
-  return P.base + kFlagBytes + (e & 1) * P.cap;
+  P.parity = static_cast<int>(++P.calls & 1);
+  return P.base + kFlagBytes + P.parity * P.cap;
 }
 
 namespace {
@@ -364,17 +365,19 @@ void launch_wait(Ctx& ctx, PeerAxis& P, uint64_t e) {
 }  // namespace
 
 void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld, bool src_bf16, int wire, float* out,
-                     int64_t ldo, bf16* outb, bf16* outlo, int64_t ldb, const float* add, int64_t ldadd) {
+                     int64_t ldo, bf16* outb, bf16* outlo, int64_t ldb, const float* add, int64_t ldadd,
+                     int64_t row0) {
   Comm& c = *ctx.comm;
   PeerAxis& P = *c.peer[axis];
   require(ld % (src_bf16 ? 8 : 4) == 0 && (!out || ldo % 4 == 0) && (!outb || ldb % 4 == 0) &&
               (!add || ldadd % 4 == 0),
           "peer_all_reduce: row strides must be whole 16-byte vectors");
-  require(static_cast<size_t>(rows * ld) * (src_bf16 ? 2 : 4) <= P.cap, "peer_all_reduce: slot not reserved");
+  const size_t esz = src_bf16 ? 2 : 4;
+  require(static_cast<size_t>((row0 + rows) * ld) * esz <= P.cap, "peer_all_reduce: slot not reserved");
   require(rows * ld < (int64_t(1) << 32), "peer_all_reduce: block too large for 32-bit unit indices");
   const uint64_t e = ++P.epoch;
   ReduceArgs a{};
-  for (int q = 0; q < P.g; ++q) a.src[q] = P.rbase[q] + kFlagBytes + (e & 1) * P.cap;
+  for (int q = 0; q < P.g; ++q) a.src[q] = P.rbase[q] + kFlagBytes + P.parity * P.cap + static_cast<size_t>(row0 * ld) * esz;
   a.g = P.g;
   a.wire = wire == GGB_BF16_WIRE ? 1 : 0;
   a.rows = rows;
@@ -496,7 +499,7 @@ void peer_pull(Ctx& ctx, const std::vector<PeerPiece>& pieces) {
     if (x.rows <= 0 || x.cols <= 0) continue;
     require(np < kMaxPieces, "peer_pull: too many pieces");
     require(x.member >= 0 && x.member < P.g, "peer_pull: member outside the group");
-    const float* base = reinterpret_cast<const float*>(P.rbase[x.member] + kFlagBytes + (e & 1) * P.cap);
+    const float* base = reinterpret_cast<const float*>(P.rbase[x.member] + kFlagBytes + P.parity * P.cap);
     PullPiece& p = a.pc[np++];
     p.src = base + x.src_off;
     p.dst = x.dst;
@@ -523,6 +526,70 @@ void peer_pull(Ctx& ctx, const std::vector<PeerPiece>& pieces) {
   k_peer_pull<<<blocks, 256, 0, ctx.stream>>>(a);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
+}
+
+namespace {
+int peer_chunks() {
+  static const int v = [] {
+    const char* e = std::getenv("GGB_PEER_CHUNKS");
+    const int c = e ? std::atoi(e) : 1;
+    return c >= 1 && c <= 16 ? c : 1;
+  }();
+  return v;
+}
+int peer_reserve() {
+  static const int v = [] {
+    const char* e = std::getenv("GGB_PEER_RESERVE");
+    const int c = e ? std::atoi(e) : 16;
+    return c >= 0 && c <= 64 ? c : 16;
+  }();
+  return v;
+}
+}  // namespace
+
+void peer_pipelined(Ctx& ctx, int64_t rows, int64_t quantum, const std::function<void(int64_t, int64_t)>& produce,
+                    const std::function<void(int64_t, int64_t)>& reduce) {
+  const int K = peer_chunks();
+  if (K <= 1 || rows < 2 * quantum) {
+    produce(0, rows);
+    reduce(0, rows);
+    return;
+  }
+  Comm& c = *ctx.comm;
+  if (!c.pstream) {
+    int lo = 0, hi = 0;
+    GGB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GGB_CUDA(cudaStreamCreateWithPriority(&c.pstream, cudaStreamNonBlocking, hi));
+  }
+  while (static_cast<int>(c.pev.size()) < K + 1) {
+    cudaEvent_t e;
+    GGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.pev.push_back(e);
+  }
+  const int64_t per = round_up(ceil_div(rows, K), quantum);
+  const int saved_reserve = ctx.sm_reserve;
+  int k = 0;
+  for (int64_t r0 = 0; r0 < rows; r0 += per, ++k) {
+    const int64_t r1 = std::min(rows, r0 + per);
+    // the producer leaves SMs to the reductions of the chunks before it
+    ctx.sm_reserve = k > 0 ? std::max(saved_reserve, peer_reserve()) : saved_reserve;
+    produce(r0, r1);
+    GGB_CUDA(cudaEventRecord(c.pev[k], ctx.stream));
+    GGB_CUDA(cudaStreamWaitEvent(c.pstream, c.pev[k], 0));
+    cudaStream_t saved = ctx.stream;
+    ctx.stream = c.pstream;
+    try {
+      reduce(r0, r1);
+    } catch (...) {
+      ctx.stream = saved;
+      ctx.sm_reserve = saved_reserve;
+      throw;
+    }
+    ctx.stream = saved;
+  }
+  ctx.sm_reserve = saved_reserve;
+  GGB_CUDA(cudaEventRecord(c.pev[K], c.pstream));
+  GGB_CUDA(cudaStreamWaitEvent(ctx.stream, c.pev[K], 0));
 }
 
 bool peer_timed_out(const Comm& c) {

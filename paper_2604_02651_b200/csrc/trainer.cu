@@ -252,8 +252,8 @@ struct PeerPart {
   void* p = nullptr;
   bool b16 = false;
   int64_t ld = 0;
-  float* f() const { return b16 ? nullptr : static_cast<float*>(p); }
-  bf16* h() const { return b16 ? static_cast<bf16*>(p) : nullptr; }
+  float* f(int64_t r0 = 0) const { return b16 ? nullptr : static_cast<float*>(p) + r0 * ld; }
+  bf16* h(int64_t r0 = 0) const { return b16 ? static_cast<bf16*>(p) + r0 * ld : nullptr; }
 };
 PeerPart peer_part(Ctx& ctx, int axis, int wire, int64_t rows, int64_t cols) {
   PeerPart pp;
@@ -335,10 +335,20 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     xin.ldb = bt.x_ld;
     if (ar && peer_ok(ctx, kInputFeatureLayout.col, wire)) {
       // partial into the peer slot; the ordered sum lands in X0 (+ its bf16 copy)
-      const PeerPart pp = peer_part(ctx, kInputFeatureLayout.col, wire, ob.rows(), ob.cols());
-      fwd_gemm(st, ob.rows(), ob.cols(), w.blk.rows(), xin, w, pp.f(), pp.ld, pp.h(), pp.ld);
-      peer_all_reduce(ctx, kInputFeatureLayout.col, ob.rows(), ob.cols(), pp.ld, pp.b16, wire, st.x0.f, st.x0.ldf,
-                      want_b ? st.x0.b : nullptr, nullptr, st.x0.ldb);
+      const int ax = kInputFeatureLayout.col;
+      const PeerPart pp = peer_part(ctx, ax, wire, ob.rows(), ob.cols());
+      peer_pipelined(
+          ctx, ob.rows(), 128,
+          [&](int64_t r0, int64_t r1) {
+            Tensor sub = xin;
+            sub.b = xin.b + r0 * xin.ldb;
+            sub.lo = xin.lo ? xin.lo + r0 * xin.ldb : nullptr;
+            fwd_gemm(st, r1 - r0, ob.cols(), w.blk.rows(), sub, w, pp.f(r0), pp.ld, pp.h(r0), pp.ld);
+          },
+          [&](int64_t r0, int64_t r1) {
+            peer_all_reduce(ctx, ax, r1 - r0, ob.cols(), pp.ld, pp.b16, wire, st.x0.f + r0 * st.x0.ldf, st.x0.ldf,
+                            want_b ? st.x0.b + r0 * st.x0.ldb : nullptr, nullptr, st.x0.ldb, nullptr, 0, r0);
+          });
     } else {
     fwd_gemm(st, ob.rows(), ob.cols(), w.blk.rows(), xin, w, st.x0.f, st.x0.ldf, (ar || !want_b) ? nullptr : st.x0.b,
              st.x0.ldb);
@@ -426,17 +436,24 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
       // partial sums over A's column blocks into the peer slot; the ordered
       // sum is written as hagg's bf16 operand copies (no fp32 hagg, no cast pass)
       const PeerPart pp = peer_part(ctx, alay.col, wire, A.n_rows, hb.cols());
-      {
-        ProfScope ps(ctx, kProfSpmmFwd, spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, pp.b16 ? 2 : 4),
-                     2.0 * A.nnz * F.cols());
-        if (accurate)
-          spmm_csr_f32(ctx, A.n_rows, arp, acol, aval, prev->f, prev->ldf, F.cols(), pp.f(), pp.ld, pp.h(), nullptr,
+      peer_pipelined(
+          ctx, A.n_rows, 128,
+          [&](int64_t r0, int64_t r1) {
+            const double frac = static_cast<double>(r1 - r0) / std::max<int64_t>(A.n_rows, 1);
+            ProfScope ps(ctx, kProfSpmmFwd, frac * spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, pp.b16 ? 2 : 4),
+                         frac * 2.0 * A.nnz * F.cols());
+            if (accurate)
+              spmm_csr_f32(ctx, r1 - r0, arp + r0, acol, aval, prev->f, prev->ldf, F.cols(), pp.f(r0), pp.ld, pp.h(r0),
+                           nullptr, pp.ld, 0);
+            else
+              spmm_csr(ctx, r1 - r0, arp + r0, acol, aval, prev->b, prev->ldb, F.cols(), pp.f(r0), pp.ld, pp.h(r0),
                        pp.ld, 0);
-        else
-          spmm_csr(ctx, A.n_rows, arp, acol, aval, prev->b, prev->ldb, F.cols(), pp.f(), pp.ld, pp.h(), pp.ld, 0);
-      }
-      peer_all_reduce(ctx, alay.col, A.n_rows, hb.cols(), pp.ld, pp.b16, wire, nullptr, 0, L.hagg.b, L.hagg.lo,
-                      L.hagg.ldb);
+          },
+          [&](int64_t r0, int64_t r1) {
+            peer_all_reduce(ctx, alay.col, r1 - r0, hb.cols(), pp.ld, pp.b16, wire, nullptr, 0,
+                            L.hagg.b + r0 * L.hagg.ldb, L.hagg.lo ? L.hagg.lo + r0 * L.hagg.ldb : nullptr, L.hagg.ldb,
+                            nullptr, 0, r0);
+          });
     } else if (ar_h) {
       // partial sums over A's column blocks: row chunks of the SpMM pipelined
       // with their all-reduce (and the bf16 split of the reduced rows)
@@ -497,9 +514,18 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     charge_all_reduce(ctx, hb.lay.col, xb.rows() * xb.cols(), wire_bytes(wire));  // contract (pmm.hpp:128)
     if (reduces(ctx, hb.lay.col, wire) && peer_ok(ctx, hb.lay.col, wire)) {
       const PeerPart pp = peer_part(ctx, hb.lay.col, wire, xb.rows(), xb.cols());
-      fwd_gemm(st, xb.rows(), xb.cols(), hb.cols(), L.hagg, w, pp.f(), pp.ld, pp.h(), pp.ld);
-      peer_all_reduce(ctx, hb.lay.col, xb.rows(), xb.cols(), pp.ld, pp.b16, wire, L.xw_t.f, L.xw_t.ldf, nullptr,
-                      nullptr, 0);
+      peer_pipelined(
+          ctx, xb.rows(), 128,
+          [&](int64_t r0, int64_t r1) {
+            Tensor sub = L.hagg;
+            sub.b = L.hagg.b + r0 * L.hagg.ldb;
+            sub.lo = L.hagg.lo ? L.hagg.lo + r0 * L.hagg.ldb : nullptr;
+            fwd_gemm(st, r1 - r0, xb.cols(), hb.cols(), sub, w, pp.f(r0), pp.ld, pp.h(r0), pp.ld);
+          },
+          [&](int64_t r0, int64_t r1) {
+            peer_all_reduce(ctx, hb.lay.col, r1 - r0, xb.cols(), pp.ld, pp.b16, wire, L.xw_t.f + r0 * L.xw_t.ldf,
+                            L.xw_t.ldf, nullptr, nullptr, 0, nullptr, 0, r0);
+          });
     } else {
     pipelined_all_reduce(ctx, hb.lay.col, xb.rows(), 128, L.xw_t.f, L.xw_t.ldf, wire, [&](int64_t r0, int64_t r1) {
       Tensor sub = L.hagg;
@@ -700,12 +726,21 @@ void backward(State& st, const Batch& bt, int precision) {
                  2.0 * db.rows() * db.cols() * lb.cols());
     charge_all_reduce(ctx, lb.lay.col, db.rows() * db.cols(), wire_bytes(wire));
     if (reduces(ctx, lb.lay.col, wire) && peer_ok(ctx, lb.lay.col, wire)) {
-      const PeerPart pp = peer_part(ctx, lb.lay.col, wire, db.rows(), db.cols());
-      gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, pp.f(),
-                pp.ld, pp.h(), pp.ld);
       ps.end();
-      peer_all_reduce(ctx, lb.lay.col, db.rows(), db.cols(), pp.ld, pp.b16, wire, dxh, ld8(db.cols()), nullptr,
-                      nullptr, 0);
+      const PeerPart pp = peer_part(ctx, lb.lay.col, wire, db.rows(), db.cols());
+      const int64_t ldd = ld8(db.cols());
+      peer_pipelined(
+          ctx, db.rows(), 128,
+          [&](int64_t r0, int64_t r1) {
+            ProfScope pc(ctx, kProfGemmDx, gemm_bytes(r1 - r0, db.cols(), lb.cols(), 2, 2, pp.b16 ? 2 : 4),
+                         2.0 * (r1 - r0) * db.cols() * lb.cols());
+            gemm_bf16(ctx, r1 - r0, db.cols(), lb.cols(), st.dlog_b.as<bf16>() + r0 * lddlog, lddlog, w.wb.as<bf16>(),
+                      w.ldb, pp.f(r0), pp.ld, pp.h(r0), pp.ld);
+          },
+          [&](int64_t r0, int64_t r1) {
+            peer_all_reduce(ctx, lb.lay.col, r1 - r0, db.cols(), pp.ld, pp.b16, wire, dxh + r0 * ldd, ldd, nullptr,
+                            nullptr, 0, nullptr, 0, r0);
+          });
     } else {
     gemm_bf16(ctx, db.rows(), db.cols(), lb.cols(), st.dlog_b.as<bf16>(), lddlog, w.wb.as<bf16>(), w.ldb, dxh,
               ld8(db.cols()), nullptr, 0);
@@ -796,10 +831,19 @@ void backward(State& st, const Batch& bt, int precision) {
     {
     ProfScope ps(ctx, kProfGemmDx, gemm_bytes(rows, hc, cols, 2, 2, ar_d ? 4 : 2), 2.0 * rows * hc * cols);
     if (ar_d && peer_ok(ctx, xb.lay.col, wire)) {
-      const PeerPart pp = peer_part(ctx, xb.lay.col, wire, rows, hc);
-      gemm_bf16(ctx, rows, hc, cols, ba.dxb, lddxw, w.wb.as<bf16>(), w.ldb, pp.f(), pp.ld, pp.h(), pp.ld);
       ps.end();
-      peer_all_reduce(ctx, xb.lay.col, rows, hc, pp.ld, pp.b16, wire, nullptr, 0, dhb, nullptr, ldhb);
+      const PeerPart pp = peer_part(ctx, xb.lay.col, wire, rows, hc);
+      peer_pipelined(
+          ctx, rows, 128,
+          [&](int64_t r0, int64_t r1) {
+            ProfScope pc(ctx, kProfGemmDx, gemm_bytes(r1 - r0, hc, cols, 2, 2, pp.b16 ? 2 : 4), 2.0 * (r1 - r0) * hc * cols);
+            gemm_bf16(ctx, r1 - r0, hc, cols, ba.dxb + r0 * lddxw, lddxw, w.wb.as<bf16>(), w.ldb, pp.f(r0), pp.ld,
+                      pp.h(r0), pp.ld);
+          },
+          [&](int64_t r0, int64_t r1) {
+            peer_all_reduce(ctx, xb.lay.col, r1 - r0, hc, pp.ld, pp.b16, wire, nullptr, 0, dhb + r0 * ldhb, nullptr,
+                            ldhb, nullptr, 0, r0);
+          });
     } else if (ar_d) {
       ps.end();
       float* dhf = grow<float>(st.dhagg_f, rows * hc);
@@ -848,11 +892,22 @@ void backward(State& st, const Batch& bt, int precision) {
       // partial into the peer slot; ordered sum + residual gradient in one pass
       float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
       const int64_t ldn = ld8(F.cols());
-      const PeerPart pp = peer_part(ctx, alay.row, wire, At.n_rows, F.cols());
-      spmm_csr(ctx, At.n_rows, At.row_ptr.as<int64_t>(), At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc,
-               pp.f(), pp.ld, pp.h(), pp.ld, 0);
       ps.end();
-      peer_all_reduce(ctx, alay.row, At.n_rows, F.cols(), pp.ld, pp.b16, wire, nd, ldn, nullptr, nullptr, 0, dres, ldn);
+      const PeerPart pp = peer_part(ctx, alay.row, wire, At.n_rows, F.cols());
+      const int64_t* trp = At.row_ptr.as<int64_t>();
+      peer_pipelined(
+          ctx, At.n_rows, 128,
+          [&](int64_t r0, int64_t r1) {
+            const double frac = static_cast<double>(r1 - r0) / std::max<int64_t>(At.n_rows, 1);
+            ProfScope pc(ctx, kProfSpmmBwd, frac * spmm_bytes(At.n_rows, At.nnz, hc, 2, pp.b16 ? 2 : 4),
+                         frac * 2.0 * At.nnz * hc);
+            spmm_csr(ctx, r1 - r0, trp + r0, At.col.as<int32_t>(), At.val.as<float>(), dhb, ldhb, hc, pp.f(r0), pp.ld,
+                     pp.h(r0), pp.ld, 0);
+          },
+          [&](int64_t r0, int64_t r1) {
+            peer_all_reduce(ctx, alay.row, r1 - r0, F.cols(), pp.ld, pp.b16, wire, nd + r0 * ldn, ldn, nullptr, nullptr,
+                            0, dres ? dres + r0 * ldn : nullptr, ldn, r0);
+          });
       std::swap(st.dxh, st.dxh2);
       dxh = nd;
     } else {
