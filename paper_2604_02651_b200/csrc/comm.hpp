@@ -20,6 +20,7 @@ struct PeerAxis {
   uint64_t epoch = 0;            // arrival barriers issued on this group
   uint64_t calls = 0;            // slots handed out (their parity picks the slot)
   int parity = 0;                // slot of the current call
+  bool pushed = false;           // the current call's producers mirror their partials (push mode)
   int* err = nullptr;            // mapped host word: a peer never arrived
   int* err_dev = nullptr;
   ~PeerAxis();
@@ -122,6 +123,16 @@ bool peer_ok(Ctx& ctx, int axis, int wire);
 // The slot the producer of the next peer_all_reduce on `axis` writes its
 // partial block into (collective when it has to grow).
 void* peer_slot(Ctx& ctx, int axis, size_t bytes);
+// Push mode (2-member groups; bf16 partials by default, GGB_PEER_PUSH=0/1
+// never / always): the producer also
+// stores its partial into the peer's copy of the slot (`mirror`, NVLink
+// stores overlapped with the producer's own HBM-bound work), so the
+// reduction reads only local HBM. mirror is null when the group pulls.
+struct PeerSlot {
+  void* local = nullptr;
+  void* mirror = nullptr;
+};
+PeerSlot peer_slot_push(Ctx& ctx, int axis, size_t bytes, bool bf16_part);
 // The ordered sum 0 + p_0 + ... + p_{g-1} (axis order) of the members' slot
 // blocks (rows x cols, stride ld elements), written as fp32 (out, optionally
 // + add) and/or bf16 hi (+ lo = x - hi) operand copies. Partials are fp32, or

@@ -177,6 +177,9 @@ struct GemmArgs {
   bf16* cb;
   bf16* cl;  // optional lo residual of the bf16 output: c == cb + cl to ~2^-16
   int64_t ldcb;
+  // push-mode peer reductions (peer.cu): tmCl is a map of the peer's copy of
+  // the output and every TMA store of c (1) or cb (2) is repeated into it
+  int mirror;
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -365,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (args.c) tma_store_2d(&tmC, ebuf, col0, r0);
             if (args.cb) tma_store_2d(&tmCb, ebuf + 2048, col0, r0);
             if (args.cl) tma_store_2d(&tmCl, ebuf + 3072, col0, r0);
+            if (args.mirror) tma_store_2d(&tmCl, args.mirror == 1 ? ebuf : ebuf + 2048, col0, r0);
             bulk_commit();
           }
           continue;
@@ -684,6 +688,16 @@ CUtensorMap encode_out_tmap(const void* base, int64_t rows, int64_t cols, int64_
   return m;
 }
 
+// GGB_PEER_PUSH_TMA=0: mirrored GEMM outputs by a copy after the kernel
+// instead of a second TMA store per tile
+bool mirror_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GGB_PEER_PUSH_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool tma_store_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -769,6 +783,18 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
     if (cb) tcb = make_out_tmap(cb, m, n, ldcb, 2);
     if (ga.cl) tcl = make_out_tmap(ga.cl, m, n, ldcb, 2);
   }
+  // push mode: mirror the one output (c or cb, no lo half) into the peer's slot
+  bool mirror_after = false;
+  if (ctx.out_mirror) {
+    require(!ga.cl && ((c != nullptr) != (cb != nullptr)), "gemm: a mirrored output is exactly one of c / cb");
+    if (ga.tma_out && mirror_tma_enabled()) {
+      ga.mirror = c ? 1 : 2;
+      tcl = c ? make_out_tmap(reinterpret_cast<char*>(c) + ctx.out_mirror, m, n, ldc, 4)
+              : make_out_tmap(reinterpret_cast<char*>(cb) + ctx.out_mirror, m, n, ldcb, 2);
+    } else {
+      mirror_after = true;
+    }
+  }
   const int smem = ga.stages * stage_bytes + static_cast<int>(ga.b_res ? bres_bytes : 0) + 1024 + kEpiSmem;
   static bool attr = false;
   if (!attr) {
@@ -781,6 +807,14 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
   k_gemm_kmajor<<<grid, kThreads, smem, ctx.stream>>>(ta, tb, tal, tbl, tc, tcb, tcl, ga);
   GGB_LAUNCH_CHECK();
   ctx.launches += 1;
+  if (mirror_after) {  // register epilogue: copy the finished block to the mirror
+    if (c)
+      GGB_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(c) + ctx.out_mirror, ldc * 4, c, ldc * 4, n * 4, m,
+                                 cudaMemcpyDeviceToDevice, ctx.stream));
+    else
+      GGB_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(cb) + ctx.out_mirror, ldcb * 2, cb, ldcb * 2, n * 2, m,
+                                 cudaMemcpyDeviceToDevice, ctx.stream));
+  }
 }
 
 void gemm_bf16(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, int64_t lda, const bf16* bt, int64_t ldb,

@@ -207,6 +207,17 @@ __global__ void __launch_bounds__(256) k_peer_reduce(ReduceArgs a) {
   }
 }
 
+// GGB_PEER_PUSH: 1 always, 0 never; default: push bf16 partials only (an
+// fp32 partial's NVLink stores outlast the SpMM that produces it: C2 1x2x2x1
+// fp32 13.3 -> 13.8 ms/step with push, bf16 wire 12.2 -> 12.1)
+int peer_push_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("GGB_PEER_PUSH");
+    return e ? (e[0] == '1' ? 1 : 0) : 2;
+  }();
+  return v;
+}
+
 bool peer_env_on() {
   static const bool on = [] {
     const char* e = std::getenv("GGB_PEER");
@@ -221,6 +232,13 @@ bool peer_env_on() {
     if (r_ != ncclSuccess)                                                                     \
       ::ggb::fail(GGB_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));              \
   } while (0)
+
+// Member q's area of the current slot in member m's buffer: every slot holds
+// one partial-sized area per member (pull mode fills only its own area of its
+// own buffer; push mode mirrors it into the same area of the peers' buffers).
+char* area(const PeerAxis& P, int m, int q) {
+  return P.rbase[m] + kFlagBytes + (static_cast<size_t>(P.parity) * P.g + q) * P.cap;
+}
 
 // group index 0..3: a grid axis; kPeerPmm: the ranks of this rank's DP group
 // (its X x Y x Z grid, contiguous world ranks)
@@ -254,7 +272,7 @@ void grow(Ctx& ctx, int axis, PeerAxis& P, size_t bytes) {
   }
   size_t want = bytes + bytes / 8;
   want = (want + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
-  GGB_CUDA(cudaMalloc(&P.base, kFlagBytes + 2 * want));
+  GGB_CUDA(cudaMalloc(&P.base, kFlagBytes + 2 * static_cast<size_t>(P.g) * want));
   GGB_CUDA(cudaMemsetAsync(P.base, 0, kFlagBytes, ctx.stream));
   P.cap = want;
   P.epoch = 0;
@@ -342,9 +360,24 @@ bool peer_ok(Ctx& ctx, int axis, int wire) {
 
 void* peer_slot(Ctx& ctx, int axis, size_t bytes) {
   PeerAxis& P = *ctx.comm->peer[axis];
+  P.pushed = false;
   if (bytes > P.cap) grow(ctx, axis, P, bytes);
   P.parity = static_cast<int>(++P.calls & 1);
-  return P.base + kFlagBytes + P.parity * P.cap;
+  return area(P, P.me, P.me);
+}
+
+PeerSlot peer_slot_push(Ctx& ctx, int axis, size_t bytes, bool bf16_part) {
+  PeerSlot r;
+  r.local = peer_slot(ctx, axis, bytes);
+  PeerAxis& P = *ctx.comm->peer[axis];
+  const int mode = peer_push_mode();
+  if (P.g == 2 && (mode == 1 || (mode == 2 && bf16_part))) {
+    r.mirror = area(P, 1 - P.me, P.me);
+    P.pushed = true;
+  } else {
+    P.pushed = false;
+  }
+  return r;
 }
 
 namespace {
@@ -377,7 +410,8 @@ void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld,
   require(rows * ld < (int64_t(1) << 32), "peer_all_reduce: block too large for 32-bit unit indices");
   const uint64_t e = ++P.epoch;
   ReduceArgs a{};
-  for (int q = 0; q < P.g; ++q) a.src[q] = P.rbase[q] + kFlagBytes + P.parity * P.cap + static_cast<size_t>(row0 * ld) * esz;
+  // member q's partial: in q's own buffer (pull), or mirrored into ours by its producer (push)
+  for (int q = 0; q < P.g; ++q) a.src[q] = area(P, P.pushed ? P.me : q, q) + static_cast<size_t>(row0 * ld) * esz;
   a.g = P.g;
   a.wire = wire == GGB_BF16_WIRE ? 1 : 0;
   a.rows = rows;
@@ -499,7 +533,7 @@ void peer_pull(Ctx& ctx, const std::vector<PeerPiece>& pieces) {
     if (x.rows <= 0 || x.cols <= 0) continue;
     require(np < kMaxPieces, "peer_pull: too many pieces");
     require(x.member >= 0 && x.member < P.g, "peer_pull: member outside the group");
-    const float* base = reinterpret_cast<const float*>(P.rbase[x.member] + kFlagBytes + P.parity * P.cap);
+    const float* base = reinterpret_cast<const float*>(area(P, x.member, x.member));
     PullPiece& p = a.pc[np++];
     p.src = base + x.src_off;
     p.dst = x.dst;

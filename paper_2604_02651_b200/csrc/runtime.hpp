@@ -2,6 +2,7 @@
 #pragma once
 
 #include <array>
+#include <cstddef>
 #include <memory>
 #include <vector>
 
@@ -82,6 +83,10 @@ struct Ctx {
   // the next SpMMs' CSR has power-law rows (the pipelined kernel then shares
   // long rows across warps); set per call site from BatchCsr::long_rows
   bool spmm_long_rows = false;
+  // push-mode peer reductions: the SpMM producers also store every output
+  // element at (its address + out_mirror) — the same slot area in the
+  // peer's buffer (peer.cu); 0 = no mirror. Set per call site (MirrorScope).
+  ptrdiff_t out_mirror = 0;
   CommStats stats;
   int phase = kPhaseOther;
   ~Ctx();
@@ -95,6 +100,15 @@ struct LongRowsScope {
   ~LongRowsScope() { ctx.spmm_long_rows = prev; }
   LongRowsScope(const LongRowsScope&) = delete;
   LongRowsScope& operator=(const LongRowsScope&) = delete;
+};
+
+struct MirrorScope {
+  Ctx& ctx;
+  ptrdiff_t prev;
+  MirrorScope(Ctx& c, ptrdiff_t d) : ctx(c), prev(c.out_mirror) { ctx.out_mirror = d; }
+  ~MirrorScope() { ctx.out_mirror = prev; }
+  MirrorScope(const MirrorScope&) = delete;
+  MirrorScope& operator=(const MirrorScope&) = delete;
 };
 
 /// PhaseScope (comm.hpp:411-421).

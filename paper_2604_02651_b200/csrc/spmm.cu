@@ -223,6 +223,18 @@ int spmm_kernel_choice() {  // GGB_SPMM=rowsplit forces the register-pipelined k
   return v;
 }
 
+// the non-pipelined kernels do not mirror their stores (push mode): copy the
+// finished block to the mirror instead
+void mirror_copy(Ctx& ctx, int64_t rows, int64_t fcols, float* out, int64_t ldo, bf16* outb, int64_t ldob) {
+  if (!ctx.out_mirror) return;
+  if (out)
+    GGB_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(out) + ctx.out_mirror, ldo * 4, out, ldo * 4, fcols * 4, rows,
+                               cudaMemcpyDeviceToDevice, ctx.stream));
+  if (outb)
+    GGB_CUDA(cudaMemcpy2DAsync(reinterpret_cast<char*>(outb) + ctx.out_mirror, ldob * 2, outb, ldob * 2, fcols * 2,
+                               rows, cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
 void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
               const bf16* f, int64_t ldf, int64_t fcols, float* out, int64_t ldo, bf16* outb,
               int64_t ldob, int accumulate) {
@@ -234,6 +246,7 @@ void spmm_csr(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, con
       spmm_pipe(ctx, rows, rp, col, val, f, 2, ldf, fcols, out, ldo, outb, nullptr, ldob, accumulate))
     return;
   dispatch<bf16>(ctx, rows, rp, col, val, f, ldf, fcols, out, ldo, outb, nullptr, ldob, accumulate);
+  mirror_copy(ctx, rows, fcols, out, ldo, outb, ldob);
 }
 
 void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, const float* val,
@@ -247,6 +260,7 @@ void spmm_csr_f32(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col,
       spmm_pipe(ctx, rows, rp, col, val, f, 4, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate))
     return;
   dispatch<float>(ctx, rows, rp, col, val, f, ldf, fcols, out, ldo, out_hi, out_lo, ldob, accumulate);
+  mirror_copy(ctx, rows, fcols, out, ldo, out_hi, ldob);
 }
 
 }  // namespace ggb

@@ -59,7 +59,13 @@ struct PipeArgs {
   int64_t* lead_row;  // [warps] row id or -1
   int64_t* tail_row;  // [warps] row id or -1
   int carry_ld;
+  ptrdiff_t mirror;   // nonzero: every output store is repeated at address + mirror (peer.cu push mode)
 };
+
+template <class T>
+__device__ __forceinline__ T* mirror_of(T* p, ptrdiff_t d) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(p) + d);
+}
 
 // Warp work split: 2 = merge path with long rows shared (default), 1 =
 // work-balanced whole rows (GGB_SPMM_SPLIT=balanced), 0 = even row split, the
@@ -282,11 +288,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
                 acc[q][v + 3] = o.w;
               }
               *reinterpret_cast<float4*>(dst + v) = o;
+              if (a.mirror) *reinterpret_cast<float4*>(mirror_of(dst + v, a.mirror)) = o;
             }
           } else {
             for (int i = 0; i < EPC && cc + i < a.fcols; ++i) {
               if (a.accumulate) acc[q][i] += dst[i];
               dst[i] = acc[q][i];
+              if (a.mirror) *mirror_of(dst + i, a.mirror) = acc[q][i];
             }
           }
         }
@@ -304,15 +312,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
             }
             if constexpr (EPC == 8) {
               *reinterpret_cast<uint4*>(db) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+              if (a.mirror) *reinterpret_cast<uint4*>(mirror_of(db, a.mirror)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
               if (dl) *reinterpret_cast<uint4*>(dl) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             } else {
               *reinterpret_cast<uint2*>(db) = make_uint2(hi[0], hi[1]);
+              if (a.mirror) *reinterpret_cast<uint2*>(mirror_of(db, a.mirror)) = make_uint2(hi[0], hi[1]);
               if (dl) *reinterpret_cast<uint2*>(dl) = make_uint2(lo[0], lo[1]);
             }
           } else {
             for (int i = 0; i < EPC && cc + i < a.fcols; ++i) {
               const bf16 h = __float2bfloat16_rn(acc[q][i]);
               db[i] = h;
+              if (a.mirror) *mirror_of(db + i, a.mirror) = h;
               if (dl) dl[i] = __float2bfloat16_rn(acc[q][i] - __bfloat162float(h));
             }
           }
@@ -412,10 +423,12 @@ __global__ void k_spmm_carry_fixup(const PipeArgs a, int64_t warps) {
       float* dst = a.out + row * a.ldo + c;
       if (a.accumulate) s += *dst;
       *dst = s;
+      if (a.mirror) *mirror_of(dst, a.mirror) = s;
     }
     if (a.outb) {
       const bf16 h = __float2bfloat16_rn(s);
       a.outb[row * a.ldob + c] = h;
+      if (a.mirror) *mirror_of(a.outb + row * a.ldob + c, a.mirror) = h;
       if (a.outlo) a.outlo[row * a.ldob + c] = __float2bfloat16_rn(s - __bfloat162float(h));
     }
   }
@@ -488,6 +501,8 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
   a.ldob = ldob;
   a.accumulate = accumulate;
   a.ocpr = a.vcpr;
+  a.mirror = ctx.out_mirror;
+  require(!(a.mirror && outlo), "spmm: a mirrored output has no lo half");
   if (esize == 2) {
     if (row_bytes <= 256)
       launch_pipe<bf16, 256>(ctx, a);

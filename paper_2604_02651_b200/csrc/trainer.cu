@@ -252,14 +252,35 @@ struct PeerPart {
   void* p = nullptr;
   bool b16 = false;
   int64_t ld = 0;
+  ptrdiff_t mirror = 0;  // push mode: byte distance to the peer's copy of the area (MirrorScope)
   float* f(int64_t r0 = 0) const { return b16 ? nullptr : static_cast<float*>(p) + r0 * ld; }
   bf16* h(int64_t r0 = 0) const { return b16 ? static_cast<bf16*>(p) + r0 * ld : nullptr; }
 };
-PeerPart peer_part(Ctx& ctx, int axis, int wire, int64_t rows, int64_t cols) {
+// push: the producer mirrors its output stores into the peer's slot
+// (2-member groups), so the reduction reads only local HBM. Used for the
+// SpMM producers, whose gather-bound runtime hides the NVLink stores (C2
+// 1x2x2x1: SpMM +5%, reduction -40%); a GEMM producer is too short to hide
+// them (its TMA stores to the peer run at NVLink speed: GEMM 0.07 -> 0.25 ms
+// per launch), so GEMM sites pull unless GGB_PEER_PUSH_GEMM=1.
+bool push_gemm() {
+  static const bool on = [] {
+    const char* e = std::getenv("GGB_PEER_PUSH_GEMM");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+PeerPart peer_part(Ctx& ctx, int axis, int wire, int64_t rows, int64_t cols, bool push = false) {
   PeerPart pp;
   pp.b16 = wire == GGB_BF16_WIRE;
   pp.ld = ld8(cols);
-  pp.p = peer_slot(ctx, axis, static_cast<size_t>(rows * pp.ld) * (pp.b16 ? 2 : 4));
+  const size_t bytes = static_cast<size_t>(rows * pp.ld) * (pp.b16 ? 2 : 4);
+  if (push) {
+    const PeerSlot sl = peer_slot_push(ctx, axis, bytes, pp.b16);
+    pp.p = sl.local;
+    if (sl.mirror) pp.mirror = static_cast<char*>(sl.mirror) - static_cast<char*>(sl.local);
+  } else {
+    pp.p = peer_slot(ctx, axis, bytes);
+  }
   return pp;
 }
 
@@ -336,10 +357,11 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     if (ar && peer_ok(ctx, kInputFeatureLayout.col, wire)) {
       // partial into the peer slot; the ordered sum lands in X0 (+ its bf16 copy)
       const int ax = kInputFeatureLayout.col;
-      const PeerPart pp = peer_part(ctx, ax, wire, ob.rows(), ob.cols());
+      const PeerPart pp = peer_part(ctx, ax, wire, ob.rows(), ob.cols(), push_gemm());
       peer_pipelined(
           ctx, ob.rows(), 128,
           [&](int64_t r0, int64_t r1) {
+            MirrorScope mirror(ctx, pp.mirror);
             Tensor sub = xin;
             sub.b = xin.b + r0 * xin.ldb;
             sub.lo = xin.lo ? xin.lo + r0 * xin.ldb : nullptr;
@@ -435,10 +457,11 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     if (ar_h && peer_ok(ctx, alay.col, wire)) {
       // partial sums over A's column blocks into the peer slot; the ordered
       // sum is written as hagg's bf16 operand copies (no fp32 hagg, no cast pass)
-      const PeerPart pp = peer_part(ctx, alay.col, wire, A.n_rows, hb.cols());
+      const PeerPart pp = peer_part(ctx, alay.col, wire, A.n_rows, hb.cols(), true);
       peer_pipelined(
           ctx, A.n_rows, 128,
           [&](int64_t r0, int64_t r1) {
+            MirrorScope mirror(ctx, pp.mirror);
             const double frac = static_cast<double>(r1 - r0) / std::max<int64_t>(A.n_rows, 1);
             ProfScope ps(ctx, kProfSpmmFwd, frac * spmm_bytes(A.n_rows, A.nnz, F.cols(), accurate ? 4 : 2, pp.b16 ? 2 : 4),
                          frac * 2.0 * A.nnz * F.cols());
@@ -513,10 +536,11 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.xw_t.f = grow<float>(L.xw, xb.rows() * L.xw_t.ldf);
     charge_all_reduce(ctx, hb.lay.col, xb.rows() * xb.cols(), wire_bytes(wire));  // contract (pmm.hpp:128)
     if (reduces(ctx, hb.lay.col, wire) && peer_ok(ctx, hb.lay.col, wire)) {
-      const PeerPart pp = peer_part(ctx, hb.lay.col, wire, xb.rows(), xb.cols());
+      const PeerPart pp = peer_part(ctx, hb.lay.col, wire, xb.rows(), xb.cols(), push_gemm());
       peer_pipelined(
           ctx, xb.rows(), 128,
           [&](int64_t r0, int64_t r1) {
+            MirrorScope mirror(ctx, pp.mirror);
             Tensor sub = L.hagg;
             sub.b = L.hagg.b + r0 * L.hagg.ldb;
             sub.lo = L.hagg.lo ? L.hagg.lo + r0 * L.hagg.ldb : nullptr;
@@ -727,11 +751,12 @@ void backward(State& st, const Batch& bt, int precision) {
     charge_all_reduce(ctx, lb.lay.col, db.rows() * db.cols(), wire_bytes(wire));
     if (reduces(ctx, lb.lay.col, wire) && peer_ok(ctx, lb.lay.col, wire)) {
       ps.end();
-      const PeerPart pp = peer_part(ctx, lb.lay.col, wire, db.rows(), db.cols());
+      const PeerPart pp = peer_part(ctx, lb.lay.col, wire, db.rows(), db.cols(), push_gemm());
       const int64_t ldd = ld8(db.cols());
       peer_pipelined(
           ctx, db.rows(), 128,
           [&](int64_t r0, int64_t r1) {
+            MirrorScope mirror(ctx, pp.mirror);
             ProfScope pc(ctx, kProfGemmDx, gemm_bytes(r1 - r0, db.cols(), lb.cols(), 2, 2, pp.b16 ? 2 : 4),
                          2.0 * (r1 - r0) * db.cols() * lb.cols());
             gemm_bf16(ctx, r1 - r0, db.cols(), lb.cols(), st.dlog_b.as<bf16>() + r0 * lddlog, lddlog, w.wb.as<bf16>(),
@@ -832,10 +857,11 @@ void backward(State& st, const Batch& bt, int precision) {
     ProfScope ps(ctx, kProfGemmDx, gemm_bytes(rows, hc, cols, 2, 2, ar_d ? 4 : 2), 2.0 * rows * hc * cols);
     if (ar_d && peer_ok(ctx, xb.lay.col, wire)) {
       ps.end();
-      const PeerPart pp = peer_part(ctx, xb.lay.col, wire, rows, hc);
+      const PeerPart pp = peer_part(ctx, xb.lay.col, wire, rows, hc, push_gemm());
       peer_pipelined(
           ctx, rows, 128,
           [&](int64_t r0, int64_t r1) {
+            MirrorScope mirror(ctx, pp.mirror);
             ProfScope pc(ctx, kProfGemmDx, gemm_bytes(r1 - r0, hc, cols, 2, 2, pp.b16 ? 2 : 4), 2.0 * (r1 - r0) * hc * cols);
             gemm_bf16(ctx, r1 - r0, hc, cols, ba.dxb + r0 * lddxw, lddxw, w.wb.as<bf16>(), w.ldb, pp.f(r0), pp.ld,
                       pp.h(r0), pp.ld);
@@ -893,11 +919,12 @@ void backward(State& st, const Batch& bt, int precision) {
       float* nd = grow<float>(st.dxh2, F.rows() * ld8(F.cols()));
       const int64_t ldn = ld8(F.cols());
       ps.end();
-      const PeerPart pp = peer_part(ctx, alay.row, wire, At.n_rows, F.cols());
+      const PeerPart pp = peer_part(ctx, alay.row, wire, At.n_rows, F.cols(), true);
       const int64_t* trp = At.row_ptr.as<int64_t>();
       peer_pipelined(
           ctx, At.n_rows, 128,
           [&](int64_t r0, int64_t r1) {
+            MirrorScope mirror(ctx, pp.mirror);
             const double frac = static_cast<double>(r1 - r0) / std::max<int64_t>(At.n_rows, 1);
             ProfScope pc(ctx, kProfSpmmBwd, frac * spmm_bytes(At.n_rows, At.nnz, hc, 2, pp.b16 ? 2 : 4),
                          frac * 2.0 * At.nnz * hc);
