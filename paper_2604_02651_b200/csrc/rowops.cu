@@ -108,7 +108,10 @@ __device__ __forceinline__ void f4(const float4& a, float* v) {
 
 // chunks of 128 columns held per row; Full: cols == 128 J; kLayer: the layer
 // API's instance (RMSNorm without ReLU, optional mask output)
-template <int J, bool Full, bool kLayer>
+// kPipe: a capped grid whose warps stride over the rows with the next row's
+// loads issued before the current row is processed (the prologue — gamma,
+// the column-term table — is paid once per warp instead of once per row)
+template <int J, bool Full, bool kLayer, bool kPipe = false>
 __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
   // Warp per row (grid-stride, so a capped grid also works), gamma and the
   // per-lane constants held across rows.
@@ -139,11 +142,9 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
   }
   const uint64_t T = p.thresh << 11;
 
-#pragma unroll 1
-  for (int64_t r = w0; r < p.rows; r += nw) {
+  // every load of a row is issued up front: one memory round trip per row
+  auto load_row = [&](int64_t r, float (&x)[J][4], float (&res)[J][4]) {
     const float* xr = p.x + r * p.ldx;
-    // every load of the row is issued up front: one memory round trip per row
-    float x[J][4], res[J][4];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       if (j >= nj) break;
@@ -155,6 +156,22 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
         f4(ld4_p24(p.resp + r * p.ldresp, p.reshoff, c, ncols), res[j]);
       else
         res[j][0] = res[j][1] = res[j][2] = res[j][3] = 0.f;
+    }
+  };
+  float xn[J][4], rn[J][4];
+  if (kPipe && w0 < p.rows) load_row(w0, xn, rn);
+
+#pragma unroll 1
+  for (int64_t r = w0; r < p.rows; r += nw) {
+    float x[J][4], res[J][4];
+    if constexpr (kPipe) {
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[j][i] = xn[j][i], res[j][i] = rn[j][i];
+      if (r + nw < p.rows) load_row(r + nw, xn, rn);
+    } else {
+      load_row(r, x, res);
     }
     float inv = 1.f;
     if (p.gamma) {  // RMSNorm on
@@ -533,7 +550,18 @@ void launch_fwd_row_k(Ctx& ctx, const FwdApply& p) {
     const char* e = std::getenv("GGB_FWD_ROW_BPS");
     return e ? std::atoi(e) : 0;
   }();
+  // GGB_FWD_ROW_PIPE=b: b blocks per SM, warps stride with the next row's
+  // loads in flight (software pipeline)
+  static const int pipe = [] {
+    const char* e = std::getenv("GGB_FWD_ROW_PIPE");
+    return e ? std::atoi(e) : 0;
+  }();
   int64_t g = ceil_div(p.rows, kRowsPerBlock);
+  if (pipe > 0 && !kLayer) {
+    g = std::min<int64_t>(g, static_cast<int64_t>(pipe) * ctx.num_sms);
+    k_fwd_row<J, Full, kLayer, true><<<static_cast<unsigned>(std::max<int64_t>(1, g)), kT, 0, ctx.stream>>>(p);
+    return;
+  }
   if (bps > 0) g = std::min<int64_t>(g, static_cast<int64_t>(bps) * ctx.num_sms);
   k_fwd_row<J, Full, kLayer><<<static_cast<unsigned>(std::max<int64_t>(1, g)), kT, 0, ctx.stream>>>(p);
 }

@@ -329,14 +329,24 @@ void launch_gather_x(const Ctx& ctx, cudaStream_t s, bool host, int64_t rows, in
                      float* xf, int64_t xfld) {
   if (rows <= 0) return;
   if (host) {
-    const unsigned blocks =
-        std::max(1u, static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 8 * 4), host_gather_blocks())));
+    // GGB_HOST_GATHER_TPB: threads per block (32 .. 256). One-warp blocks
+    // (2K registers) would fit beside a persistent SpMM CTA on the same SM,
+    // where a 256-thread block (16K) does not, but they measured slower
+    // end to end (C2 e2e 13.9-14.4 vs 12.7-13.2 ms/step): 256 stays
+    static const int tpb = [] {
+      const char* e = std::getenv("GGB_HOST_GATHER_TPB");
+      const int t = e ? std::atoi(e) : 256;
+      return t >= 32 && t <= 256 && t % 32 == 0 ? t : 256;
+    }();
+    const int wpb = tpb / 32;
+    const unsigned blocks = std::max(
+        1u, static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 4 * wpb), 8 * host_gather_blocks() / wpb)));
     if (ld <= 128)
-      k_gather_x<4, 1><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+      k_gather_x<4, 1><<<blocks, tpb, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
     else if (ld <= 256)
-      k_gather_x<4, 2><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+      k_gather_x<4, 2><<<blocks, tpb, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
     else
-      k_gather_x<4, 4><<<blocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+      k_gather_x<4, 4><<<blocks, tpb, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
   } else {
     const unsigned blocks =
         static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8), ctx.num_sms * 64)));

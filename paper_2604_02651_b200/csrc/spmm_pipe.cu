@@ -59,7 +59,7 @@ struct PipeArgs {
   int64_t* lead_row;  // [warps] row id or -1
   int64_t* tail_row;  // [warps] row id or -1
   int carry_ld;
-  ptrdiff_t mirror;   // nonzero: every output store is repeated at address + mirror (peer.cu push mode)
+  ptrdiff_t mirror;   // push mode (peer.cu): every output store is repeated at address + mirror
 };
 
 template <class T>
@@ -159,8 +159,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 
 // TIn: element type of F; RB: smem bytes per gathered row; kMerge: merge-path
 // ranges with long rows shared across warps (power-law inputs) — a separate
-// instance, so the whole-row kernel keeps its code generation.
-template <class TIn, int RB, bool kMerge>
+// instance, so the whole-row kernel keeps its code generation; kMirror: the
+// push-mode instance (peer.cu) that repeats every output store into the
+// peer's slot (separate, so the plain kernels keep their code too: the
+// runtime-offset stores may alias for the compiler and serialized the
+// backward's accumulate loads, 2.2 -> 3.3 ms/step).
+template <class TIn, int RB, bool kMerge, bool kMirror = false>
 __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) {
   constexpr bool kP24 = std::is_same_v<TIn, P24>;
   constexpr int EPC = kP24 ? 8 : 16 / static_cast<int>(sizeof(TIn));  // elements per lane chunk
@@ -288,13 +292,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
                 acc[q][v + 3] = o.w;
               }
               *reinterpret_cast<float4*>(dst + v) = o;
-              if (a.mirror) *reinterpret_cast<float4*>(mirror_of(dst + v, a.mirror)) = o;
+              if constexpr (kMirror) *reinterpret_cast<float4*>(mirror_of(dst + v, a.mirror)) = o;
             }
           } else {
             for (int i = 0; i < EPC && cc + i < a.fcols; ++i) {
               if (a.accumulate) acc[q][i] += dst[i];
               dst[i] = acc[q][i];
-              if (a.mirror) *mirror_of(dst + i, a.mirror) = acc[q][i];
+              if constexpr (kMirror) *mirror_of(dst + i, a.mirror) = acc[q][i];
             }
           }
         }
@@ -312,18 +316,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) k_spmm_pipe(const PipeArgs a) 
             }
             if constexpr (EPC == 8) {
               *reinterpret_cast<uint4*>(db) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-              if (a.mirror) *reinterpret_cast<uint4*>(mirror_of(db, a.mirror)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+              if constexpr (kMirror) *reinterpret_cast<uint4*>(mirror_of(db, a.mirror)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
               if (dl) *reinterpret_cast<uint4*>(dl) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             } else {
               *reinterpret_cast<uint2*>(db) = make_uint2(hi[0], hi[1]);
-              if (a.mirror) *reinterpret_cast<uint2*>(mirror_of(db, a.mirror)) = make_uint2(hi[0], hi[1]);
+              if constexpr (kMirror) *reinterpret_cast<uint2*>(mirror_of(db, a.mirror)) = make_uint2(hi[0], hi[1]);
               if (dl) *reinterpret_cast<uint2*>(dl) = make_uint2(lo[0], lo[1]);
             }
           } else {
             for (int i = 0; i < EPC && cc + i < a.fcols; ++i) {
               const bf16 h = __float2bfloat16_rn(acc[q][i]);
               db[i] = h;
-              if (a.mirror) *mirror_of(db + i, a.mirror) = h;
+              if constexpr (kMirror) *mirror_of(db + i, a.mirror) = h;
               if (dl) dl[i] = __float2bfloat16_rn(acc[q][i] - __bfloat162float(h));
             }
           }
@@ -434,11 +438,11 @@ __global__ void k_spmm_carry_fixup(const PipeArgs a, int64_t warps) {
   }
 }
 
-template <class TIn, int RB, bool kMerge>
+template <class TIn, int RB, bool kMerge, bool kMirror>
 void set_smem_attr() {
   static bool attr = false;
   if (!attr) {
-    GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB, kMerge>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB, kMerge, kMirror>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kWarps * kStages * kStageBytes + kWarps * kStages * 32 * 4));
     attr = true;
   }
@@ -462,12 +466,24 @@ void launch_pipe(Ctx& ctx, PipeArgs a) {
     a.lead_row = reinterpret_cast<int64_t*>(base + 2 * warps * a.carry_ld);
     a.tail_row = a.lead_row + warps;
   }
-  if (mode == 2) {
-    set_smem_attr<TIn, RB, true>();
-    k_spmm_pipe<TIn, RB, true><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+  const bool mirror = a.mirror != 0;
+  if constexpr (std::is_same_v<TIn, P24>) require(!mirror, "spmm: no mirrored 24-bit instance");
+  if (mode == 2 && mirror) {
+    if constexpr (!std::is_same_v<TIn, P24>) {
+      set_smem_attr<TIn, RB, true, true>();
+      k_spmm_pipe<TIn, RB, true, true><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+    }
+  } else if (mode == 2) {
+    set_smem_attr<TIn, RB, true, false>();
+    k_spmm_pipe<TIn, RB, true, false><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+  } else if (mirror) {
+    if constexpr (!std::is_same_v<TIn, P24>) {
+      set_smem_attr<TIn, RB, false, true>();
+      k_spmm_pipe<TIn, RB, false, true><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+    }
   } else {
-    set_smem_attr<TIn, RB, false>();
-    k_spmm_pipe<TIn, RB, false><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
+    set_smem_attr<TIn, RB, false, false>();
+    k_spmm_pipe<TIn, RB, false, false><<<grid, kWarps * 32, smem, ctx.stream>>>(a);
   }
   if (mode == 2) {
     k_spmm_carry_fixup<<<static_cast<unsigned>(ceil_div(warps, 8)), 256, 0, ctx.stream>>>(a, warps);
@@ -502,7 +518,7 @@ bool spmm_pipe(Ctx& ctx, int64_t rows, const int64_t* rp, const int32_t* col, co
   a.accumulate = accumulate;
   a.ocpr = a.vcpr;
   a.mirror = ctx.out_mirror;
-  require(!(a.mirror && outlo), "spmm: a mirrored output has no lo half");
+  require(!(a.mirror && (outlo || accumulate)), "spmm: a mirrored output is a plain partial (no lo half, no accumulate)");
   if (esize == 2) {
     if (row_bytes <= 256)
       launch_pipe<bf16, 256>(ctx, a);
