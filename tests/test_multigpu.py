@@ -54,3 +54,30 @@ def test_collective_timeout_raises_comm_timeout():
     assert lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
     assert res["ok"], res
+
+
+# The peer-memory reductions (ordered sum 0 + p_0 + p_1 in axis order, the
+# consumer's cast / residual add fused) and the peer-memory reshard compute
+# exactly what the NCCL path computes on 2-member groups: equal bytes.
+PEER_GRIDS = [("1x2x1x1", 0), ("1x2x1x1", 1), ("1x1x2x1", 0), ("1x2x2x1", 0), ("1x2x2x1", 1)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grid,prec", PEER_GRIDS)
+def test_peer_matches_nccl(grid, prec):
+    world = 1
+    for d in grid.split("x"):
+        world *= int(d)
+    if _ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    res = {}
+    for peer in ("0", "1"):
+        env = dict(os.environ, GGB_PEER=peer)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr=127.0.0.1", "--master-port=29535", os.path.join(ROOT, "tests", "mgpu_peer_worker.py"),
+               grid, str(prec)]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+        res[peer] = json.loads(lines[-1])["ranks"]
+    assert res["0"] == res["1"], (res["0"], res["1"])
