@@ -314,12 +314,14 @@ __global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t
 // rows in flight per warp, so the gather, which runs for milliseconds on the
 // sampling stream, holds only part of a few SMs while keeping enough reads
 // outstanding for the link (measured at C2: 245 MB in ~5 ms, ~49 GB/s, the
-// same from 32 to 296 blocks).
+// same from 32 to 296 blocks; round 2, e2e ms/step: 16 blocks 11.24-11.58,
+// 24 11.51, 32 11.75-11.81 — the fewer SMs it touches, the less it slows the
+// step's persistent kernels).
 int host_gather_blocks() {
   static int v = [] {
     const char* e = std::getenv("GGB_HOST_GATHER_BLOCKS");
-    const int b = e ? std::atoi(e) : 32;
-    return b > 0 ? b : 32;
+    const int b = e ? std::atoi(e) : 16;
+    return b > 0 ? b : 16;
   }();
   return v;
 }
