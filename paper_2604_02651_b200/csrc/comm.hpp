@@ -23,6 +23,7 @@ struct PeerAxis {
   bool pushed = false;           // the current call's producers mirror their partials (push mode)
   int* err = nullptr;            // mapped host word: a peer never arrived
   int* err_dev = nullptr;
+  DevBuf stage;                  // handle exchange / barrier staging (grow)
   ~PeerAxis();
 };
 

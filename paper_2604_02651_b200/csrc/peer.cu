@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(32) k_peer_wait(WaitArgs a) {
   if (q < a.g && q != a.me) {
     __threadfence_system();
     st_release_sys(a.arrive[q], a.epoch);
+    // a member already timed out: the host raises CommTimeout at its next
+    // wait; later barriers return at once instead of each spinning to the deadline
+    if (*reinterpret_cast<volatile int*>(a.err)) return;
     const unsigned long long t0 = globaltimer();
     while (ld_acquire_sys(a.mine + q) < a.epoch) {
       if (globaltimer() - t0 > a.timeout_ns) {
@@ -265,7 +268,7 @@ void grow(Ctx& ctx, int axis, PeerAxis& P, size_t bytes) {
   Comm& c = *ctx.comm;
   auto* nc = static_cast<ncclComm_t>(group_comm(c, axis));
   if (P.base) {  // every member done reading the old buffers
-    float* one = c.gather.reserve_n<float>(1);
+    float* one = P.stage.reserve_n<float>(1);
     GGB_NCCL_P(ncclAllReduce(one, one, 1, ncclFloat32, ncclSum, nc, ctx.stream));
     sync_stream(ctx, ctx.stream);
     close_mappings(P);
@@ -280,7 +283,9 @@ void grow(Ctx& ctx, int axis, PeerAxis& P, size_t bytes) {
   cudaIpcMemHandle_t h;
   GGB_CUDA(cudaIpcGetMemHandle(&h, P.base));
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  uint8_t* d = c.gather.reserve_n<uint8_t>(64 * (P.g + 1));
+  // staging of its own: grow may run on the reshard stream while the compute
+  // stream uses the communicator's staging buffers
+  uint8_t* d = P.stage.reserve_n<uint8_t>(64 * (P.g + 1));
   GGB_CUDA(cudaMemcpyAsync(d + 64 * P.g, &h, 64, cudaMemcpyHostToDevice, ctx.stream));
   GGB_NCCL_P(ncclAllGather(d + 64 * P.g, d, 64, ncclUint8, nc, ctx.stream));
   std::vector<uint8_t> all(64 * P.g);
