@@ -67,6 +67,8 @@ int ggb_version(void);
  * work; any collective over a group larger than one fails GGB_ECONTRACT.
  * stream: the CUDA stream compute is launched on (NULL = library-owned). */
 int ggb_get_unique_id(uint8_t out[128]);
+/* number of visible CUDA devices (0 and GGB_ECUDA without a usable driver) */
+int ggb_device_count(int32_t* out);
 int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const uint8_t* nccl_uid,
                    void* stream, ggb_ctx_t* out);
 int ggb_ctx_destroy(ggb_ctx_t ctx);

@@ -47,6 +47,7 @@ _SIGS = [
     ("ggb_last_error", C.c_char_p, []),
     ("ggb_version", C.c_int, []),
     ("ggb_get_unique_id", C.c_int, [P]),
+    ("ggb_device_count", C.c_int, [P]),
     ("ggb_ctx_create", C.c_int, [P, I32, I32, P, P, P]),
     ("ggb_ctx_destroy", C.c_int, [P]),
     ("ggb_ctx_set_stream", C.c_int, [P, P]),

@@ -363,6 +363,15 @@ int ggb_get_unique_id(uint8_t out[128]) {
   return guard([&] { comm_get_unique_id(out); });
 }
 
+int ggb_device_count(int32_t* out) {
+  return guard([&] {
+    *out = 0;
+    int n = 0;
+    GGB_CUDA(cudaGetDeviceCount(&n));
+    *out = n;
+  });
+}
+
 int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const uint8_t* nccl_uid, void* stream,
                    ggb_ctx_t* out) {
   return guard([&] {

@@ -1,5 +1,6 @@
 // Internal helpers shared by every translation unit of libggb.so.
 #pragma once
+#include <atomic>
 
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -43,6 +44,16 @@ inline void contract(bool ok, const char* msg) {
 #define GGB_LAUNCH_CHECK() GGB_CUDA(cudaGetLastError())
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+/// True the first time per CUDA device: kernel attributes set with
+/// cudaFuncSetAttribute apply to the calling thread's current device, and one
+/// process may drive several GPUs (the CLI runs a thread per rank).
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const uint64_t bit = uint64_t{1} << dev;
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 /// Grow-only device buffer; contents are not preserved on growth.

@@ -796,11 +796,10 @@ void gemm_bf16_impl(Ctx& ctx, int64_t m, int64_t n, int64_t k, const bf16* a, co
     }
   }
   const int smem = ga.stages * stage_bytes + static_cast<int>(ga.b_res ? bres_bytes : 0) + 1024 + kEpiSmem;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     GGB_CUDA(cudaFuncSetAttribute(k_gemm_kmajor, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBudget));
-    attr = true;
   }
   const int64_t tiles = ceil_div(m, kBM) * ga.n_tiles;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, std::min(sm_count(), ctx.persistent_sms())));
@@ -862,11 +861,10 @@ void gemm_wgrad_bf16(Ctx& ctx, int64_t m, int64_t kw, int64_t nw, const bf16* x,
   const CUtensorMap tx = make_tmap(x, m, kw, ldx, 64, kBK);
   const CUtensorMap td = make_tmap(dy, m, nw, lddy, 64, kBK);
   const int smem = wa.stages * stage_bytes + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     GGB_CUDA(cudaFuncSetAttribute(k_gemm_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemBudget));
-    attr = true;
   }
   dim3 grid(tiles, wa.splits);
   k_gemm_wgrad<<<grid, kWgradThreads, smem, ctx.stream>>>(tx, td, wa);

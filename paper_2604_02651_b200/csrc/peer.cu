@@ -321,25 +321,30 @@ bool peer_ok(Ctx& ctx, int axis, int wire) {
     auto* nc = static_cast<ncclComm_t>(group_comm(c, axis));
     const int g = group_size(ctx, axis);
     int dev = ctx.device;
-    int* d = c.gather.reserve_n<int>(2 * g);
+    // {host hash, device, process id} of every member: IPC needs peers on
+    // this host, peer-accessible, and in other processes (a process cannot
+    // open its own IPC handles; one-process grids, e.g. the CLI's thread per
+    // rank, keep NCCL)
+    int* d = c.gather.reserve_n<int>(3 * g);
     char host[256] = {};
     gethostname(host, sizeof(host) - 1);
     int hh = 5381;
     for (const char* p = host; *p; ++p) hh = hh * 33 + *p;
-    int mine[2] = {hh, dev};
-    int* dm = c.wire.reserve_n<int>(2);
+    const int pid = static_cast<int>(getpid());
+    int mine[3] = {hh, dev, pid};
+    int* dm = c.wire.reserve_n<int>(3);
     GGB_CUDA(cudaMemcpyAsync(dm, mine, sizeof(mine), cudaMemcpyHostToDevice, ctx.stream));
-    GGB_NCCL_P(ncclAllGather(dm, d, 2, ncclInt32, nc, ctx.stream));
-    std::vector<int> all(2 * g);
-    GGB_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(int) * 2 * g, cudaMemcpyDeviceToHost, ctx.stream));
+    GGB_NCCL_P(ncclAllGather(dm, d, 3, ncclInt32, nc, ctx.stream));
+    std::vector<int> all(3 * g);
+    GGB_CUDA(cudaMemcpyAsync(all.data(), d, sizeof(int) * 3 * g, cudaMemcpyDeviceToHost, ctx.stream));
     sync_stream(ctx, ctx.stream);
     bool ok = true;
     for (int q = 0; q < g; ++q) {
-      if (all[2 * q] != hh) ok = false;
+      if (all[3 * q] != hh) ok = false;
+      if (q == group_pos(ctx, axis)) continue;
+      if (all[3 * q + 2] == pid) ok = false;
       int can = 0;
-      if (ok && q != group_pos(ctx, axis)) {
-        if (cudaDeviceCanAccessPeer(&can, dev, all[2 * q + 1]) != cudaSuccess || !can) ok = false;
-      }
+      if (ok && (cudaDeviceCanAccessPeer(&can, dev, all[3 * q + 1]) != cudaSuccess || !can)) ok = false;
     }
     // agreement: the minimum over the group
     float* f = c.gather.reserve_n<float>(1);

@@ -440,11 +440,10 @@ __global__ void k_spmm_carry_fixup(const PipeArgs a, int64_t warps) {
 
 template <class TIn, int RB, bool kMerge, bool kMirror>
 void set_smem_attr() {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     GGB_CUDA(cudaFuncSetAttribute(k_spmm_pipe<TIn, RB, kMerge, kMirror>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kWarps * kStages * kStageBytes + kWarps * kStages * 32 * 4));
-    attr = true;
   }
 }
 
