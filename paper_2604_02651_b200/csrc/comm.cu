@@ -260,6 +260,16 @@ void all_reduce_sum_on(Ctx& ctx, int axis, float* buf, int64_t count, int mode, 
 }
 }  // namespace
 
+// GGB_PEER_SMALL=0: the in-place sums (row statistics, cross-entropy terms,
+// logits, dp_sync) stay on NCCL while the contraction sums use peer memory
+bool peer_small() {
+  static const bool on = [] {
+    const char* e = std::getenv("GGB_PEER_SMALL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, int wire) {
   if (count <= 0) return;
   if (trivial(ctx, axis)) {  // one member: the bf16 wires still round its contribution
@@ -271,6 +281,10 @@ void all_reduce_sum(Ctx& ctx, int axis, float* buf, int64_t count, int wire) {
     return;
   }
   need(ctx, axis);
+  if (peer_small() && peer_inplace_ok(ctx, axis, wire, buf)) {
+    peer_all_reduce_inplace(ctx, axis, buf, count, wire, false);
+    return;
+  }
   all_reduce_sum_on(ctx, axis, buf, count, wire, ctx.stream, ctx.comm->wire, ctx.comm->gather);
 }
 
@@ -399,6 +413,10 @@ void pipelined_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t quantum, flo
 void all_reduce_max(Ctx& ctx, int axis, float* buf, int64_t count) {
   if (trivial(ctx, axis) || count <= 0) return;
   need(ctx, axis);
+  if (peer_small() && peer_inplace_ok(ctx, axis, GGB_FP32, buf)) {
+    peer_all_reduce_inplace(ctx, axis, buf, count, GGB_FP32, true);
+    return;
+  }
   GGB_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat32, ncclMax,
                          as_nccl(ctx.comm->axis[axis]), ctx.stream));
 }

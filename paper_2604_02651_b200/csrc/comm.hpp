@@ -153,6 +153,13 @@ void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld,
 void peer_pipelined(Ctx& ctx, int64_t rows, int64_t quantum, const std::function<void(int64_t, int64_t)>& produce,
                     const std::function<void(int64_t, int64_t)>& reduce);
 bool peer_timed_out(const Comm& c);
+// In-place all-reduce of a device buffer through peer memory (the buffer is
+// copied into the group's slot, then summed / maxed in axis order back into
+// it): the row statistics, cross-entropy terms, logits and dp_sync sums on
+// the compute stream. peer_inplace_ok: the group is peer-capable and the
+// call is on the compute stream (16-byte aligned buffer).
+bool peer_inplace_ok(Ctx& ctx, int axis, int wire, const float* buf);
+void peer_all_reduce_inplace(Ctx& ctx, int axis, float* buf, int64_t count, int wire, bool max);
 // The reshard's block permutation through peer memory (group kPeerPmm, the
 // ranks of this DP group): every rank stages its source block (rows x cols,
 // packed with ld_stage) in its group slot, then pulls the pieces of its

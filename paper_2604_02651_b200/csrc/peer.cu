@@ -636,6 +636,81 @@ void peer_pipelined(Ctx& ctx, int64_t rows, int64_t quantum, const std::function
   GGB_CUDA(cudaStreamWaitEvent(ctx.stream, c.pev[K], 0));
 }
 
+namespace {
+
+// In-place flat reduction of the members' copies of one buffer: out[i] =
+// 0 + p_0[i] + ... (axis order; each bf16-rounded under the bf16 wire) or the
+// max; float4 body, scalar tail.
+struct FlatArgs {
+  const float* src[kMaxPeers];
+  int g, op, wire;  // op 0 sum, 1 max
+  int64_t n;
+  float* out;
+};
+__device__ __forceinline__ float flat_combine(const FlatArgs& a, float acc, float v, bool first) {
+  if (a.op == 1) return first ? v : fmaxf(acc, v);
+  return acc + (a.wire ? bf16_round_ref(v) : v);
+}
+__global__ void __launch_bounds__(256) k_peer_flat(FlatArgs a) {
+  const int64_t n4 = a.n / 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 v[kMaxPeers];
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+      if (q < a.g) v[q] = reinterpret_cast<const float4*>(a.src[q])[i];
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q) {
+      if (q >= a.g) break;
+      r.x = flat_combine(a, r.x, v[q].x, q == 0);
+      r.y = flat_combine(a, r.y, v[q].y, q == 0);
+      r.z = flat_combine(a, r.z, v[q].z, q == 0);
+      r.w = flat_combine(a, r.w, v[q].w, q == 0);
+    }
+    reinterpret_cast<float4*>(a.out)[i] = r;
+  }
+  for (int64_t i = 4 * n4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    float r = 0.f;
+    for (int q = 0; q < a.g; ++q) r = flat_combine(a, r, a.src[q][i], q == 0);
+    a.out[i] = r;
+  }
+}
+
+}  // namespace
+
+bool peer_inplace_ok(Ctx& ctx, int axis, int wire, const float* buf) {
+  if (!ctx.comm || wire == GGB_BF16_SUM || (reinterpret_cast<uintptr_t>(buf) & 15) != 0) return false;
+  const Comm& c = *ctx.comm;
+  // one stream per group carries the peer protocol: the compute stream
+  if (ctx.stream == c.gstream || ctx.stream == c.cstream || ctx.stream == c.pstream || ctx.stream == c.rstream)
+    return false;
+  return peer_ok(ctx, axis, wire);
+}
+
+void peer_all_reduce_inplace(Ctx& ctx, int axis, float* buf, int64_t count, int wire, bool max) {
+  if (count <= 0) return;
+  Comm& c = *ctx.comm;
+  float* slot = static_cast<float*>(peer_slot(ctx, axis, static_cast<size_t>(round_up(count, 4)) * 4));
+  PeerAxis& P = *c.peer[axis];
+  GGB_CUDA(cudaMemcpyAsync(slot, buf, static_cast<size_t>(count) * 4, cudaMemcpyDeviceToDevice, ctx.stream));
+  const uint64_t e = ++P.epoch;
+  FlatArgs a{};
+  for (int q = 0; q < P.g; ++q) a.src[q] = reinterpret_cast<const float*>(area(P, q, q));
+  a.g = P.g;
+  a.op = max ? 1 : 0;
+  a.wire = (!max && wire == GGB_BF16_WIRE) ? 1 : 0;
+  a.n = count;
+  a.out = buf;
+  ProfScope ps(ctx, kProfComm, 4.0 * count * (P.g - 1), 0);
+  launch_wait(ctx, P, e);
+  const unsigned blocks =
+      static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms * 4, ceil_div(count, 4 * 256))));
+  k_peer_flat<<<blocks, 256, 0, ctx.stream>>>(a);
+  GGB_LAUNCH_CHECK();
+  ctx.launches += 1;
+}
+
 bool peer_timed_out(const Comm& c) {
   for (const auto& p : c.peer)
     if (p && p->err && *reinterpret_cast<volatile int*>(p->err)) return true;
