@@ -399,7 +399,10 @@ int ggb_ctx_create(const int32_t dims[4], int32_t rank, int32_t device, const ui
       GGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       c->own_stream = true;
     }
-    if (nccl_uid && c->grid.total() > 1) c->comm = comm_create(c->grid, rank, nccl_uid);
+    if (nccl_uid && c->grid.total() > 1) {
+      c->comm = comm_create(c->grid, rank, nccl_uid);
+      peer_setup(*c);  // every rank is here together: decide the peer-memory groups now
+    }
     *out = c.release();
   });
 }

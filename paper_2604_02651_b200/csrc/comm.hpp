@@ -118,9 +118,12 @@ void barrier(Ctx& ctx);
 
 // ---- peer-memory all-reduce over NVLink (peer.cu) ----------------------------
 // peer_ok: the axis group can sum through mapped peer memory (every member
-// on this node, IPC-mappable; GGB_PEER=0 disables; not for the NCCL-bf16
-// wire). The first call per axis is collective (a probe agreed by all).
+// on this node, IPC-mappable, in another process; GGB_PEER=0 disables; not
+// for the NCCL-bf16 wire, not the D axis).
 bool peer_ok(Ctx& ctx, int axis, int wire);
+// Collective, at context creation: probes every eligible group (X, Y, Z axes,
+// the DP group's PMM grid) so no later call blocks on a probe.
+void peer_setup(Ctx& ctx);
 // The slot the producer of the next peer_all_reduce on `axis` writes its
 // partial block into (collective when it has to grow).
 void* peer_slot(Ctx& ctx, int axis, size_t bytes);

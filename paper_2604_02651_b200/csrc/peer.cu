@@ -311,12 +311,11 @@ PeerAxis::~PeerAxis() {
   if (err) cudaFreeHost(err);
 }
 
-bool peer_ok(Ctx& ctx, int axis, int wire) {
-  if (!peer_env_on() || !ctx.comm || ctx.comm->aborted || wire == GGB_BF16_SUM) return false;
-  if (axis == kPeerPmm ? pmm_size(ctx) == 1 : trivial(ctx, axis)) return false;
+namespace {
+// The collective probe of one group (every member calls it, in the same order).
+void probe(Ctx& ctx, int axis) {
   Comm& c = *ctx.comm;
-  if (group_size(ctx, axis) > kMaxPeers || !group_comm(c, axis)) return false;
-  if (c.peer_state[axis] == 0) {
+  {
     // one probe per axis, agreed by every member: IPC-mappable peers on this node
     auto* nc = static_cast<ncclComm_t>(group_comm(c, axis));
     const int g = group_size(ctx, axis);
@@ -365,7 +364,26 @@ bool peer_ok(Ctx& ctx, int axis, int wire) {
       c.peer[axis] = std::move(P);
     }
   }
-  return c.peer_state[axis] == 1;
+}
+
+bool eligible(const Ctx& ctx, int axis) {
+  // the contraction axes X, Y, Z and the DP group's PMM grid; the D axis
+  // (dp_sync's gradient sum, 1 MB a step) stays on NCCL
+  if (!peer_env_on() || !ctx.comm || axis == kD) return false;
+  if (axis == kPeerPmm ? pmm_size(ctx) == 1 : trivial(ctx, axis)) return false;
+  return group_size(ctx, axis) <= kMaxPeers && group_comm(*ctx.comm, axis) != nullptr;
+}
+}  // namespace
+
+void peer_setup(Ctx& ctx) {
+  if (!ctx.comm) return;
+  for (int axis : {1, 2, 3, kPeerPmm})
+    if (eligible(ctx, axis)) probe(ctx, axis);
+}
+
+bool peer_ok(Ctx& ctx, int axis, int wire) {
+  if (!ctx.comm || ctx.comm->aborted || wire == GGB_BF16_SUM || !eligible(ctx, axis)) return false;
+  return ctx.comm->peer_state[axis] == 1;  // decided at context creation (peer_setup)
 }
 
 void* peer_slot(Ctx& ctx, int axis, size_t bytes) {
