@@ -3,6 +3,7 @@ PMM grids, data-parallel training == the reference's DP run. Needs >= 2 GPUs
 (skipped otherwise); run with `gpurun --gpus 2|4`."""
 import json
 import os
+import signal
 import subprocess
 import sys
 
@@ -10,6 +11,21 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WORKER = os.path.join(ROOT, "tests", "mgpu_worker.py")
+
+
+def _run_group(cmd, timeout, env=None):
+    """Runs a torchrun launch in its own process group; on a timeout the
+    whole group (the launcher and every rank) is killed, so no rank outlives
+    the test holding a GPU."""
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=ROOT, env=env,
+                         start_new_session=True)
+    try:
+        out, err = p.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        out, err = p.communicate()
+        pytest.fail(f"timed out after {timeout} s: {out[-2000:]} {err[-2000:]}")
+    return subprocess.CompletedProcess(cmd, p.returncode, out, err)
 
 
 def _ngpus():
@@ -34,7 +50,7 @@ def test_sharded_matches_serial(grid, prec):
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29531", WORKER, grid, str(prec)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    r = _run_group(cmd, 600)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
@@ -49,7 +65,7 @@ def test_collective_timeout_raises_comm_timeout():
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mgpu_timeout_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    r = _run_group(cmd, 300)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
@@ -76,7 +92,7 @@ def test_peer_matches_nccl(grid, prec):
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                "--master-addr=127.0.0.1", "--master-port=29535", os.path.join(ROOT, "tests", "mgpu_peer_worker.py"),
                grid, str(prec)]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        r = _run_group(cmd, 600, env)
         lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
         assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
         res[peer] = json.loads(lines[-1])["ranks"]
