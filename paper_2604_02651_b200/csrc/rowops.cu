@@ -111,8 +111,11 @@ __device__ __forceinline__ void f4(const float4& a, float* v) {
 // kPipe: a capped grid whose warps stride over the rows with the next row's
 // loads issued before the current row is processed (the prologue — gamma,
 // the column-term table — is paid once per warp instead of once per row)
-template <int J, bool Full, bool kLayer, bool kPipe = false>
-__global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
+// TPB: threads per block (rows per block = TPB / 32; the per-block column
+// term table and barrier are shared by more rows at 512)
+template <int J, bool Full, bool kLayer, bool kPipe = false, int TPB = kT>
+__global__ void __launch_bounds__(TPB) k_fwd_row(FwdApply p) {
+  constexpr int kRowsPerBlock = TPB / 32;
   // Warp per row (grid-stride, so a capped grid also works), gamma and the
   // per-lane constants held across rows.
   const int64_t ncols = Full ? static_cast<int64_t>(J) * kRowChunk : p.cols;
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kT) k_fwd_row(FwdApply p) {
   __shared__ __align__(16) uint8_t s_kb[kRowsPerBlock][kRowChunk * J];
   __shared__ uint64_t s_cj[kRowChunk * J];  // column_term of every local column
   if (hash) {
-    for (int c = threadIdx.x; c < kRowChunk * J; c += kT) s_cj[c] = column_term(static_cast<uint64_t>(p.col_g0 + c));
+    for (int c = threadIdx.x; c < kRowChunk * J; c += TPB) s_cj[c] = column_term(static_cast<uint64_t>(p.col_g0 + c));
     __syncthreads();
   }
   const uint64_t T = p.thresh << 11;
@@ -560,6 +563,16 @@ void launch_fwd_row_k(Ctx& ctx, const FwdApply& p) {
   if (pipe > 0 && !kLayer) {
     g = std::min<int64_t>(g, static_cast<int64_t>(pipe) * ctx.num_sms);
     k_fwd_row<J, Full, kLayer, true><<<static_cast<unsigned>(std::max<int64_t>(1, g)), kT, 0, ctx.stream>>>(p);
+    return;
+  }
+  // GGB_FWD_ROW_TPB=512: 16 rows per block
+  static const int tpb = [] {
+    const char* e = std::getenv("GGB_FWD_ROW_TPB");
+    return e && std::atoi(e) == 512 ? 512 : 256;
+  }();
+  if (tpb == 512 && !kLayer && bps == 0) {
+    k_fwd_row<J, Full, kLayer, false, 512>
+        <<<static_cast<unsigned>(std::max<int64_t>(1, ceil_div(p.rows, 16))), 512, 0, ctx.stream>>>(p);
     return;
   }
   if (bps > 0) g = std::min<int64_t>(g, static_cast<int64_t>(bps) * ctx.num_sms);
