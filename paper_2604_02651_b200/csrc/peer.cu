@@ -15,13 +15,23 @@
 //     holds the SMs another stream's arrival kernel needs;
 //   * the consumer's format is written directly: fp32, bf16 hi (+ lo) operand
 //     copies for the next tcgen05 GEMM, or fp32 plus the residual gradient —
-//     the cast / add passes that follow an NCCL all-reduce are fused away.
-// Slots alternate between two buffers per axis: a member writes slot e&1 for
-// call e only after its call e-1 kernel saw every peer arrive at e-1, and a
-// peer arrives at e-1 only after its call e-2 kernel (the last reader of
-// slot e&1) finished, so no partial is overwritten while a peer reads it.
-// A wait longer than the communicator timeout raises a device flag that the
-// host watchdog (sync_stream) turns into CommTimeout.
+//     the cast / add passes that follow an NCCL all-reduce are fused away;
+//   * push mode (2-member groups, bf16 partials of an SpMM): the producer's
+//     epilogue also stores its partial into the peer's copy of the slot, so
+//     the NVLink transfer rides under the gather-bound SpMM and the reduction
+//     reads local HBM only;
+//   * the reshard's block permutation pulls its pieces from the members'
+//     staged source blocks on a stream of its own (peer_stage / peer_pull);
+//   * in-place sums (row statistics, cross-entropy terms, logits) copy the
+//     buffer into the slot and sum it back in axis order (k_peer_flat).
+// Every slot holds one area per member; slots alternate per call (parity of
+// the call count): a member writes slot c&1 for call c only after its call
+// c-1 reduction saw every peer arrive, and a peer arrives at c-1 only after
+// its call c-2 reduction (the last reader of slot c&1) finished, so no
+// partial is overwritten while a peer reads it. Groups are probed once, at
+// context creation (every member on this host, peer-accessible, in another
+// process). A wait longer than the communicator timeout raises a mapped host
+// flag that the host watchdog (sync_stream) turns into CommTimeout.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
