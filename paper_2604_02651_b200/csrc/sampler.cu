@@ -310,6 +310,37 @@ __global__ void k_gather_x(int64_t rows, int64_t cols, int64_t ld, const int64_t
   }
 }
 
+// Rows that do not split into 16-byte vectors (d_in % 4 != 0, e.g. 602)
+// from host memory: every lane issues its K column loads of the row before
+// storing any, so a warp keeps a whole row of PCIe reads in flight instead of
+// one load per lane (the plain scalar loop: ~12 GB/s at C3).
+template <int K>
+__global__ void k_gather_x_wide(int64_t rows, int64_t cols, int64_t ld, const int64_t* __restrict__ sample,
+                                int64_t row_lo, const float* __restrict__ feats, int64_t fld, bf16* __restrict__ xb,
+                                bf16* __restrict__ xl, float* __restrict__ xf, int64_t xfld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w0; r < rows; r += nw) {
+    const float* src = feats + sample[row_lo + r] * fld;
+    float v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t c = lane + 32 * k;
+      v[k] = c < cols ? __ldg(src + c) : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int64_t c = lane + 32 * k;
+      if (c >= ld) break;
+      const bf16 h = __float2bfloat16_rn(v[k]);
+      if (xb) xb[r * ld + c] = h;
+      if (xl) xl[r * ld + c] = __float2bfloat16_rn(v[k] - __bfloat162float(h));
+      if (xf && c < xfld) xf[r * xfld + c] = v[k];
+    }
+  }
+}
+
 // Host-resident features are read over PCIe by a small grid with several
 // rows in flight per warp, so the gather, which runs for milliseconds on the
 // sampling stream, holds only part of a few SMs while keeping enough reads
@@ -343,7 +374,11 @@ void launch_gather_x(const Ctx& ctx, cudaStream_t s, bool host, int64_t rows, in
     const int wpb = tpb / 32;
     const unsigned blocks = std::max(
         1u, static_cast<unsigned>(std::min<int64_t>(ceil_div(rows, 4 * wpb), 8 * host_gather_blocks() / wpb)));
-    if (ld <= 128)
+    const bool vec4 = (cols & 3) == 0 && (fld & 3) == 0 && (ld & 3) == 0 && (!xf || (xfld & 3) == 0) && ld <= 512;
+    if (!vec4 && ld <= 640) {
+      const unsigned wblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8 * 4), 4 * host_gather_blocks())));
+      k_gather_x_wide<20><<<wblocks, 256, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
+    } else if (ld <= 128)
       k_gather_x<4, 1><<<blocks, tpb, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);
     else if (ld <= 256)
       k_gather_x<4, 2><<<blocks, tpb, 0, s>>>(rows, cols, ld, sample, row_lo, feats, fld, xb, xl, xf, xfld);

@@ -225,11 +225,13 @@ def test_async_loss_readback_matches_sync(gg, orc):
     assert host.tolist() == want
 
 
-def test_host_resident_features(gg, orc):
+@pytest.mark.parametrize("d_in", [20, 602, 301])
+def test_host_resident_features(gg, orc, d_in):
     """Features kept in host memory (the reference's Dataset) and gathered over
     PCIe per batch: bit-identical x_in and losses to the HBM-resident graph,
-    direct and prefetched, with the PCIe bytes counted."""
-    n, d_in, ncls, b, seed = 3000, 20, 5, 700, 5
+    direct and prefetched, with the PCIe bytes counted. d_in 602 / 301 take
+    the wide-row gather (rows that are not 16-byte vectors)."""
+    n, ncls, b, seed = 3000, 5, 700, 5
     ds = orc.generate_synthetic(n, 9.0, d_in, ncls, 8)
     ctx = gg.Context()
     mk = lambda: gg.Graph.from_csr(ctx, n, ds.adj.row_ptr, ds.adj.col_idx, ds.adj.values, ds.features,
