@@ -15,9 +15,13 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <exception>
+#include <functional>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../../include/ggb.h"
@@ -653,6 +657,63 @@ inline TrainReport train_run(RankComm& rc, const DeviceDataset& ds, const ModelC
   report.comm_total = prev_snapshot - run_start_stats;
   report.wall_ms = ms_since(run_start);
   return report;
+}
+
+/// Every rank of `grid` as a host thread driving its own GPU (rank r on
+/// device r mod #devices), NCCL between the threads' contexts — the
+/// reference's Communicator runs its ranks on threads of one process too.
+/// body(rc) runs per rank; the first exception of any rank is rethrown after
+/// every thread joined.
+inline void run_ranks(const DeviceGrid& grid, const std::function<void(RankComm&)>& body) {
+  std::int32_t ndev = 0;
+  detail::check(ggb_device_count(&ndev));
+  const int world = grid.total();
+  if (ndev < 1) throw std::runtime_error("no CUDA device");
+  if (world > ndev)
+    throw std::invalid_argument("grid of " + std::to_string(world) + " ranks on " + std::to_string(ndev) +
+                                " GPU(s): one rank per GPU");
+  std::vector<std::uint8_t> uid;
+  if (world > 1) uid = RankComm::unique_id();
+  std::mutex m;
+  std::exception_ptr err;
+  std::vector<std::thread> threads;
+  for (int r = 0; r < world; ++r)
+    threads.emplace_back([&, r] {
+      try {
+        RankComm rc(grid, r, r % ndev, world > 1 ? uid.data() : nullptr);
+        body(rc);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(m);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& t : threads) t.join();
+  if (err) std::rethrow_exception(err);
+}
+
+/// train_run_fp32 (model.hpp:544-545, src/model.cpp:5-8): the whole grid of
+/// tcfg.grid trained on `ds`; rank 0's report (the reference returns the
+/// report of its rank 0 thread too).
+inline TrainReport train_run_fp32(const Dataset& ds, const ModelConfig& mcfg, const TrainConfig& tcfg) {
+  TrainReport out;
+  std::mutex m;
+  run_ranks(tcfg.grid, [&](RankComm& rc) {
+    DeviceDataset dds(rc, ds, mcfg.layers);
+    TrainReport rep = train_run(rc, dds, mcfg, tcfg);
+    if (rc.rank() == 0) {
+      std::lock_guard<std::mutex> lk(m);
+      out = std::move(rep);
+    }
+  });
+  return out;
+}
+
+/// reference_train (model.hpp:549-552): the same run on the degenerate
+/// grid with the same DP replica count, fp32 sums.
+inline TrainReport reference_train(const Dataset& ds, const ModelConfig& mcfg, TrainConfig tcfg) {
+  tcfg.grid = DeviceGrid(tcfg.grid.dims[0], 1, 1, 1);
+  tcfg.precision = Precision::kFp32;
+  return train_run_fp32(ds, mcfg, tcfg);
 }
 
 }  // namespace gridgnn

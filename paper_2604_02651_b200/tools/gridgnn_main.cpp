@@ -28,8 +28,11 @@
 #include <thread>
 #include <vector>
 
-#include "gridgnn/ggb.hpp"
+#include "gridgnn/dataset.hpp"
+#include "gridgnn/metrics.hpp"
+#include "gridgnn/model.hpp"
 #include "gridgnn/pmm.hpp"
+#include "gridgnn/sampling.hpp"
 
 namespace gg = gridgnn;
 
@@ -217,42 +220,13 @@ gg::TrainConfig train_config(const RunConfig& rc, gg::index_t n) {
   return t;
 }
 
-// Every rank of the grid as a host thread on its own GPU; body(rc) per rank.
-// The first exception of any rank is rethrown after all threads joined.
-void run_ranks(const gg::DeviceGrid& grid, const std::function<void(gg::RankComm&)>& body) {
-  std::int32_t ndev = 0;
-  gg::detail::check(ggb_device_count(&ndev));
-  if (ndev < 1) throw std::runtime_error("no CUDA device");
-  const int world = grid.total();
-  if (world > ndev)
-    throw UsageError("--grid " + std::to_string(world) + " ranks, " + std::to_string(ndev) +
-                     " GPU(s): one rank per GPU");
-  std::vector<std::uint8_t> uid;
-  if (world > 1) uid = gg::RankComm::unique_id();
-  std::mutex m;
-  std::exception_ptr err;
-  std::vector<std::thread> threads;
-  for (int r = 0; r < world; ++r)
-    threads.emplace_back([&, r] {
-      try {
-        gg::RankComm rc(grid, r, r % ndev, world > 1 ? uid.data() : nullptr);
-        body(rc);
-      } catch (...) {
-        std::lock_guard<std::mutex> lk(m);
-        if (!err) err = std::current_exception();
-      }
-    });
-  for (auto& t : threads) t.join();
-  if (err) std::rethrow_exception(err);
-}
-
 // train_run on every rank of the grid; rank 0's report. make: the rank's
 // DeviceDataset (make_rank_context of the run's dataset).
 gg::TrainReport train_on_grid(const gg::ModelConfig& mcfg, const gg::TrainConfig& tcfg,
                               const std::function<gg::DeviceDataset(gg::RankComm&)>& make) {
   gg::TrainReport out;
   std::mutex m;
-  run_ranks(tcfg.grid, [&](gg::RankComm& rc) {
+  gg::run_ranks(tcfg.grid, [&](gg::RankComm& rc) {
     gg::DeviceDataset dds = make(rc);
     gg::TrainReport rep = gg::train_run(rc, dds, mcfg, tcfg);
     if (rc.rank() == 0) {
@@ -263,15 +237,12 @@ gg::TrainReport train_on_grid(const gg::ModelConfig& mcfg, const gg::TrainConfig
   return out;
 }
 
-gg::TrainReport train_on_grid(const gg::Dataset& ds, const gg::ModelConfig& mcfg, const gg::TrainConfig& tcfg) {
-  return train_on_grid(mcfg, tcfg, [&](gg::RankComm& rc) { return gg::DeviceDataset(rc, ds, mcfg.layers); });
-}
 
 int cmd_train(const RunConfig& rc) {
   const gg::Dataset ds = load_or_generate(rc);
   const gg::ModelConfig mcfg = model_config(rc, ds);
   const gg::TrainConfig tcfg = train_config(rc, ds.n());
-  const gg::TrainReport rep = train_on_grid(ds, mcfg, tcfg);
+  const gg::TrainReport rep = gg::train_run_fp32(ds, mcfg, tcfg);
   const std::string out = rc.out.empty() ? "metrics.csv" : rc.out;
   gg::write_metrics_csv(out, rep);
   std::printf("wrote %s (%zu epochs)\n", out.c_str(), rep.epochs.size());
@@ -375,7 +346,7 @@ int cmd_verify(const RunConfig& rc) {
     gg::TrainConfig tref = tcfg;
     tref.grid = gg::DeviceGrid(tcfg.grid.dims[0], 1, 1, 1);
     tref.precision = gg::Precision::kFp32;
-    const gg::TrainReport ref = train_on_grid(ds, mcfg, tref);
+    const gg::TrainReport ref = gg::train_run_fp32(ds, mcfg, tref);
     // the run under test, optionally with one input feature offset (the
     // reference's check-failure hook)
     gg::Dataset ds_run = load_or_generate(small);
@@ -420,7 +391,7 @@ int cmd_verify(const RunConfig& rc) {
     mcfg.use_dropout = false;
     mcfg.dropout_rate = 0.0;
     double worst = 0.0;
-    run_ranks(gg::DeviceGrid(1, 1, 1, 1), [&](gg::RankComm& r) {
+    gg::run_ranks(gg::DeviceGrid(1, 1, 1, 1), [&](gg::RankComm& r) {
       gg::DeviceDataset dds(r, ds, mcfg.layers);
       worst = directional_gradient_check(r, dds, mcfg, ds.n() / 2, rc.seed);
     });
@@ -450,7 +421,7 @@ int cmd_sample_stats(const RunConfig& rc) {
     for (std::int64_t e = rp[r]; e < rp[r + 1]; ++e) full[static_cast<size_t>(r)] += val[static_cast<size_t>(e)];
   std::vector<std::uint64_t> included(static_cast<size_t>(n), 0);
   std::vector<double> agg(static_cast<size_t>(n), 0.0);
-  run_ranks(gg::DeviceGrid(1, 1, 1, 1), [&](gg::RankComm& r) {
+  gg::run_ranks(gg::DeviceGrid(1, 1, 1, 1), [&](gg::RankComm& r) {
     gg::DeviceDataset dds(r, ds, 1);
     gg::StepBatch batch;
     for (std::uint64_t d = 0; d < draws; ++d) {
