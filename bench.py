@@ -61,6 +61,7 @@ CONFIGS = {
                no_reference=True),
 }
 DATA_SEED, RUN_SEED, LR, DROPOUT = 7, 1, 1e-3, 0.1
+NVLINK_GBPS = 900.0  # B200 NVLink 5, per direction per GPU (nominal; no measured figure in MEASURED_PEAKS.json)
 
 
 def _peaks():
@@ -487,7 +488,11 @@ def main():
     hbm, bf16_burst, bf16_sust, peak_kind = _peaks()
     # dominant kernel class of the step
     kernels = {k: v for k, v in prof.items() if v["launches"] > 0}
-    dom_name, dom = max(kernels.items(), key=lambda kv: kv[1]["ms"])
+    # the dominant KERNEL class (the collectives class of a PMM grid — NVLink
+    # transfers plus waits for the slowest member — is reported beside it as
+    # roofline_comm against the NVLink 5 peak)
+    compute = {k: v for k, v in kernels.items() if k != "collectives"} or kernels
+    dom_name, dom = max(compute.items(), key=lambda kv: kv[1]["ms"])
     tensor_bound = dom_name.startswith("gemm") and dom["flops"] / max(dom["bytes"], 1) > 200
     per_launch_ms = dom["ms"] / dom["launches"]
     if tensor_bound:
@@ -513,6 +518,15 @@ def main():
             roof["traffic_source"] = {k: tr[k] for k in ("kernel", "us", "dram_TBps", "source")}
     except Exception:
         pass
+    roof_comm = None
+    comm = kernels.get("collectives")
+    if comm and comm["ms"] > 0 and world > 1:
+        nv = comm["bytes"] / (comm["ms"] / 1e3) / 1e9  # bytes moved between GPUs per rank / class time
+        roof_comm = {"bound": "nvlink", "achieved": nv, "peak": NVLINK_GBPS, "unit": "GB/s",
+                     "frac": nv / NVLINK_GBPS, "ms_per_step": comm["ms"] / prof_steps,
+                     "note": "per-rank NVLink bytes (pulled / pushed partials, reshard pieces, NCCL ring bytes) over the "
+                             "class's CUDA-event time, which includes waiting for the slowest group member; peak = "
+                             "NVLink 5 unidirectional per GPU (18 links x 50 GB/s, nominal)"}
     breakdown = {k: {"ms_per_step": v["ms"] / prof_steps,
                      "GB_per_s": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None,
                      "TFLOP_per_s": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] else None,
@@ -548,6 +562,7 @@ def main():
         "iters_per_s": 1000.0 / ms_step,
         "sampled_vertices_per_s": b * gd * 1000.0 / ms_step,
         "roofline": roof,
+        "roofline_comm": roof_comm,
         "kernels": breakdown,
         "kernels_note": f"per-kernel-class CUDA events over {prof_steps} further steps run after the timed "
                         "region (the timed steps carry no per-kernel events)",
