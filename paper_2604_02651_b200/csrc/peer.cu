@@ -466,7 +466,12 @@ void peer_all_reduce(Ctx& ctx, int axis, int64_t rows, int64_t cols, int64_t ld,
   const double pulled = static_cast<double>(rows) * cols * (src_bf16 ? 2 : 4) * (P.g - 1);
   ProfScope ps(ctx, kProfComm, pulled, 0);
   launch_wait(ctx, P, e);
-  const int blocks = ctx.num_sms * 3;
+  static const int bps = [] {  // GGB_PEER_BPS: reduction blocks per SM
+    const char* e = std::getenv("GGB_PEER_BPS");
+    const int v = e ? std::atoi(e) : 3;
+    return v >= 1 && v <= 8 ? v : 3;
+  }();
+  const int blocks = ctx.num_sms * bps;
   if (src_bf16) {
     if (P.g == 2)
       k_peer_reduce<bf16, 2><<<blocks, 256, 0, ctx.stream>>>(a);
