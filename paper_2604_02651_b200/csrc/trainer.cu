@@ -584,10 +584,12 @@ void forward(State& st, const Batch& bt, int precision, bool training, uint64_t 
     L.x.blk = xb;
     L.x.ldf = ld8(xb.cols());
     L.x.ldb = ld8(xb.cols());
-    L.x.f = grow<float>(L.x_f, xb.rows() * L.x.ldf);
     // bf16 copy: next SpMM operand (fast) and, for the last layer, the
-    // out-head operand (hi + lo in the accurate mode) and dW_out operand
+    // out-head operand (hi + lo in the accurate mode) and dW_out operand; the
+    // last layer's fp32 rows have no reader (no next SpMM, no residual), so
+    // they are not written
     const bool last = l == cfg.layers;
+    L.x.f = last ? nullptr : grow<float>(L.x_f, xb.rows() * L.x.ldf);
     L.x.b = (!accurate || last) ? grow<bf16>(L.x_b, xb.rows() * L.x.ldb) : nullptr;
     L.x.lo = (accurate && last) ? grow<bf16>(L.x_lo, xb.rows() * L.x.ldb) : nullptr;
     L.ldm = mask_words(std::max<int64_t>(xb.cols(), 1));
